@@ -1,0 +1,138 @@
+/*
+ * rsim.h -- C ABI of librsim, the B200-native multiplicative router.
+ *
+ * The reference (routesim, pure Python) has no FFI; each entry point below
+ * replaces one Python call on the routing hot path and is what a ctypes /
+ * cffi binding of the reference's ClusterSim would bind.
+ *
+ * Conventions: every call returns an rsim_status (0 = ok). Inputs are plain
+ * host pointers copied on entry; outputs are caller-allocated host buffers
+ * filled before return; no pointer is retained. A handle owns one CUDA
+ * device context + stream and is not thread-safe. There is no CPU fallback:
+ * without a usable sm_100 device rsim_create fails with RSIM_E_CUDA.
+ */
+#ifndef RSIM_H
+#define RSIM_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RSIM_OK = 0,
+    RSIM_E_INVALID = 1,        /* bad argument / config (reference: ValueError, cluster.py:36-64) */
+    RSIM_E_TRACE = 2,          /* malformed trace (reference: TraceError, trace.py:30-38)          */
+    RSIM_E_CACHE_FULL = 3,     /* pinned blocks exceed capacity (reference: CacheFullError, kvcache.py:163) */
+    RSIM_E_DUPLICATE = 4,      /* request enqueued twice (reference: DuplicateRequestError, engine.py:266) */
+    RSIM_E_INVARIANT = 5,      /* device consistency check failed (reference: InvariantError / unpin ValueError) */
+    RSIM_E_CUDA = 6,           /* CUDA runtime / launch failure                                    */
+    RSIM_E_QUEUE_OVERFLOW = 7, /* per-instance queue ring full: recreate with larger queue_capacity */
+    RSIM_E_TABLE_FULL = 8,     /* per-instance KV$ hash table too small: recreate with larger table */
+    RSIM_E_UNSUPPORTED = 9,    /* feature outside the device path (detector, staleness > 0, ...)  */
+    RSIM_E_COMM = 10,          /* multi-GPU exchange failure                                        */
+    RSIM_E_NO_INSTANCES = 11   /* empty candidate set (reference: NoInstancesError, policies.py:226) */
+} rsim_status;
+
+enum { RSIM_POLICY_MULTIPLICATIVE = 0, RSIM_POLICY_VLLM = 1, RSIM_POLICY_LEAST_BS = 2 };
+enum { RSIM_KV_P_TOKENS = 0, RSIM_KV_ONE_MINUS_HIT = 1 };
+enum { RSIM_BAL_BS = 0, RSIM_BAL_TOTAL_TOKENS = 1 };
+
+/* Mirrors ClusterConfig + CostModel + CacheConfig + PolicyConfig
+ * (reference cluster.py:32-64, engine.py:46-55, policies.py:37-53). */
+typedef struct rsim_config {
+    int32_t n_instances;            /* ClusterConfig.n_instances                              */
+    int32_t block_size;             /* CacheConfig.block_size                                 */
+    int64_t capacity_blocks;        /* CacheConfig.capacity_blocks, -1 = infinite (None)      */
+    double prefill_base_ms, prefill_per_token_ms;             /* CostModel                    */
+    double decode_base_ms, decode_per_seq_ms, decode_per_ctx_token_ms;
+    int64_t chunk_tokens, max_batch_requests;
+    int32_t policy;                 /* RSIM_POLICY_*                                           */
+    int32_t kv_indicator;           /* RSIM_KV_*   (multiplicative)                            */
+    int32_t balance_indicator;      /* RSIM_BAL_*  (multiplicative)                            */
+    int32_t debug_checks;           /* ClusterConfig.debug_checks                              */
+    double q_weight;                /* PolicyConfig.q_weight (vllm)                            */
+    uint64_t tie_seed_lo, tie_seed_hi; /* TieBreaker counter = stable_key(seed, tie_break_seed), cluster.py:90-94 */
+    int32_t device;                 /* CUDA ordinal                                            */
+    int32_t queue_capacity;         /* per-instance queue ring entries, 0 = auto               */
+    int32_t table_slots_log2;       /* per-instance KV$ table slots (log2), 0 = auto           */
+    int32_t ctas;                   /* replay cluster size (1..16), 0 = auto                   */
+    int32_t warps_per_cta;          /* 0 = auto                                                */
+    int32_t record_steps;           /* keep the per-step log (RunReport.steps / bs_series)     */
+    int64_t step_log_capacity;      /* records, 0 = auto                                       */
+    int64_t expected_keys;          /* sizing hint: upper bound on keys one instance holds, 0 = from trace */
+} rsim_config;
+
+typedef struct rsim rsim_t;
+
+/* ClusterSim.__init__ (cluster.py:73-102): allocate device state for N instances. */
+rsim_status rsim_create(const rsim_config *cfg, rsim_t **out);
+void rsim_destroy(rsim_t *h);
+/* Last error message of the handle (or of the last failed create when h == NULL). */
+const char *rsim_last_error(const rsim_t *h);
+/* Clear all instance, KV$ and tie-break state back to ClusterSim.__init__'s. */
+rsim_status rsim_reset(rsim_t *h);
+
+/* run_trace's input (cluster.py:172-201 + TraceRecord, trace.py:42-54), CSR-packed:
+ * request i has blocks[blk_off[i] .. blk_off[i+1]). arrival_us = round(arrival_s*1e6).
+ * Copies to HBM and runs the chain-hash kernel (hashing.chain_keys, hashing.py:36-47,
+ * plus the output-block keys of engine.py:363-372) over every request. */
+rsim_status rsim_load_trace(rsim_t *h, int64_t n_requests, const int64_t *arrival_us,
+                            const int64_t *input_tokens, const int64_t *output_tokens,
+                            const uint64_t *request_id, const int64_t *blk_off,
+                            const uint64_t *blocks);
+
+/* _loop_parallel's body (cluster.py:244-287) for decisions [first, first+count):
+ * per arrival, advance every instance through steps starting before it, then
+ * route (cluster.py:130-154) and enqueue on the winner -- entirely on device. */
+rsim_status rsim_replay(rsim_t *h, int64_t first, int64_t count);
+/* drain(until) (cluster.py:250-273); until = INT64_MAX runs every instance to idle. */
+rsim_status rsim_drain(rsim_t *h, int64_t until_us);
+
+/* Outputs of the loaded trace (RequestMetrics, metrics.py:31-41); -1 = not reached. */
+rsim_status rsim_read_decisions(rsim_t *h, int64_t first, int64_t count,
+                                int32_t *chosen_instance, int64_t *hit_tokens);
+rsim_status rsim_read_request_times(rsim_t *h, int64_t first, int64_t count,
+                                    int64_t *first_sched_us, int64_t *first_token_us,
+                                    int64_t *finish_us);
+/* Per-instance state: 12 int64 per instance:
+ * r_bs, q_bs, pending, total, dc (live), view r, q, pending, total, dc, busy_until_us, occupancy. */
+rsim_status rsim_read_instances(rsim_t *h, int64_t *out12xN);
+/* Step log: 6 int64 per record (instance, start_us, end_us, prefill_us, bs_after, step_index),
+ * unordered; *n_records receives the total (may exceed cap: then RSIM_E_INVALID). */
+rsim_status rsim_read_step_log(rsim_t *h, int64_t *out, int64_t cap, int64_t *n_records);
+/* Per-request batch size right after its enqueue (Collector.record_bs at route, cluster.py:152). */
+rsim_status rsim_read_route_bs(rsim_t *h, int64_t first, int64_t count, int64_t *bs);
+
+/* One ClusterSim.route(record, now_us) call WITHOUT advancing engine steps
+ * (cluster.py:130-154) on loaded request r. scores (N doubles) may be NULL. */
+rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen,
+                           int64_t *hit_tokens, double *scores);
+/* InstanceSim.enqueue(record r, now_us) on a given instance (engine.py:262-289). */
+rsim_status rsim_enqueue(rsim_t *h, int32_t instance, int64_t r, int64_t now_us, int64_t *hit_tokens);
+
+/* PrefixCache on one instance (kvcache.py:65-104), keys = chain keys. */
+rsim_status rsim_cache_insert_keys(rsim_t *h, int32_t instance, const uint64_t *keys, int64_t n,
+                                   int64_t now_us, int64_t *evicted);
+rsim_status rsim_cache_match_keys(rsim_t *h, int32_t instance, const uint64_t *keys, int64_t n,
+                                  int64_t *hit_blocks);
+
+/* Batched what-if probe (no commits): hit blocks of requests [first, first+count) on
+ * every instance against the current state -> out[count x N] (int32). */
+rsim_status rsim_probe_batch(rsim_t *h, int64_t first, int64_t count, int32_t *hit_blocks_out);
+
+/* hashing.chain_keys on the device (K1) for an ad-hoc block list. */
+rsim_status rsim_chain_keys(rsim_t *h, const uint64_t *blocks, int64_t n, uint64_t *keys_out);
+
+/* Timing of the last rsim_replay / rsim_drain / K1 launch (CUDA events on the handle's stream). */
+rsim_status rsim_last_timings(rsim_t *h, double *replay_ms, double *k1_ms, double *drain_ms);
+/* Per-decision device timestamps (%globaltimer ns) of the last replay, count entries. */
+rsim_status rsim_read_decision_ns(rsim_t *h, int64_t first, int64_t count, int64_t *ns);
+/* Number of kernels librsim launched since create (evidence for bench gpu_launches). */
+int64_t rsim_launch_count(const rsim_t *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSIM_H */

@@ -1,0 +1,249 @@
+"""ctypes binding of librsim (include/rsim.h).
+
+The product path: every routing decision of this package is computed by
+librsim's sm_100a kernels. If the library or a suitable GPU is missing,
+``lib()`` / ``Handle`` raise -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .config import (CacheFullError, DuplicateRequestError, InvariantError, NoInstancesError,
+                     UnsupportedConfigError)
+from .trace import TraceError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librsim.so")
+
+RSIM_OK = 0
+E_INVALID, E_TRACE, E_CACHE_FULL, E_DUPLICATE, E_INVARIANT, E_CUDA = 1, 2, 3, 4, 5, 6
+E_QUEUE_OVERFLOW, E_TABLE_FULL, E_UNSUPPORTED, E_COMM, E_NO_INSTANCES = 7, 8, 9, 10, 11
+
+
+class RsimError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"[rsim status {status}] {message}")
+        self.status = status
+
+
+class CapacityError(RsimError):
+    """A device ring/table was sized too small; the caller may retry larger."""
+
+
+_EXC = {
+    E_INVALID: ValueError, E_TRACE: TraceError, E_CACHE_FULL: CacheFullError,
+    E_DUPLICATE: DuplicateRequestError, E_INVARIANT: InvariantError,
+    E_UNSUPPORTED: UnsupportedConfigError, E_NO_INSTANCES: NoInstancesError,
+}
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("n_instances", C.c_int32), ("block_size", C.c_int32), ("capacity_blocks", C.c_int64),
+        ("prefill_base_ms", C.c_double), ("prefill_per_token_ms", C.c_double),
+        ("decode_base_ms", C.c_double), ("decode_per_seq_ms", C.c_double),
+        ("decode_per_ctx_token_ms", C.c_double),
+        ("chunk_tokens", C.c_int64), ("max_batch_requests", C.c_int64),
+        ("policy", C.c_int32), ("kv_indicator", C.c_int32), ("balance_indicator", C.c_int32),
+        ("debug_checks", C.c_int32), ("q_weight", C.c_double),
+        ("tie_seed_lo", C.c_uint64), ("tie_seed_hi", C.c_uint64),
+        ("device", C.c_int32), ("queue_capacity", C.c_int32), ("table_slots_log2", C.c_int32),
+        ("ctas", C.c_int32), ("warps_per_cta", C.c_int32), ("record_steps", C.c_int32),
+        ("step_log_capacity", C.c_int64), ("expected_keys", C.c_int64),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load librsim.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                           "(the router has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    P, I64, I32 = C.c_void_p, C.c_int64, C.c_int32
+    sig = {
+        "rsim_create": ([C.POINTER(Config), C.POINTER(C.c_void_p)], C.c_int),
+        "rsim_destroy": ([P], None),
+        "rsim_last_error": ([P], C.c_char_p),
+        "rsim_reset": ([P], C.c_int),
+        "rsim_load_trace": ([P, I64, P, P, P, P, P, P], C.c_int),
+        "rsim_replay": ([P, I64, I64], C.c_int),
+        "rsim_drain": ([P, I64], C.c_int),
+        "rsim_read_decisions": ([P, I64, I64, P, P], C.c_int),
+        "rsim_read_request_times": ([P, I64, I64, P, P, P], C.c_int),
+        "rsim_read_instances": ([P, P], C.c_int),
+        "rsim_read_step_log": ([P, P, I64, P], C.c_int),
+        "rsim_read_route_bs": ([P, I64, I64, P], C.c_int),
+        "rsim_route_one": ([P, I64, I64, P, P, P], C.c_int),
+        "rsim_enqueue": ([P, I32, I64, I64, P], C.c_int),
+        "rsim_cache_insert_keys": ([P, I32, P, I64, I64, P], C.c_int),
+        "rsim_cache_match_keys": ([P, I32, P, I64, P], C.c_int),
+        "rsim_probe_batch": ([P, I64, I64, P], C.c_int),
+        "rsim_chain_keys": ([P, P, I64, P], C.c_int),
+        "rsim_last_timings": ([P, P, P, P], C.c_int),
+        "rsim_read_decision_ns": ([P, I64, I64, P], C.c_int),
+        "rsim_launch_count": ([P], I64),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+EXPORTED = ("rsim_create", "rsim_destroy", "rsim_last_error", "rsim_reset", "rsim_load_trace", "rsim_replay",
+            "rsim_drain", "rsim_read_decisions", "rsim_read_request_times", "rsim_read_instances",
+            "rsim_read_step_log", "rsim_read_route_bs", "rsim_route_one", "rsim_enqueue",
+            "rsim_cache_insert_keys", "rsim_cache_match_keys", "rsim_probe_batch", "rsim_chain_keys",
+            "rsim_last_timings", "rsim_read_decision_ns", "rsim_launch_count")
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _c64(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+class Handle:
+    """Owns one librsim handle (one GPU's instance shard)."""
+
+    def __init__(self, cfg: Config):
+        self._L = lib()
+        h = C.c_void_p()
+        st = self._L.rsim_create(C.byref(cfg), C.byref(h))
+        if st != RSIM_OK:
+            self._h = None
+            self._raise(st, self._L.rsim_last_error(None).decode())
+        self._h = h
+        self.cfg = cfg
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.rsim_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _raise(self, st: int, msg: str | None = None):
+        if msg is None:
+            msg = self._L.rsim_last_error(self._h).decode()
+        if st in (E_QUEUE_OVERFLOW, E_TABLE_FULL):
+            raise CapacityError(st, msg)
+        exc = _EXC.get(st)
+        if exc is not None:
+            raise exc(msg)
+        raise RsimError(st, msg)
+
+    def _ck(self, st: int):
+        if st != RSIM_OK:
+            self._raise(st)
+
+    # -- calls ------------------------------------------------------------------------
+    def reset(self):
+        self._ck(self._L.rsim_reset(self._h))
+
+    def load(self, arrival_us, in_tok, out_tok, rid, blk_off, blocks):
+        n = len(arrival_us)
+        arrays = (_c64(arrival_us, np.int64), _c64(in_tok, np.int64), _c64(out_tok, np.int64),
+                  _c64(rid, np.uint64), _c64(blk_off, np.int64), _c64(blocks, np.uint64))
+        if arrays[5].size == 0:
+            arrays = arrays[:5] + (np.zeros(1, np.uint64),)
+        self._ck(self._L.rsim_load_trace(self._h, n, *(_p(a) for a in arrays)))
+
+    def replay(self, first: int, count: int):
+        self._ck(self._L.rsim_replay(self._h, first, count))
+
+    def drain(self, until_us: int = (1 << 63) - 1):
+        self._ck(self._L.rsim_drain(self._h, until_us))
+
+    def decisions(self, first: int, count: int):
+        ch = np.empty(count, np.int32)
+        ht = np.empty(count, np.int64)
+        self._ck(self._L.rsim_read_decisions(self._h, first, count, _p(ch), _p(ht)))
+        return ch, ht
+
+    def request_times(self, first: int, count: int):
+        a, b, c = (np.empty(count, np.int64) for _ in range(3))
+        self._ck(self._L.rsim_read_request_times(self._h, first, count, _p(a), _p(b), _p(c)))
+        return a, b, c
+
+    def route_bs(self, first: int, count: int):
+        a = np.empty(count, np.int64)
+        self._ck(self._L.rsim_read_route_bs(self._h, first, count, _p(a)))
+        return a
+
+    def decision_ns(self, first: int, count: int):
+        a = np.empty(count, np.int64)
+        self._ck(self._L.rsim_read_decision_ns(self._h, first, count, _p(a)))
+        return a
+
+    def instances(self) -> np.ndarray:
+        out = np.empty((self.cfg.n_instances, 12), np.int64)
+        self._ck(self._L.rsim_read_instances(self._h, _p(out)))
+        return out
+
+    def step_log(self):
+        """(records[n, 6], n) -- records is None when the device log overflowed."""
+        n = C.c_int64(0)
+        self._L.rsim_read_step_log(self._h, None, 0, C.byref(n))
+        if n.value > self.cfg.step_log_capacity and self.cfg.step_log_capacity > 0:
+            return None, n.value
+        out = np.empty((max(n.value, 1), 6), np.int64)
+        self._ck(self._L.rsim_read_step_log(self._h, _p(out), n.value, C.byref(n)))
+        return out[: n.value], n.value
+
+    def route_one(self, r: int, now_us: int, want_scores: bool = True):
+        ch = np.zeros(1, np.int32)
+        ht = np.zeros(1, np.int64)
+        sc = np.empty(self.cfg.n_instances, np.float64) if want_scores else None
+        self._ck(self._L.rsim_route_one(self._h, r, now_us, _p(ch), _p(ht), _p(sc)))
+        return int(ch[0]), int(ht[0]), sc
+
+    def enqueue(self, instance: int, r: int, now_us: int) -> int:
+        ht = np.zeros(1, np.int64)
+        self._ck(self._L.rsim_enqueue(self._h, instance, r, now_us, _p(ht)))
+        return int(ht[0])
+
+    def cache_insert_keys(self, instance: int, keys, now_us: int) -> int:
+        k = _c64(keys, np.uint64)
+        ev = np.zeros(1, np.int64)
+        self._ck(self._L.rsim_cache_insert_keys(self._h, instance, _p(k), k.size, now_us, _p(ev)))
+        return int(ev[0])
+
+    def cache_match_keys(self, instance: int, keys) -> int:
+        k = _c64(keys, np.uint64)
+        hit = np.zeros(1, np.int64)
+        self._ck(self._L.rsim_cache_match_keys(self._h, instance, _p(k), k.size, _p(hit)))
+        return int(hit[0])
+
+    def probe_batch(self, first: int, count: int) -> np.ndarray:
+        out = np.empty((count, self.cfg.n_instances), np.int32)
+        self._ck(self._L.rsim_probe_batch(self._h, first, count, _p(out)))
+        return out
+
+    def chain_keys(self, blocks) -> np.ndarray:
+        b = _c64(blocks, np.uint64)
+        out = np.empty_like(b)
+        self._ck(self._L.rsim_chain_keys(self._h, _p(b), b.size, _p(out)))
+        return out
+
+    def timings(self):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        self._ck(self._L.rsim_last_timings(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def launch_count(self) -> int:
+        return int(self._L.rsim_launch_count(self._h))

@@ -1,0 +1,568 @@
+// rsim.cu -- librsim: host side of the C ABI declared in include/rsim.h.
+//
+// Owns all device memory of one GPU's instance shard, a CUDA stream and the
+// launch configuration of the persistent replay cluster. Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -lineinfo
+//        -Xcompiler -fPIC -shared -o librsim.so rsim.cu
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cstdarg>
+#include <vector>
+#include <algorithm>
+
+#include "../../include/rsim.h"
+#include "rsim_kernels.cuh"
+
+namespace {
+
+char g_create_err[512] = "";
+
+template <typename T>
+struct DevArr {
+    T *p = nullptr;
+    size_t cap = 0;
+    void free_() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+    // grow keeping the first `keep` elements
+    cudaError_t reserve(size_t n, size_t keep, cudaStream_t s) {
+        if (n <= cap) return cudaSuccess;
+        size_t nc = std::max(n, cap * 2 + 16);
+        T *q = nullptr;
+        cudaError_t e = cudaMalloc(&q, nc * sizeof(T));
+        if (e != cudaSuccess) return e;
+        if (p && keep) {
+            e = cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) { cudaFree(q); return e; }
+            cudaStreamSynchronize(s);
+        }
+        if (p) cudaFree(p);
+        p = q; cap = nc;
+        return cudaSuccess;
+    }
+};
+
+}  // namespace
+
+struct rsim {
+    rsim_config cfg;
+    char err[512];
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int C = 1, W = 1, ipw = 1, per_cta = 1;
+    size_t smem_bytes = 0;
+    int qlog2 = 0, slog2 = 0;
+    i64 max_occ = 0;
+    i64 R = 0, nblk = 0, nout = 0;       // loaded requests, blocks, output keys
+    i64 launches = 0;
+    float last_replay_ms = 0, last_k1_ms = 0, last_drain_ms = 0;
+    // trace
+    DevArr<i64> arrival, in_tok, out_tok, blk_off, ooff;
+    DevArr<u64> rid, blocks, ckeys, okeys;
+    DevArr<int> hit_blocks, chosen;
+    DevArr<i64> hit_tokens, first_sched, first_token, finish, route_bs, dec_ns;
+    // instances
+    Inst *inst = nullptr;
+    QEnt *qbuf = nullptr;
+    REnt *rbuf = nullptr;
+    u64 *tkeys = nullptr;
+    Meta *tmeta = nullptr;
+    u64 *tie = nullptr;
+    int *errbuf = nullptr;
+    int *flag = nullptr;
+    i64 *log = nullptr;
+    u64 *log_n = nullptr;
+    i64 log_cap = 0;
+    double *scores = nullptr;
+    u64 *scratch_keys = nullptr;
+    size_t scratch_cap = 0;
+    i64 *scratch_res = nullptr;
+};
+
+static rsim_status fail(rsim_t *h, rsim_status st, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    if (h) vsnprintf(h->err, sizeof(h->err), fmt, ap);
+    else vsnprintf(g_create_err, sizeof(g_create_err), fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+#define CK(h, call)                                                                            \
+    do {                                                                                       \
+        cudaError_t _e = (call);                                                               \
+        if (_e != cudaSuccess)                                                                 \
+            return fail((h), RSIM_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), \
+                        __FILE__, __LINE__);                                                   \
+    } while (0)
+
+static int ilog2_ceil(i64 v) { int l = 0; while ((1LL << l) < v) l++; return l; }
+
+static Params make_params(rsim_t *h) {
+    Params P;
+    memset(&P, 0, sizeof(P));
+    P.arrival = h->arrival.p; P.in_tok = h->in_tok.p; P.out_tok = h->out_tok.p;
+    P.blk_off = h->blk_off.p; P.ooff = h->ooff.p;
+    P.rid = h->rid.p; P.ckeys = h->ckeys.p; P.okeys = h->okeys.p;
+    P.hit_blocks = h->hit_blocks.p; P.chosen = h->chosen.p; P.hit_tokens = h->hit_tokens.p;
+    P.first_sched = h->first_sched.p; P.first_token = h->first_token.p; P.finish = h->finish.p;
+    P.route_bs = h->route_bs.p; P.dec_ns = h->dec_ns.p;
+    P.N = h->cfg.n_instances; P.C = h->C; P.W = h->W; P.ipw = h->ipw; P.per_cta = h->per_cta;
+    P.bs = h->cfg.block_size; P.policy = h->cfg.policy; P.kv_ind = h->cfg.kv_indicator;
+    P.bal_ind = h->cfg.balance_indicator; P.debug = h->cfg.debug_checks;
+    P.cap = h->cfg.capacity_blocks; P.chunk = h->cfg.chunk_tokens; P.max_batch = h->cfg.max_batch_requests;
+    P.pb = h->cfg.prefill_base_ms; P.pt = h->cfg.prefill_per_token_ms; P.db = h->cfg.decode_base_ms;
+    P.ds = h->cfg.decode_per_seq_ms; P.dcc = h->cfg.decode_per_ctx_token_ms; P.qw = h->cfg.q_weight;
+    P.inst = h->inst; P.qbuf = h->qbuf; P.qlog2 = h->qlog2; P.rbuf = h->rbuf;
+    P.tkeys = h->tkeys; P.tmeta = h->tmeta; P.slog2 = h->slog2; P.max_occ = h->max_occ; P.empty = 0;
+    P.tie = h->tie; P.err = h->errbuf;
+    P.log = h->log; P.log_cap = h->log_cap; P.log_n = h->log_n;
+    P.scores = nullptr;
+    return P;
+}
+
+static rsim_status check_device_error(rsim_t *h) {
+    int e[4];
+    CK(h, cudaMemcpyAsync(e, h->errbuf, sizeof(e), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (e[0] == 0) return RSIM_OK;
+    CK(h, cudaMemsetAsync(h->errbuf, 0, 4 * sizeof(int), h->stream));
+    switch (e[0]) {
+        case DEV_E_CACHE_FULL: return fail(h, RSIM_E_CACHE_FULL, "pinned blocks exceed capacity");
+        case DEV_E_INVARIANT: return fail(h, RSIM_E_INVARIANT, "unpin of a chain that is not pinned / missing chain");
+        case DEV_E_QUEUE_OVERFLOW: return fail(h, RSIM_E_QUEUE_OVERFLOW, "instance queue ring full (queue_capacity=%d)", 1 << h->qlog2);
+        case DEV_E_TABLE_FULL: return fail(h, RSIM_E_TABLE_FULL, "instance KV$ table over 3/4 load (slots=%d)", 1 << h->slog2);
+        case 11: return fail(h, RSIM_E_NO_INSTANCES, "no instances to route to");
+        default: return fail(h, RSIM_E_INVARIANT, "device error %d", e[0]);
+    }
+}
+
+static rsim_status init_state(rsim_t *h) {
+    const int N = h->cfg.n_instances;
+    std::vector<Inst> hs(N);
+    for (auto &s : hs) {
+        memset(&s, 0, sizeof(s));
+        s.next_step = RSIM_NONE; s.due = RSIM_NONE; s.next_finish = RSIM_NONE;
+    }
+    CK(h, cudaMemcpyAsync(h->inst, hs.data(), N * sizeof(Inst), cudaMemcpyHostToDevice, h->stream));
+    const size_t slots = (size_t)N << h->slog2;
+    CK(h, cudaMemsetAsync(h->tkeys, 0, slots * sizeof(u64), h->stream));   // EMPTY = 0
+    CK(h, cudaMemsetAsync(h->tmeta, 0, slots * sizeof(Meta), h->stream));
+    u64 tie[2] = {h->cfg.tie_seed_lo, h->cfg.tie_seed_hi};
+    CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemsetAsync(h->errbuf, 0, 4 * sizeof(int), h->stream));
+    CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    h->R = 0; h->nblk = 0; h->nout = 0;
+    // blk_off / ooff hold a leading 0
+    CK(h, h->blk_off.reserve(1, 0, h->stream));
+    CK(h, h->ooff.reserve(1, 0, h->stream));
+    CK(h, cudaMemsetAsync(h->blk_off.p, 0, sizeof(i64), h->stream));
+    CK(h, cudaMemsetAsync(h->ooff.p, 0, sizeof(i64), h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    return RSIM_OK;
+}
+
+extern "C" {
+
+const char *rsim_last_error(const rsim_t *h) { return h ? h->err : g_create_err; }
+int64_t rsim_launch_count(const rsim_t *h) { return h ? h->launches : 0; }
+
+rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
+    if (!cfg || !out) return fail(nullptr, RSIM_E_INVALID, "null argument");
+    *out = nullptr;
+    const rsim_config &c = *cfg;
+    if (c.n_instances < 1) return fail(nullptr, RSIM_E_INVALID, "n_instances must be >= 1");
+    if (c.block_size < 1) return fail(nullptr, RSIM_E_INVALID, "block_size must be >= 1");
+    if (c.capacity_blocks == 0 || c.capacity_blocks < -1) return fail(nullptr, RSIM_E_INVALID, "capacity_blocks must be >= 1 or -1");
+    if (c.chunk_tokens < 1 || c.max_batch_requests < 1) return fail(nullptr, RSIM_E_INVALID, "chunk_tokens and max_batch_requests must be >= 1");
+    if (c.policy < 0 || c.policy > 2) return fail(nullptr, RSIM_E_UNSUPPORTED, "policy %d not on the device path", c.policy);
+    if (c.prefill_base_ms < 0 || c.prefill_per_token_ms < 0 || c.decode_base_ms < 0 || c.decode_per_seq_ms < 0 ||
+        c.decode_per_ctx_token_ms < 0)
+        return fail(nullptr, RSIM_E_INVALID, "cost model coefficients must be non-negative");
+    if (c.max_batch_requests > (1 << 20)) return fail(nullptr, RSIM_E_INVALID, "max_batch_requests too large");
+
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(nullptr, RSIM_E_CUDA, "no CUDA device available (librsim has no CPU fallback): %s",
+                    cudaGetErrorString(e));
+    if (c.device < 0 || c.device >= ndev) return fail(nullptr, RSIM_E_INVALID, "device %d out of range", c.device);
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, c.device);
+    if (prop.major < 10) return fail(nullptr, RSIM_E_CUDA, "device %s (sm_%d%d) is not sm_100", prop.name, prop.major, prop.minor);
+
+    rsim_t *h = new rsim_t();
+    h->cfg = c;
+    h->err[0] = 0;
+    if (cudaSetDevice(c.device) != cudaSuccess) { delete h; return fail(nullptr, RSIM_E_CUDA, "cudaSetDevice failed"); }
+    CK(nullptr, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CK(nullptr, cudaEventCreate(&h->ev0));
+    CK(nullptr, cudaEventCreate(&h->ev1));
+
+    // ---- replay cluster shape
+    const int N = c.n_instances;
+    int C = c.ctas;
+    if (C <= 0) C = N <= 128 ? 1 : std::min(16, (N + 63) / 64);
+    C = std::max(1, std::min(16, std::min(C, N)));
+    int per_cta = (N + C - 1) / C;
+    int W = c.warps_per_cta > 0 ? c.warps_per_cta : std::min(32, per_cta);
+    W = std::max(1, std::min(32, W));
+    int ipw = (per_cta + W - 1) / W;
+    if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
+    h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
+    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(2 * W + 2 * C) * sizeof(Part);
+    if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
+    cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
+    if (C > 8) cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+
+    // ---- sizing
+    int ql = c.queue_capacity > 0 ? ilog2_ceil(c.queue_capacity) : 10;
+    h->qlog2 = std::max(4, ql);
+    int sl = c.table_slots_log2;
+    if (sl <= 0) {
+        i64 expect = c.expected_keys > 0 ? c.expected_keys : 3000;   // callers size from the trace
+        sl = ilog2_ceil(expect * 4 / 3 + 64);
+    }
+    h->slog2 = std::max(6, std::min(30, sl));
+    h->max_occ = ((i64)3 << h->slog2) / 4;
+    const size_t slots = (size_t)N << h->slog2;
+    CK(nullptr, cudaMalloc(&h->inst, N * sizeof(Inst)));
+    CK(nullptr, cudaMalloc(&h->qbuf, ((size_t)N << h->qlog2) * sizeof(QEnt)));
+    CK(nullptr, cudaMalloc(&h->rbuf, (size_t)N * c.max_batch_requests * sizeof(REnt)));
+    CK(nullptr, cudaMalloc(&h->tkeys, slots * sizeof(u64)));
+    CK(nullptr, cudaMalloc(&h->tmeta, slots * sizeof(Meta)));
+    CK(nullptr, cudaMalloc(&h->tie, 2 * sizeof(u64)));
+    CK(nullptr, cudaMalloc(&h->errbuf, 4 * sizeof(int)));
+    CK(nullptr, cudaMalloc(&h->flag, sizeof(int)));
+    CK(nullptr, cudaMalloc(&h->log_n, sizeof(u64)));
+    CK(nullptr, cudaMalloc(&h->scores, N * sizeof(double)));
+    CK(nullptr, cudaMalloc(&h->scratch_res, 4 * sizeof(i64)));
+    if (c.record_steps) {
+        h->log_cap = c.step_log_capacity > 0 ? c.step_log_capacity : (1 << 20);
+        CK(nullptr, cudaMalloc(&h->log, (size_t)h->log_cap * 6 * sizeof(i64)));
+    }
+    rsim_status st = init_state(h);
+    if (st != RSIM_OK) { snprintf(g_create_err, sizeof(g_create_err), "%s", h->err); rsim_destroy(h); return st; }
+    *out = h;
+    return RSIM_OK;
+}
+
+void rsim_destroy(rsim_t *h) {
+    if (!h) return;
+    cudaSetDevice(h->cfg.device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    DevArr<i64> *ai[] = {&h->arrival, &h->in_tok, &h->out_tok, &h->blk_off, &h->ooff, &h->hit_tokens,
+                         &h->first_sched, &h->first_token, &h->finish, &h->route_bs, &h->dec_ns};
+    for (auto *a : ai) a->free_();
+    h->rid.free_(); h->blocks.free_(); h->ckeys.free_(); h->okeys.free_();
+    h->hit_blocks.free_(); h->chosen.free_();
+    void *ps[] = {h->inst, h->qbuf, h->rbuf, h->tkeys, h->tmeta, h->tie, h->errbuf, h->flag, h->log, h->log_n,
+                  h->scores, h->scratch_keys, h->scratch_res};
+    for (void *p : ps) if (p) cudaFree(p);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+rsim_status rsim_reset(rsim_t *h) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    return init_state(h);
+}
+
+rsim_status rsim_load_trace(rsim_t *h, int64_t n, const int64_t *arrival_us, const int64_t *input_tokens,
+                            const int64_t *output_tokens, const uint64_t *request_id, const int64_t *blk_off,
+                            const uint64_t *blocks) {
+    if (!h) return RSIM_E_INVALID;
+    if (n < 0) return fail(h, RSIM_E_INVALID, "negative request count");
+    if (n == 0) return RSIM_OK;
+    if (!arrival_us || !input_tokens || !output_tokens || !request_id || !blk_off || !blocks)
+        return fail(h, RSIM_E_INVALID, "null trace array");
+    CK(h, cudaSetDevice(h->cfg.device));
+    if (blk_off[0] != 0) return fail(h, RSIM_E_TRACE, "blk_off[0] must be 0");
+    const i64 bs = h->cfg.block_size;
+    std::vector<i64> off(n + 1), oo(n + 1);
+    oo[0] = h->nout;
+    for (i64 i = 0; i < n; i++) {
+        const i64 B = blk_off[i + 1] - blk_off[i];
+        if (B < 1) return fail(h, RSIM_E_TRACE, "request %lld has no blocks", (long long)i);
+        if (input_tokens[i] < 1 || output_tokens[i] < 1) return fail(h, RSIM_E_TRACE, "request %lld: in/out must be >= 1", (long long)i);
+        if (input_tokens[i] > (1LL << 40) || output_tokens[i] > (1LL << 31)) return fail(h, RSIM_E_TRACE, "request %lld: token count too large", (long long)i);
+        if (i > 0 && arrival_us[i] < arrival_us[i - 1]) return fail(h, RSIM_E_TRACE, "arrivals are not sorted");
+        off[i] = h->nblk + blk_off[i];
+        oo[i + 1] = oo[i] + (output_tokens[i] + bs - 1) / bs;
+    }
+    off[n] = h->nblk + blk_off[n];
+    if (h->R > 0) {
+        i64 last = 0;
+        CK(h, cudaMemcpy(&last, h->arrival.p + h->R - 1, sizeof(i64), cudaMemcpyDeviceToHost));
+        if (arrival_us[0] < last) return fail(h, RSIM_E_TRACE, "appended arrivals precede the loaded trace");
+    }
+    const i64 R0 = h->R, R1 = h->R + n, nb = blk_off[n], no = oo[n] - h->nout;
+    cudaStream_t s = h->stream;
+    CK(h, h->arrival.reserve(R1, R0, s)); CK(h, h->in_tok.reserve(R1, R0, s)); CK(h, h->out_tok.reserve(R1, R0, s));
+    CK(h, h->rid.reserve(R1, R0, s)); CK(h, h->blk_off.reserve(R1 + 1, R0 + 1, s)); CK(h, h->ooff.reserve(R1 + 1, R0 + 1, s));
+    CK(h, h->blocks.reserve(h->nblk + nb, h->nblk, s)); CK(h, h->ckeys.reserve(h->nblk + nb, h->nblk, s));
+    CK(h, h->okeys.reserve(h->nout + no + 1, h->nout, s));
+    CK(h, h->hit_blocks.reserve(R1, R0, s)); CK(h, h->chosen.reserve(R1, R0, s));
+    DevArr<i64> *outs[] = {&h->hit_tokens, &h->first_sched, &h->first_token, &h->finish, &h->route_bs, &h->dec_ns};
+    for (auto *a : outs) CK(h, a->reserve(R1, R0, s));
+    CK(h, cudaMemcpyAsync(h->arrival.p + R0, arrival_us, n * sizeof(i64), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemcpyAsync(h->in_tok.p + R0, input_tokens, n * sizeof(i64), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemcpyAsync(h->out_tok.p + R0, output_tokens, n * sizeof(i64), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemcpyAsync(h->rid.p + R0, request_id, n * sizeof(u64), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemcpyAsync(h->blk_off.p + R0, off.data(), (n + 1) * sizeof(i64), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemcpyAsync(h->ooff.p + R0, oo.data(), (n + 1) * sizeof(i64), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemcpyAsync(h->blocks.p + h->nblk, blocks, nb * sizeof(u64), cudaMemcpyHostToDevice, s));
+    for (auto *a : outs) CK(h, cudaMemsetAsync(a->p + R0, 0xff, n * sizeof(i64), s));   // -1
+    CK(h, cudaMemsetAsync(h->chosen.p + R0, 0xff, n * sizeof(int), s));
+    CK(h, cudaMemsetAsync(h->hit_blocks.p + R0, 0, n * sizeof(int), s));
+    CK(h, cudaMemsetAsync(h->flag, 0, sizeof(int), s));
+    // K1
+    const i64 nwarps = (n + 31) / 32;
+    const int grid = (int)((nwarps + K1_WARPS - 1) / K1_WARPS);
+    CK(h, cudaEventRecord(h->ev0, s));
+    k1_chain_keys<<<grid, 32 * K1_WARPS, 0, s>>>(h->blk_off.p, h->blocks.p, h->ckeys.p, h->ooff.p, h->okeys.p,
+                                                   h->rid.p, R0, R1, 0ULL, h->flag);
+    h->launches++;
+    CK(h, cudaGetLastError());
+    CK(h, cudaEventRecord(h->ev1, s));
+    int flag = 0;
+    CK(h, cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(h, cudaStreamSynchronize(s));
+    cudaEventElapsedTime(&h->last_k1_ms, h->ev0, h->ev1);
+    h->R = R1; h->nblk += nb; h->nout += no;
+    if (flag) return fail(h, RSIM_E_TRACE, "a chain key equals the table sentinel 0 (probability 2^-64 per key)");
+    return RSIM_OK;
+}
+
+static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode, int target, double *scores_dev,
+                                 float *ms_out) {
+    Params P = make_params(h);
+    P.scores = scores_dev;
+    cudaLaunchConfig_t lc;
+    memset(&lc, 0, sizeof(lc));
+    lc.gridDim = dim3(h->C, 1, 1);
+    lc.blockDim = dim3(32 * h->W, 1, 1);
+    lc.dynamicSmemBytes = h->smem_bytes;
+    lc.stream = h->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = h->C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(h, cudaEventRecord(h->ev0, h->stream));
+    CK(h, cudaLaunchKernelEx(&lc, replay_kernel, P, (i64)k0, (i64)k1, (i64)until, mode, target));
+    h->launches++;
+    CK(h, cudaEventRecord(h->ev1, h->stream));
+    CK(h, cudaEventSynchronize(h->ev1));
+    if (ms_out) cudaEventElapsedTime(ms_out, h->ev0, h->ev1);
+    return check_device_error(h);
+}
+
+rsim_status rsim_replay(rsim_t *h, int64_t first, int64_t count) {
+    if (!h) return RSIM_E_INVALID;
+    if (first < 0 || count < 0 || first + count > h->R) return fail(h, RSIM_E_INVALID, "decision range out of the loaded trace");
+    if (count == 0) return RSIM_OK;
+    CK(h, cudaSetDevice(h->cfg.device));
+    return launch_replay(h, first, first + count, 0, MODE_REPLAY, -1, nullptr, &h->last_replay_ms);
+}
+
+rsim_status rsim_drain(rsim_t *h, int64_t until_us) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    return launch_replay(h, 0, 0, until_us, MODE_DRAIN, -1, nullptr, &h->last_drain_ms);
+}
+
+rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen, int64_t *hit_tokens, double *scores) {
+    if (!h) return RSIM_E_INVALID;
+    if (r < 0 || r >= h->R) return fail(h, RSIM_E_INVALID, "request index out of range");
+    CK(h, cudaSetDevice(h->cfg.device));
+    rsim_status st = launch_replay(h, r, r + 1, now_us, MODE_ROUTE, -1, scores ? h->scores : nullptr, nullptr);
+    if (st != RSIM_OK) return st;
+    if (chosen) CK(h, cudaMemcpy(chosen, h->chosen.p + r, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hit_tokens) CK(h, cudaMemcpy(hit_tokens, h->hit_tokens.p + r, sizeof(i64), cudaMemcpyDeviceToHost));
+    if (scores) CK(h, cudaMemcpy(scores, h->scores, h->cfg.n_instances * sizeof(double), cudaMemcpyDeviceToHost));
+    return RSIM_OK;
+}
+
+rsim_status rsim_enqueue(rsim_t *h, int32_t instance, int64_t r, int64_t now_us, int64_t *hit_tokens) {
+    if (!h) return RSIM_E_INVALID;
+    if (r < 0 || r >= h->R) return fail(h, RSIM_E_INVALID, "request index out of range");
+    if (instance < 0 || instance >= h->cfg.n_instances) return fail(h, RSIM_E_INVALID, "instance out of range");
+    CK(h, cudaSetDevice(h->cfg.device));
+    rsim_status st = launch_replay(h, r, r + 1, now_us, MODE_ENQUEUE, instance, nullptr, nullptr);
+    if (st != RSIM_OK) return st;
+    if (hit_tokens) CK(h, cudaMemcpy(hit_tokens, h->hit_tokens.p + r, sizeof(i64), cudaMemcpyDeviceToHost));
+    return RSIM_OK;
+}
+
+static rsim_status stage_keys(rsim_t *h, const uint64_t *keys, int64_t n) {
+    if ((size_t)n > h->scratch_cap) {
+        if (h->scratch_keys) cudaFree(h->scratch_keys);
+        h->scratch_cap = std::max<size_t>(n, 1024);
+        CK(h, cudaMalloc(&h->scratch_keys, h->scratch_cap * sizeof(u64)));
+    }
+    if (n) CK(h, cudaMemcpy(h->scratch_keys, keys, n * sizeof(u64), cudaMemcpyHostToDevice));
+    return RSIM_OK;
+}
+
+rsim_status rsim_cache_insert_keys(rsim_t *h, int32_t instance, const uint64_t *keys, int64_t n, int64_t now_us,
+                                   int64_t *evicted) {
+    if (!h) return RSIM_E_INVALID;
+    if (instance < 0 || instance >= h->cfg.n_instances) return fail(h, RSIM_E_INVALID, "instance out of range");
+    for (i64 i = 0; i < n; i++) if (keys[i] == 0) return fail(h, RSIM_E_INVALID, "key equals the table sentinel 0");
+    CK(h, cudaSetDevice(h->cfg.device));
+    rsim_status st = stage_keys(h, keys, n);
+    if (st) return st;
+    cache_op_kernel<<<1, 32, 0, h->stream>>>(make_params(h), instance, 0, h->scratch_keys, (int)n, now_us, h->scratch_res);
+    h->launches++;
+    CK(h, cudaGetLastError());
+    i64 res = 0;
+    CK(h, cudaMemcpyAsync(&res, h->scratch_res, sizeof(i64), cudaMemcpyDeviceToHost, h->stream));
+    st = check_device_error(h);
+    if (st) return st;
+    if (evicted) *evicted = res;
+    return RSIM_OK;
+}
+
+rsim_status rsim_cache_match_keys(rsim_t *h, int32_t instance, const uint64_t *keys, int64_t n, int64_t *hit) {
+    if (!h) return RSIM_E_INVALID;
+    if (instance < 0 || instance >= h->cfg.n_instances) return fail(h, RSIM_E_INVALID, "instance out of range");
+    CK(h, cudaSetDevice(h->cfg.device));
+    rsim_status st = stage_keys(h, keys, n);
+    if (st) return st;
+    cache_op_kernel<<<1, 32, 0, h->stream>>>(make_params(h), instance, 1, h->scratch_keys, (int)n, 0, h->scratch_res);
+    h->launches++;
+    CK(h, cudaGetLastError());
+    i64 res = 0;
+    CK(h, cudaMemcpyAsync(&res, h->scratch_res, sizeof(i64), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (hit) *hit = res;
+    return RSIM_OK;
+}
+
+rsim_status rsim_probe_batch(rsim_t *h, int64_t first, int64_t count, int32_t *out) {
+    if (!h) return RSIM_E_INVALID;
+    if (first < 0 || count < 0 || first + count > h->R) return fail(h, RSIM_E_INVALID, "request range out of the loaded trace");
+    CK(h, cudaSetDevice(h->cfg.device));
+    int *d = nullptr;
+    const size_t n = (size_t)count * h->cfg.n_instances;
+    CK(h, cudaMalloc(&d, std::max<size_t>(n, 1) * sizeof(int)));
+    const i64 warps = (i64)n;
+    const int grid = (int)std::min<i64>((warps * 32 + 255) / 256, 148 * 8);
+    CK(h, cudaEventRecord(h->ev0, h->stream));
+    probe_batch_kernel<<<std::max(grid, 1), 256, 0, h->stream>>>(make_params(h), first, count, d);
+    h->launches++;
+    CK(h, cudaGetLastError());
+    CK(h, cudaEventRecord(h->ev1, h->stream));
+    CK(h, cudaMemcpyAsync(out, d, n * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    cudaEventElapsedTime(&h->last_replay_ms, h->ev0, h->ev1);
+    cudaFree(d);
+    return RSIM_OK;
+}
+
+rsim_status rsim_chain_keys(rsim_t *h, const uint64_t *blocks, int64_t n, uint64_t *keys_out) {
+    if (!h) return RSIM_E_INVALID;
+    if (n <= 0) return RSIM_OK;
+    CK(h, cudaSetDevice(h->cfg.device));
+    u64 *db = nullptr, *dk = nullptr, *dok = nullptr, *drid = nullptr;
+    i64 *doff = nullptr, *doo = nullptr;
+    int *dflag = nullptr;
+    i64 off[2] = {0, n}, oo[2] = {0, 0};
+    u64 rid0 = 0;
+    CK(h, cudaMalloc(&db, n * sizeof(u64))); CK(h, cudaMalloc(&dk, n * sizeof(u64)));
+    CK(h, cudaMalloc(&dok, sizeof(u64))); CK(h, cudaMalloc(&drid, sizeof(u64)));
+    CK(h, cudaMalloc(&doff, 2 * sizeof(i64))); CK(h, cudaMalloc(&doo, 2 * sizeof(i64)));
+    CK(h, cudaMalloc(&dflag, sizeof(int)));
+    CK(h, cudaMemcpy(db, blocks, n * sizeof(u64), cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(doff, off, sizeof(off), cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(doo, oo, sizeof(oo), cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(drid, &rid0, sizeof(u64), cudaMemcpyHostToDevice));
+    k1_chain_keys<<<1, 32 * K1_WARPS, 0, h->stream>>>(doff, db, dk, doo, dok, drid, 0, 1, 0ULL, dflag);
+    h->launches++;
+    CK(h, cudaGetLastError());
+    CK(h, cudaStreamSynchronize(h->stream));
+    CK(h, cudaMemcpy(keys_out, dk, n * sizeof(u64), cudaMemcpyDeviceToHost));
+    cudaFree(db); cudaFree(dk); cudaFree(dok); cudaFree(drid); cudaFree(doff); cudaFree(doo); cudaFree(dflag);
+    return RSIM_OK;
+}
+
+static rsim_status read_range(rsim_t *h, void *dst, const void *src, size_t elem, i64 first, i64 count) {
+    if (!dst || count == 0) return RSIM_OK;
+    if (first < 0 || count < 0 || first + count > h->R) return fail(h, RSIM_E_INVALID, "range out of the loaded trace");
+    CK(h, cudaMemcpy(dst, (const char *)src + first * elem, count * elem, cudaMemcpyDeviceToHost));
+    return RSIM_OK;
+}
+
+rsim_status rsim_read_decisions(rsim_t *h, int64_t first, int64_t count, int32_t *chosen, int64_t *hit) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    rsim_status st = read_range(h, chosen, h->chosen.p, sizeof(int), first, count);
+    if (st) return st;
+    return read_range(h, hit, h->hit_tokens.p, sizeof(i64), first, count);
+}
+
+rsim_status rsim_read_request_times(rsim_t *h, int64_t first, int64_t count, int64_t *fs, int64_t *ft, int64_t *fin) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    rsim_status st = read_range(h, fs, h->first_sched.p, sizeof(i64), first, count);
+    if (st) return st;
+    st = read_range(h, ft, h->first_token.p, sizeof(i64), first, count);
+    if (st) return st;
+    return read_range(h, fin, h->finish.p, sizeof(i64), first, count);
+}
+
+rsim_status rsim_read_route_bs(rsim_t *h, int64_t first, int64_t count, int64_t *bs) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    return read_range(h, bs, h->route_bs.p, sizeof(i64), first, count);
+}
+
+rsim_status rsim_read_decision_ns(rsim_t *h, int64_t first, int64_t count, int64_t *ns) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    return read_range(h, ns, h->dec_ns.p, sizeof(i64), first, count);
+}
+
+rsim_status rsim_read_instances(rsim_t *h, int64_t *out) {
+    if (!h || !out) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    const int N = h->cfg.n_instances;
+    std::vector<Inst> hs(N);
+    CK(h, cudaMemcpy(hs.data(), h->inst, N * sizeof(Inst), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < N; i++) {
+        const Inst &s = hs[i];
+        int64_t *o = out + 12 * i;
+        o[0] = s.r; o[1] = s.q; o[2] = s.pend; o[3] = s.total; o[4] = s.dcs;
+        o[5] = s.v_r; o[6] = s.v_q; o[7] = s.v_pend; o[8] = s.v_total; o[9] = s.v_dc;
+        o[10] = s.busy_until; o[11] = s.occ;
+    }
+    return RSIM_OK;
+}
+
+rsim_status rsim_read_step_log(rsim_t *h, int64_t *out, int64_t cap, int64_t *n_records) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    u64 n = 0;
+    CK(h, cudaMemcpy(&n, h->log_n, sizeof(u64), cudaMemcpyDeviceToHost));
+    if (n_records) *n_records = (i64)n;
+    if (!h->log) return fail(h, RSIM_E_INVALID, "step log disabled (record_steps = 0)");
+    if ((i64)n > h->log_cap) return fail(h, RSIM_E_INVALID, "step log overflowed its capacity (%lld)", (long long)h->log_cap);
+    if ((i64)n > cap) return fail(h, RSIM_E_INVALID, "output buffer too small");
+    if (n) CK(h, cudaMemcpy(out, h->log, n * 6 * sizeof(i64), cudaMemcpyDeviceToHost));
+    return RSIM_OK;
+}
+
+rsim_status rsim_last_timings(rsim_t *h, double *replay_ms, double *k1_ms, double *drain_ms) {
+    if (!h) return RSIM_E_INVALID;
+    if (replay_ms) *replay_ms = h->last_replay_ms;
+    if (k1_ms) *k1_ms = h->last_k1_ms;
+    if (drain_ms) *drain_ms = h->last_drain_ms;
+    return RSIM_OK;
+}
+
+}  // extern "C"

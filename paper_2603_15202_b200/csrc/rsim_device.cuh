@@ -1,0 +1,122 @@
+// rsim_device.cuh -- device-side data layout and warp primitives of librsim.
+//
+// Layout in HBM (one handle = one GPU's shard of instances):
+//   trace (CSR, replicated):   arrival_us/in/out/rid [R], blk_off [R+1], blocks [sum B]
+//   chain keys (K1 output):    ckeys (same CSR as blocks), okeys (output-block keys, CSR ooff)
+//   per-request outputs:       chosen, hit_tokens, first_sched/first_token/finish, hit_blocks
+//   per-instance engine state: Inst (loaded into shared memory for a persistent launch)
+//   per-instance FIFO queue:   QEnt ring [Qcap]                 (engine.py:212)
+//   per-instance running list: REnt [max_batch]                 (engine.py:213)
+//   per-instance KV$ index:    open-addressing table, keys u64 [S] + Meta [S] (kvcache.py:47-60)
+#pragma once
+#include <stdint.h>
+
+typedef long long i64;
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+#define RSIM_NONE 0x7fffffffffffffffLL
+#define RSIM_GOLDEN 0x9E3779B97F4A7C15ULL
+#define RSIM_OUTPUT_SALT 0x0F0C0DEULL
+
+// Error codes (match rsim_status in include/rsim.h)
+#define DEV_E_CACHE_FULL 3
+#define DEV_E_INVARIANT 5
+#define DEV_E_QUEUE_OVERFLOW 7
+#define DEV_E_TABLE_FULL 8
+
+// Engine + router state of one instance. Live aggregates are the engine's
+// truth (engine.py:219-222); v_* is the router-visible view that only syncs at
+// step end (engine.py:224-246). next_finish caches min(finish_step) over the
+// running list so steps without a finish never touch the list.
+struct __align__(16) Inst {
+    i64 next_step;    // next engine step start (RSIM_NONE = idle)     cluster.py:244-285 next_step[]
+    i64 busy_until;   // engine.py:214
+    i64 due;          // view sync due time (RSIM_NONE = none)         engine.py:227
+    i64 pend, total, dcs;          // live pending / total / decode-context tokens
+    i64 v_pend, v_total, v_dc;     // view
+    i64 step_idx;     // steps executed so far
+    i64 next_finish;  // min finish step among running (RSIM_NONE if none)
+    i64 occ;          // KV$ occupancy (live chains)
+    int r, q;         // live running / queued counts
+    int v_r, v_q;     // view counts
+    int q_head;       // queue ring head index
+    int pad;
+};
+
+struct QEnt { int req; int flags; i64 pending; };    // flags bit0: prefill already scheduled once
+struct REnt { int req; int pad; i64 finish_step; };   // finish_step = join step + out - 1
+struct Meta { i64 touch; int depth; int pin; };       // kvcache.py:34-41 (parent implied by the chain)
+
+struct Params {
+    // trace (device)
+    const i64 *arrival, *in_tok, *out_tok, *blk_off, *ooff;
+    const u64 *rid, *ckeys, *okeys;
+    // per-request outputs / state
+    int *hit_blocks, *chosen;
+    i64 *hit_tokens, *first_sched, *first_token, *finish, *route_bs, *dec_ns;
+    // cluster shape
+    int N, C, W, ipw, per_cta;
+    // model
+    int bs, policy, kv_ind, bal_ind, debug;
+    i64 cap, chunk, max_batch;
+    double pb, pt, db, ds, dcc, qw;
+    // instance state
+    Inst *inst;
+    QEnt *qbuf; int qlog2;
+    REnt *rbuf;
+    u64 *tkeys; Meta *tmeta; int slog2; i64 max_occ; u64 empty;
+    // control
+    u64 *tie;      // [2] = lo, hi of the TieBreaker counter
+    int *err;      // [0] = first error code, [1] = instance, [2..3] info
+    i64 *log; i64 log_cap; u64 *log_n;
+    double *scores;   // optional per-instance scores of a route_one call
+};
+
+// ---------------- hashing (hashing.py:15-25) ----------------
+__device__ __forceinline__ u64 splitmix64(u64 z) {
+    z += RSIM_GOLDEN;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ u64 combine64(u64 acc, u64 v) { return splitmix64(acc ^ v); }
+
+// table home slot: Fibonacci hashing of the (already mixed) chain key
+__device__ __forceinline__ u32 tab_home(u64 key, int slog2) {
+    return (u32)((key * 0x9E3779B97F4A7C15ULL) >> (64 - slog2));
+}
+
+// ---------------- warp helpers ----------------
+#define FULL 0xffffffffu
+__device__ __forceinline__ u32 lanemask_lt() { u32 m; asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m)); return m; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ i64 warp_min_i64(i64 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { i64 w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
+    return v;
+}
+__device__ __forceinline__ u64 warp_min_u64(u64 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { u64 w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { T w = __shfl_up_sync(FULL, v, o); if (lane >= o) v += w; }
+    return v;
+}
+// position of the k-th (0-based) set bit of m
+__device__ __forceinline__ int nth_set_bit(u32 m, int k) {
+    for (int i = 0; i < k; i++) m &= m - 1;
+    return __ffs(m) - 1;
+}
+
+__device__ __forceinline__ u64 ldcg_u64(const u64 *p) { return __ldcg(p); }

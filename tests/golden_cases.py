@@ -1,0 +1,53 @@
+"""Golden fixtures produced by running the reference (tools/make_golden.py).
+
+Each case is rebuilt from its recipe with this repo's workload builders and
+checked against the recorded trace fingerprint before use, so a fixture can
+never silently be compared against a different trace.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+
+from paper_2603_15202_b200 import workloads as W
+from paper_2603_15202_b200.config import CacheConfig, ClusterConfig, CostModel, PolicyConfig
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def index():
+    with open(os.path.join(GOLDEN, "index.json")) as fh:
+        return json.load(fh)
+
+
+def fingerprint(trace) -> str:
+    h = hashlib.sha256()
+    for a in (trace.request_id, trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.blk_off, trace.blocks):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def build(name: str):
+    meta = index()[name]
+    env = {"W": W, "ClusterConfig": ClusterConfig, "CacheConfig": CacheConfig, "CostModel": CostModel,
+           "PolicyConfig": PolicyConfig}
+    trace, cfg = eval(meta["expr"], env)
+    if meta["prefix"] is not None:
+        trace = trace.slice(min(meta["prefix"], len(trace)))
+    assert fingerprint(trace) == meta["fingerprint"], f"{name}: trace drifted from the golden recipe"
+    return trace, cfg
+
+
+def expected(name: str) -> dict:
+    return dict(np.load(os.path.join(GOLDEN, f"{name}.npz")))
+
+
+def names(max_requests: int | None = None):
+    idx = index()
+    return sorted(n for n, m in idx.items() if max_requests is None or m["n_requests"] <= max_requests)
+
+
+def kats() -> dict:
+    with open(os.path.join(GOLDEN, "hash_kats.json")) as fh:
+        return json.load(fh)

@@ -1,0 +1,147 @@
+"""Generate golden fixtures by running the REFERENCE routesim in this container.
+
+    python tools/make_golden.py            # writes tests/golden/*.npz
+
+Each fixture stores the workload recipe (so tests can rebuild the identical
+trace with ``paper_2603_15202_b200.workloads``), a fingerprint of the packed
+trace, and the reference's outputs: per-request chosen instance, hit tokens,
+first-sched / first-token / finish times, the step log, end_us,
+queued_at_last_arrival and finished. Hash known-answer values come from the
+reference's ``routesim.hashing``.
+
+/root/reference is absent on the GPU box; the committed fixtures travel
+instead.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+from refcompat import import_reference, to_ref_config, to_ref_records  # noqa: E402
+
+from paper_2603_15202_b200 import workloads as W  # noqa: E402
+from paper_2603_15202_b200.config import (CacheConfig, ClusterConfig, CostModel,  # noqa: E402
+                                          PolicyConfig)
+
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def fingerprint(trace) -> str:
+    h = hashlib.sha256()
+    for a in (trace.request_id, trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.blk_off,
+              trace.blocks):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+# Recipes: name -> (builder expression, prefix length or None). The builder is
+# evaluated against paper_2603_15202_b200.workloads / .config by tests/golden_cases.py.
+CASES = {
+    "cfg1_chatbot_full": ("W.config1_chatbot()", None),
+    "cfg2_api_prefix4000": ("W.config2_api()", 4000),
+    "cfg3_agent_prefix1200": ("W.config3_agent(1200)", None),
+    "cfg3_agent_evict_n16": ("W.config3_agent(1500, n_instances=16, capacity=4096, rate_per_instance=1.0)", None),
+    "cfg4_large_prefix300": ("W.config4_large(20000)", 300),
+    "chat1024_prefix800": ("W.chat_cluster(1024, 3000)", 800),
+    "adv_same_time_ties": ("W.adversarial('same_time_ties', 16, 0)", None),
+    "adv_zero_bs": ("W.adversarial('zero_bs', 16, 0)", None),
+    "adv_full_hits": ("W.adversarial('full_hits', 16, 0)", None),
+    "adv_ragged": ("W.adversarial('ragged', 16, 0)", None),
+    "adv_out1": ("W.adversarial('out1', 16, 0)", None),
+    "adv_step_boundary": ("W.adversarial('step_boundary', 16, 0)", None),
+    "adv_tight_capacity": ("W.adversarial('tight_capacity', 16, 0)", None),
+    "adv_mixed_n16": ("W.adversarial('mixed', 16, 0)", None),
+    "adv_mixed_n3": ("W.adversarial('mixed', 3, 1)", None),
+    "adv_mixed_n33": ("W.adversarial('mixed', 33, 2)", None),
+    "adv_mixed_n64": ("W.adversarial('mixed', 64, 3)", None),
+    "evict_heavy_n4": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=4, cache=CacheConfig(16, 300), seed=5))", 1500),
+    "policy_vllm": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, cache=CacheConfig(16, None), policy=PolicyConfig(kind='vllm'), seed=2))", 1000),
+    "policy_least_bs": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='least_bs'), seed=3))", 1000),
+    "policy_omh_total": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kv_indicator='one_minus_hit', balance_indicator='total_tokens'), seed=3))", 1000),
+    "policy_omh_bs": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=12, policy=PolicyConfig(kv_indicator='one_minus_hit', tie_break_seed=9), seed=1))", 1000),
+    "cost_fma_sensitive": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, cost_model=CostModel(3.3, 0.0371, 17.1, 0.77, 0.0013, 512, 16), cache=CacheConfig(16, 2000), seed=4))", 1000),
+    "cost_small_batch": ("(W.config2_api()[0], ClusterConfig(n_instances=6, cost_model=CostModel(1.0, 0.2, 4.0, 0.5, 0.01, 300, 3), cache=CacheConfig(16, 5000), seed=7))", 1500),
+    "block_size_4": ("W.generate_synthetic_packed(W.SyntheticSpec(60.0, 20.0, (W.ClassSpec(0.5, 6, (1, 5), (1, 30)), W.ClassSpec(0.5, 2, (0, 3), (1, 9))), seed=11, block_size=4)), ClusterConfig(n_instances=5, cache=CacheConfig(4, 500), seed=11)", None),
+}
+
+
+def build_case(expr: str, prefix):
+    env = {"W": W, "ClusterConfig": ClusterConfig, "CacheConfig": CacheConfig, "CostModel": CostModel,
+           "PolicyConfig": PolicyConfig}
+    trace, cfg = eval(expr, env)
+    if prefix is not None:
+        trace = trace.slice(min(prefix, len(trace)))
+    return trace, cfg
+
+
+def run_reference(trace, cfg):
+    rs = import_reference()
+    t0 = time.perf_counter()
+    rep = rs.run(to_ref_records(trace), to_ref_config(cfg))
+    dt = time.perf_counter() - t0
+
+    def col(name):
+        return np.asarray([-1 if getattr(r, name) is None else getattr(r, name) for r in rep.requests],
+                          dtype=np.int64)
+
+    steps = np.asarray([(s.instance, s.start_us, s.end_us, s.prefill_us) for s in rep.steps],
+                       dtype=np.int64).reshape(-1, 4)
+    return dict(
+        chosen=np.asarray([r.chosen_instance for r in rep.requests], dtype=np.int32),
+        hit_tokens=col("hit_tokens"), first_sched_us=col("first_sched_us"),
+        first_token_us=col("first_token_us"), finish_us=col("finish_us"), steps=steps,
+        summary=np.asarray([rep.end_us, rep.queued_at_last_arrival, rep.finished, rep.routed],
+                           dtype=np.int64),
+    ), dt
+
+
+def kats():
+    rs = import_reference()
+    from routesim import hashing as h
+    from routesim.detector import class_key
+    vals = [0, 1, 2, 0x9E3779B97F4A7C15, (1 << 64) - 1, 12345678901234567, 1 << 63]
+    return {
+        "splitmix64": [[v, h.splitmix64(v)] for v in vals],
+        "combine64": [[a, b, h.combine64(a, b)] for a in vals[:4] for b in vals[:4]],
+        "stable_key": [[list(t), h.stable_key(*t)] for t in
+                       [(0, 0), (1, 0), (0x0F0C0DE, 7, 0), (0x0F0C0DE, 0, 0), (0, 1), (5, 9), (2**64 - 1,)]],
+        "chain_keys": [[list(b), h.chain_keys(b)] for b in
+                       [[1, 2, 3], [0], list(range(40)), [2**64 - 1, 0, 2**63]]],
+        "class_key": [[list(b), class_key(b)] for b in [[1, 2, 3], [7], [9, 9]]],
+        "_source": "routesim.hashing / routesim.detector.class_key run in this container",
+    }
+
+
+def main(only=None):
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "hash_kats.json"), "w") as fh:
+        json.dump(kats(), fh, indent=1)
+    index = {}
+    for name, (expr, prefix) in CASES.items():
+        if only and name not in only:
+            continue
+        trace, cfg = build_case(expr, prefix)
+        out, dt = run_reference(trace, cfg)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
+        index[name] = {"expr": expr, "prefix": prefix, "n_requests": len(trace),
+                       "fingerprint": fingerprint(trace), "reference_seconds": round(dt, 3)}
+        print(f"{name:28s} R={len(trace):6d}  ref {dt:7.2f}s", flush=True)
+    path = os.path.join(OUT, "index.json")
+    old = json.load(open(path)) if (only and os.path.exists(path)) else {}
+    old.update(index)
+    with open(path, "w") as fh:
+        json.dump(old, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main(set(sys.argv[1:]) or None)
