@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark: routing decisions/s of the multiplicative router (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload api64|chat1024|...]
+    python bench.py --impl reference ...        # the reference's own CPU scheduler
+
+A *step* is one full replay of the workload trace: every routing decision
+(chain hash, KV$ probe of every instance, multiplicative score, rotating
+tie-break argmin, enqueue) plus every engine step and KV$ update between
+arrivals, then the final drain -- exactly ``run(records, config)``.
+
+* ``value``  : decisions/s with the trace resident in HBM (device time of
+               reset + K1 + replay + drain, CUDA events on librsim's stream).
+* ``e2e``    : decisions/s through the public API ``ClusterSim.run_trace``
+               with host numpy inputs: H2D of the trace, K1, replay, drain and
+               D2H of every per-request result are inside the timed region.
+* ``roofline``: the replay kernel's algorithmic bytes per launch
+               over its CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
+* ``cpu_baseline``: the reference (routesim, CPython, 1 core) on a bounded
+               prefix sample of the same trace, timed on this host; the C
+               oracle port over the full trace is reported beside it.
+
+The trace and L2 working set are larger than the 126 MB L2 for api64 and the
+replay rewrites the device tables every step; an explicit 512 MB L2 flush
+is also done between timed steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (builder, description)
+    "api64": ("config2_api()", "synthetic API-call trace, 32 shared 1024-token system prompts, 64 instances, ~100k requests (BASELINE configs[1])"),
+    "chat1024": ("chat_cluster(1024, 100_000)", "synthetic chat trace (8 classes), 1024 instances at 3 req/s/instance, ~100k requests (north-star 1024-instance target)"),
+    "chat16": ("config1_chatbot()", "synthetic chatbot trace, 16 instances, ~10k requests (BASELINE configs[0])"),
+    "agent256": ("config3_agent(20_000)", "multi-turn coding-agent trace, 32k-token prompts, 256 instances, capacity 16384 (BASELINE configs[2])"),
+    "large4096": ("config4_large(1_000_000)", "4096-instance chat cluster, ~1M requests (BASELINE configs[3])"),
+}
+METRIC = "routing decisions/sec"
+
+
+def build_workload(name: str):
+    from paper_2603_15202_b200 import workloads as W
+    return eval("W." + WORKLOADS[name][0], {"W": W})
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def flush_l2(dev):
+    import torch
+    buf = getattr(flush_l2, "_buf", None)
+    if buf is None:
+        buf = flush_l2._buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    buf.fill_(1)
+    torch.cuda.synchronize(dev)
+
+
+# ------------------------------------------------------------------------------ reference arm
+def reference_samples(trace, cfg, budget_s: float):
+    """Prefix length of the trace the reference replays in about ``budget_s``."""
+    rate = 2400.0 * (16.0 / max(cfg.n_instances, 16)) ** 0.6   # CPython e2e decisions/s
+    return min(len(trace), max(200, int(budget_s * rate)))
+
+
+def import_reference():
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(path, "routesim")):
+        if path not in sys.path:
+            sys.path.insert(0, path)
+        import routesim  # noqa: F401
+        return routesim
+    return None
+
+
+def ref_records_and_config(trace, cfg):
+    import routesim
+    from routesim.cluster import CacheConfig, ClusterConfig
+    from routesim.engine import CostModel
+    from routesim.policies import PolicyConfig
+    from routesim.trace import TraceRecord
+    cm = cfg.cost_model
+    rcfg = ClusterConfig(n_instances=cfg.n_instances,
+                         cost_model=CostModel(cm.prefill_base_ms, cm.prefill_per_token_ms, cm.decode_base_ms,
+                                              cm.decode_per_seq_ms, cm.decode_per_ctx_token_ms, cm.chunk_tokens,
+                                              cm.max_batch_requests),
+                         cache=CacheConfig(cfg.cache.block_size, cfg.cache.capacity_blocks),
+                         policy=PolicyConfig(kind=cfg.policy.kind), seed=cfg.seed)
+    recs = [TraceRecord(r.request_id, r.arrival_s, r.prefix_blocks, r.input_tokens, r.output_tokens, r.class_key)
+            for r in trace.records()]
+    return routesim, recs, rcfg
+
+
+def time_reference(trace, cfg, n_sample: int, repeats: int = 1):
+    """CPython reference ``routesim.run`` on the first n_sample records; best decisions/s."""
+    rs = import_reference()
+    if rs is None:
+        return None
+    sample = trace.slice(n_sample)
+    routesim, recs, rcfg = ref_records_and_config(sample, cfg)
+    best = 0.0
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        routesim.run(recs, rcfg)
+        dt = time.perf_counter() - t0
+        best = max(best, len(recs) / dt)
+    return best
+
+
+def time_port(trace, cfg):
+    """The C oracle port (oracle/rsim_oracle.c, 1 thread) over the whole trace."""
+    from oracle.oracle import run_oracle
+    t0 = time.perf_counter()
+    run_oracle(trace, cfg)
+    return len(trace) / (time.perf_counter() - t0)
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    trace, cfg = build_workload(args.workload)
+    rs = import_reference()
+    cores = 1
+    if rs is not None:
+        n = reference_samples(trace, cfg, args.ref_budget_s)
+        routesim, recs, rcfg = ref_records_and_config(trace.slice(n), cfg)
+        kind, sample = "reference", f"first {n} of {len(trace)} requests of {args.workload}, routesim.run (CPython, 1 thread)"
+        run_step = lambda: routesim.run(recs, rcfg)  # noqa: E731
+    else:
+        from oracle.oracle import run_oracle
+        n = len(trace)
+        kind, sample = "port", f"all {n} requests of {args.workload}, C oracle port (1 thread)"
+        run_step = lambda: run_oracle(trace, cfg)  # noqa: E731
+    for _ in range(args.warmup):
+        run_step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run_step()
+        times.append(time.perf_counter() - t0)
+    value = n * len(times) / sum(times)
+    line = {"metric": METRIC, "value": value, "unit": "decisions/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": {"workload": args.workload, "description": WORKLOADS[args.workload][1],
+                                            "n_instances": cfg.n_instances, "requests": n},
+            "cpu_baseline": {"value": value, "unit": "decisions/s", "cores": cores, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
+    import torch
+    from paper_2603_15202_b200 import _native
+    from paper_2603_15202_b200.cluster import ClusterSim, native_config, sizing_for
+
+    trace, cfg = build_workload(name)
+    R = len(trace)
+    dev = torch.device("cuda", dev_index)
+    # resident handle: trace loaded once; each step = rsim_rerun
+    sizing = sizing_for(trace, cfg)
+    for _ in range(6):
+        h = _native.Handle(native_config(cfg, sizing, device=dev_index))
+        h.load(trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.request_id, trace.blk_off, trace.blocks)
+        try:
+            h.rerun()
+            break
+        except _native.CapacityError:
+            h.close()
+            sizing = sizing.grown()
+    for _ in range(max(args.warmup - 1, 0)):
+        h.rerun()
+    launches0 = h.launch_count()
+    dev_ms, replay_ms = [], []
+    with ClockSampler(dev_index) as clk:
+        for _ in range(args.steps):
+            flush_l2(dev)
+            dev_ms.append(h.rerun())
+            replay_ms.append(h.timings()[0])
+    launches = h.launch_count() - launches0
+    ctr = h.counters()
+    ns = h.decision_ns(0, R)
+    lat = np.diff(ns[ns > 0]) / 1000.0
+    chosen_dev, _ = h.decisions(0, R)
+    h.close()
+
+    # e2e through the public API: host arrays in, results out
+    sim = ClusterSim(cfg, device=dev_index, record_steps=False)
+    for _ in range(args.warmup):
+        sim.run_trace(trace)
+    e2e_s = []
+    for _ in range(args.steps):
+        flush_l2(dev)
+        t0 = time.perf_counter()
+        rep = sim.run_trace(trace)
+        e2e_s.append(time.perf_counter() - t0)
+    assert np.array_equal(rep.chosen, chosen_dev), "e2e and resident replays disagree"
+    sim.close()
+
+    h2d = int(trace.arrival_us.nbytes + trace.in_tokens.nbytes + trace.out_tokens.nbytes +
+              trace.request_id.nbytes + trace.blk_off.nbytes + trace.blocks.nbytes)
+    d2h = R * (4 + 8 * 5)   # chosen, hit_tokens, first_sched, first_token, finish, route_bs
+    peaks, peak_src = measured_peaks()
+    avg_replay_s = statistics.mean(replay_ms) / 1000.0
+    achieved = ctr[0] / avg_replay_s / 1e9
+    out = {
+        "R": R, "cfg": cfg, "trace": trace,
+        "value": R * len(dev_ms) / (sum(dev_ms) / 1000.0),
+        "ms_per_step": statistics.mean(dev_ms),
+        "e2e": R * len(e2e_s) / sum(e2e_s), "h2d": h2d, "d2h": d2h,
+        "launches": launches, "clocks": clk.summary(),
+        "lat_p50_us": float(np.percentile(lat, 50)) if lat.size else None,
+        "lat_p99_us": float(np.percentile(lat, 99)) if lat.size else None,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "kernel": "replay_kernel", "algorithmic_bytes_per_launch": int(ctr[0]),
+                     "avg_launch_ms": avg_replay_s * 1000.0, "peak_source": f"{peak_src} hbm_gbs (burst copy)",
+                     "engine_steps_per_launch": int(ctr[1])},
+    }
+    if with_cpu:
+        n = reference_samples(trace, cfg, args.ref_budget_s)
+        ref = time_reference(trace, cfg, n)
+        port = time_port(trace, cfg)
+        if ref is not None:
+            out["cpu_baseline"] = {"value": ref, "unit": "decisions/s", "cores": 1, "kind": "reference",
+                                   "sample": f"first {n} of {R} requests, routesim.run from baseline/_ref (CPython, 1 thread)"}
+        else:
+            out["cpu_baseline"] = {"value": port, "unit": "decisions/s", "cores": 1, "kind": "port",
+                                   "sample": f"all {R} requests, C oracle port (1 thread)"}
+        out["cpu_port"] = {"value": port, "unit": "decisions/s", "cores": 1, "kind": "port",
+                           "sample": f"all {R} requests, oracle/rsim_oracle.c (1 thread)"}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="api64", choices=sorted(WORKLOADS))
+    ap.add_argument("--extra", default="chat1024", help="comma list of extra workloads reported beside the headline")
+    ap.add_argument("--ref-budget-s", type=float, default=4.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    res = measure_workload(args.workload, args, local, with_cpu=(rank == 0 and world == 1 and not args.no_cpu),
+                           rank=rank)
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+        t = torch.tensor([res["ms_per_step"]], device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        res["ms_per_step"] = float(t.item())
+    extras = {}
+    if rank == 0 and world == 1:
+        for name in [x for x in args.extra.split(",") if x and x != args.workload]:
+            e = measure_workload(name, args, local, with_cpu=not args.no_cpu, rank=rank)
+            extras[name] = {"value": e["value"], "e2e": e["e2e"], "ms_per_step": e["ms_per_step"],
+                            "n_instances": e["cfg"].n_instances, "requests": e["R"],
+                            "decision_latency_us": {"p50": e["lat_p50_us"], "p99": e["lat_p99_us"]},
+                            "roofline": e["roofline"], "cpu_baseline": e.get("cpu_baseline"),
+                            "cpu_port": e.get("cpu_port"),
+                            "e2e_vs_cpu_baseline": (e["e2e"] / e["cpu_baseline"]["value"]) if e.get("cpu_baseline") else None,
+                            "description": WORKLOADS[name][1]}
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+    R = res["R"]
+    value = R * world / (res["ms_per_step"] / 1000.0)
+    line = {
+        "metric": METRIC, "value": value, "unit": "decisions/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": args.workload, "description": WORKLOADS[args.workload][1],
+                   "n_instances": res["cfg"].n_instances, "requests": R, "block_size": res["cfg"].cache.block_size,
+                   "capacity_blocks": res["cfg"].cache.capacity_blocks, "policy": res["cfg"].policy.kind,
+                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "l2": "512 MB flush between timed steps; trace + tables exceed L2"},
+        "decision_latency_us": {"p50": res["lat_p50_us"], "p99": res["lat_p99_us"],
+                                "source": "%globaltimer at each commit, consecutive differences"},
+        "roofline": res["roofline"],
+        "e2e": {"value": res["e2e"] * world, "unit": "decisions/s", "h2d_bytes_per_step": res["h2d"],
+                "d2h_bytes_per_step": res["d2h"]},
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+    }
+    if "cpu_baseline" in res:
+        line["cpu_baseline"] = res["cpu_baseline"]
+        line["cpu_port"] = res["cpu_port"]
+        line["e2e_vs_cpu_baseline"] = res["e2e"] / res["cpu_baseline"]["value"]
+    if extras:
+        line["extra_workloads"] = extras
+    print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

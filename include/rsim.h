@@ -129,6 +129,14 @@ rsim_status rsim_chain_keys(rsim_t *h, const uint64_t *blocks, int64_t n, uint64
 rsim_status rsim_last_timings(rsim_t *h, double *replay_ms, double *k1_ms, double *drain_ms);
 /* Per-decision device timestamps (%globaltimer ns) of the last replay, count entries. */
 rsim_status rsim_read_decision_ns(rsim_t *h, int64_t first, int64_t count, int64_t *ns);
+/* Resident re-run (bench "value"): reset engine/KV$/tie state, rerun K1 over the
+ * loaded trace, replay every decision and drain to idle; *device_ms = CUDA-event
+ * time of the whole sequence on the handle's stream. Equals reset+K1+replay+drain. */
+rsim_status rsim_rerun(rsim_t *h, double *device_ms);
+/* Counters of the last replay: [0] algorithmic probe bytes (8*B per decision
+ * + sum_i 8*min(h_i+1,B) + 16 per instance probed), [1] engine steps, [2] evictions,
+ * [3] reserved, [4] requests loaded, [5] blocks, [6] output keys, [7] instances. */
+rsim_status rsim_read_counters(rsim_t *h, int64_t *out8);
 /* Number of kernels librsim launched since create (evidence for bench gpu_launches). */
 int64_t rsim_launch_count(const rsim_t *h);
 

@@ -92,6 +92,8 @@ def lib():
         "rsim_last_timings": ([P, P, P, P], C.c_int),
         "rsim_read_decision_ns": ([P, I64, I64, P], C.c_int),
         "rsim_launch_count": ([P], I64),
+        "rsim_rerun": ([P, P], C.c_int),
+        "rsim_read_counters": ([P, P], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -105,7 +107,8 @@ EXPORTED = ("rsim_create", "rsim_destroy", "rsim_last_error", "rsim_reset", "rsi
             "rsim_drain", "rsim_read_decisions", "rsim_read_request_times", "rsim_read_instances",
             "rsim_read_step_log", "rsim_read_route_bs", "rsim_route_one", "rsim_enqueue",
             "rsim_cache_insert_keys", "rsim_cache_match_keys", "rsim_probe_batch", "rsim_chain_keys",
-            "rsim_last_timings", "rsim_read_decision_ns", "rsim_launch_count")
+            "rsim_last_timings", "rsim_read_decision_ns", "rsim_launch_count", "rsim_rerun",
+            "rsim_read_counters")
 
 
 def _p(a):
@@ -244,6 +247,17 @@ class Handle:
         a, b, c = C.c_double(), C.c_double(), C.c_double()
         self._ck(self._L.rsim_last_timings(self._h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
+
+    def rerun(self) -> float:
+        """Resident full replay; returns device milliseconds."""
+        ms = C.c_double()
+        self._ck(self._L.rsim_rerun(self._h, C.byref(ms)))
+        return ms.value
+
+    def counters(self) -> np.ndarray:
+        out = np.zeros(8, np.int64)
+        self._ck(self._L.rsim_read_counters(self._h, _p(out)))
+        return out
 
     def launch_count(self) -> int:
         return int(self._L.rsim_launch_count(self._h))

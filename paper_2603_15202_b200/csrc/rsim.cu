@@ -77,6 +77,7 @@ struct rsim {
     u64 *scratch_keys = nullptr;
     size_t scratch_cap = 0;
     i64 *scratch_res = nullptr;
+    u64 *ctr = nullptr;            // device counters (Params.ctr)
 };
 
 static rsim_status fail(rsim_t *h, rsim_status st, const char *fmt, ...) {
@@ -118,6 +119,7 @@ static Params make_params(rsim_t *h) {
     P.tie = h->tie; P.err = h->errbuf;
     P.log = h->log; P.log_cap = h->log_cap; P.log_n = h->log_n;
     P.scores = nullptr;
+    P.ctr = h->ctr;
     return P;
 }
 
@@ -152,6 +154,7 @@ static rsim_status init_state(rsim_t *h) {
     CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaMemsetAsync(h->errbuf, 0, 4 * sizeof(int), h->stream));
     CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), h->stream));
+    CK(h, cudaMemsetAsync(h->ctr, 0, 8 * sizeof(u64), h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     h->R = 0; h->nblk = 0; h->nout = 0;
     // blk_off / ooff hold a leading 0
@@ -238,6 +241,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaMalloc(&h->log_n, sizeof(u64)));
     CK(nullptr, cudaMalloc(&h->scores, N * sizeof(double)));
     CK(nullptr, cudaMalloc(&h->scratch_res, 4 * sizeof(i64)));
+    CK(nullptr, cudaMalloc(&h->ctr, 8 * sizeof(u64)));
     if (c.record_steps) {
         h->log_cap = c.step_log_capacity > 0 ? c.step_log_capacity : (1 << 20);
         CK(nullptr, cudaMalloc(&h->log, (size_t)h->log_cap * 6 * sizeof(i64)));
@@ -258,7 +262,7 @@ void rsim_destroy(rsim_t *h) {
     h->rid.free_(); h->blocks.free_(); h->ckeys.free_(); h->okeys.free_();
     h->hit_blocks.free_(); h->chosen.free_();
     void *ps[] = {h->inst, h->qbuf, h->rbuf, h->tkeys, h->tmeta, h->tie, h->errbuf, h->flag, h->log, h->log_n,
-                  h->scores, h->scratch_keys, h->scratch_res};
+                  h->scores, h->scratch_keys, h->scratch_res, h->ctr};
     for (void *p : ps) if (p) cudaFree(p);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
@@ -554,6 +558,61 @@ rsim_status rsim_read_step_log(rsim_t *h, int64_t *out, int64_t cap, int64_t *n_
     if ((i64)n > h->log_cap) return fail(h, RSIM_E_INVALID, "step log overflowed its capacity (%lld)", (long long)h->log_cap);
     if ((i64)n > cap) return fail(h, RSIM_E_INVALID, "output buffer too small");
     if (n) CK(h, cudaMemcpy(out, h->log, n * 6 * sizeof(i64), cudaMemcpyDeviceToHost));
+    return RSIM_OK;
+}
+
+// Whole-trace replay on the resident trace: reset engine/KV$/tie state, rerun
+// K1 over the loaded trace, replay every decision, drain to idle. The device
+// time of that sequence (CUDA events on the handle's stream) -> *device_ms.
+rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    cudaStream_t s = h->stream;
+    const int N = h->cfg.n_instances;
+    std::vector<Inst> hs(N);
+    for (auto &x : hs) { memset(&x, 0, sizeof(x)); x.next_step = RSIM_NONE; x.due = RSIM_NONE; x.next_finish = RSIM_NONE; }
+    u64 tie[2] = {h->cfg.tie_seed_lo, h->cfg.tie_seed_hi};
+    cudaEvent_t e0, e1;
+    CK(h, cudaEventCreate(&e0));
+    CK(h, cudaEventCreate(&e1));
+    CK(h, cudaEventRecord(e0, s));
+    const size_t slots = (size_t)N << h->slog2;
+    CK(h, cudaMemcpyAsync(h->inst, hs.data(), N * sizeof(Inst), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemsetAsync(h->tkeys, 0, slots * sizeof(u64), s));
+    CK(h, cudaMemsetAsync(h->tmeta, 0, slots * sizeof(Meta), s));
+    CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), s));
+    CK(h, cudaMemsetAsync(h->ctr, 0, 8 * sizeof(u64), s));
+    if (h->R > 0) {
+        DevArr<i64> *outs[] = {&h->hit_tokens, &h->first_sched, &h->first_token, &h->finish, &h->route_bs, &h->dec_ns};
+        for (auto *a : outs) CK(h, cudaMemsetAsync(a->p, 0xff, h->R * sizeof(i64), s));
+        CK(h, cudaMemsetAsync(h->chosen.p, 0xff, h->R * sizeof(int), s));
+        const i64 nwarps = (h->R + 31) / 32;
+        k1_chain_keys<<<(int)((nwarps + K1_WARPS - 1) / K1_WARPS), 32 * K1_WARPS, 0, s>>>(
+            h->blk_off.p, h->blocks.p, h->ckeys.p, h->ooff.p, h->okeys.p, h->rid.p, 0, h->R, 0ULL, h->flag);
+        h->launches++;
+        CK(h, cudaGetLastError());
+        rsim_status st = launch_replay(h, 0, h->R, 0, MODE_REPLAY, -1, nullptr, &h->last_replay_ms);
+        if (st != RSIM_OK) { cudaEventDestroy(e0); cudaEventDestroy(e1); return st; }
+    }
+    rsim_status st = launch_replay(h, 0, 0, RSIM_NONE, MODE_DRAIN, -1, nullptr, &h->last_drain_ms);
+    CK(h, cudaEventRecord(e1, s));
+    CK(h, cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (device_ms) *device_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return st;
+}
+
+rsim_status rsim_read_counters(rsim_t *h, int64_t *out8) {
+    if (!h || !out8) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    u64 c[8];
+    CK(h, cudaMemcpy(c, h->ctr, sizeof(c), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 8; i++) out8[i] = (int64_t)c[i];
+    out8[4] = h->R; out8[5] = h->nblk; out8[6] = h->nout; out8[7] = h->cfg.n_instances;
     return RSIM_OK;
 }
 

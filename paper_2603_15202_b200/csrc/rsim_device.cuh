@@ -71,6 +71,7 @@ struct Params {
     int *err;      // [0] = first error code, [1] = instance, [2..3] info
     i64 *log; i64 log_cap; u64 *log_n;
     double *scores;   // optional per-instance scores of a route_one call
+    u64 *ctr;         // [0] algorithmic probe bytes, [1] engine steps, [2] evictions
 };
 
 // ---------------- hashing (hashing.py:15-25) ----------------

@@ -62,8 +62,9 @@ __device__ __forceinline__ void log_step(const Params &P, int gi, i64 start, i64
     }
 }
 
-// One engine step of instance gi starting at s.next_step.
-__device__ void inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr) {
+// One engine step of instance gi starting at s.next_step. Returns false if
+// the plan was empty (the instance went idle).
+__device__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr) {
     Inst s = *sp;
     const i64 t = s.next_step;
     flush_view(s, t);                                              // form_batch flush, engine.py:293
@@ -99,7 +100,7 @@ __device__ void inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr
         __syncwarp();
         if (lane == 0) *sp = s;
         __syncwarp();
-        return;
+        return false;
     }
     const i64 pre = prefill_cost_us(P, ptok);
     const i64 end = t + pre + decode_cost_us(P, ndec, s.dcs);      // ctx = sum(in+gen) over decode = dcs
@@ -225,4 +226,5 @@ __device__ void inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr
     __syncwarp();
     if (lane == 0) *sp = s;
     __syncwarp();
+    return true;
 }

@@ -164,11 +164,12 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
     const int l0 = warp * ipw;
     const int nmine = max(0, min(ipw, nloc - l0));
     int werr = 0;
+    u64 c_bytes = 0, c_steps = 0;   // algorithmic probe bytes / engine steps of this warp
 
     if (mode == MODE_DRAIN) {
         for (int s = 0; s < nmine; s++) {
             Inst *sp = st + l0 + s;
-            while (!werr && sp->next_step < until) inst_step(P, sp, base + l0 + s, lane, werr);
+            while (!werr && sp->next_step < until) c_steps += inst_step(P, sp, base + l0 + s, lane, werr);
         }
     } else {
         for (i64 k = k0; k < k1; k++) {
@@ -178,7 +179,7 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
             if (mode == MODE_REPLAY) {
                 for (int s = 0; s < nmine; s++) {
                     Inst *sp = st + l0 + s;
-                    while (!werr && sp->next_step < t) inst_step(P, sp, base + l0 + s, lane, werr);
+                    while (!werr && sp->next_step < t) c_steps += inst_step(P, sp, base + l0 + s, lane, werr);
                 }
             }
             // ---- K2: flush views, probe, score (cluster.py:106-128, policies.py:117-139)
@@ -202,10 +203,13 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
                 if (cand) {
                     h = warp_probe(table_of(P, gi), keys, B, lane);
                     sc = score_of(P, *sp, h, in);
+                    // one 8-B key compare per reference dict lookup + 16 B of view
+                    c_bytes += 8ULL * (u64)min(h + 1, B) + 16ULL;
                     if (P.scores != nullptr && lane == 0) P.scores[gi] = sc;
                 }
                 if (lane == s) { mybits = cand ? (u64)__double_as_longlong(sc) : ~0ULL; myh = h; }
             }
+            if (cta == 0 && warp == 0) c_bytes += 8ULL * (u64)B;   // request chain keys, read once
             const u64 wmin = warp_min_u64(mybits);
             const u32 tmask = __ballot_sync(FULL, lane < nmine && mybits == wmin && wmin != ~0ULL);
             if (lane == 0) { Part q; q.minb = wmin; q.cnt = __popc(tmask); q.err = (u32)werr; wp[par * W + warp] = q; }
@@ -283,6 +287,10 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     }
     if (werr && lane == 0) atomicCAS(P.err, 0, werr);
+    if (lane == 0 && P.ctr != nullptr) {
+        if (c_bytes) atomicAdd(P.ctr + 0, c_bytes);
+        if (c_steps) atomicAdd(P.ctr + 1, c_steps);
+    }
     if (cta == 0 && threadIdx.x == 0 && mode != MODE_DRAIN) {
         P.tie[0] = (u64)counter;
         P.tie[1] = (u64)(counter >> 64);

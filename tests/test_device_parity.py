@@ -41,7 +41,7 @@ def test_replay_matches_reference_golden(native, name):
     _assert_report(rep, G.expected(name), name)
 
 
-@pytest.mark.parametrize("shape", [(1, 1), (1, 4), (2, 8), (4, 2), (16, 1)])
+@pytest.mark.parametrize("shape", [(1, 2), (1, 4), (2, 8), (4, 2), (16, 1)])
 def test_cluster_shapes_agree(native, shape):
     """The same decisions for every CTA-cluster / warp split of the instances."""
     from paper_2603_15202_b200.cluster import run
