@@ -209,8 +209,8 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (C <= 0) C = N <= 128 ? 1 : std::min(16, (N + 63) / 64);
     C = std::max(1, std::min(16, std::min(C, N)));
     int per_cta = (N + C - 1) / C;
-    int W = c.warps_per_cta > 0 ? c.warps_per_cta : std::min(32, per_cta);
-    W = std::max(1, std::min(32, W));
+    int W = c.warps_per_cta > 0 ? c.warps_per_cta : std::min(RSIM_MAX_WARPS, per_cta);
+    W = std::max(1, std::min(RSIM_MAX_WARPS, W));
     int ipw = (per_cta + W - 1) / W;
     if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;

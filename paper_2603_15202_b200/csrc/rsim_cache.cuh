@@ -3,14 +3,20 @@
 //   match      = longest present prefix               (kvcache.py:65-74)
 //   insert     = create or touch=max(touch, now)      (kvcache.py:81-104)
 //   touch/pin  = on keys[:upto]                       (kvcache.py:109-130)
-//   unpin      = -1, error if not pinned              (kvcache.py:132-138)
+//   unpin      = -1 on keys[:upto]                    (kvcache.py:132-138)
 //   evict      = while occupancy > capacity remove the smallest unpinned entry
 //                in (touch asc, depth desc, key asc) order (kvcache.py:142-168;
 //                that order is the reference lazy heap's effective total order)
-// Only the owning warp touches an instance's table during a launch, so the
-// only races are between lanes of one warp; duplicate keys inside a 32-key
-// chunk are collapsed with __match_any_sync and slot claims are arbitrated
-// the same way. Loads use ld.global.cg so a lane never reads a stale L1 line.
+//
+// Latency is the budget here (one decision is a serial chain of these calls),
+// so every operation is shaped to cost one memory round trip per 128 keys:
+//  * a warp handles 128 chain depths per round, 4 per lane, all loads in flight;
+//  * linear probing reads an aligned 16-byte slot pair per load (tables run at
+//    <= 3/4 load, usually far below, so the home pair nearly always decides);
+//  * slot claims use atomicCAS (duplicate keys and racing lanes resolve in L2);
+//  * touch / pin / unpin are fire-and-forget atomics (RED): max and +/- are
+//    commutative, so no read-modify-write round trip is needed;
+//  * table loads use ld.global.cg, so a lane never reads a stale L1 line.
 #pragma once
 #include "rsim_device.cuh"
 
@@ -28,25 +34,40 @@ __device__ __forceinline__ Table table_of(const Params &P, int gi) {
     return t;
 }
 
-// Linear probing, four slots per round trip (the four loads are independent).
-__device__ __forceinline__ int tab_find(const Table &T, u64 key) {
-    u32 i = tab_home(key, T.slog2);
-#pragma unroll 1
-    for (;;) {
-        u64 a0 = __ldcg(T.k + i);
-        u64 a1 = __ldcg(T.k + ((i + 1) & T.mask));
-        u64 a2 = __ldcg(T.k + ((i + 2) & T.mask));
-        u64 a3 = __ldcg(T.k + ((i + 3) & T.mask));
-        if (a0 == key) return (int)i;
-        if (a0 == T.empty) return -1;
-        if (a1 == key) return (int)((i + 1) & T.mask);
-        if (a1 == T.empty) return -1;
-        if (a2 == key) return (int)((i + 2) & T.mask);
-        if (a2 == T.empty) return -1;
-        if (a3 == key) return (int)((i + 3) & T.mask);
-        if (a3 == T.empty) return -1;
-        i = (i + 4) & T.mask;
+__device__ __forceinline__ ulonglong2 ld_pair(const Table &T, u32 i) {
+    return __ldcg(reinterpret_cast<const ulonglong2 *>(T.k) + (i >> 1));
+}
+
+// Evaluate one aligned pair starting the probe at slot i.
+// st: 0 found (returns slot), 1 absent (returns the first EMPTY slot), 2 continue (returns next i)
+__device__ __forceinline__ u32 eval_pair(const Table &T, ulonglong2 pr, u32 i, u64 key, int &st) {
+    if ((i & 1u) == 0) {
+        if (pr.x == key) { st = 0; return i; }
+        if (pr.x == T.empty) { st = 1; return i; }
     }
+    const u32 j = i | 1u;
+    if (pr.y == key) { st = 0; return j; }
+    if (pr.y == T.empty) { st = 1; return j; }
+    st = 2;
+    return (j + 1) & T.mask;
+}
+
+// Finish a probe that did not resolve in its first pair.
+__device__ __noinline__ u32 probe_rest(const Table &T, u32 i, u64 key, int &st) {
+    for (;;) {
+        ulonglong2 pr = ld_pair(T, i);
+        u32 r = eval_pair(T, pr, i, key, st);
+        if (st != 2) return r;
+        i = r;
+    }
+}
+
+__device__ __forceinline__ int tab_find(const Table &T, u64 key) {
+    int st;
+    u32 i = tab_home(key, T.slog2);
+    u32 r = eval_pair(T, ld_pair(T, i), i, key, st);
+    if (st == 2) r = probe_rest(T, r, key, st);
+    return st == 0 ? (int)r : -1;
 }
 
 __device__ __forceinline__ Meta load_meta(const Meta *p) {
@@ -57,127 +78,200 @@ __device__ __forceinline__ Meta load_meta(const Meta *p) {
     return m;
 }
 
-// Longest present prefix of keys[0..B) (match_keys). Lane j probes depth j;
-// the hit mask's leading ones are the match. Beyond 32 present blocks a
-// 32-ary search over depth finds the boundary (presence is monotone in depth
-// by prefix closure, kvcache.py:4-7), so a 2048-block prompt costs ~4 rounds.
-__device__ int warp_probe(const Table &T, const u64 *keys, int B, int lane) {
-    bool f = false;
-    if (lane < B) f = tab_find(T, keys[lane]) >= 0;
-    u32 m = __ballot_sync(FULL, f);
-    if (m != FULL) return __ffs(~m) - 1;
-    if (B <= 32) return 32;
-    int lo = 32, hi = B;
+// Batched lookup of up to 128 keys (lane-major: key k of lane = depth 32k+lane).
+// slot[k] = found slot or -1; freepos[k] = first EMPTY slot when absent.
+__device__ __forceinline__ void find128(const Table &T, const u64 kk[4], const bool act[4], int slot[4],
+                                        u32 freepos[4]) {
+    ulonglong2 pr[4];
+    u32 home[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        home[k] = tab_home(kk[k], T.slog2);
+        if (act[k]) pr[k] = ld_pair(T, home[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        slot[k] = -1;
+        freepos[k] = 0;
+        if (act[k]) {
+            int st;
+            u32 r = eval_pair(T, pr[k], home[k], kk[k], st);
+            if (st == 2) r = probe_rest(T, r, kk[k], st);
+            if (st == 0) slot[k] = (int)r; else freepos[k] = r;
+        }
+    }
+}
+
+// Hit masks for the first 128 depths of NI instances at once (loads of all
+// instances in flight together). m[s][k] bit lane = depth 32k+lane present.
+template <int NI>
+__device__ __forceinline__ void probe128(const Table *T, const u64 kk[4], int B, int lane, u32 m[NI][4]) {
+    ulonglong2 pr[NI][4];
+    u32 home[NI][4];
+#pragma unroll
+    for (int s = 0; s < NI; s++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            home[s][k] = tab_home(kk[k], T[s].slog2);
+            if (32 * k + lane < B) pr[s][k] = ld_pair(T[s], home[s][k]);
+        }
+#pragma unroll
+    for (int s = 0; s < NI; s++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            bool f = false;
+            if (32 * k + lane < B) {
+                int st;
+                u32 r = eval_pair(T[s], pr[s][k], home[s][k], kk[k], st);
+                if (st == 2) r = probe_rest(T[s], r, kk[k], st);
+                f = st == 0;
+            }
+            m[s][k] = __ballot_sync(FULL, f);
+        }
+}
+
+__device__ __forceinline__ int lead_hits(const u32 m[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+        if (m[k] != FULL) return 32 * k + __ffs(~m[k]) - 1;
+    return 128;
+}
+
+// Longest present prefix beyond the first 128 depths: 128-ary search over
+// depth (presence is monotone in depth by prefix closure, kvcache.py:4-7),
+// ~3 rounds for a 2048-block prompt. keys = the request's chain keys.
+__device__ __noinline__ int deep_match(const Table &T, const u64 *keys, int B, int lane) {
+    int lo = 128, hi = B;
     while (lo < hi) {
-        int span = hi - lo, d;
-        bool valid;
-        if (span <= 32) { d = lo + lane; valid = lane < span; }
-        else { d = lo + (int)(((i64)lane * span) >> 5); valid = true; }
-        f = valid && tab_find(T, keys[d]) >= 0;
-        m = __ballot_sync(FULL, f);
-        u32 vm = __ballot_sync(FULL, valid);
-        u32 miss = ~m & vm;
-        int fm = miss ? __ffs(miss) - 1 : -1;
-        if (fm == 0) break;                       // depth lo absent -> match = lo
-        int last_ok = fm < 0 ? 31 - __clz(vm) : fm - 1;
-        int d_ok = __shfl_sync(FULL, d, last_ok);
-        int d_miss = __shfl_sync(FULL, d, fm < 0 ? 0 : fm);
+        const int span = hi - lo;
+        int d[4];
+        bool valid[4], f[4];
+        u64 kk[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int idx = 32 * k + lane;
+            if (span <= 128) { d[k] = lo + idx; valid[k] = idx < span; }
+            else { d[k] = lo + (int)(((i64)idx * span) >> 7); valid[k] = true; }
+            kk[k] = valid[k] ? keys[d[k]] : 0;
+        }
+        int slot[4];
+        u32 fp[4];
+        find128(T, kk, valid, slot, fp);
+        u32 miss[4], vm[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            f[k] = valid[k] && slot[k] >= 0;
+            miss[k] = __ballot_sync(FULL, valid[k] && !f[k]);
+            vm[k] = __ballot_sync(FULL, valid[k]);
+        }
+        int fm = -1, last = -1;
+#pragma unroll
+        for (int k = 3; k >= 0; k--) if (vm[k] && last < 0) last = 32 * k + 31 - __clz(vm[k]);
+#pragma unroll
+        for (int k = 0; k < 4; k++) if (miss[k] && fm < 0) fm = 32 * k + __ffs(miss[k]) - 1;
+        if (fm == 0) break;                                   // depth lo absent: match = lo
+        const int ok = fm < 0 ? last : fm - 1;
+        const int d_ok = __shfl_sync(FULL, d[ok >> 5], ok & 31);
+        if (fm > 0) hi = __shfl_sync(FULL, d[fm >> 5], fm & 31);
         lo = d_ok + 1;
-        if (fm > 0) hi = d_miss;
     }
     return lo;
 }
 
+// Longest present prefix of one instance (match_keys) -- the API / batch path.
+__device__ int warp_probe(const Table &T, const u64 *keys, int B, int lane) {
+    u64 kk[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) kk[k] = (32 * k + lane < B) ? keys[32 * k + lane] : 0;
+    u32 m[1][4];
+    probe128<1>(&T, kk, B, lane, m);
+    int h = lead_hits(m[0]);
+    if (h < 128) return min(h, B);
+    if (B <= 128) return B;
+    return deep_match(T, keys, B, lane);
+}
+
 // touch keys[:h] at now and pin them (InstanceSim.enqueue, engine.py:275-276).
-__device__ void warp_touch_pin(const Table &T, const u64 *keys, int h, i64 now, int lane, int &werr) {
-    for (int j0 = 0; j0 < h; j0 += 32) {
-        int j = j0 + lane;
-        bool act = j < h;
-        u64 key = act ? keys[j] : 0;
-        u32 am = __ballot_sync(FULL, act);
-        if (act) {
-            u32 peers = __match_any_sync(am, key);
-            if (__ffs(peers) - 1 == lane) {
-                int s = tab_find(T, key);
-                if (s < 0) werr = DEV_E_INVARIANT;
-                else {
-                    Meta *mp = T.m + s;
-                    i64 t0 = __ldcg(&mp->touch);
-                    if (now > t0) mp->touch = now;
-                    mp->pin = __ldcg(&mp->pin) + __popc(peers);
-                }
-            }
+// kk0 holds the first 128 keys (already in registers from the probe).
+__device__ void warp_touch_pin(const Table &T, const u64 *keys, const u64 kk0[4], int h, i64 now, int lane,
+                               int &werr) {
+    for (int j0 = 0; j0 < h; j0 += 128) {
+        u64 kk[4];
+        bool act[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int j = j0 + 32 * k + lane;
+            act[k] = j < h;
+            kk[k] = j0 == 0 ? kk0[k] : (act[k] ? keys[j] : 0);
         }
-        __syncwarp();
+        int slot[4];
+        u32 fp[4];
+        find128(T, kk, act, slot, fp);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (!act[k]) continue;
+            if (slot[k] < 0) { werr = DEV_E_INVARIANT; continue; }
+            Meta *mp = T.m + slot[k];
+            atomicMax(&mp->touch, now);
+            atomicAdd(&mp->pin, 1);
+        }
     }
     werr = __reduce_max_sync(FULL, werr);
 }
 
-// unpin keys[:h] (engine.py:360 -> kvcache.py:132-138)
-__device__ void warp_unpin(const Table &T, const u64 *keys, int h, int lane, int &werr) {
-    for (int j0 = 0; j0 < h; j0 += 32) {
-        int j = j0 + lane;
-        bool act = j < h;
-        u64 key = act ? keys[j] : 0;
-        u32 am = __ballot_sync(FULL, act);
-        if (act) {
-            u32 peers = __match_any_sync(am, key);
-            if (__ffs(peers) - 1 == lane) {
-                int s = tab_find(T, key);
-                int cnt = __popc(peers);
-                if (s < 0) werr = DEV_E_INVARIANT;
-                else {
-                    int p = __ldcg(&T.m[s].pin);
-                    if (p < cnt) werr = DEV_E_INVARIANT;
-                    else T.m[s].pin = p - cnt;
-                }
-            }
+// Fused _finish cache work (engine.py:357-361): unpin keys[:hb], then insert
+// the full chain (prefix keys pk[0..B) then output keys ok[0..L-B)) at `now`.
+// Returns the number of created entries.
+__device__ int warp_unpin_insert(const Table &T, const u64 *pk, int B, const u64 *ok, int L, int hb, i64 now,
+                                 int lane, int &werr) {
+    int created_total = 0;
+    for (int j0 = 0; j0 < L; j0 += 128) {
+        u64 kk[4];
+        bool act[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int j = j0 + 32 * k + lane;
+            act[k] = j < L;
+            kk[k] = act[k] ? (j < B ? pk[j] : ok[j - B]) : 0;
         }
-        __syncwarp();
-    }
-    werr = __reduce_max_sync(FULL, werr);
-}
-
-// Insert (or touch) one chunk of <= 32 keys; lane j carries key/depth.
-// Returns the number of newly created entries.
-__device__ int warp_insert_chunk(const Table &T, bool act, u64 key, int depth, i64 now, int lane) {
-    u32 am = __ballot_sync(FULL, act);
-    bool lead = false;
-    if (act) {
-        u32 peers = __match_any_sync(am, key);
-        lead = (__ffs(peers) - 1) == lane;   // first occurrence creates (its depth), kvcache.py:88-91
-    }
-    bool pend = lead, created = false;
-    u32 pos = lead ? tab_home(key, T.slog2) : 0;
-    int slot = -1;
-    while (__ballot_sync(FULL, pend)) {
-        if (pend) {
+        int slot[4];
+        u32 fp[4];
+        find128(T, kk, act, slot, fp);
+        bool created[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            created[k] = false;
+            if (!act[k] || slot[k] >= 0) continue;
+            // claim the first EMPTY slot; a lost race continues the probe
+            u32 i = fp[k];
             for (;;) {
-                u64 v = __ldcg(T.k + pos);
-                if (v == key) { slot = (int)pos; pend = false; break; }
-                if (v == T.empty) break;
-                pos = (pos + 1) & T.mask;
+                u64 old = atomicCAS(T.k + i, T.empty, kk[k]);
+                if (old == T.empty) { slot[k] = (int)i; created[k] = true; break; }
+                if (old == kk[k]) { slot[k] = (int)i; break; }
+                int st;
+                u32 r = probe_rest(T, (i + 1) & T.mask, kk[k], st);
+                if (st == 0) { slot[k] = (int)r; break; }
+                i = r;
             }
         }
-        u32 cm = __ballot_sync(FULL, pend);
-        if (pend) {
-            u32 peers = __match_any_sync(cm, pos);
-            if (__ffs(peers) - 1 == lane) {
-                T.k[pos] = key;
-                slot = (int)pos; created = true; pend = false;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (!act[k]) continue;
+            const int j = j0 + 32 * k + lane;
+            Meta *mp = T.m + slot[k];
+            if (created[k]) {
+                Meta m; m.touch = now; m.depth = j + 1; m.pin = 0;
+                *mp = m;
+                if (j < hb) werr = DEV_E_INVARIANT;         // a pinned chain cannot be absent
             } else {
-                pos = (pos + 1) & T.mask;
+                atomicMax(&mp->touch, now);
+                if (j < hb) atomicSub(&mp->pin, 1);
             }
+            created_total += created[k];
         }
-        __syncwarp();
     }
-    if (slot >= 0) {
-        Meta *mp = T.m + slot;
-        if (created) { mp->touch = now; mp->depth = depth; mp->pin = 0; }
-        else { i64 t0 = __ldcg(&mp->touch); if (now > t0) mp->touch = now; }
-    }
-    __syncwarp();
-    return __popc(__ballot_sync(FULL, created));
+    werr = __reduce_max_sync(FULL, werr);
+    return __reduce_add_sync(FULL, created_total);
 }
 
 // Backward-shift deletion (no tombstones, so probe chains never degrade).
@@ -205,9 +299,10 @@ __device__ __forceinline__ bool lru_before(i64 t, int d, u64 k, i64 bt, int bd, 
 // Exact LRU eviction down to capacity (kvcache.py:142-168): repeatedly
 // remove the smallest unpinned entry in (touch asc, depth desc, key asc).
 // Full-table warp scan per victim; the minimum is always a leaf, so prefix
-// closure is preserved.
+// closure is preserved. A pinned-out table raises CacheFullError.
 __device__ void warp_evict(const Table &T, i64 cap, i64 &occ, int lane, int &werr) {
     const u32 S = T.mask + 1;
+    __threadfence();                     // order the preceding RED touch/pin updates
     while (occ > cap) {
         i64 bt = RSIM_NONE; int bd = -1; u64 bk = ~0ULL; int bs = -1;
         for (u32 i = lane; i < S; i += 32) {

@@ -36,17 +36,9 @@ __device__ void finish_cache(const Params &P, int gi, i64 &occ, int req, i64 end
     Table T = table_of(P, gi);
     const i64 a = P.blk_off[req];
     const int B = (int)(P.blk_off[req + 1] - a);
-    const u64 *pk = P.ckeys + a;
     const i64 oa = P.ooff[req];
     const int L = B + (int)(P.ooff[req + 1] - oa);
-    const u64 *ok = P.okeys + oa;
-    warp_unpin(T, pk, P.hit_blocks[req], lane, werr);
-    for (int j0 = 0; j0 < L; j0 += 32) {
-        int j = j0 + lane;
-        bool act = j < L;
-        u64 key = act ? (j < B ? pk[j] : ok[j - B]) : 0;
-        occ += warp_insert_chunk(T, act, key, j + 1, end, lane);
-    }
+    occ += warp_unpin_insert(T, P.ckeys + a, B, P.okeys + oa, L, P.hit_blocks[req], end, lane, werr);
     if (occ > P.max_occ) werr = DEV_E_TABLE_FULL;
     if (P.cap >= 0 && occ > P.cap && !werr) warp_evict(T, P.cap, occ, lane, werr);
 }

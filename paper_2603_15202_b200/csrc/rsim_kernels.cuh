@@ -104,11 +104,10 @@ __device__ __forceinline__ double score_of(const Params &P, const Inst &s, int h
 }
 
 // enqueue on the winner (InstanceSim.enqueue, engine.py:262-289) + route bookkeeping
-__device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, int lane, int &werr) {
+__device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, const u64 kk0[4], i64 in,
+                       int lane, int &werr) {
     Table T = table_of(P, gi);
-    const i64 a = P.blk_off[k];
-    const i64 in = P.in_tok[k];
-    warp_touch_pin(T, P.ckeys + a, h, t, lane, werr);
+    warp_touch_pin(T, P.ckeys + P.blk_off[k], kk0, h, t, lane, werr);
     Inst s = *sp;
     i64 ht = (i64)h * P.bs; if (ht > in) ht = in;
     i64 pending = in - ht; if (pending < 1) pending = 1;
@@ -138,7 +137,8 @@ enum { MODE_REPLAY = 0, MODE_DRAIN = 1, MODE_ROUTE = 2, MODE_ENQUEUE = 3 };
 // partials are pushed to every CTA of the cluster over DSMEM, one hardware
 // cluster barrier, then every CTA derives the same global winner and the
 // owning warp commits. No host round trip per decision.
-__global__ void __launch_bounds__(1024, 1)
+#define RSIM_MAX_WARPS 16
+__global__ void __launch_bounds__(32 * RSIM_MAX_WARPS, 1)
 replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = P.C, W = P.W, ipw = P.ipw;
@@ -187,27 +187,53 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
             const int B = (int)(P.blk_off[k + 1] - a);
             const i64 in = P.in_tok[k];
             const u64 *keys = P.ckeys + a;
+            u64 kk0[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) kk0[q] = (32 * q + lane < B) ? keys[32 * q + lane] : 0;
             u64 mybits = ~0ULL;
             int myh = 0;
-            for (int s = 0; s < nmine; s++) {
-                Inst *sp = st + l0 + s;
-                const int gi = base + l0 + s;
-                const bool cand = (mode != MODE_ENQUEUE) || gi == target;
-                if (cand && sp->due <= t) {      // snapshot() flushes every candidate (indicators.py:36-65)
-                    __syncwarp();
-                    if (lane == 0) flush_view(*sp, t);
-                    __syncwarp();
+            for (int s0 = 0; s0 < nmine; s0 += 2) {
+                const int ns = min(2, nmine - s0);
+                Table T2[2];
+                bool cand[2];
+                int hh[2] = {0, 0};
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    const int gi = base + l0 + s0 + q;
+                    cand[q] = q < ns && ((mode != MODE_ENQUEUE) || gi == target);
+                    T2[q] = table_of(P, q < ns ? gi : base + l0 + s0);
                 }
-                int h = 0;
-                double sc = 0.0;
-                if (cand) {
-                    h = warp_probe(table_of(P, gi), keys, B, lane);
-                    sc = score_of(P, *sp, h, in);
-                    // SURVEY 8d: one 8-B key compare per reference dict lookup + 16 B of view
-                    c_bytes += 8ULL * (u64)min(h + 1, B) + 16ULL;
+                if (cand[0] && cand[1]) {
+                    u32 m[2][4];
+                    probe128<2>(T2, kk0, B, lane, m);
+                    hh[0] = lead_hits(m[0]);
+                    hh[1] = lead_hits(m[1]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 2; q++) if (cand[q]) {
+                        u32 m[1][4];
+                        probe128<1>(&T2[q], kk0, B, lane, m);
+                        hh[q] = lead_hits(m[0]);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    if (!cand[q]) continue;
+                    if (hh[q] >= 128) hh[q] = B <= 128 ? B : deep_match(T2[q], keys, B, lane);
+                    else hh[q] = min(hh[q], B);
+                    Inst *sp = st + l0 + s0 + q;
+                    const int gi = base + l0 + s0 + q;
+                    if (sp->due <= t) {      // snapshot() flushes every candidate (indicators.py:36-65)
+                        __syncwarp();
+                        if (lane == 0) flush_view(*sp, t);
+                        __syncwarp();
+                    }
+                    const double sc = score_of(P, *sp, hh[q], in);
                     if (P.scores != nullptr && lane == 0) P.scores[gi] = sc;
+                    // SURVEY 8d: one 8-B key compare per reference dict lookup + 16 B of view
+                    c_bytes += 8ULL * (u64)min(hh[q] + 1, B) + 16ULL;
+                    if (lane == s0 + q) { mybits = (u64)__double_as_longlong(sc); myh = hh[q]; }
                 }
-                if (lane == s) { mybits = cand ? (u64)__double_as_longlong(sc) : ~0ULL; myh = h; }
             }
             if (cta == 0 && warp == 0) c_bytes += 8ULL * (u64)B;   // request chain keys, read once
             const u64 wmin = warp_min_u64(mybits);
@@ -272,7 +298,7 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
                     const int s = nth_set_bit(tmask, (int)(kk_local - before));
                     const int h = __shfl_sync(FULL, myh, s);
                     const int gi = base + l0 + s;
-                    commit(P, st + l0 + s, gi, k, h, t, lane, werr);
+                    commit(P, st + l0 + s, gi, k, h, t, kk0, in, lane, werr);
                     if (P.dec_ns != nullptr && lane == 0) P.dec_ns[k] = (i64)globaltimer();
                 }
             }
@@ -329,11 +355,7 @@ __global__ void cache_op_kernel(Params P, int gi, int op, const u64 *keys, int n
     Inst *sp = P.inst + gi;
     i64 occ = sp->occ;
     const i64 occ0 = occ;
-    for (int j0 = 0; j0 < n; j0 += 32) {
-        int j = j0 + lane;
-        bool act = j < n;
-        occ += warp_insert_chunk(T, act, act ? keys[j] : 0, j + 1, now, lane);
-    }
+    occ += warp_unpin_insert(T, keys, n, keys, n, 0, now, lane, werr);
     i64 before_evict = occ;
     if (occ > P.max_occ) werr = DEV_E_TABLE_FULL;
     if (P.cap >= 0 && occ > P.cap && !werr) warp_evict(T, P.cap, occ, lane, werr);

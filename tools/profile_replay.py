@@ -1,0 +1,32 @@
+"""Time (or profile under ncu) one resident replay of a workload slice.
+
+    python tools/profile_replay.py api64 20000 [ctas warps]
+"""
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+from paper_2603_15202_b200 import _native  # noqa: E402
+from paper_2603_15202_b200.cluster import native_config, sizing_for  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "api64"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
+shapes = [(int(sys.argv[3]), int(sys.argv[4]))] if len(sys.argv) > 4 else [(0, 0)]
+if len(sys.argv) > 3 and sys.argv[3] == "sweep":
+    shapes = [(c, w) for c in (1, 2, 4, 8, 16) for w in (4, 8, 16)]
+trace, cfg = bench.build_workload(name)
+trace = trace.slice(min(n, len(trace)))
+for c, w in shapes:
+    if c and c > cfg.n_instances:
+        continue
+    h = _native.Handle(native_config(cfg, sizing_for(trace, cfg), ctas=c, warps_per_cta=w))
+    h.load(trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.request_id, trace.blk_off, trace.blocks)
+    h.rerun()
+    best = min(h.rerun() for _ in range(3))
+    rep, k1, dr = h.timings()
+    print(f"{name} R={len(trace)} ctas={c} warps={w}: total {best:.2f} ms  replay {rep:.2f} ms "
+          f"({1000 * rep / len(trace):.2f} us/decision)  k1 {k1:.3f} ms  drain {dr:.2f} ms", flush=True)
+    h.close()
