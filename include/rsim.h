@@ -62,6 +62,13 @@ typedef struct rsim_config {
     int32_t record_steps;           /* keep the per-step log (RunReport.steps / bs_series)     */
     int64_t step_log_capacity;      /* records, 0 = auto                                       */
     int64_t expected_keys;          /* sizing hint: upper bound on keys one instance holds, 0 = from trace */
+    /* Multi-GPU sharding: n_instances is the GLOBAL cluster size; this handle owns
+     * the contiguous shard [lo, hi) of rank `rank` of `world` (sizes differ by at most one).
+     * Every decision exchanges one (min score, tie count) partial per rank through peer-mapped
+     * mailboxes (rsim_set_peer / rsim_open_peer_ipc); all ranks replay collectively. */
+    int32_t world;                  /* ranks sharing the cluster (1 = unsharded), <= 8         */
+    int32_t rank;
+    int64_t comm_timeout_ms;        /* a rank waiting longer on a peer fails with RSIM_E_COMM  */
 } rsim_config;
 
 typedef struct rsim rsim_t;
@@ -137,6 +144,12 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms);
  * + sum_i 8*min(h_i+1,B) + 16 per instance probed), [1] engine steps, [2] evictions,
  * [3] reserved, [4] requests loaded, [5] blocks, [6] output keys, [7] instances. */
 rsim_status rsim_read_counters(rsim_t *h, int64_t *out8);
+/* Sharded replay plumbing. The mailbox is device memory peers write into. */
+rsim_status rsim_shard_bounds(const rsim_t *h, int32_t *lo, int32_t *hi);
+rsim_status rsim_mailbox(rsim_t *h, void **dev_ptr);
+rsim_status rsim_mailbox_ipc_handle(rsim_t *h, unsigned char out64[64]);   /* cudaIpcGetMemHandle */
+rsim_status rsim_set_peer(rsim_t *h, int32_t rank, void *peer_mailbox);    /* same-process peer    */
+rsim_status rsim_open_peer_ipc(rsim_t *h, int32_t rank, const unsigned char in64[64]);
 /* Number of kernels librsim launched since create (evidence for bench gpu_launches). */
 int64_t rsim_launch_count(const rsim_t *h);
 

@@ -54,6 +54,7 @@ class Config(C.Structure):
         ("device", C.c_int32), ("queue_capacity", C.c_int32), ("table_slots_log2", C.c_int32),
         ("ctas", C.c_int32), ("warps_per_cta", C.c_int32), ("record_steps", C.c_int32),
         ("step_log_capacity", C.c_int64), ("expected_keys", C.c_int64),
+        ("world", C.c_int32), ("rank", C.c_int32), ("comm_timeout_ms", C.c_int64),
     ]
 
 
@@ -93,6 +94,11 @@ def lib():
         "rsim_read_decision_ns": ([P, I64, I64, P], C.c_int),
         "rsim_launch_count": ([P], I64),
         "rsim_rerun": ([P, P], C.c_int),
+        "rsim_shard_bounds": ([P, P, P], C.c_int),
+        "rsim_mailbox": ([P, P], C.c_int),
+        "rsim_mailbox_ipc_handle": ([P, P], C.c_int),
+        "rsim_set_peer": ([P, I32, P], C.c_int),
+        "rsim_open_peer_ipc": ([P, I32, P], C.c_int),
         "rsim_read_counters": ([P, P], C.c_int),
     }
     for name, (args, res) in sig.items():
@@ -108,7 +114,8 @@ EXPORTED = ("rsim_create", "rsim_destroy", "rsim_last_error", "rsim_reset", "rsi
             "rsim_read_step_log", "rsim_read_route_bs", "rsim_route_one", "rsim_enqueue",
             "rsim_cache_insert_keys", "rsim_cache_match_keys", "rsim_probe_batch", "rsim_chain_keys",
             "rsim_last_timings", "rsim_read_decision_ns", "rsim_launch_count", "rsim_rerun",
-            "rsim_read_counters")
+            "rsim_read_counters", "rsim_shard_bounds", "rsim_mailbox", "rsim_mailbox_ipc_handle",
+            "rsim_set_peer", "rsim_open_peer_ipc")
 
 
 def _p(a):
@@ -131,6 +138,8 @@ class Handle:
             self._raise(st, self._L.rsim_last_error(None).decode())
         self._h = h
         self.cfg = cfg
+        lo, hi = self.shard_bounds()
+        self.lo, self.n_local = lo, hi - lo
 
     def close(self):
         if getattr(self, "_h", None):
@@ -194,7 +203,7 @@ class Handle:
         return a
 
     def instances(self) -> np.ndarray:
-        out = np.empty((self.cfg.n_instances, 12), np.int64)
+        out = np.empty((self.n_local, 12), np.int64)
         self._ck(self._L.rsim_read_instances(self._h, _p(out)))
         return out
 
@@ -211,7 +220,7 @@ class Handle:
     def route_one(self, r: int, now_us: int, want_scores: bool = True):
         ch = np.zeros(1, np.int32)
         ht = np.zeros(1, np.int64)
-        sc = np.empty(self.cfg.n_instances, np.float64) if want_scores else None
+        sc = np.empty(self.n_local, np.float64) if want_scores else None
         self._ck(self._L.rsim_route_one(self._h, r, now_us, _p(ch), _p(ht), _p(sc)))
         return int(ch[0]), int(ht[0]), sc
 
@@ -233,7 +242,7 @@ class Handle:
         return int(hit[0])
 
     def probe_batch(self, first: int, count: int) -> np.ndarray:
-        out = np.empty((count, self.cfg.n_instances), np.int32)
+        out = np.empty((count, self.n_local), np.int32)
         self._ck(self._L.rsim_probe_batch(self._h, first, count, _p(out)))
         return out
 
@@ -258,6 +267,28 @@ class Handle:
         out = np.zeros(8, np.int64)
         self._ck(self._L.rsim_read_counters(self._h, _p(out)))
         return out
+
+    def shard_bounds(self):
+        lo, hi = C.c_int32(), C.c_int32()
+        self._ck(self._L.rsim_shard_bounds(self._h, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def mailbox(self) -> int:
+        p = C.c_void_p()
+        self._ck(self._L.rsim_mailbox(self._h, C.byref(p)))
+        return p.value
+
+    def mailbox_ipc_handle(self) -> bytes:
+        buf = (C.c_ubyte * 64)()
+        self._ck(self._L.rsim_mailbox_ipc_handle(self._h, buf))
+        return bytes(buf)
+
+    def set_peer(self, rank: int, ptr: int):
+        self._ck(self._L.rsim_set_peer(self._h, rank, C.c_void_p(ptr)))
+
+    def open_peer_ipc(self, rank: int, handle: bytes):
+        buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+        self._ck(self._L.rsim_open_peer_ipc(self._h, rank, buf))
 
     def launch_count(self) -> int:
         return int(self._L.rsim_launch_count(self._h))

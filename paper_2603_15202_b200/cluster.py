@@ -71,7 +71,8 @@ def sizing_for(trace: PackedTrace | None, config: ClusterConfig) -> Sizing:
 
 
 def native_config(config: ClusterConfig, sizing: Sizing, *, device: int = 0, record_steps: bool = False,
-                  step_log_capacity: int = 0, ctas: int = 0, warps_per_cta: int = 0) -> _native.Config:
+                  step_log_capacity: int = 0, ctas: int = 0, warps_per_cta: int = 0, world: int = 1,
+                  rank: int = 0, comm_timeout_ms: int = 20000) -> _native.Config:
     cm, cache, pol = config.cost_model, config.cache, config.policy
     tie = stable_key(config.seed, pol.tie_break_seed)            # cluster.py:90-94
     c = _native.Config()
@@ -100,6 +101,9 @@ def native_config(config: ClusterConfig, sizing: Sizing, *, device: int = 0, rec
     c.warps_per_cta = warps_per_cta
     c.record_steps = int(record_steps)
     c.step_log_capacity = step_log_capacity
+    c.world = world
+    c.rank = rank
+    c.comm_timeout_ms = comm_timeout_ms
     return c
 
 

@@ -78,6 +78,11 @@ struct rsim {
     size_t scratch_cap = 0;
     i64 *scratch_res = nullptr;
     u64 *ctr = nullptr;            // device counters (Params.ctr)
+    int N = 0, gbase = 0;          // local shard size, global id of local instance 0
+    u64 *mbox = nullptr;           // multi-GPU mailbox [2][8][4]
+    u64 *peer[8] = {nullptr};
+    bool peer_ipc[8] = {false};
+    u64 epoch = 1;
 };
 
 static rsim_status fail(rsim_t *h, rsim_status st, const char *fmt, ...) {
@@ -108,7 +113,7 @@ static Params make_params(rsim_t *h) {
     P.hit_blocks = h->hit_blocks.p; P.chosen = h->chosen.p; P.hit_tokens = h->hit_tokens.p;
     P.first_sched = h->first_sched.p; P.first_token = h->first_token.p; P.finish = h->finish.p;
     P.route_bs = h->route_bs.p; P.dec_ns = h->dec_ns.p;
-    P.N = h->cfg.n_instances; P.C = h->C; P.W = h->W; P.ipw = h->ipw; P.per_cta = h->per_cta;
+    P.N = h->N; P.C = h->C; P.W = h->W; P.ipw = h->ipw; P.per_cta = h->per_cta;
     P.bs = h->cfg.block_size; P.policy = h->cfg.policy; P.kv_ind = h->cfg.kv_indicator;
     P.bal_ind = h->cfg.balance_indicator; P.debug = h->cfg.debug_checks;
     P.cap = h->cfg.capacity_blocks; P.chunk = h->cfg.chunk_tokens; P.max_batch = h->cfg.max_batch_requests;
@@ -120,6 +125,11 @@ static Params make_params(rsim_t *h) {
     P.log = h->log; P.log_cap = h->log_cap; P.log_n = h->log_n;
     P.scores = nullptr;
     P.ctr = h->ctr;
+    P.gbase = h->gbase; P.world = h->cfg.world > 1 ? h->cfg.world : 1; P.rank = h->cfg.rank;
+    P.mbox = h->mbox;
+    for (int i = 0; i < 8; i++) P.peer[i] = h->peer[i];
+    P.epoch = h->epoch;
+    P.timeout_ns = (h->cfg.comm_timeout_ms > 0 ? h->cfg.comm_timeout_ms : 10000) * 1000000LL;
     return P;
 }
 
@@ -135,12 +145,14 @@ static rsim_status check_device_error(rsim_t *h) {
         case DEV_E_QUEUE_OVERFLOW: return fail(h, RSIM_E_QUEUE_OVERFLOW, "instance queue ring full (queue_capacity=%d)", 1 << h->qlog2);
         case DEV_E_TABLE_FULL: return fail(h, RSIM_E_TABLE_FULL, "instance KV$ table over 3/4 load (slots=%d)", 1 << h->slog2);
         case 11: return fail(h, RSIM_E_NO_INSTANCES, "no instances to route to");
+        case DEV_E_COMM: return fail(h, RSIM_E_COMM, "timed out waiting for a peer rank's decision partial");
         default: return fail(h, RSIM_E_INVARIANT, "device error %d", e[0]);
     }
 }
 
 static rsim_status init_state(rsim_t *h) {
-    const int N = h->cfg.n_instances;
+    const int N = h->N;
+    h->epoch += 1;
     std::vector<Inst> hs(N);
     for (auto &s : hs) {
         memset(&s, 0, sizeof(s));
@@ -204,7 +216,15 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaEventCreate(&h->ev1));
 
     // ---- replay cluster shape
-    const int N = c.n_instances;
+    const int world = c.world > 1 ? c.world : 1;
+    if (world > 8 || c.rank < 0 || c.rank >= world) { delete h; return fail(nullptr, RSIM_E_INVALID, "world must be 1..8 and 0 <= rank < world"); }
+    if (c.n_instances < world) { delete h; return fail(nullptr, RSIM_E_INVALID, "fewer instances than ranks"); }
+    {   // contiguous shard of this rank (paper_2603_15202_b200/sharding.py: shard_bounds)
+        const int base = c.n_instances / world, extra = c.n_instances % world;
+        h->gbase = c.rank * base + std::min(c.rank, extra);
+        h->N = base + (c.rank < extra ? 1 : 0);
+    }
+    const int N = h->N;
     int C = c.ctas;
     if (C <= 0) C = N <= 128 ? 1 : std::min(16, (N + 63) / 64);
     C = std::max(1, std::min(16, std::min(C, N)));
@@ -213,8 +233,9 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     W = std::max(1, std::min(RSIM_MAX_WARPS, W));
     int ipw = (per_cta + W - 1) / W;
     if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
+    if (C * W > 256) { delete h; return fail(nullptr, RSIM_E_INVALID, "cluster too large"); }
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
-    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(2 * W + 2 * C) * sizeof(Part);
+    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(2 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 6 * sizeof(u64) + (size_t)W * sizeof(WarpBuf);
     if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
     cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
     if (C > 8) cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -242,6 +263,9 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaMalloc(&h->scores, N * sizeof(double)));
     CK(nullptr, cudaMalloc(&h->scratch_res, 4 * sizeof(i64)));
     CK(nullptr, cudaMalloc(&h->ctr, 8 * sizeof(u64)));
+    CK(nullptr, cudaMalloc(&h->mbox, 2 * 8 * 4 * sizeof(u64)));
+    CK(nullptr, cudaMemset(h->mbox, 0, 2 * 8 * 4 * sizeof(u64)));
+    h->peer[world > 1 ? c.rank : 0] = h->mbox;
     if (c.record_steps) {
         h->log_cap = c.step_log_capacity > 0 ? c.step_log_capacity : (1 << 20);
         CK(nullptr, cudaMalloc(&h->log, (size_t)h->log_cap * 6 * sizeof(i64)));
@@ -262,7 +286,8 @@ void rsim_destroy(rsim_t *h) {
     h->rid.free_(); h->blocks.free_(); h->ckeys.free_(); h->okeys.free_();
     h->hit_blocks.free_(); h->chosen.free_();
     void *ps[] = {h->inst, h->qbuf, h->rbuf, h->tkeys, h->tmeta, h->tie, h->errbuf, h->flag, h->log, h->log_n,
-                  h->scores, h->scratch_keys, h->scratch_res, h->ctr};
+                  h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox};
+    for (int i = 0; i < 8; i++) if (h->peer_ipc[i] && h->peer[i]) cudaIpcCloseMemHandle(h->peer[i]);
     for (void *p : ps) if (p) cudaFree(p);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
@@ -344,12 +369,19 @@ rsim_status rsim_load_trace(rsim_t *h, int64_t n, const int64_t *arrival_us, con
 
 static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode, int target, double *scores_dev,
                                  float *ms_out) {
+    if (h->cfg.world > 1) {
+        if (mode == MODE_ROUTE || mode == MODE_ENQUEUE)
+            return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls are single-rank only");
+        for (int r = 0; r < h->cfg.world; r++)
+            if (!h->peer[r]) return fail(h, RSIM_E_COMM, "peer mailbox of rank %d not set", r);
+    }
     Params P = make_params(h);
     P.scores = scores_dev;
     cudaLaunchConfig_t lc;
     memset(&lc, 0, sizeof(lc));
     lc.gridDim = dim3(h->C, 1, 1);
-    lc.blockDim = dim3(32 * h->W, 1, 1);
+    lc.blockDim = dim3(32 * (h->W + 1), 1, 1);   // + the request-staging warp
+    cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
     lc.dynamicSmemBytes = h->smem_bytes;
     lc.stream = h->stream;
     cudaLaunchAttribute at[1];
@@ -388,14 +420,14 @@ rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen
     if (st != RSIM_OK) return st;
     if (chosen) CK(h, cudaMemcpy(chosen, h->chosen.p + r, sizeof(int), cudaMemcpyDeviceToHost));
     if (hit_tokens) CK(h, cudaMemcpy(hit_tokens, h->hit_tokens.p + r, sizeof(i64), cudaMemcpyDeviceToHost));
-    if (scores) CK(h, cudaMemcpy(scores, h->scores, h->cfg.n_instances * sizeof(double), cudaMemcpyDeviceToHost));
+    if (scores) CK(h, cudaMemcpy(scores, h->scores, h->N * sizeof(double), cudaMemcpyDeviceToHost));
     return RSIM_OK;
 }
 
 rsim_status rsim_enqueue(rsim_t *h, int32_t instance, int64_t r, int64_t now_us, int64_t *hit_tokens) {
     if (!h) return RSIM_E_INVALID;
     if (r < 0 || r >= h->R) return fail(h, RSIM_E_INVALID, "request index out of range");
-    if (instance < 0 || instance >= h->cfg.n_instances) return fail(h, RSIM_E_INVALID, "instance out of range");
+    if (instance < 0 || instance >= h->N) return fail(h, RSIM_E_INVALID, "instance out of range");
     CK(h, cudaSetDevice(h->cfg.device));
     rsim_status st = launch_replay(h, r, r + 1, now_us, MODE_ENQUEUE, instance, nullptr, nullptr);
     if (st != RSIM_OK) return st;
@@ -416,7 +448,7 @@ static rsim_status stage_keys(rsim_t *h, const uint64_t *keys, int64_t n) {
 rsim_status rsim_cache_insert_keys(rsim_t *h, int32_t instance, const uint64_t *keys, int64_t n, int64_t now_us,
                                    int64_t *evicted) {
     if (!h) return RSIM_E_INVALID;
-    if (instance < 0 || instance >= h->cfg.n_instances) return fail(h, RSIM_E_INVALID, "instance out of range");
+    if (instance < 0 || instance >= h->N) return fail(h, RSIM_E_INVALID, "instance out of range");
     for (i64 i = 0; i < n; i++) if (keys[i] == 0) return fail(h, RSIM_E_INVALID, "key equals the table sentinel 0");
     CK(h, cudaSetDevice(h->cfg.device));
     rsim_status st = stage_keys(h, keys, n);
@@ -434,7 +466,7 @@ rsim_status rsim_cache_insert_keys(rsim_t *h, int32_t instance, const uint64_t *
 
 rsim_status rsim_cache_match_keys(rsim_t *h, int32_t instance, const uint64_t *keys, int64_t n, int64_t *hit) {
     if (!h) return RSIM_E_INVALID;
-    if (instance < 0 || instance >= h->cfg.n_instances) return fail(h, RSIM_E_INVALID, "instance out of range");
+    if (instance < 0 || instance >= h->N) return fail(h, RSIM_E_INVALID, "instance out of range");
     CK(h, cudaSetDevice(h->cfg.device));
     rsim_status st = stage_keys(h, keys, n);
     if (st) return st;
@@ -453,7 +485,7 @@ rsim_status rsim_probe_batch(rsim_t *h, int64_t first, int64_t count, int32_t *o
     if (first < 0 || count < 0 || first + count > h->R) return fail(h, RSIM_E_INVALID, "request range out of the loaded trace");
     CK(h, cudaSetDevice(h->cfg.device));
     int *d = nullptr;
-    const size_t n = (size_t)count * h->cfg.n_instances;
+    const size_t n = (size_t)count * h->N;
     CK(h, cudaMalloc(&d, std::max<size_t>(n, 1) * sizeof(int)));
     const i64 warps = (i64)n;
     const int grid = (int)std::min<i64>((warps * 32 + 255) / 256, 148 * 8);
@@ -535,7 +567,7 @@ rsim_status rsim_read_decision_ns(rsim_t *h, int64_t first, int64_t count, int64
 rsim_status rsim_read_instances(rsim_t *h, int64_t *out) {
     if (!h || !out) return RSIM_E_INVALID;
     CK(h, cudaSetDevice(h->cfg.device));
-    const int N = h->cfg.n_instances;
+    const int N = h->N;
     std::vector<Inst> hs(N);
     CK(h, cudaMemcpy(hs.data(), h->inst, N * sizeof(Inst), cudaMemcpyDeviceToHost));
     for (int i = 0; i < N; i++) {
@@ -568,7 +600,8 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
     if (!h) return RSIM_E_INVALID;
     CK(h, cudaSetDevice(h->cfg.device));
     cudaStream_t s = h->stream;
-    const int N = h->cfg.n_instances;
+    const int N = h->N;
+    h->epoch += 1;
     std::vector<Inst> hs(N);
     for (auto &x : hs) { memset(&x, 0, sizeof(x)); x.next_step = RSIM_NONE; x.due = RSIM_NONE; x.next_finish = RSIM_NONE; }
     u64 tie[2] = {h->cfg.tie_seed_lo, h->cfg.tie_seed_hi};
@@ -612,7 +645,47 @@ rsim_status rsim_read_counters(rsim_t *h, int64_t *out8) {
     u64 c[8];
     CK(h, cudaMemcpy(c, h->ctr, sizeof(c), cudaMemcpyDeviceToHost));
     for (int i = 0; i < 8; i++) out8[i] = (int64_t)c[i];
-    out8[4] = h->R; out8[5] = h->nblk; out8[6] = h->nout; out8[7] = h->cfg.n_instances;
+    out8[4] = h->R; out8[5] = h->nblk; out8[6] = h->nout; out8[7] = h->N;
+    return RSIM_OK;
+}
+
+rsim_status rsim_shard_bounds(const rsim_t *h, int32_t *lo, int32_t *hi) {
+    if (!h) return RSIM_E_INVALID;
+    if (lo) *lo = h->gbase;
+    if (hi) *hi = h->gbase + h->N;
+    return RSIM_OK;
+}
+
+rsim_status rsim_mailbox(rsim_t *h, void **dev_ptr) {
+    if (!h || !dev_ptr) return RSIM_E_INVALID;
+    *dev_ptr = h->mbox;
+    return RSIM_OK;
+}
+
+rsim_status rsim_mailbox_ipc_handle(rsim_t *h, unsigned char out64[64]) {
+    if (!h || !out64) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    cudaIpcMemHandle_t ih;
+    CK(h, cudaIpcGetMemHandle(&ih, h->mbox));
+    memcpy(out64, &ih, 64);
+    return RSIM_OK;
+}
+
+rsim_status rsim_set_peer(rsim_t *h, int32_t rank, void *peer_mailbox) {
+    if (!h || rank < 0 || rank >= 8 || !peer_mailbox) return RSIM_E_INVALID;
+    h->peer[rank] = (u64 *)peer_mailbox;
+    return RSIM_OK;
+}
+
+rsim_status rsim_open_peer_ipc(rsim_t *h, int32_t rank, const unsigned char in64[64]) {
+    if (!h || rank < 0 || rank >= 8 || !in64) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    cudaIpcMemHandle_t ih;
+    memcpy(&ih, in64, 64);
+    void *p = nullptr;
+    CK(h, cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+    h->peer[rank] = (u64 *)p;
+    h->peer_ipc[rank] = true;
     return RSIM_OK;
 }
 

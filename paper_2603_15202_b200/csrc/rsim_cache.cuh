@@ -105,26 +105,26 @@ __device__ __forceinline__ void find128(const Table &T, const u64 kk[4], const b
 // Hit masks for the first 128 depths of NI instances at once (loads of all
 // instances in flight together). m[s][k] bit lane = depth 32k+lane present.
 template <int NI>
-__device__ __forceinline__ void probe128(const Table *T, const u64 kk[4], int B, int lane, u32 m[NI][4]) {
+__device__ __forceinline__ void probe128(const Table *T, const u64 kk[4], const u32 hm[4], int B, int lane,
+                                         u32 m[NI][4], int slot[NI][4]) {
     ulonglong2 pr[NI][4];
-    u32 home[NI][4];
 #pragma unroll
     for (int s = 0; s < NI; s++)
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            home[s][k] = tab_home(kk[k], T[s].slog2);
-            if (32 * k + lane < B) pr[s][k] = ld_pair(T[s], home[s][k]);
-        }
+        for (int k = 0; k < 4; k++)
+            if (32 * k + lane < B) pr[s][k] = ld_pair(T[s], hm[k]);
 #pragma unroll
     for (int s = 0; s < NI; s++)
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             bool f = false;
+            slot[s][k] = -1;
             if (32 * k + lane < B) {
                 int st;
-                u32 r = eval_pair(T[s], pr[s][k], home[s][k], kk[k], st);
+                u32 r = eval_pair(T[s], pr[s][k], hm[k], kk[k], st);
                 if (st == 2) r = probe_rest(T[s], r, kk[k], st);
                 f = st == 0;
+                if (f) slot[s][k] = (int)r;
             }
             m[s][k] = __ballot_sync(FULL, f);
         }
@@ -183,8 +183,11 @@ __device__ int warp_probe(const Table &T, const u64 *keys, int B, int lane) {
     u64 kk[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) kk[k] = (32 * k + lane < B) ? keys[32 * k + lane] : 0;
-    u32 m[1][4];
-    probe128<1>(&T, kk, B, lane, m);
+    u32 m[1][4], hm[4];
+    int sl[1][4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) hm[k] = tab_home(kk[k], T.slog2);
+    probe128<1>(&T, kk, hm, B, lane, m, sl);
     int h = lead_hits(m[0]);
     if (h < 128) return min(h, B);
     if (B <= 128) return B;
@@ -192,21 +195,27 @@ __device__ int warp_probe(const Table &T, const u64 *keys, int B, int lane) {
 }
 
 // touch keys[:h] at now and pin them (InstanceSim.enqueue, engine.py:275-276).
-// kk0 holds the first 128 keys (already in registers from the probe).
-__device__ void warp_touch_pin(const Table &T, const u64 *keys, const u64 kk0[4], int h, i64 now, int lane,
-                               int &werr) {
+// kk0 holds the first 128 keys (already in registers from the probe); slot0,
+// when non-null, holds their slots as found by that probe (no lookup needed).
+__device__ void warp_touch_pin(const Table &T, const u64 *keys, const u64 kk0[4], const int *slot0, int h, i64 now,
+                               int lane, int &werr) {
     for (int j0 = 0; j0 < h; j0 += 128) {
         u64 kk[4];
         bool act[4];
+        int slot[4];
+        u32 fp[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const int j = j0 + 32 * k + lane;
             act[k] = j < h;
             kk[k] = j0 == 0 ? kk0[k] : (act[k] ? keys[j] : 0);
         }
-        int slot[4];
-        u32 fp[4];
-        find128(T, kk, act, slot, fp);
+        if (j0 == 0 && slot0 != nullptr) {
+#pragma unroll
+            for (int k = 0; k < 4; k++) slot[k] = slot0[k];
+        } else {
+            find128(T, kk, act, slot, fp);
+        }
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             if (!act[k]) continue;
@@ -266,6 +275,76 @@ __device__ int warp_unpin_insert(const Table &T, const u64 *pk, int B, const u64
             } else {
                 atomicMax(&mp->touch, now);
                 if (j < hb) atomicSub(&mp->pin, 1);
+            }
+            created_total += created[k];
+        }
+    }
+    werr = __reduce_max_sync(FULL, werr);
+    return __reduce_add_sync(FULL, created_total);
+}
+
+// Finish cache work of several requests of one engine step at once (legal
+// when no eviction can occur in between: inserts, touches and unpins commute).
+// Flattened over all chains, 128 keys per round: one load, one lookup and one
+// claim round trip per round instead of per request.
+struct FinBuf {
+    i64 a[32], oa[32];
+    int B[32], L[32], hb[32], pre[33];
+};
+
+__device__ int warp_finish_many(const Table &T, const u64 *ckeys, const u64 *okeys, const FinBuf &F, int nf, i64 now,
+                                int lane, int &werr) {
+    const int K = F.pre[nf];
+    int created_total = 0;
+    for (int x0 = 0; x0 < K; x0 += 128) {
+        u64 kk[4];
+        bool act[4];
+        int dep[4];
+        bool unp[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int x = x0 + 32 * k + lane;
+            act[k] = x < K;
+            kk[k] = 0; dep[k] = 0; unp[k] = false;
+            if (act[k]) {
+                int f = 0;
+                while (f + 1 < nf && F.pre[f + 1] <= x) f++;
+                const int j = x - F.pre[f];
+                kk[k] = j < F.B[f] ? ckeys[F.a[f] + j] : okeys[F.oa[f] + j - F.B[f]];
+                dep[k] = j + 1;
+                unp[k] = j < F.hb[f];
+            }
+        }
+        int slot[4];
+        u32 fp[4];
+        find128(T, kk, act, slot, fp);
+        bool created[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            created[k] = false;
+            if (!act[k] || slot[k] >= 0) continue;
+            u32 i = fp[k];
+            for (;;) {
+                u64 old = atomicCAS(T.k + i, T.empty, kk[k]);
+                if (old == T.empty) { slot[k] = (int)i; created[k] = true; break; }
+                if (old == kk[k]) { slot[k] = (int)i; break; }
+                int st;
+                u32 r = probe_rest(T, (i + 1) & T.mask, kk[k], st);
+                if (st == 0) { slot[k] = (int)r; break; }
+                i = r;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (!act[k]) continue;
+            Meta *mp = T.m + slot[k];
+            if (created[k]) {
+                Meta m; m.touch = now; m.depth = dep[k]; m.pin = 0;
+                *mp = m;
+                if (unp[k]) werr = DEV_E_INVARIANT;
+            } else {
+                atomicMax(&mp->touch, now);
+                if (unp[k]) atomicSub(&mp->pin, 1);
             }
             created_total += created[k];
         }

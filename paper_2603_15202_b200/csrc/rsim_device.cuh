@@ -24,6 +24,7 @@ typedef unsigned int u32;
 #define DEV_E_INVARIANT 5
 #define DEV_E_QUEUE_OVERFLOW 7
 #define DEV_E_TABLE_FULL 8
+#define DEV_E_COMM 10
 
 // Engine + router state of one instance. Live aggregates are the engine's
 // truth (engine.py:219-222); v_* is the router-visible view that only syncs at
@@ -44,8 +45,31 @@ struct __align__(16) Inst {
     int pad;
 };
 
-struct QEnt { int req; int flags; i64 pending; };    // flags bit0: prefill already scheduled once
-struct REnt { int req; int pad; i64 finish_step; };   // finish_step = join step + out - 1
+// A request on an instance: one 64-byte record used by the FIFO queue (v =
+// pending prefill tokens) and the running list (v = finish step = join step +
+// out - 1). It carries everything a step needs, so pops and finishes never
+// reload per-request metadata.
+struct __align__(16) Ent {
+    i64 v;            // queue: pending prefill tokens; running: finish step
+    i64 in;           // input tokens
+    i64 a;            // offset of the request's prefix chain keys (ckeys)
+    i64 oa;           // offset of its output-block keys (okeys)
+    int req, flags;   // flags bit0: prefill scheduled at least once
+    int out, B, L, hb;   // output tokens, prefix blocks, full chain length, admission hit blocks
+    int pad0, pad1;
+};
+typedef Ent QEnt;
+typedef Ent REnt;
+
+__device__ __forceinline__ Ent shfl_ent(const Ent &e, int src) {
+    Ent r;
+    const u64 *p = reinterpret_cast<const u64 *>(&e);
+    u64 *q = reinterpret_cast<u64 *>(&r);
+#pragma unroll
+    for (int i = 0; i < 8; i++) q[i] = __shfl_sync(0xffffffffu, p[i], src);
+    return r;
+}
+
 struct Meta { i64 touch; int depth; int pin; };       // kvcache.py:34-41 (parent implied by the chain)
 
 struct Params {
@@ -72,6 +96,12 @@ struct Params {
     i64 *log; i64 log_cap; u64 *log_n;
     double *scores;   // optional per-instance scores of a route_one call
     u64 *ctr;         // [0] algorithmic probe bytes, [1] engine steps, [2] evictions
+    // multi-GPU shard: local instance i is global instance gbase + i
+    int gbase, world, rank;
+    u64 *mbox;        // this rank's mailbox [2 parity][8 ranks][4 words]
+    u64 *peer[8];     // every rank's mailbox (peer-mapped), peer[rank] == mbox
+    u64 epoch;        // run epoch, distinguishes mailbox contents of successive replays
+    i64 timeout_ns;
 };
 
 // ---------------- hashing (hashing.py:15-25) ----------------

@@ -30,17 +30,31 @@ __device__ __forceinline__ void flush_view(Inst &s, i64 now) {   // engine.py:24
     }
 }
 
-// _finish (engine.py:357-372): unpin the admission hit, insert the full
-// prefix+output chain stamped with the step end, evict down to capacity.
-__device__ void finish_cache(const Params &P, int gi, i64 &occ, int req, i64 end, int lane, int &werr) {
+// _finish (engine.py:357-372) for one request: unpin the admission hit, insert
+// the full prefix+output chain stamped with the step end, evict to capacity.
+__device__ void finish_one(const Params &P, int gi, i64 &occ, i64 a, int B, i64 oa, int L, int hb, i64 end, int lane,
+                           int &werr) {
     Table T = table_of(P, gi);
-    const i64 a = P.blk_off[req];
-    const int B = (int)(P.blk_off[req + 1] - a);
-    const i64 oa = P.ooff[req];
-    const int L = B + (int)(P.ooff[req + 1] - oa);
-    occ += warp_unpin_insert(T, P.ckeys + a, B, P.okeys + oa, L, P.hit_blocks[req], end, lane, werr);
+    occ += warp_unpin_insert(T, P.ckeys + a, B, P.okeys + oa, L, hb, end, lane, werr);
     if (occ > P.max_occ) werr = DEV_E_TABLE_FULL;
     if (P.cap >= 0 && occ > P.cap && !werr) warp_evict(T, P.cap, occ, lane, werr);
+}
+
+// Process the finishers collected in F, in collection order (= the reference's:
+// queue-pop finishes, then decode finishes in running order). When no eviction
+// can happen before the last insert, all chains go in one batched pass.
+__device__ void flush_finishers(const Params &P, int gi, i64 &occ, FinBuf &F, int nf, i64 end, int lane, int &werr) {
+    if (nf == 0 || werr) return;
+    __syncwarp();
+    if (P.cap < 0 || occ + F.pre[nf] <= P.cap) {
+        Table T = table_of(P, gi);
+        occ += warp_finish_many(T, P.ckeys, P.okeys, F, nf, end, lane, werr);
+        if (occ > P.max_occ) werr = DEV_E_TABLE_FULL;
+    } else {
+        for (int f = 0; f < nf && !werr; f++)
+            finish_one(P, gi, occ, F.a[f], F.B[f], F.oa[f], F.L[f], F.hb[f], end, lane, werr);
+    }
+    __syncwarp();
 }
 
 __device__ __forceinline__ void log_step(const Params &P, int gi, i64 start, i64 end, i64 pre, i64 bs_after,
@@ -55,8 +69,8 @@ __device__ __forceinline__ void log_step(const Params &P, int gi, i64 start, i64
 }
 
 // One engine step of instance gi starting at s.next_step. Returns false if
-// the plan was empty (the instance went idle).
-__device__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr) {
+// the plan was empty (the instance went idle). F is this warp's finisher buffer.
+__device__ __noinline__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr, FinBuf &F) {
     Inst s = *sp;
     const i64 t = s.next_step;
     flush_view(s, t);                                              // form_batch flush, engine.py:293
@@ -64,25 +78,38 @@ __device__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr
     const i64 budget = P.chunk - ndec > 0 ? P.chunk - ndec : 0;   // engine.py:296
     const i64 slots = P.max_batch - ndec;                          // engine.py:297
     QEnt *qb = P.qbuf + ((size_t)gi << P.qlog2);
+    REnt *rb = P.rbuf + (size_t)gi * (size_t)P.max_batch;
     const u32 qmask = (1u << P.qlog2) - 1u;
+    const bool fin_step = ndec > 0 && s.next_finish == s.step_idx;
+    // the running list's first 32 records load together with the queue head
+    Ent r0;
+    r0.v = RSIM_NONE;
+    if (fin_step && lane < ndec) r0 = rb[lane];
 
     // pass 1: FIFO plan (_plan_allocations, engine.py:174-184). Entry j is
     // allocated iff j < slots and the budget left before it is positive.
+    // The first 32 entries stay in registers for pass 2.
     i64 ptok = 0;
     int nalloc = 0;
+    Ent e0;
+    e0.v = 0;
     {
         i64 cum = 0;
         for (int j0 = 0; j0 < s.q && j0 < slots && cum < budget; j0 += 32) {
-            int j = j0 + lane;
-            bool valid = j < s.q && j < slots;
-            i64 p = valid ? qb[(s.q_head + j) & qmask].pending : 0;
-            i64 incl = warp_incl_scan(p, lane);
-            i64 excl = cum + incl - p;
-            bool alloc = valid && excl < budget;
-            i64 take = alloc ? min(budget - excl, p) : 0;
-            int na = __popc(__ballot_sync(FULL, alloc));
-            i64 ts = warp_sum(take);
-            nalloc += na; ptok += ts;
+            const int j = j0 + lane;
+            const bool valid = j < s.q && j < slots;
+            Ent e;
+            e.v = 0;
+            if (valid) e = qb[(s.q_head + j) & qmask];
+            if (j0 == 0) e0 = e;
+            const i64 p = valid ? e.v : 0;
+            const i64 incl = warp_incl_scan(p, lane);
+            const i64 excl = cum + incl - p;
+            const bool alloc = valid && excl < budget;
+            const i64 take = alloc ? min(budget - excl, p) : 0;
+            const int na = __popc(__ballot_sync(FULL, alloc));
+            nalloc += na;
+            ptok += warp_sum(take);
             cum += __shfl_sync(FULL, incl, 31);
             if (na < 32) break;
         }
@@ -97,51 +124,65 @@ __device__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr
     const i64 pre = prefill_cost_us(P, ptok);
     const i64 end = t + pre + decode_cost_us(P, ndec, s.dcs);      // ctx = sum(in+gen) over decode = dcs
 
-    // pass 2: apply allocations (engine.py:314-319)
+    // pass 2: apply allocations (engine.py:314-319); pops = allocated entries
+    // left with pending == 0 (a prefix of the allocation)
     int npop = 0;
     {
         i64 cum = 0;
         for (int j0 = 0; j0 < nalloc; j0 += 32) {
-            int j = j0 + lane;
-            bool alloc = j < nalloc;
-            QEnt e;
-            e.pending = 0; e.req = 0; e.flags = 0;
-            if (alloc) e = qb[(s.q_head + j) & qmask];
-            i64 p = alloc ? e.pending : 0;
-            i64 incl = warp_incl_scan(p, lane);
-            i64 excl = cum + incl - p;
-            i64 take = alloc ? min(budget - excl, p) : 0;
+            const int j = j0 + lane;
+            const bool alloc = j < nalloc;
+            Ent e = e0;
+            if (j0 > 0 && alloc) e = qb[(s.q_head + j) & qmask];
+            const i64 p = alloc ? e.v : 0;
+            const i64 incl = warp_incl_scan(p, lane);
+            const i64 excl = cum + incl - p;
+            const i64 take = alloc ? min(budget - excl, p) : 0;
             if (alloc) {
                 if (!(e.flags & 1)) P.first_sched[e.req] = t;
-                e.pending = p - take;
-                e.flags |= 1;
-                qb[(s.q_head + j) & qmask] = e;
+                if (p - take != 0) {                        // a popped record is consumed below as is
+                    Ent u = e;
+                    u.v = p - take;
+                    u.flags |= 1;
+                    qb[(s.q_head + j) & qmask] = u;
+                }
             }
-            npop += __popc(__ballot_sync(FULL, alloc && e.pending == 0));
+            npop += __popc(__ballot_sync(FULL, alloc && p - take == 0));
             cum += __shfl_sync(FULL, incl, 31);
         }
     }
     s.pend -= ptok;
     __syncwarp();
 
+    int nf = 0;
+    auto add_fin = [&](const Ent &f) {
+        if (nf == 32) { flush_finishers(P, gi, s.occ, F, nf, end, lane, werr); nf = 0; }
+        if (lane == 0) {
+            if (nf == 0) F.pre[0] = 0;
+            F.a[nf] = f.a; F.oa[nf] = f.oa; F.B[nf] = f.B; F.L[nf] = f.L; F.hb[nf] = f.hb;
+            F.pre[nf + 1] = F.pre[nf] + f.L;
+        }
+        nf++;
+    };
+
     // queue heads with pending == 0 get their first token (engine.py:321-331);
     // out == 1 finishes right away, in pop order.
     const int head0 = s.q_head;
     s.total += npop;
     for (int j0 = 0; j0 < npop; j0 += 32) {
-        int j = j0 + lane;
-        bool pop = j < npop;
-        int req = pop ? qb[(head0 + j) & qmask].req : 0;
-        i64 out = pop ? P.out_tok[req] : 0;
-        if (pop) P.first_token[req] = end;
-        u32 fm = __ballot_sync(FULL, pop && out == 1);
+        const int j = j0 + lane;
+        const bool pop = j < npop;
+        Ent e = e0;
+        if (j0 > 0 && pop) e = qb[(head0 + j) & qmask];
+        if (pop) P.first_token[e.req] = end;
+        u32 fm = __ballot_sync(FULL, pop && e.out == 1);
         while (fm) {
-            int l = __ffs(fm) - 1;
+            const int l = __ffs(fm) - 1;
             fm &= fm - 1;
-            int rq = __shfl_sync(FULL, req, l);
-            if (lane == 0) P.finish[rq] = end;
-            s.total -= P.in_tok[rq] + 1;
-            if (!werr) finish_cache(P, gi, s.occ, rq, end, lane, werr);
+            const Ent f = shfl_ent(e, l);
+            if (lane == 0) P.finish[f.req] = end;
+            s.total -= f.in + 1;
+            add_fin(f);
         }
     }
     s.q_head = (s.q_head + npop) & (int)qmask;
@@ -149,65 +190,63 @@ __device__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr
 
     // decode (engine.py:333-347): every running request gains a token; those
     // whose finish step is now leave in running order.
-    REnt *rb = P.rbuf + (size_t)gi * (size_t)P.max_batch;
     s.total += ndec;
     s.dcs += ndec;
-    if (ndec > 0 && s.next_finish == s.step_idx) {
+    if (fin_step) {
         int w = 0;
-        i64 nf = RSIM_NONE;
+        i64 nf_step = RSIM_NONE;
         for (int j0 = 0; j0 < ndec; j0 += 32) {
-            int j = j0 + lane;
-            bool valid = j < ndec;
-            REnt e;
-            e.req = 0; e.pad = 0; e.finish_step = 0;
-            if (valid) e = rb[j];
+            const int j = j0 + lane;
+            const bool valid = j < ndec;
+            Ent e = r0;
+            if (j0 > 0) { e.v = RSIM_NONE; if (valid) e = rb[j]; }
             __syncwarp();
-            bool fin = valid && e.finish_step == s.step_idx;
-            bool keep = valid && !fin;
-            u32 km = __ballot_sync(FULL, keep);
+            const bool fin = valid && e.v == s.step_idx;
+            const bool keep = valid && !fin;
+            const u32 km = __ballot_sync(FULL, keep);
             if (keep) {
-                rb[w + __popc(km & lanemask_lt())] = e;
-                nf = e.finish_step < nf ? e.finish_step : nf;
+                const int dst = w + __popc(km & lanemask_lt());
+                if (dst != j) rb[dst] = e;
+                nf_step = e.v < nf_step ? e.v : nf_step;
             }
             w += __popc(km);
             u32 fm = __ballot_sync(FULL, fin);
             while (fm) {
-                int l = __ffs(fm) - 1;
+                const int l = __ffs(fm) - 1;
                 fm &= fm - 1;
-                int rq = __shfl_sync(FULL, e.req, l);
-                i64 gone = P.in_tok[rq] + P.out_tok[rq];        // generated == out at finish
-                if (lane == 0) P.finish[rq] = end;
+                const Ent f = shfl_ent(e, l);
+                const i64 gone = f.in + f.out;                     // generated == out at finish
+                if (lane == 0) P.finish[f.req] = end;
                 s.dcs -= gone;
                 s.total -= gone;
-                if (!werr) finish_cache(P, gi, s.occ, rq, end, lane, werr);
+                add_fin(f);
             }
             __syncwarp();
         }
         s.r = w;
-        s.next_finish = warp_min_i64(nf);
+        s.next_finish = warp_min_i64(nf_step);
     }
+    flush_finishers(P, gi, s.occ, F, nf, end, lane, werr);
 
     // popped requests with out > 1 join the running list (after the removals)
     {
-        i64 nf = s.next_finish;
+        i64 nfin = s.next_finish;
         for (int j0 = 0; j0 < npop; j0 += 32) {
-            int j = j0 + lane;
-            bool pop = j < npop;
-            int req = pop ? qb[(head0 + j) & qmask].req : 0;
-            i64 out = pop ? P.out_tok[req] : 0;
-            bool join = pop && out > 1;
-            u32 jm = __ballot_sync(FULL, join);
-            i64 fs = s.step_idx + out - 1;
+            const int j = j0 + lane;
+            const bool pop = j < npop;
+            Ent e = e0;
+            if (j0 > 0 && pop) e = qb[(head0 + j) & qmask];
+            const bool join = pop && e.out > 1;
+            const u32 jm = __ballot_sync(FULL, join);
             if (join) {
-                REnt e;
-                e.req = req; e.pad = 0; e.finish_step = fs;
+                e.v = s.step_idx + e.out - 1;
                 rb[s.r + __popc(jm & lanemask_lt())] = e;
-                nf = fs < nf ? fs : nf;
+                nfin = e.v < nfin ? e.v : nfin;
             }
-            s.dcs += warp_sum(join ? P.in_tok[req] + 1 : (i64)0);
+            s.dcs += warp_sum(join ? e.in + 1 : (i64)0);
             s.r += __popc(jm);
         }
-        s.next_finish = warp_min_i64(nf);
+        s.next_finish = warp_min_i64(nfin);
     }
 
     s.busy_until = end;                                            // engine.py:349-352

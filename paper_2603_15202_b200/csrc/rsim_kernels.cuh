@@ -75,12 +75,53 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ u32 smem_addr(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+// ---- mbarrier + st.async: the cross-CTA partial exchange (no global-memory fence involved)
+__device__ __forceinline__ void mbar_init(u64 *mb, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_addr(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect(u64 *mb, u32 bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1;\n\t}"
+                 :: "r"(smem_addr(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(u64 *mb, u32 parity) {
+    u32 ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_addr(mb)), "r"(parity) : "memory");
+    return ok != 0;
+}
+// 16-byte store into CTA `rank`'s shared memory that completes 16 tx-bytes on its mbarrier
+__device__ __forceinline__ void st_async_16(const void *local_dst, const u64 *local_mb, u32 rank, u64 a, u64 b) {
+    u32 rd, rm;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rd) : "r"(smem_addr(local_dst)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rm) : "r"(smem_addr(local_mb)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.u64 [%0], {%1, %2}, [%3];"
+                 :: "r"(rd), "l"(a), "l"(b), "r"(rm) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void st_cluster_u64(u32 local_addr, u32 rank, u64 v) {
     u32 remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
     asm volatile("st.shared::cluster.u64 [%0], %1;" :: "r"(remote), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_release_sys(u64 *p, u64 v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(u64 *p, u64 v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 ld_acquire_sys(const u64 *p) {
+    u64 v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ u64 ld_relaxed_sys(const u64 *p) {
+    u64 v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ u64 globaltimer() { u64 t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 
 struct __align__(16) Part { u64 minb; u32 cnt; u32 err; };
@@ -104,19 +145,22 @@ __device__ __forceinline__ double score_of(const Params &P, const Inst &s, int h
 }
 
 // enqueue on the winner (InstanceSim.enqueue, engine.py:262-289) + route bookkeeping
-__device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, const u64 kk0[4], i64 in,
-                       int lane, int &werr) {
+__device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, const u64 kk0[4], const int *slot0,
+                       i64 a, int B, i64 in, int out, i64 oa, int lane, int &werr) {
     Table T = table_of(P, gi);
-    warp_touch_pin(T, P.ckeys + P.blk_off[k], kk0, h, t, lane, werr);
+    warp_touch_pin(T, P.ckeys + a, kk0, slot0, h, t, lane, werr);
     Inst s = *sp;
     i64 ht = (i64)h * P.bs; if (ht > in) ht = in;
     i64 pending = in - ht; if (pending < 1) pending = 1;
     if (s.q >= (1 << P.qlog2)) { werr = DEV_E_QUEUE_OVERFLOW; return; }
     if (lane == 0) {
-        QEnt e; e.req = (int)k; e.flags = 0; e.pending = pending;
+        Ent e;
+        e.v = pending; e.in = in; e.a = a; e.oa = oa;
+        e.req = (int)k; e.flags = 0; e.out = out; e.B = B;
+        e.L = B + (int)((out + P.bs - 1) / P.bs); e.hb = h; e.pad0 = 0; e.pad1 = 0;
         P.qbuf[((size_t)gi << P.qlog2) + ((s.q_head + s.q) & ((1 << P.qlog2) - 1))] = e;
         P.hit_blocks[k] = h;
-        P.chosen[k] = gi;
+        P.chosen[k] = P.gbase + gi;
         P.hit_tokens[k] = ht;
         P.route_bs[k] = (i64)s.q + 1 + s.r;
     }
@@ -130,177 +174,360 @@ __device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, c
 
 enum { MODE_REPLAY = 0, MODE_DRAIN = 1, MODE_ROUTE = 2, MODE_ENQUEUE = 3 };
 
+// One decision's request, staged once per CTA in shared memory by the CTA's
+// loader warp, two decisions ahead (slot k % 4).
+struct __align__(16) ReqStage {
+    i64 t, a, in, oa;
+    int B, out;
+    u64 keys[128];
+};
+struct __align__(16) Dec { int owner_warp; int kk; int err; int pad; };
+
+// Per-warp hand-off state between the phases of a decision.
+struct __align__(16) WarpBuf {
+    int slot[2][4][32];    // probe-found table slots of the warp's first two instances (commit reuses them)
+    int hit[32];           // hit blocks of each of the warp's instances
+    FinBuf fin;            // finishers of one engine step
+};
+
+// counter mod T for the 128-bit TieBreaker counter (hi:lo) without a 128-bit
+// division: Horner over 32-bit limbs, each step a 64-by-32 remainder.
+__device__ __forceinline__ u32 mod_counter(u64 lo, u64 hi, u32 T) {
+    u64 r = 0;
+    if (hi) {
+        r = ((u64)(u32)(hi >> 32)) % T;
+        r = ((r << 32) | (u32)hi) % T;
+    }
+    r = ((r << 32) | (u32)(lo >> 32)) % T;
+    r = ((r << 32) | (u32)lo) % T;
+    return (u32)r;
+}
+
+#define RSIM_SLOTS 8            // request staging ring depth (loader runs up to 6 decisions ahead)
+#define RSIM_MAX_WARPS 8
+
+// ---- loader: stage decision k's request (scalars + first 128 chain keys)
+__device__ __noinline__ void stage_request(const Params &P, ReqStage &R, i64 k, int mode, i64 until, int lane) {
+    const i64 a = P.blk_off[k], e = P.blk_off[k + 1];
+    const i64 t = (mode == MODE_REPLAY) ? P.arrival[k] : until;
+    const i64 in = P.in_tok[k], oa = P.ooff[k], out = P.out_tok[k];
+    const int B = (int)(e - a);
+    u64 kk[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) kk[q] = (32 * q + lane < B) ? P.ckeys[a + 32 * q + lane] : 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) if (32 * q + lane < B) R.keys[32 * q + lane] = kk[q];
+    if (lane == 0) { R.t = t; R.a = a; R.in = in; R.oa = oa; R.B = B; R.out = (int)out; }
+}
+
+// ---- drain: advance instances [l0, l0+n) of this warp through steps starting before `until`
+//      (cluster.py:250-273); skip_mask marks instances that must not move yet
+__device__ __noinline__ u64 drain_phase(const Params &P, Inst *st, int base, int l0, int n, i64 until, u32 skip_mask,
+                                        int lane, int &werr, FinBuf &F) {
+    u64 steps = 0;
+    for (int s = 0; s < n; s++) {
+        if ((skip_mask >> s) & 1u) continue;
+        Inst *sp = st + l0 + s;
+        while (!werr && sp->next_step < until) steps += inst_step(P, sp, base + l0 + s, lane, werr, F);
+    }
+    return steps;
+}
+
+// ---- probe + score this warp's instances (cluster.py:106-128, policies.py:117-139).
+// Lane s returns instance s's score bits (~0 = not a candidate); hits go to WB.hit.
+__device__ __noinline__ u64 probe_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
+                                        int mode, int target, int lane, WarpBuf &WB, u64 &c_bytes) {
+    const i64 t = R.t, in = R.in;
+    const int B = R.B;
+    u64 kk0[4];
+    u32 hm[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        kk0[q] = (32 * q + lane < B) ? R.keys[32 * q + lane] : 0;
+        hm[q] = tab_home(kk0[q], P.slog2);
+    }
+    u64 mybits = ~0ULL;
+    for (int s0 = 0; s0 < n; s0 += 2) {
+        const int ns = min(2, n - s0);
+        Table T2[2];
+        bool cand[2];
+        int hh[2] = {0, 0};
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            const int gi = base + l0 + s0 + q;
+            cand[q] = q < ns && ((mode != MODE_ENQUEUE) || gi == target);
+            T2[q] = table_of(P, q < ns ? gi : base + l0 + s0);
+        }
+        int sl[2][4];
+        u32 m[2][4];
+        if (cand[0] && cand[1]) {
+            probe128<2>(T2, kk0, hm, B, lane, m, sl);
+            hh[0] = lead_hits(m[0]);
+            hh[1] = lead_hits(m[1]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                u32 mq[1][4];
+                int sq[1][4];
+                sq[0][0] = sq[0][1] = sq[0][2] = sq[0][3] = -1;
+                if (cand[q]) {
+                    probe128<1>(&T2[q], kk0, hm, B, lane, mq, sq);
+                    hh[q] = lead_hits(mq[0]);
+                }
+#pragma unroll
+                for (int kq = 0; kq < 4; kq++) sl[q][kq] = sq[0][kq];
+            }
+        }
+        if (s0 == 0) {
+#pragma unroll
+            for (int q = 0; q < 2; q++)
+#pragma unroll
+                for (int kq = 0; kq < 4; kq++) WB.slot[q][kq][lane] = sl[q][kq];
+        }
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            if (!cand[q]) continue;
+            if (hh[q] >= 128) hh[q] = B <= 128 ? B : deep_match(T2[q], P.ckeys + R.a, B, lane);
+            else hh[q] = min(hh[q], B);
+            Inst *sp = st + l0 + s0 + q;
+            if (sp->due <= t) {          // snapshot() flushes every candidate (indicators.py:36-65)
+                __syncwarp();
+                if (lane == 0) flush_view(*sp, t);
+                __syncwarp();
+            }
+            const double sc = score_of(P, *sp, hh[q], in);
+            if (lane == 0) {
+                WB.hit[s0 + q] = hh[q];
+                if (P.scores != nullptr) P.scores[base + l0 + s0 + q] = sc;
+            }
+            // one 8-B key compare per reference dict lookup + 16 B of view
+            c_bytes += 8ULL * (u64)min(hh[q] + 1, B) + 16ULL;
+            if (lane == s0 + q) mybits = (u64)__double_as_longlong(sc);
+        }
+    }
+    __syncwarp();
+    return mybits;
+}
+
+// ---- the argmin with the rotating tie-break (policies.py:160-165, 92-101), by warp 0 of
+// every CTA from all C*W partials; for world > 1 one more level across ranks through
+// peer-mapped mailboxes. Writes the owner warp (or -1) and its local tie index to dec.
+__device__ __noinline__ void decide_phase(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
+                                          Dec &dec, u64 &ctr_lo, u64 &ctr_hi, int lane) {
+    // lane-major: lane holds flat partials [8*lane, 8*lane+8) (ascending instance id order)
+    u64 pm[8];
+    u32 pc[8];
+    u64 mn = ~0ULL;
+    u32 er = 0;
+    const Part *pp = part + par * CW;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const int idx = lane * 8 + j;
+        pm[j] = ~0ULL; pc[j] = 0;
+        if (idx < CW) { const Part q = pp[idx]; pm[j] = q.minb; pc[j] = q.cnt; er |= q.err; mn = min(mn, q.minb); }
+    }
+    // 64-bit min with two 32-bit redux ops
+    const u32 hmin = __reduce_min_sync(FULL, (u32)(mn >> 32));
+    const u32 lmin = __reduce_min_sync(FULL, (u32)(mn >> 32) == hmin ? (u32)mn : 0xffffffffu);
+    const u64 gmin = ((u64)hmin << 32) | lmin;
+    er = __reduce_or_sync(FULL, er);
+    u32 lc = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) { pc[j] = pm[j] == gmin ? pc[j] : 0u; lc += pc[j]; }
+    const u32 T = __reduce_add_sync(FULL, lc);
+    Dec d; d.owner_warp = -1; d.kk = 0; d.err = (int)er; d.pad = 0;
+    u32 kk = 0;
+    bool mine = true;
+    u32 Tg = T;
+    if (P.world > 1) {          // ---- one (min, tie count) partial per rank over peer-mapped mailboxes
+        const u64 seq = (P.epoch << 40) | (u64)(k + 1);
+        if (cta == 0 && lane < P.world) {
+            u64 *slot = P.peer[lane] + (size_t)((par * 8 + P.rank) * 4);
+            st_relaxed_sys(slot + 0, gmin);
+            st_relaxed_sys(slot + 1, ((u64)er << 32) | T);
+            st_release_sys(slot + 2, seq);
+        }
+        u64 rmin = ~0ULL;
+        u32 rT = 0, rer = 0;
+        if (lane < P.world) {
+            const u64 *slot = P.mbox + (size_t)((par * 8 + lane) * 4);
+            const u64 t0 = globaltimer();
+            while (ld_acquire_sys(slot + 2) != seq) {
+                if ((i64)(globaltimer() - t0) > P.timeout_ns) { rer = DEV_E_COMM; break; }
+            }
+            if (!rer) {
+                rmin = ld_relaxed_sys(slot + 0);
+                const u64 ce = ld_relaxed_sys(slot + 1);
+                rT = (u32)ce; rer = (u32)(ce >> 32);
+            }
+        }
+        const u64 xmin = warp_min_u64(rmin);
+        const u32 xer = __reduce_or_sync(FULL, rer);
+        const u32 cr = (lane < P.world && rmin == xmin) ? rT : 0u;
+        Tg = __reduce_add_sync(FULL, cr);
+        const u32 incl = warp_incl_scan(cr, lane);
+        d.err = (int)xer;
+        if (!xer && Tg > 0) {
+            if (Tg > 1) { kk = mod_counter(ctr_lo, ctr_hi, Tg); ctr_lo += 1; ctr_hi += (ctr_lo == 0); }
+            const u32 ge = __ballot_sync(FULL, lane < P.world && incl > kk && cr > 0);
+            const int owner_rank = __ffs(ge) - 1;
+            const u32 bef = owner_rank > 0 ? __shfl_sync(FULL, incl, owner_rank - 1) : 0u;
+            mine = owner_rank == P.rank;
+            kk -= bef;                            // this rank's local tie index if it owns
+        }
+    } else if (!d.err && T > 1) {                 // TieBreaker.pick: tied[counter % len]; counter += 1
+        kk = mod_counter(ctr_lo, ctr_hi, T);
+        ctr_lo += 1; ctr_hi += (ctr_lo == 0);
+    }
+    if (!d.err && Tg == 0) d.err = 11;            // NoInstancesError
+    if (!d.err && mine) {
+        const u32 incl = warp_incl_scan(lc, lane);
+        const u32 ge = __ballot_sync(FULL, lc > 0 && incl > kk && incl - lc <= kk);
+        const int L = __ffs(ge) - 1;
+        int owner = -1;
+        u32 okk = 0;
+        if (lane == L) {
+            u32 c = incl - lc;
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (owner < 0 && pc[j] > 0) {
+                    if (kk < c + pc[j]) { owner = lane * 8 + j; okk = kk - c; }
+                    c += pc[j];
+                }
+        }
+        owner = __shfl_sync(FULL, owner, L);
+        okk = __shfl_sync(FULL, okk, L);
+        if (owner / W == cta) { d.owner_warp = owner % W; d.kk = (int)okk; }
+    }
+    if (lane == 0) dec = d;
+}
+
+__device__ __forceinline__ void bar_warps(int nthreads) {       // named barrier 1: the instance warps only
+    asm volatile("bar.sync 1, %0;" :: "r"(nthreads) : "memory");
+}
+
 // ---------------------------------------------------------------- replay
 // Persistent launch over a cluster of C CTAs (C <= 16, one instance shard per
-// CTA, engine state in shared memory). Per decision: every warp drains and
-// probes its own instances, warp partials meet in shared memory, CTA
-// partials are pushed to every CTA of the cluster over DSMEM, one hardware
-// cluster barrier, then every CTA derives the same global winner and the
-// owning warp commits. No host round trip per decision.
-#define RSIM_MAX_WARPS 16
-__global__ void __launch_bounds__(32 * RSIM_MAX_WARPS, 1)
+// CTA, engine state in shared memory, warps 0..W-1 own ipw instances each).
+// Warp W of every CTA is a decoupled request loader: it stages requests into a
+// shared-memory ring up to RSIM_SLOTS-1 decisions ahead and never joins the
+// decision barriers. Per decision: every instance warp drains and probes its
+// instances and pushes one (min score, tie count) partial into every CTA of
+// the cluster with st.async (completing tx-bytes on the receiver's mbarrier);
+// non-candidate instances are drained to the next arrival while the partials
+// are in flight; warp 0 of every CTA derives the same winner; one named
+// barrier releases the owning warp, which commits. No host round trip.
+__global__ void __launch_bounds__(32 * (RSIM_MAX_WARPS + 1), 1)
 replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int C = P.C, W = P.W, ipw = P.ipw;
+    const int C = P.C, W = P.W, ipw = P.ipw, CW = P.C * P.W;
     const int cta = (C > 1) ? (int)cluster_ctarank() : 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool loader = warp == W;
     const int base = cta * P.per_cta;
     const int nloc = max(0, min(P.per_cta, P.N - base));
     Inst *st = (Inst *)smem;
-    Part *wp = (Part *)(st + P.per_cta);      // [2][W]
-    Part *cp = wp + 2 * W;                    // [2][C]
+    Part *part = (Part *)(st + P.per_cta);                 // [2][C*W], flat index cta*W + warp
+    ReqStage *rq = (ReqStage *)(part + 2 * CW);            // [RSIM_SLOTS] request ring (k % RSIM_SLOTS)
+    Dec *dec = (Dec *)(rq + RSIM_SLOTS);                   // [2]
+    u64 *mb = (u64 *)(dec + 2);                            // [2] partial-exchange mbarriers
+    volatile i64 *ctl = (volatile i64 *)(mb + 2);          // [0] staged_upto [1] freed_upto [2] abort
+    WarpBuf *wbuf = (WarpBuf *)(mb + 6);                   // [W]
+    WarpBuf &WB = wbuf[loader ? 0 : warp];
 
-    // load this CTA's instance shard
-    {
+    {   // load this CTA's instance shard
         const u64 *src = (const u64 *)(P.inst + base);
         u64 *dst = (u64 *)st;
         const int words = nloc * (int)(sizeof(Inst) / 8);
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     }
-    unsigned __int128 counter = ((unsigned __int128)P.tie[1] << 64) | P.tie[0];
+    u64 ctr_lo = P.tie[0], ctr_hi = P.tie[1];              // evolved by warp 0 only
+    const int l0 = warp * ipw;
+    const int nmine = loader ? 0 : max(0, min(ipw, nloc - l0));
+    int werr = 0;
+    u64 c_bytes = 0, c_steps = 0;   // algorithmic probe bytes / engine steps of this warp
+    if (threadIdx.x == 0) {
+        mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_fence_init();
+        ctl[0] = k0; ctl[1] = k0; ctl[2] = 0;
+    }
+    u32 mb_phase[2] = {0u, 0u};                            // tracked by warp 0
     __syncthreads();
     if (C > 1) cluster_sync_all();
 
-    const int l0 = warp * ipw;
-    const int nmine = max(0, min(ipw, nloc - l0));
-    int werr = 0;
-    u64 c_bytes = 0, c_steps = 0;   // algorithmic probe bytes / engine steps of this warp
-
     if (mode == MODE_DRAIN) {
-        for (int s = 0; s < nmine; s++) {
-            Inst *sp = st + l0 + s;
-            while (!werr && sp->next_step < until) c_steps += inst_step(P, sp, base + l0 + s, lane, werr);
+        if (!loader) c_steps += drain_phase(P, st, base, l0, nmine, until, 0u, lane, werr, WB.fin);
+    } else if (loader) {
+        // ---- decoupled loader: keep the ring filled ahead of the decisions
+        i64 kk = k0;
+        while (kk < k1 && ctl[2] == 0) {
+            const i64 lim = min(k1, ctl[1] + RSIM_SLOTS);  // slot of decision j is reused once j-SLOTS is freed
+            if (kk >= lim) { __nanosleep(64); continue; }
+            stage_request(P, rq[kk % RSIM_SLOTS], kk, mode, until, lane);
+            __threadfence_block();
+            __syncwarp();
+            kk += 1;
+            if (lane == 0) ctl[0] = kk;
         }
     } else {
         for (i64 k = k0; k < k1; k++) {
             const int par = (int)(k & 1);
-            const i64 t = (mode == MODE_REPLAY) ? P.arrival[k] : until;
-            // ---- K4: advance my instances through steps starting before t (cluster.py:250-273)
-            if (mode == MODE_REPLAY) {
-                for (int s = 0; s < nmine; s++) {
-                    Inst *sp = st + l0 + s;
-                    while (!werr && sp->next_step < t) c_steps += inst_step(P, sp, base + l0 + s, lane, werr);
-                }
-            }
-            // ---- K2: flush views, probe, score (cluster.py:106-128, policies.py:117-139)
-            const i64 a = P.blk_off[k];
-            const int B = (int)(P.blk_off[k + 1] - a);
-            const i64 in = P.in_tok[k];
-            const u64 *keys = P.ckeys + a;
-            u64 kk0[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) kk0[q] = (32 * q + lane < B) ? keys[32 * q + lane] : 0;
-            u64 mybits = ~0ULL;
-            int myh = 0;
-            for (int s0 = 0; s0 < nmine; s0 += 2) {
-                const int ns = min(2, nmine - s0);
-                Table T2[2];
-                bool cand[2];
-                int hh[2] = {0, 0};
-#pragma unroll
-                for (int q = 0; q < 2; q++) {
-                    const int gi = base + l0 + s0 + q;
-                    cand[q] = q < ns && ((mode != MODE_ENQUEUE) || gi == target);
-                    T2[q] = table_of(P, q < ns ? gi : base + l0 + s0);
-                }
-                if (cand[0] && cand[1]) {
-                    u32 m[2][4];
-                    probe128<2>(T2, kk0, B, lane, m);
-                    hh[0] = lead_hits(m[0]);
-                    hh[1] = lead_hits(m[1]);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 2; q++) if (cand[q]) {
-                        u32 m[1][4];
-                        probe128<1>(&T2[q], kk0, B, lane, m);
-                        hh[q] = lead_hits(m[0]);
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 2; q++) {
-                    if (!cand[q]) continue;
-                    if (hh[q] >= 128) hh[q] = B <= 128 ? B : deep_match(T2[q], keys, B, lane);
-                    else hh[q] = min(hh[q], B);
-                    Inst *sp = st + l0 + s0 + q;
-                    const int gi = base + l0 + s0 + q;
-                    if (sp->due <= t) {      // snapshot() flushes every candidate (indicators.py:36-65)
-                        __syncwarp();
-                        if (lane == 0) flush_view(*sp, t);
-                        __syncwarp();
-                    }
-                    const double sc = score_of(P, *sp, hh[q], in);
-                    if (P.scores != nullptr && lane == 0) P.scores[gi] = sc;
-                    // one 8-B key compare per reference dict lookup + 16 B of view
-                    c_bytes += 8ULL * (u64)min(hh[q] + 1, B) + 16ULL;
-                    if (lane == s0 + q) { mybits = (u64)__double_as_longlong(sc); myh = hh[q]; }
-                }
-            }
-            if (cta == 0 && warp == 0) c_bytes += 8ULL * (u64)B;   // request chain keys, read once
+            while (ctl[0] <= k) { }                         // request k staged (normally long done)
+            __threadfence_block();
+            const ReqStage &R = rq[k % RSIM_SLOTS];
+            // ---- K4: advance my instances through steps starting before t
+            if (mode == MODE_REPLAY) c_steps += drain_phase(P, st, base, l0, nmine, R.t, 0u, lane, werr, WB.fin);
+            // ---- K2: probe + score
+            const u64 mybits = probe_phase(P, st, base, l0, nmine, R, mode, target, lane, WB, c_bytes);
+            if (cta == 0 && warp == 0) c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once
             const u64 wmin = warp_min_u64(mybits);
             const u32 tmask = __ballot_sync(FULL, lane < nmine && mybits == wmin && wmin != ~0ULL);
-            if (lane == 0) { Part q; q.minb = wmin; q.cnt = __popc(tmask); q.err = (u32)werr; wp[par * W + warp] = q; }
-            __syncthreads();
-            // ---- argmin with the rotating tie-break (policies.py:160-165, 92-101)
-            u64 gmin; u32 T; u32 gerr; u32 cincl = 0;
-            if (C == 1) {
-                Part q; q.minb = ~0ULL; q.cnt = 0; q.err = 0;
-                if (lane < W) q = wp[par * W + lane];
-                gmin = warp_min_u64(q.minb);
-                T = warp_sum(q.minb == gmin ? q.cnt : 0u);
-                gerr = __reduce_or_sync(FULL, q.err);
-            } else {
-                if (warp == 0) {
-                    Part q; q.minb = ~0ULL; q.cnt = 0; q.err = 0;
-                    if (lane < W) q = wp[par * W + lane];
-                    const u64 cmin = warp_min_u64(q.minb);
-                    const u32 cc = warp_sum(q.minb == cmin ? q.cnt : 0u);
-                    const u32 ce = __reduce_or_sync(FULL, q.err);
-                    if (lane < C) {   // push this CTA's partial into every CTA of the cluster (DSMEM)
-                        Part *dst = cp + par * C + cta;
-                        st_cluster_u64(smem_addr(&dst->minb), (u32)lane, cmin);
-                        st_cluster_u64(smem_addr(&dst->cnt), (u32)lane, ((u64)ce << 32) | cc);
-                    }
+            werr = __reduce_max_sync(FULL, werr);
+            {   // publish this warp's partial to every CTA of the cluster
+                const u64 w1 = ((u64)(u32)werr << 32) | (u32)__popc(tmask);
+                Part *dst = part + par * CW + cta * W + warp;
+                if (C == 1) {
+                    if (lane == 0) { Part q; q.minb = wmin; q.cnt = (u32)w1; q.err = (u32)(w1 >> 32); *dst = q; }
+                } else if (lane < C) {
+                    st_async_16(dst, &mb[par], (u32)lane, wmin, w1);
                 }
-                cluster_sync_all();
-                Part q; q.minb = ~0ULL; q.cnt = 0; q.err = 0;
-                if (lane < C) q = cp[par * C + lane];
-                gmin = warp_min_u64(q.minb);
-                const u32 c = (lane < C && q.minb == gmin) ? q.cnt : 0u;
-                T = warp_sum(c);
-                gerr = __reduce_or_sync(FULL, q.err);
-                cincl = warp_incl_scan(c, lane);
             }
-            if (gerr) { if (werr == 0) werr = (int)gerr; break; }
-            if (T == 0) { werr = 11; break; }                       // NoInstancesError
-            u32 kk = 0;
-            if (T > 1) {                                            // TieBreaker.pick: tied[counter % len]; counter += 1
-                kk = (u32)(counter % (unsigned __int128)T);
-                counter += 1;
+            if (C == 1) bar_warps(32 * W);
+            // instances that cannot win this decision advance to the next arrival meanwhile
+            if (mode == MODE_REPLAY && k + 1 < k1 && ctl[0] > k + 1) {
+                __threadfence_block();
+                u32 skip = 0;
+                for (int s = 0; s < nmine; s++)
+                    if (__shfl_sync(FULL, mybits, s) == wmin) skip |= 1u << s;
+                c_steps += drain_phase(P, st, base, l0, nmine, rq[(k + 1) % RSIM_SLOTS].t, skip, lane, werr, WB.fin);
             }
-            int owner_cta = 0;
-            u32 kk_local = kk;
-            if (C > 1) {                                            // ascending id order = CTA-major
-                const u32 ge = __ballot_sync(FULL, lane < C && cincl > kk);
-                owner_cta = __ffs(ge) - 1;
-                const u32 before = owner_cta > 0 ? __shfl_sync(FULL, cincl, owner_cta - 1) : 0u;
-                kk_local = kk - before;
-            }
-            if (owner_cta == cta) {
-                // locate the warp inside this CTA (ascending instance id = warp-major, lane-minor)
-                Part q; q.minb = ~0ULL; q.cnt = 0; q.err = 0;
-                if (lane < W) q = wp[par * W + lane];
-                const u32 c = q.minb == gmin ? q.cnt : 0u;
-                const u32 incl = warp_incl_scan(c, lane);
-                const u32 ge = __ballot_sync(FULL, lane < W && incl > kk_local);
-                const int ow = __ffs(ge) - 1;
-                if (warp == ow) {
-                    const u32 before = ow > 0 ? __shfl_sync(FULL, incl, ow - 1) : 0u;
-                    const int s = nth_set_bit(tmask, (int)(kk_local - before));
-                    const int h = __shfl_sync(FULL, myh, s);
-                    const int gi = base + l0 + s;
-                    commit(P, st + l0 + s, gi, k, h, t, kk0, in, lane, werr);
-                    if (P.dec_ns != nullptr && lane == 0) P.dec_ns[k] = (i64)globaltimer();
+            if (warp == 0) {
+                if (C > 1) {            // all C*W partials of decision k have landed in this CTA
+                    if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * 16));
+                    while (!mbar_try_wait(&mb[par], mb_phase[par])) { }
+                    mb_phase[par] ^= 1u;
                 }
+                decide_phase(P, part, CW, W, cta, k, par, dec[par], ctr_lo, ctr_hi, lane);
+            }
+            bar_warps(32 * W);
+            if (warp == 0 && lane == 0) ctl[1] = k;         // decision k-1's slot is free again
+            const Dec d = dec[par];
+            if (d.err) {
+                if (werr == 0) werr = d.err;
+                if (warp == 0 && lane == 0) ctl[2] = 1;     // release the loader
+                break;
+            }
+            if (warp == d.owner_warp) {
+                const int s = nth_set_bit(tmask, d.kk);
+                const int h = WB.hit[s];
+                u64 kk0[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) kk0[q] = (32 * q + lane < R.B) ? R.keys[32 * q + lane] : 0;
+                int cs[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) cs[q] = s < 2 ? WB.slot[s][q][lane] : -1;
+                commit(P, st + l0 + s, base + l0 + s, k, h, R.t, kk0, s < 2 ? cs : nullptr, R.a, R.B, R.in, R.out,
+                       R.oa, lane, werr);
+                if (P.dec_ns != nullptr && lane == 0) P.dec_ns[k] = (i64)globaltimer();
             }
         }
     }
@@ -318,8 +545,8 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
         if (c_steps) atomicAdd(P.ctr + 1, c_steps);
     }
     if (cta == 0 && threadIdx.x == 0 && mode != MODE_DRAIN) {
-        P.tie[0] = (u64)counter;
-        P.tie[1] = (u64)(counter >> 64);
+        P.tie[0] = ctr_lo;
+        P.tie[1] = ctr_hi;
     }
     if (C > 1) cluster_sync_all();
 }

@@ -17,12 +17,22 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
 shapes = [(int(sys.argv[3]), int(sys.argv[4]))] if len(sys.argv) > 4 else [(0, 0)]
 if len(sys.argv) > 3 and sys.argv[3] == "sweep":
     shapes = [(c, w) for c in (1, 2, 4, 8, 16) for w in (4, 8, 16)]
-trace, cfg = bench.build_workload(name)
+burst = name.endswith("-burst")            # all arrivals at t=0: no engine steps, pure route cost
+trace, cfg = bench.build_workload(name.replace("-burst", ""))
 trace = trace.slice(min(n, len(trace)))
+if burst:
+    import numpy as np
+    from paper_2603_15202_b200.trace import PackedTrace
+    trace = PackedTrace(trace.request_id, np.zeros_like(trace.arrival_s), trace.in_tokens, trace.out_tokens,
+                        trace.class_key, trace.blk_off, trace.blocks)
 for c, w in shapes:
     if c and c > cfg.n_instances:
         continue
-    h = _native.Handle(native_config(cfg, sizing_for(trace, cfg), ctas=c, warps_per_cta=w))
+    try:
+        h = _native.Handle(native_config(cfg, sizing_for(trace, cfg), ctas=c, warps_per_cta=w))
+    except ValueError as exc:
+        print(f"{name} ctas={c} warps={w}: skipped ({exc})")
+        continue
     h.load(trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.request_id, trace.blk_off, trace.blocks)
     h.rerun()
     best = min(h.rerun() for _ in range(3))
