@@ -140,10 +140,12 @@ rsim_status rsim_read_decision_ns(rsim_t *h, int64_t first, int64_t count, int64
  * loaded trace, replay every decision and drain to idle; *device_ms = CUDA-event
  * time of the whole sequence on the handle's stream. Equals reset+K1+replay+drain. */
 rsim_status rsim_rerun(rsim_t *h, double *device_ms);
-/* Counters of the last replay: [0] algorithmic probe bytes (8*B per decision
- * + sum_i 8*min(h_i+1,B) + 16 per instance probed), [1] engine steps, [2] evictions,
- * [3] reserved, [4] requests loaded, [5] blocks, [6] output keys, [7] instances. */
-rsim_status rsim_read_counters(rsim_t *h, int64_t *out8);
+/* Counters of the last replay (16 int64): [0] algorithmic probe bytes (8*B per
+ * decision + sum_i 8*min(h_i+1,B) + 16 per instance probed), [1] engine steps, [2] evictions,
+ * [3] reserved, [4] requests loaded, [5] blocks, [6] output keys, [7] local instances,
+ * [8..15] SM cycles of CTA 0 / warp 0 per decision phase: staging wait, drain, probe,
+ * publish + speculative drain, exchange wait, decide, barrier, commit. */
+rsim_status rsim_read_counters(rsim_t *h, int64_t *out16);
 /* Sharded replay plumbing. The mailbox is device memory peers write into. */
 rsim_status rsim_shard_bounds(const rsim_t *h, int32_t *lo, int32_t *hi);
 rsim_status rsim_mailbox(rsim_t *h, void **dev_ptr);

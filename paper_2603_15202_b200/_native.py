@@ -264,7 +264,7 @@ class Handle:
         return ms.value
 
     def counters(self) -> np.ndarray:
-        out = np.zeros(8, np.int64)
+        out = np.zeros(16, np.int64)
         self._ck(self._L.rsim_read_counters(self._h, _p(out)))
         return out
 

@@ -166,7 +166,7 @@ static rsim_status init_state(rsim_t *h) {
     CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaMemsetAsync(h->errbuf, 0, 4 * sizeof(int), h->stream));
     CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), h->stream));
-    CK(h, cudaMemsetAsync(h->ctr, 0, 8 * sizeof(u64), h->stream));
+    CK(h, cudaMemsetAsync(h->ctr, 0, 16 * sizeof(u64), h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     h->R = 0; h->nblk = 0; h->nout = 0;
     // blk_off / ooff hold a leading 0
@@ -235,7 +235,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
     if (C * W > 256) { delete h; return fail(nullptr, RSIM_E_INVALID, "cluster too large"); }
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
-    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(2 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 6 * sizeof(u64) + (size_t)W * sizeof(WarpBuf);
+    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(2 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 6 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf);
     if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
     cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
     if (C > 8) cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -262,7 +262,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaMalloc(&h->log_n, sizeof(u64)));
     CK(nullptr, cudaMalloc(&h->scores, N * sizeof(double)));
     CK(nullptr, cudaMalloc(&h->scratch_res, 4 * sizeof(i64)));
-    CK(nullptr, cudaMalloc(&h->ctr, 8 * sizeof(u64)));
+    CK(nullptr, cudaMalloc(&h->ctr, 16 * sizeof(u64)));
     CK(nullptr, cudaMalloc(&h->mbox, 2 * 8 * 4 * sizeof(u64)));
     CK(nullptr, cudaMemset(h->mbox, 0, 2 * 8 * 4 * sizeof(u64)));
     h->peer[world > 1 ? c.rank : 0] = h->mbox;
@@ -615,7 +615,7 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
     CK(h, cudaMemsetAsync(h->tmeta, 0, slots * sizeof(Meta), s));
     CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, s));
     CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), s));
-    CK(h, cudaMemsetAsync(h->ctr, 0, 8 * sizeof(u64), s));
+    CK(h, cudaMemsetAsync(h->ctr, 0, 16 * sizeof(u64), s));
     if (h->R > 0) {
         DevArr<i64> *outs[] = {&h->hit_tokens, &h->first_sched, &h->first_token, &h->finish, &h->route_bs, &h->dec_ns};
         for (auto *a : outs) CK(h, cudaMemsetAsync(a->p, 0xff, h->R * sizeof(i64), s));
@@ -639,13 +639,13 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
     return st;
 }
 
-rsim_status rsim_read_counters(rsim_t *h, int64_t *out8) {
-    if (!h || !out8) return RSIM_E_INVALID;
+rsim_status rsim_read_counters(rsim_t *h, int64_t *out16) {
+    if (!h || !out16) return RSIM_E_INVALID;
     CK(h, cudaSetDevice(h->cfg.device));
-    u64 c[8];
+    u64 c[16];
     CK(h, cudaMemcpy(c, h->ctr, sizeof(c), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 8; i++) out8[i] = (int64_t)c[i];
-    out8[4] = h->R; out8[5] = h->nblk; out8[6] = h->nout; out8[7] = h->N;
+    for (int i = 0; i < 16; i++) out16[i] = (int64_t)c[i];
+    out16[4] = h->R; out16[5] = h->nblk; out16[6] = h->nout; out16[7] = h->N;
     return RSIM_OK;
 }
 

@@ -13,10 +13,12 @@
 //  * a warp handles 128 chain depths per round, 4 per lane, all loads in flight;
 //  * linear probing reads an aligned 16-byte slot pair per load (tables run at
 //    <= 3/4 load, usually far below, so the home pair nearly always decides);
-//  * slot claims use atomicCAS (duplicate keys and racing lanes resolve in L2);
-//  * touch / pin / unpin are fire-and-forget atomics (RED): max and +/- are
-//    commutative, so no read-modify-write round trip is needed;
-//  * table loads use ld.global.cg, so a lane never reads a stale L1 line.
+//  * an instance's table is written only by its owning warp (one SM) during a
+//    launch, so key probes are L1-cached (ld.global.ca) and slot claims are
+//    plain stores arbitrated among the warp's own lanes (__match_any_sync);
+//  * touch / pin / unpin are fire-and-forget atomics (RED) on the metadata:
+//    max and +/- are commutative, so no read-modify-write round trip is
+//    needed; metadata is only ever read through L2 (ld.global.cg).
 #pragma once
 #include "rsim_device.cuh"
 
@@ -35,7 +37,7 @@ __device__ __forceinline__ Table table_of(const Params &P, int gi) {
 }
 
 __device__ __forceinline__ ulonglong2 ld_pair(const Table &T, u32 i) {
-    return __ldcg(reinterpret_cast<const ulonglong2 *>(T.k) + (i >> 1));
+    return __ldca(reinterpret_cast<const ulonglong2 *>(T.k) + (i >> 1));
 }
 
 // Evaluate one aligned pair starting the probe at slot i.
@@ -104,36 +106,52 @@ __device__ __forceinline__ void find128(const Table &T, const u64 kk[4], const b
 
 // Hit masks for the first 128 depths of NI instances at once (loads of all
 // instances in flight together). m[s][k] bit lane = depth 32k+lane present.
+// Branch-free evaluation of a key's first aligned pair (linear probing from
+// slot i): f = found in the pair, c = pair full of other keys (probe goes on).
+__device__ __forceinline__ void eval_first(const Table &T, ulonglong2 pr, u32 i, u64 key, bool &f, bool &c) {
+    const bool ev = (i & 1u) == 0;
+    const bool xk = ev && pr.x == key, xe = ev && pr.x == T.empty;
+    f = xk || (!xe && pr.y == key);
+    c = !xk && !xe && pr.y != key && pr.y != T.empty;
+}
+
 template <int NI>
 __device__ __forceinline__ void probe128(const Table *T, const u64 kk[4], const u32 hm[4], int B, int lane,
                                          u32 m[NI][4], int slot[NI][4]) {
     ulonglong2 pr[NI][4];
+    const int nk = (B + 31) >> 5;                       // warp-uniform: depth slots in use
 #pragma unroll
     for (int s = 0; s < NI; s++)
 #pragma unroll
         for (int k = 0; k < 4; k++)
-            if (32 * k + lane < B) pr[s][k] = ld_pair(T[s], hm[k]);
+            if (k < nk && 32 * k + lane < B) pr[s][k] = ld_pair(T[s], hm[k]);
 #pragma unroll
     for (int s = 0; s < NI; s++)
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            bool f = false;
             slot[s][k] = -1;
-            if (32 * k + lane < B) {
-                int st;
-                u32 r = eval_pair(T[s], pr[s][k], hm[k], kk[k], st);
-                if (st == 2) r = probe_rest(T[s], r, kk[k], st);
-                f = st == 0;
-                if (f) slot[s][k] = (int)r;
+            m[s][k] = 0;
+            if (k < nk) {
+                bool f = false, c = false;
+                if (32 * k + lane < B) eval_first(T[s], pr[s][k], hm[k], kk[k], f, c);
+                if (__any_sync(FULL, c) && c) {     // rare: the home pair is full of other keys
+                    int st;
+                    const u32 r = probe_rest(T[s], (hm[k] | 1u) + 1u & T[s].mask, kk[k], st);
+                    f = st == 0;
+                    if (f) slot[s][k] = (int)r;
+                } else if (f) {
+                    slot[s][k] = (int)((hm[k] & 1u) == 0 && pr[s][k].x == kk[k] ? hm[k] : hm[k] | 1u);
+                }
+                m[s][k] = __ballot_sync(FULL, f);
             }
-            m[s][k] = __ballot_sync(FULL, f);
         }
 }
 
-__device__ __forceinline__ int lead_hits(const u32 m[4]) {
-#pragma unroll
-    for (int k = 0; k < 4; k++)
-        if (m[k] != FULL) return 32 * k + __ffs(~m[k]) - 1;
+__device__ __forceinline__ int lead_hits(const u32 m[4]) {   // leading present depths
+    if (m[0] != FULL) return __ffs(~m[0]) - 1;
+    if (m[1] != FULL) return 32 + __ffs(~m[1]) - 1;
+    if (m[2] != FULL) return 64 + __ffs(~m[2]) - 1;
+    if (m[3] != FULL) return 96 + __ffs(~m[3]) - 1;
     return 128;
 }
 
@@ -228,6 +246,35 @@ __device__ void warp_touch_pin(const Table &T, const u64 *keys, const u64 kk0[4]
     werr = __reduce_max_sync(FULL, werr);
 }
 
+// Claim slots for the absent keys of a 128-key batch with plain stores. One
+// k-slot at a time, every claimant re-probes from its key's home (L1), so a
+// duplicate key already inserted or a slot taken by an earlier claim is seen;
+// lanes aiming at the same EMPTY slot are arbitrated with __match_any_sync.
+__device__ __forceinline__ void claim128(const Table &T, const u64 kk[4], const bool need[4], int slot[4],
+                                         bool created[4], int lane) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        bool pend = need[k];
+        while (__ballot_sync(FULL, pend)) {
+            u32 pos = 0;
+            if (pend) {
+                int st;
+                const u32 i = tab_home(kk[k], T.slog2);
+                u32 r = eval_pair(T, ld_pair(T, i), i, kk[k], st);
+                if (st == 2) r = probe_rest(T, r, kk[k], st);
+                if (st == 0) { slot[k] = (int)r; pend = false; }
+                else pos = r;
+            }
+            const u32 cm = __ballot_sync(FULL, pend);
+            if (pend) {
+                const u32 peers = __match_any_sync(cm, pos);
+                if (__ffs(peers) - 1 == lane) { T.k[pos] = kk[k]; slot[k] = (int)pos; created[k] = true; pend = false; }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // Fused _finish cache work (engine.py:357-361): unpin keys[:hb], then insert
 // the full chain (prefix keys pk[0..B) then output keys ok[0..L-B)) at `now`.
 // Returns the number of created entries.
@@ -246,23 +293,10 @@ __device__ int warp_unpin_insert(const Table &T, const u64 *pk, int B, const u64
         int slot[4];
         u32 fp[4];
         find128(T, kk, act, slot, fp);
-        bool created[4];
+        bool created[4], need[4];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            created[k] = false;
-            if (!act[k] || slot[k] >= 0) continue;
-            // claim the first EMPTY slot; a lost race continues the probe
-            u32 i = fp[k];
-            for (;;) {
-                u64 old = atomicCAS(T.k + i, T.empty, kk[k]);
-                if (old == T.empty) { slot[k] = (int)i; created[k] = true; break; }
-                if (old == kk[k]) { slot[k] = (int)i; break; }
-                int st;
-                u32 r = probe_rest(T, (i + 1) & T.mask, kk[k], st);
-                if (st == 0) { slot[k] = (int)r; break; }
-                i = r;
-            }
-        }
+        for (int k = 0; k < 4; k++) { created[k] = false; need[k] = act[k] && slot[k] < 0; }
+        claim128(T, kk, need, slot, created, lane);
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             if (!act[k]) continue;
@@ -318,22 +352,10 @@ __device__ int warp_finish_many(const Table &T, const u64 *ckeys, const u64 *oke
         int slot[4];
         u32 fp[4];
         find128(T, kk, act, slot, fp);
-        bool created[4];
+        bool created[4], need[4];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            created[k] = false;
-            if (!act[k] || slot[k] >= 0) continue;
-            u32 i = fp[k];
-            for (;;) {
-                u64 old = atomicCAS(T.k + i, T.empty, kk[k]);
-                if (old == T.empty) { slot[k] = (int)i; created[k] = true; break; }
-                if (old == kk[k]) { slot[k] = (int)i; break; }
-                int st;
-                u32 r = probe_rest(T, (i + 1) & T.mask, kk[k], st);
-                if (st == 0) { slot[k] = (int)r; break; }
-                i = r;
-            }
-        }
+        for (int k = 0; k < 4; k++) { created[k] = false; need[k] = act[k] && slot[k] < 0; }
+        claim128(T, kk, need, slot, created, lane);
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             if (!act[k]) continue;

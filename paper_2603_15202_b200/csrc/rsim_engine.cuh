@@ -70,7 +70,7 @@ __device__ __forceinline__ void log_step(const Params &P, int gi, i64 start, i64
 
 // One engine step of instance gi starting at s.next_step. Returns false if
 // the plan was empty (the instance went idle). F is this warp's finisher buffer.
-__device__ __noinline__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int &werr, FinBuf &F) {
+__device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi, int lane, int &werr, FinBuf &F) {
     Inst s = *sp;
     const i64 t = s.next_step;
     flush_view(s, t);                                              // form_batch flush, engine.py:293
@@ -258,4 +258,15 @@ __device__ __noinline__ bool inst_step(const Params &P, Inst *sp, int gi, int la
     if (lane == 0) *sp = s;
     __syncwarp();
     return true;
+}
+
+// Non-inlined entry used by the replay loop: the error word lives in shared
+// memory so no caller register has its address taken.
+__device__ __noinline__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int *werr_sm, FinBuf &F) {
+    int werr = *werr_sm;
+    const bool ran = inst_step_body(P, sp, gi, lane, werr, F);
+    __syncwarp();
+    if (lane == 0 && werr) *werr_sm = werr;
+    __syncwarp();
+    return ran;
 }

@@ -180,6 +180,7 @@ struct __align__(16) ReqStage {
     i64 t, a, in, oa;
     int B, out;
     u64 keys[128];
+    u32 home[128];      // table home slot of each key (all instances share slog2)
 };
 struct __align__(16) Dec { int owner_warp; int kk; int err; int pad; };
 
@@ -188,6 +189,8 @@ struct __align__(16) WarpBuf {
     int slot[2][4][32];    // probe-found table slots of the warp's first two instances (commit reuses them)
     int hit[32];           // hit blocks of each of the warp's instances
     FinBuf fin;            // finishers of one engine step
+    u64 c_bytes, c_steps;  // algorithmic probe bytes / engine steps of this warp
+    int werr, pad;         // first device error seen by this warp
 };
 
 // counter mod T for the 128-bit TieBreaker counter (hi:lo) without a 128-bit
@@ -216,35 +219,40 @@ __device__ __noinline__ void stage_request(const Params &P, ReqStage &R, i64 k, 
 #pragma unroll
     for (int q = 0; q < 4; q++) kk[q] = (32 * q + lane < B) ? P.ckeys[a + 32 * q + lane] : 0;
 #pragma unroll
-    for (int q = 0; q < 4; q++) if (32 * q + lane < B) R.keys[32 * q + lane] = kk[q];
+    for (int q = 0; q < 4; q++)
+        if (32 * q + lane < B) { R.keys[32 * q + lane] = kk[q]; R.home[32 * q + lane] = tab_home(kk[q], P.slog2); }
     if (lane == 0) { R.t = t; R.a = a; R.in = in; R.oa = oa; R.B = B; R.out = (int)out; }
 }
 
 // ---- drain: advance instances [l0, l0+n) of this warp through steps starting before `until`
-//      (cluster.py:250-273); skip_mask marks instances that must not move yet
-__device__ __noinline__ u64 drain_phase(const Params &P, Inst *st, int base, int l0, int n, i64 until, u32 skip_mask,
-                                        int lane, int &werr, FinBuf &F) {
-    u64 steps = 0;
+//      (cluster.py:250-273); skip_mask marks instances that must not move yet. The check is
+//      inline; the (noinline) step function is only called when a step is due.
+__device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base, int l0, int n, i64 until,
+                                            u32 skip_mask, int lane, WarpBuf &WB) {
     for (int s = 0; s < n; s++) {
         if ((skip_mask >> s) & 1u) continue;
         Inst *sp = st + l0 + s;
-        while (!werr && sp->next_step < until) steps += inst_step(P, sp, base + l0 + s, lane, werr, F);
+        if (sp->next_step >= until) continue;
+        u64 steps = 0;
+        while (sp->next_step < until && !WB.werr) steps += inst_step(P, sp, base + l0 + s, lane, &WB.werr, WB.fin);
+        if (lane == 0) WB.c_steps += steps;
     }
-    return steps;
 }
 
 // ---- probe + score this warp's instances (cluster.py:106-128, policies.py:117-139).
 // Lane s returns instance s's score bits (~0 = not a candidate); hits go to WB.hit.
-__device__ __noinline__ u64 probe_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
-                                        int mode, int target, int lane, WarpBuf &WB, u64 &c_bytes) {
+__device__ __forceinline__ u64 probe_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
+                                           int mode, int target, int lane, WarpBuf &WB) {
+    u64 c_bytes = 0;
     const i64 t = R.t, in = R.in;
     const int B = R.B;
     u64 kk0[4];
     u32 hm[4];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-        kk0[q] = (32 * q + lane < B) ? R.keys[32 * q + lane] : 0;
-        hm[q] = tab_home(kk0[q], P.slog2);
+        const bool v = 32 * q + lane < B;
+        kk0[q] = v ? R.keys[32 * q + lane] : 0;
+        hm[q] = v ? R.home[32 * q + lane] : 0;
     }
     u64 mybits = ~0ULL;
     for (int s0 = 0; s0 < n; s0 += 2) {
@@ -305,6 +313,7 @@ __device__ __noinline__ u64 probe_phase(const Params &P, Inst *st, int base, int
             if (lane == s0 + q) mybits = (u64)__double_as_longlong(sc);
         }
     }
+    if (lane == 0) WB.c_bytes += c_bytes;
     __syncwarp();
     return mybits;
 }
@@ -312,8 +321,20 @@ __device__ __noinline__ u64 probe_phase(const Params &P, Inst *st, int base, int
 // ---- the argmin with the rotating tie-break (policies.py:160-165, 92-101), by warp 0 of
 // every CTA from all C*W partials; for world > 1 one more level across ranks through
 // peer-mapped mailboxes. Writes the owner warp (or -1) and its local tie index to dec.
+// TieBreaker counter at decision time = c0 + ties, c0 the launch-start value: counter mod T
+// is (c0 mod T + ties mod T) mod T with c0 mod T precomputed per T (modtab, T < RSIM_MODTAB).
+#define RSIM_MODTAB 2048
+__device__ __forceinline__ u32 tie_index(const u32 *modtab, u64 c0_lo, u64 c0_hi, u32 ties, u32 T) {
+    if (T < RSIM_MODTAB) {
+        u32 r = modtab[T] + ties % T;
+        return r >= T ? r - T : r;
+    }
+    u64 lo = c0_lo + ties;
+    return mod_counter(lo, c0_hi + (lo < c0_lo), T);
+}
+
 __device__ __noinline__ void decide_phase(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
-                                          Dec &dec, u64 &ctr_lo, u64 &ctr_hi, int lane) {
+                                          Dec &dec, const u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane) {
     // lane-major: lane holds flat partials [8*lane, 8*lane+8) (ascending instance id order)
     u64 pm[8];
     u32 pc[8];
@@ -368,7 +389,7 @@ __device__ __noinline__ void decide_phase(const Params &P, const Part *part, int
         const u32 incl = warp_incl_scan(cr, lane);
         d.err = (int)xer;
         if (!xer && Tg > 0) {
-            if (Tg > 1) { kk = mod_counter(ctr_lo, ctr_hi, Tg); ctr_lo += 1; ctr_hi += (ctr_lo == 0); }
+            if (Tg > 1) { kk = tie_index(modtab, c0_lo, c0_hi, ties, Tg); ties += 1; }
             const u32 ge = __ballot_sync(FULL, lane < P.world && incl > kk && cr > 0);
             const int owner_rank = __ffs(ge) - 1;
             const u32 bef = owner_rank > 0 ? __shfl_sync(FULL, incl, owner_rank - 1) : 0u;
@@ -376,8 +397,8 @@ __device__ __noinline__ void decide_phase(const Params &P, const Part *part, int
             kk -= bef;                            // this rank's local tie index if it owns
         }
     } else if (!d.err && T > 1) {                 // TieBreaker.pick: tied[counter % len]; counter += 1
-        kk = mod_counter(ctr_lo, ctr_hi, T);
-        ctr_lo += 1; ctr_hi += (ctr_lo == 0);
+        kk = tie_index(modtab, c0_lo, c0_hi, ties, T);
+        ties += 1;
     }
     if (!d.err && Tg == 0) d.err = 11;            // NoInstancesError
     if (!d.err && mine) {
@@ -432,7 +453,8 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
     Dec *dec = (Dec *)(rq + RSIM_SLOTS);                   // [2]
     u64 *mb = (u64 *)(dec + 2);                            // [2] partial-exchange mbarriers
     volatile i64 *ctl = (volatile i64 *)(mb + 2);          // [0] staged_upto [1] freed_upto [2] abort
-    WarpBuf *wbuf = (WarpBuf *)(mb + 6);                   // [W]
+    u32 *modtab = (u32 *)(mb + 6);                         // [RSIM_MODTAB] launch counter mod T
+    WarpBuf *wbuf = (WarpBuf *)(modtab + RSIM_MODTAB);     // [W]
     WarpBuf &WB = wbuf[loader ? 0 : warp];
 
     {   // load this CTA's instance shard
@@ -441,21 +463,23 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
         const int words = nloc * (int)(sizeof(Inst) / 8);
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     }
-    u64 ctr_lo = P.tie[0], ctr_hi = P.tie[1];              // evolved by warp 0 only
+    const u64 c0_lo = P.tie[0], c0_hi = P.tie[1];          // TieBreaker counter at launch
+    u32 ties = 0;                                          // ties resolved in this launch (warp 0)
     const int l0 = warp * ipw;
     const int nmine = loader ? 0 : max(0, min(ipw, nloc - l0));
-    int werr = 0;
-    u64 c_bytes = 0, c_steps = 0;   // algorithmic probe bytes / engine steps of this warp
+    if (!loader && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; }
     if (threadIdx.x == 0) {
         mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_fence_init();
         ctl[0] = k0; ctl[1] = k0; ctl[2] = 0;
     }
     u32 mb_phase[2] = {0u, 0u};                            // tracked by warp 0
+    if (mode != MODE_DRAIN)
+        for (int T = threadIdx.x; T < RSIM_MODTAB; T += blockDim.x) modtab[T] = T > 1 ? mod_counter(c0_lo, c0_hi, (u32)T) : 0u;
     __syncthreads();
     if (C > 1) cluster_sync_all();
 
     if (mode == MODE_DRAIN) {
-        if (!loader) c_steps += drain_phase(P, st, base, l0, nmine, until, 0u, lane, werr, WB.fin);
+        if (!loader) drain_phase(P, st, base, l0, nmine, until, 0u, lane, WB);
     } else if (loader) {
         // ---- decoupled loader: keep the ring filled ahead of the decisions
         i64 kk = k0;
@@ -469,21 +493,33 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
             if (lane == 0) ctl[0] = kk;
         }
     } else {
+        // per-phase SM-cycle accounting of CTA 0 / warp 0 (ctr[8..15]): staging wait,
+        // drain, probe, publish + speculative drain, exchange wait, decide, barrier, commit
+        const bool prof = P.ctr != nullptr && cta == 0 && warp == 0;
+        u64 ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        long long tc = clock64();
+#define PHASE(i) do { if (prof) { const long long t2 = clock64(); ph[i] += (u64)(t2 - tc); tc = t2; } } while (0)
+        i64 staged_seen = k0;
         for (i64 k = k0; k < k1; k++) {
             const int par = (int)(k & 1);
-            while (ctl[0] <= k) { }                         // request k staged (normally long done)
-            __threadfence_block();
+            if (staged_seen <= k + 1) {                     // request k (and k+1) staged? normally long done
+                while ((staged_seen = ctl[0]) <= k) { }
+                __threadfence_block();
+            }
             const ReqStage &R = rq[k % RSIM_SLOTS];
+            PHASE(0);
             // ---- K4: advance my instances through steps starting before t
-            if (mode == MODE_REPLAY) c_steps += drain_phase(P, st, base, l0, nmine, R.t, 0u, lane, werr, WB.fin);
+            if (mode == MODE_REPLAY) drain_phase(P, st, base, l0, nmine, R.t, 0u, lane, WB);
+            PHASE(1);
             // ---- K2: probe + score
-            const u64 mybits = probe_phase(P, st, base, l0, nmine, R, mode, target, lane, WB, c_bytes);
-            if (cta == 0 && warp == 0) c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once
-            const u64 wmin = warp_min_u64(mybits);
+            const u64 mybits = probe_phase(P, st, base, l0, nmine, R, mode, target, lane, WB);
+            PHASE(2);
+            if (cta == 0 && warp == 0 && lane == 0) WB.c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once
+            const u32 whi = __reduce_min_sync(FULL, (u32)(mybits >> 32));
+            const u64 wmin = ((u64)whi << 32) | __reduce_min_sync(FULL, (u32)(mybits >> 32) == whi ? (u32)mybits : ~0u);
             const u32 tmask = __ballot_sync(FULL, lane < nmine && mybits == wmin && wmin != ~0ULL);
-            werr = __reduce_max_sync(FULL, werr);
             {   // publish this warp's partial to every CTA of the cluster
-                const u64 w1 = ((u64)(u32)werr << 32) | (u32)__popc(tmask);
+                const u64 w1 = ((u64)(u32)WB.werr << 32) | (u32)__popc(tmask);
                 Part *dst = part + par * CW + cta * W + warp;
                 if (C == 1) {
                     if (lane == 0) { Part q; q.minb = wmin; q.cnt = (u32)w1; q.err = (u32)(w1 >> 32); *dst = q; }
@@ -493,26 +529,29 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
             }
             if (C == 1) bar_warps(32 * W);
             // instances that cannot win this decision advance to the next arrival meanwhile
-            if (mode == MODE_REPLAY && k + 1 < k1 && ctl[0] > k + 1) {
-                __threadfence_block();
+            if (mode == MODE_REPLAY && k + 1 < k1 && staged_seen > k + 1) {
                 u32 skip = 0;
                 for (int s = 0; s < nmine; s++)
                     if (__shfl_sync(FULL, mybits, s) == wmin) skip |= 1u << s;
-                c_steps += drain_phase(P, st, base, l0, nmine, rq[(k + 1) % RSIM_SLOTS].t, skip, lane, werr, WB.fin);
+                drain_phase(P, st, base, l0, nmine, rq[(k + 1) % RSIM_SLOTS].t, skip, lane, WB);
             }
+            PHASE(3);
             if (warp == 0) {
                 if (C > 1) {            // all C*W partials of decision k have landed in this CTA
                     if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * 16));
                     while (!mbar_try_wait(&mb[par], mb_phase[par])) { }
                     mb_phase[par] ^= 1u;
                 }
-                decide_phase(P, part, CW, W, cta, k, par, dec[par], ctr_lo, ctr_hi, lane);
+                PHASE(4);
+                decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane);
+                PHASE(5);
             }
             bar_warps(32 * W);
+            PHASE(6);
             if (warp == 0 && lane == 0) ctl[1] = k;         // decision k-1's slot is free again
             const Dec d = dec[par];
             if (d.err) {
-                if (werr == 0) werr = d.err;
+                if (lane == 0 && WB.werr == 0) WB.werr = d.err;
                 if (warp == 0 && lane == 0) ctl[2] = 1;     // release the loader
                 break;
             }
@@ -525,11 +564,17 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
                 int cs[4];
 #pragma unroll
                 for (int q = 0; q < 4; q++) cs[q] = s < 2 ? WB.slot[s][q][lane] : -1;
+                int werr = 0;
                 commit(P, st + l0 + s, base + l0 + s, k, h, R.t, kk0, s < 2 ? cs : nullptr, R.a, R.B, R.in, R.out,
                        R.oa, lane, werr);
+                if (lane == 0 && werr) WB.werr = werr;
                 if (P.dec_ns != nullptr && lane == 0) P.dec_ns[k] = (i64)globaltimer();
             }
+            PHASE(7);
         }
+#undef PHASE
+        if (prof && lane == 0)
+            for (int i = 0; i < 8; i++) atomicAdd(P.ctr + 8 + i, ph[i]);
     }
     // write back
     __syncthreads();
@@ -539,14 +584,17 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
         const int words = nloc * (int)(sizeof(Inst) / 8);
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     }
-    if (werr && lane == 0) atomicCAS(P.err, 0, werr);
-    if (lane == 0 && P.ctr != nullptr) {
-        if (c_bytes) atomicAdd(P.ctr + 0, c_bytes);
-        if (c_steps) atomicAdd(P.ctr + 1, c_steps);
+    if (!loader && lane == 0) {
+        if (WB.werr) atomicCAS(P.err, 0, WB.werr);
+        if (P.ctr != nullptr) {
+            if (WB.c_bytes) atomicAdd(P.ctr + 0, WB.c_bytes);
+            if (WB.c_steps) atomicAdd(P.ctr + 1, WB.c_steps);
+        }
     }
     if (cta == 0 && threadIdx.x == 0 && mode != MODE_DRAIN) {
-        P.tie[0] = ctr_lo;
-        P.tie[1] = ctr_hi;
+        const u64 lo = c0_lo + ties;
+        P.tie[0] = lo;
+        P.tie[1] = c0_hi + (lo < c0_lo);
     }
     if (C > 1) cluster_sync_all();
 }

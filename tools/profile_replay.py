@@ -15,6 +15,7 @@ from paper_2603_15202_b200.cluster import native_config, sizing_for  # noqa: E40
 name = sys.argv[1] if len(sys.argv) > 1 else "api64"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
 shapes = [(int(sys.argv[3]), int(sys.argv[4]))] if len(sys.argv) > 4 else [(0, 0)]
+world = int(sys.argv[5]) if len(sys.argv) > 5 else 1
 if len(sys.argv) > 3 and sys.argv[3] == "sweep":
     shapes = [(c, w) for c in (1, 2, 4, 8, 16) for w in (4, 8, 16)]
 burst = name.endswith("-burst")            # all arrivals at t=0: no engine steps, pure route cost
@@ -25,6 +26,14 @@ if burst:
     from paper_2603_15202_b200.trace import PackedTrace
     trace = PackedTrace(trace.request_id, np.zeros_like(trace.arrival_s), trace.in_tokens, trace.out_tokens,
                         trace.class_key, trace.blk_off, trace.blocks)
+if world > 1:
+    from paper_2603_15202_b200.distributed import run_sharded_local
+    for c, w in shapes:
+        r = run_sharded_local(trace, cfg, world, ctas=c, warps_per_cta=w, repeats=3)
+        best = min(r["device_ms"])
+        print(f"{name} R={len(trace)} world={world} ctas={c} warps={w}: total {best:.2f} ms "
+              f"({1000 * best / len(trace):.2f} us/decision)", flush=True)
+    sys.exit(0)
 for c, w in shapes:
     if c and c > cfg.n_instances:
         continue
@@ -39,4 +48,9 @@ for c, w in shapes:
     rep, k1, dr = h.timings()
     print(f"{name} R={len(trace)} ctas={c} warps={w}: total {best:.2f} ms  replay {rep:.2f} ms "
           f"({1000 * rep / len(trace):.2f} us/decision)  k1 {k1:.3f} ms  drain {dr:.2f} ms", flush=True)
+    ctr = h.counters()
+    names = ["stage", "drain", "probe", "pub+spec", "xwait", "decide", "barrier", "commit"]
+    cyc = ctr[8:16].astype(float) / len(trace)
+    print("   cycles/decision (CTA0 warp0): " + "  ".join(f"{n}={c:.0f}" for n, c in zip(names, cyc))
+          + f"  sum={cyc.sum():.0f}", flush=True)
     h.close()
