@@ -69,6 +69,7 @@ typedef struct rsim_config {
     int32_t world;                  /* ranks sharing the cluster (1 = unsharded), <= 8         */
     int32_t rank;
     int64_t comm_timeout_ms;        /* a rank waiting longer on a peer fails with RSIM_E_COMM  */
+    int64_t runs_capacity;          /* per-instance touch-run ring (finite capacity), 0 = auto */
 } rsim_config;
 
 typedef struct rsim rsim_t;
@@ -141,8 +142,9 @@ rsim_status rsim_read_decision_ns(rsim_t *h, int64_t first, int64_t count, int64
  * time of the whole sequence on the handle's stream. Equals reset+K1+replay+drain. */
 rsim_status rsim_rerun(rsim_t *h, double *device_ms);
 /* Counters of the last replay (16 int64): [0] algorithmic probe bytes (8*B per
- * decision + sum_i 8*min(h_i+1,B) + 16 per instance probed), [1] engine steps, [2] evictions,
- * [3] reserved, [4] requests loaded, [5] blocks, [6] output keys, [7] local instances,
+ * decision + sum_i 8*min(h_i+1,B) + 16 per instance probed), [1] engine steps, [2] SM cycles
+ * in engine steps, [3] SM cycles finishing requests, [4] requests loaded, [5] blocks,
+ * [6] finisher batches, [7] local instances,
  * [8..15] SM cycles of CTA 0 / warp 0 per decision phase: staging wait, drain, probe,
  * publish + speculative drain, exchange wait, decide, barrier, commit. */
 rsim_status rsim_read_counters(rsim_t *h, int64_t *out16);

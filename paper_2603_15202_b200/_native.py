@@ -55,6 +55,7 @@ class Config(C.Structure):
         ("ctas", C.c_int32), ("warps_per_cta", C.c_int32), ("record_steps", C.c_int32),
         ("step_log_capacity", C.c_int64), ("expected_keys", C.c_int64),
         ("world", C.c_int32), ("rank", C.c_int32), ("comm_timeout_ms", C.c_int64),
+        ("runs_capacity", C.c_int64),
     ]
 
 

@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <vector>
 #include <algorithm>
+#include <mutex>
 
 #include "../../include/rsim.h"
 #include "rsim_kernels.cuh"
@@ -83,6 +84,10 @@ struct rsim {
     u64 *peer[8] = {nullptr};
     bool peer_ipc[8] = {false};
     u64 epoch = 1;
+    Run *runs = nullptr;
+    int rlog2 = 0;
+    DevArr<u64> arena;             // API-inserted chain keys (named by eviction runs)
+    i64 narena = 0;
 };
 
 static rsim_status fail(rsim_t *h, rsim_status st, const char *fmt, ...) {
@@ -129,6 +134,7 @@ static Params make_params(rsim_t *h) {
     P.mbox = h->mbox;
     for (int i = 0; i < 8; i++) P.peer[i] = h->peer[i];
     P.epoch = h->epoch;
+    P.runs = h->runs; P.rlog2 = h->rlog2; P.arena = h->arena.p;
     P.timeout_ns = (h->cfg.comm_timeout_ms > 0 ? h->cfg.comm_timeout_ms : 10000) * 1000000LL;
     return P;
 }
@@ -168,7 +174,7 @@ static rsim_status init_state(rsim_t *h) {
     CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), h->stream));
     CK(h, cudaMemsetAsync(h->ctr, 0, 16 * sizeof(u64), h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
-    h->R = 0; h->nblk = 0; h->nout = 0;
+    h->R = 0; h->nblk = 0; h->nout = 0; h->narena = 0;
     // blk_off / ooff hold a leading 0
     CK(h, h->blk_off.reserve(1, 0, h->stream));
     CK(h, h->ooff.reserve(1, 0, h->stream));
@@ -226,7 +232,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     }
     const int N = h->N;
     int C = c.ctas;
-    if (C <= 0) C = N <= 128 ? 1 : std::min(16, (N + 63) / 64);
+    if (C <= 0) C = std::min(16, N);       // measured: spreading instances over SMs wins (profiles/)
     C = std::max(1, std::min(16, std::min(C, N)));
     int per_cta = (N + C - 1) / C;
     int W = c.warps_per_cta > 0 ? c.warps_per_cta : std::min(RSIM_MAX_WARPS, per_cta);
@@ -237,8 +243,13 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
     h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(2 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 6 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf);
     if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
-    cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
-    if (C > 8) cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    {   // kernel attributes are process-global: set the ceiling once (handles on other threads launch concurrently)
+        static std::once_flag once;
+        std::call_once(once, [] {
+            cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        });
+    }
 
     // ---- sizing
     int ql = c.queue_capacity > 0 ? ilog2_ceil(c.queue_capacity) : 10;
@@ -256,6 +267,11 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaMalloc(&h->rbuf, (size_t)N * c.max_batch_requests * sizeof(REnt)));
     CK(nullptr, cudaMalloc(&h->tkeys, slots * sizeof(u64)));
     CK(nullptr, cudaMalloc(&h->tmeta, slots * sizeof(Meta)));
+    if (c.capacity_blocks > 0) {   // touch-run rings for exact LRU eviction (rsim_lru.cuh)
+        const i64 want = c.runs_capacity > 0 ? c.runs_capacity : 4 * (1LL << h->qlog2) + 1024;
+        h->rlog2 = std::max(6, std::min(26, ilog2_ceil(want)));
+        CK(nullptr, cudaMalloc(&h->runs, ((size_t)N << h->rlog2) * sizeof(Run)));
+    }
     CK(nullptr, cudaMalloc(&h->tie, 2 * sizeof(u64)));
     CK(nullptr, cudaMalloc(&h->errbuf, 4 * sizeof(int)));
     CK(nullptr, cudaMalloc(&h->flag, sizeof(int)));
@@ -286,7 +302,8 @@ void rsim_destroy(rsim_t *h) {
     h->rid.free_(); h->blocks.free_(); h->ckeys.free_(); h->okeys.free_();
     h->hit_blocks.free_(); h->chosen.free_();
     void *ps[] = {h->inst, h->qbuf, h->rbuf, h->tkeys, h->tmeta, h->tie, h->errbuf, h->flag, h->log, h->log_n,
-                  h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox};
+                  h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs};
+    h->arena.free_();
     for (int i = 0; i < 8; i++) if (h->peer_ipc[i] && h->peer[i]) cudaIpcCloseMemHandle(h->peer[i]);
     for (void *p : ps) if (p) cudaFree(p);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -381,7 +398,6 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     memset(&lc, 0, sizeof(lc));
     lc.gridDim = dim3(h->C, 1, 1);
     lc.blockDim = dim3(32 * (h->W + 1), 1, 1);   // + the request-staging warp
-    cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_bytes);
     lc.dynamicSmemBytes = h->smem_bytes;
     lc.stream = h->stream;
     cudaLaunchAttribute at[1];
@@ -445,15 +461,24 @@ static rsim_status stage_keys(rsim_t *h, const uint64_t *keys, int64_t n) {
     return RSIM_OK;
 }
 
+static rsim_status arena_append(rsim_t *h, const uint64_t *keys, int64_t n, i64 *a0) {
+    CK(h, h->arena.reserve(h->narena + n + 1, h->narena, h->stream));
+    if (n) CK(h, cudaMemcpy(h->arena.p + h->narena, keys, n * sizeof(u64), cudaMemcpyHostToDevice));
+    *a0 = h->narena;
+    h->narena += n;
+    return RSIM_OK;
+}
+
 rsim_status rsim_cache_insert_keys(rsim_t *h, int32_t instance, const uint64_t *keys, int64_t n, int64_t now_us,
                                    int64_t *evicted) {
     if (!h) return RSIM_E_INVALID;
     if (instance < 0 || instance >= h->N) return fail(h, RSIM_E_INVALID, "instance out of range");
     for (i64 i = 0; i < n; i++) if (keys[i] == 0) return fail(h, RSIM_E_INVALID, "key equals the table sentinel 0");
     CK(h, cudaSetDevice(h->cfg.device));
-    rsim_status st = stage_keys(h, keys, n);
+    i64 a0 = 0;
+    rsim_status st = arena_append(h, keys, n, &a0);
     if (st) return st;
-    cache_op_kernel<<<1, 32, 0, h->stream>>>(make_params(h), instance, 0, h->scratch_keys, (int)n, now_us, h->scratch_res);
+    cache_op_kernel<<<1, 32, 0, h->stream>>>(make_params(h), instance, 0, a0, (int)n, now_us, h->scratch_res);
     h->launches++;
     CK(h, cudaGetLastError());
     i64 res = 0;
@@ -468,9 +493,11 @@ rsim_status rsim_cache_match_keys(rsim_t *h, int32_t instance, const uint64_t *k
     if (!h) return RSIM_E_INVALID;
     if (instance < 0 || instance >= h->N) return fail(h, RSIM_E_INVALID, "instance out of range");
     CK(h, cudaSetDevice(h->cfg.device));
-    rsim_status st = stage_keys(h, keys, n);
+    i64 a0 = 0;
+    rsim_status st = arena_append(h, keys, n, &a0);     // (match keys are not named by runs; reuse the slot)
     if (st) return st;
-    cache_op_kernel<<<1, 32, 0, h->stream>>>(make_params(h), instance, 1, h->scratch_keys, (int)n, 0, h->scratch_res);
+    h->narena = a0;
+    cache_op_kernel<<<1, 32, 0, h->stream>>>(make_params(h), instance, 1, a0, (int)n, 0, h->scratch_res);
     h->launches++;
     CK(h, cudaGetLastError());
     i64 res = 0;
@@ -645,7 +672,7 @@ rsim_status rsim_read_counters(rsim_t *h, int64_t *out16) {
     u64 c[16];
     CK(h, cudaMemcpy(c, h->ctr, sizeof(c), cudaMemcpyDeviceToHost));
     for (int i = 0; i < 16; i++) out16[i] = (int64_t)c[i];
-    out16[4] = h->R; out16[5] = h->nblk; out16[6] = h->nout; out16[7] = h->N;
+    out16[4] = h->R; out16[5] = h->nblk; out16[7] = h->N;
     return RSIM_OK;
 }
 

@@ -39,6 +39,8 @@ struct __align__(16) Inst {
     i64 step_idx;     // steps executed so far
     i64 next_finish;  // min finish step among running (RSIM_NONE if none)
     i64 occ;          // KV$ occupancy (live chains)
+    i64 r_head, r_tail, r_tailT;   // touch-run ring (finite capacity): positions and newest T
+    i64 pad2;
     int r, q;         // live running / queued counts
     int v_r, v_q;     // view counts
     int q_head;       // queue ring head index
@@ -96,6 +98,8 @@ struct Params {
     i64 *log; i64 log_cap; u64 *log_n;
     double *scores;   // optional per-instance scores of a route_one call
     u64 *ctr;         // [0] algorithmic probe bytes, [1] engine steps, [2] evictions
+    struct Run *runs; int rlog2;   // per-instance touch-run rings (rsim_lru.cuh), null for infinite capacity
+    const u64 *arena; // chain keys of API-inserted runs
     // multi-GPU shard: local instance i is global instance gbase + i
     int gbase, world, rank;
     u64 *mbox;        // this rank's mailbox [2 parity][8 ranks][4 words]

@@ -7,7 +7,7 @@
 // request's finish step is known when it joins (finish = join + out - 1), so
 // the running list is only scanned on steps where something finishes.
 #pragma once
-#include "rsim_cache.cuh"
+#include "rsim_lru.cuh"
 
 // Python round() of the double expression, evaluated in the reference's
 // operation order with explicit round-to-nearest ops (no FMA contraction).
@@ -32,29 +32,43 @@ __device__ __forceinline__ void flush_view(Inst &s, i64 now) {   // engine.py:24
 
 // _finish (engine.py:357-372) for one request: unpin the admission hit, insert
 // the full prefix+output chain stamped with the step end, evict to capacity.
-__device__ void finish_one(const Params &P, int gi, i64 &occ, i64 a, int B, i64 oa, int L, int hb, i64 end, int lane,
+__device__ __forceinline__ void evict_to_capacity(const Params &P, const Table &T, Inst &s, int gi, int lane,
+                                                  int &werr) {
+    if (P.cap >= 0 && s.occ > P.cap && !werr)
+        if (!evict_runs(P, T, s, gi, s.occ, lane, werr)) warp_evict(T, P.cap, s.occ, lane, werr);
+}
+
+__device__ void finish_one(const Params &P, int gi, Inst &s, i64 a, int B, i64 oa, int L, int hb, i64 end, int lane,
                            int &werr) {
     Table T = table_of(P, gi);
-    occ += warp_unpin_insert(T, P.ckeys + a, B, P.okeys + oa, L, hb, end, lane, werr);
-    if (occ > P.max_occ) werr = DEV_E_TABLE_FULL;
-    if (P.cap >= 0 && occ > P.cap && !werr) warp_evict(T, P.cap, occ, lane, werr);
+    Run r; r.T = end; r.a = a; r.oa = oa; r.B = B; r.dhi = L; r.kind = 0; r.pad = 0;
+    run_add(P, s, gi, r, lane, werr);
+    s.occ += warp_unpin_insert(T, P.ckeys + a, B, P.okeys + oa, L, hb, end, lane, werr);
+    if (s.occ > P.max_occ) werr = DEV_E_TABLE_FULL;
+    evict_to_capacity(P, T, s, gi, lane, werr);
 }
 
 // Process the finishers collected in F, in collection order (= the reference's:
 // queue-pop finishes, then decode finishes in running order). When no eviction
 // can happen before the last insert, all chains go in one batched pass.
-__device__ void flush_finishers(const Params &P, int gi, i64 &occ, FinBuf &F, int nf, i64 end, int lane, int &werr) {
+__device__ void flush_finishers(const Params &P, int gi, Inst &s, FinBuf &F, int nf, i64 end, int lane, int &werr) {
     if (nf == 0 || werr) return;
+    const long long c0 = clock64();
     __syncwarp();
-    if (P.cap < 0 || occ + F.pre[nf] <= P.cap) {
+    if (P.cap < 0 || s.occ + F.pre[nf] <= P.cap) {
         Table T = table_of(P, gi);
-        occ += warp_finish_many(T, P.ckeys, P.okeys, F, nf, end, lane, werr);
-        if (occ > P.max_occ) werr = DEV_E_TABLE_FULL;
+        for (int f = 0; f < nf; f++) {
+            Run r; r.T = end; r.a = F.a[f]; r.oa = F.oa[f]; r.B = F.B[f]; r.dhi = F.L[f]; r.kind = 0; r.pad = 0;
+            run_add(P, s, gi, r, lane, werr);
+        }
+        s.occ += warp_finish_many(T, P.ckeys, P.okeys, F, nf, end, lane, werr);
+        if (s.occ > P.max_occ) werr = DEV_E_TABLE_FULL;
     } else {
         for (int f = 0; f < nf && !werr; f++)
-            finish_one(P, gi, occ, F.a[f], F.B[f], F.oa[f], F.L[f], F.hb[f], end, lane, werr);
+            finish_one(P, gi, s, F.a[f], F.B[f], F.oa[f], F.L[f], F.hb[f], end, lane, werr);
     }
     __syncwarp();
+    if (P.ctr != nullptr && lane == 0) { atomicAdd(P.ctr + 3, (u64)(clock64() - c0)); atomicAdd(P.ctr + 6, (u64)1); }
 }
 
 __device__ __forceinline__ void log_step(const Params &P, int gi, i64 start, i64 end, i64 pre, i64 bs_after,
@@ -156,7 +170,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
 
     int nf = 0;
     auto add_fin = [&](const Ent &f) {
-        if (nf == 32) { flush_finishers(P, gi, s.occ, F, nf, end, lane, werr); nf = 0; }
+        if (nf == 32) { flush_finishers(P, gi, s, F, nf, end, lane, werr); nf = 0; }
         if (lane == 0) {
             if (nf == 0) F.pre[0] = 0;
             F.a[nf] = f.a; F.oa[nf] = f.oa; F.B[nf] = f.B; F.L[nf] = f.L; F.hb[nf] = f.hb;
@@ -226,7 +240,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         s.r = w;
         s.next_finish = warp_min_i64(nf_step);
     }
-    flush_finishers(P, gi, s.occ, F, nf, end, lane, werr);
+    flush_finishers(P, gi, s, F, nf, end, lane, werr);
 
     // popped requests with out > 1 join the running list (after the removals)
     {
@@ -264,7 +278,9 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
 // memory so no caller register has its address taken.
 __device__ __noinline__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int *werr_sm, FinBuf &F) {
     int werr = *werr_sm;
+    const long long c0 = clock64();
     const bool ran = inst_step_body(P, sp, gi, lane, werr, F);
+    if (P.ctr != nullptr && lane == 0) atomicAdd(P.ctr + 2, (u64)(clock64() - c0));   // SM cycles in engine steps
     __syncwarp();
     if (lane == 0 && werr) *werr_sm = werr;
     __syncwarp();

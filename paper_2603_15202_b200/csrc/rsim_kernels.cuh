@@ -186,7 +186,7 @@ struct __align__(16) Dec { int owner_warp; int kk; int err; int pad; };
 
 // Per-warp hand-off state between the phases of a decision.
 struct __align__(16) WarpBuf {
-    int slot[2][4][32];    // probe-found table slots of the warp's first two instances (commit reuses them)
+    int slot[2][128];      // probe-found table slot per depth of the warp's first two instances (commit reuses them)
     int hit[32];           // hit blocks of each of the warp's instances
     FinBuf fin;            // finishers of one engine step
     u64 c_bytes, c_steps;  // algorithmic probe bytes / engine steps of this warp
@@ -240,87 +240,99 @@ __device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base,
 }
 
 // ---- probe + score this warp's instances (cluster.py:106-128, policies.py:117-139).
-// Lane s returns instance s's score bits (~0 = not a candidate); hits go to WB.hit.
+// Short prompts are probed several instances at a time: the warp splits into G
+// lane groups of LP = 32/G lanes, lane li of group g probing depths j*LP+li
+// (j < 4) of instance s0+g, so one round trip and one instruction stream
+// cover G instances. Lane s returns instance s's score bits (~0 = not a
+// candidate); hit blocks go to WB.hit, found slots of instances 0/1 to WB.slot.
 __device__ __forceinline__ u64 probe_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
                                            int mode, int target, int lane, WarpBuf &WB) {
-    u64 c_bytes = 0;
     const i64 t = R.t, in = R.in;
     const int B = R.B;
-    u64 kk0[4];
+    const int Bc = min(B, 128);
+    const int G = Bc <= 32 ? 4 : (Bc <= 64 ? 2 : 1);       // instances per round (warp-uniform)
+    const int LP = 32 / G, DS = (Bc + LP - 1) / LP;         // lanes per instance, depth slots per lane
+    const int g = lane / LP, li = lane - g * LP;
+    const u32 gmask = LP == 32 ? FULL : ((1u << LP) - 1u);
+    u64 kk[4];
     u32 hm[4];
+    bool vd[4];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-        const bool v = 32 * q + lane < B;
-        kk0[q] = v ? R.keys[32 * q + lane] : 0;
-        hm[q] = v ? R.home[32 * q + lane] : 0;
+    for (int j = 0; j < 4; j++) {
+        const int d = j * LP + li;
+        vd[j] = j < DS && d < B;
+        kk[j] = vd[j] ? R.keys[d] : 0;
+        hm[j] = vd[j] ? R.home[d] : 0;
     }
     u64 mybits = ~0ULL;
-    for (int s0 = 0; s0 < n; s0 += 2) {
-        const int ns = min(2, n - s0);
-        Table T2[2];
-        bool cand[2];
-        int hh[2] = {0, 0};
+    u32 cb = 0;                       // algorithmic probe bytes of my group's instances
+    for (int s0 = 0; s0 < n; s0 += G) {
+        const int s = s0 + g;
+        const bool have = s < n;
+        const int gi = base + l0 + (have ? s : s0);
+        const bool cand = have && ((mode != MODE_ENQUEUE) || gi == target);
+        const Table T = table_of(P, gi);
+        ulonglong2 pr[4];
 #pragma unroll
-        for (int q = 0; q < 2; q++) {
-            const int gi = base + l0 + s0 + q;
-            cand[q] = q < ns && ((mode != MODE_ENQUEUE) || gi == target);
-            T2[q] = table_of(P, q < ns ? gi : base + l0 + s0);
-        }
-        int sl[2][4];
-        u32 m[2][4];
-        if (cand[0] && cand[1]) {
-            probe128<2>(T2, kk0, hm, B, lane, m, sl);
-            hh[0] = lead_hits(m[0]);
-            hh[1] = lead_hits(m[1]);
-        } else {
+        for (int j = 0; j < 4; j++)
+            if (cand && vd[j]) pr[j] = ld_pair(T, hm[j]);
+        u32 mk[4];
 #pragma unroll
-            for (int q = 0; q < 2; q++) {
-                u32 mq[1][4];
-                int sq[1][4];
-                sq[0][0] = sq[0][1] = sq[0][2] = sq[0][3] = -1;
-                if (cand[q]) {
-                    probe128<1>(&T2[q], kk0, hm, B, lane, mq, sq);
-                    hh[q] = lead_hits(mq[0]);
+        for (int j = 0; j < 4; j++) {
+            mk[j] = 0;
+            if (j < DS) {
+                bool f = false, c = false;
+                if (cand && vd[j]) eval_first(T, pr[j], hm[j], kk[j], f, c);
+                int sl = -1;
+                if (__any_sync(FULL, c) && c) {          // rare: the home pair is full of other keys
+                    int stt;
+                    const u32 r = probe_rest(T, ((hm[j] | 1u) + 1u) & T.mask, kk[j], stt);
+                    f = stt == 0;
+                    if (f) sl = (int)r;
+                } else if (f) {
+                    sl = (int)((hm[j] & 1u) == 0 && pr[j].x == kk[j] ? hm[j] : hm[j] | 1u);
                 }
-#pragma unroll
-                for (int kq = 0; kq < 4; kq++) sl[q][kq] = sq[0][kq];
+                if (s < 2 && vd[j]) WB.slot[s][j * LP + li] = sl;
+                mk[j] = __ballot_sync(FULL, f);
             }
         }
-        if (s0 == 0) {
+        // leading present depths of my group's instance
+        int h = DS * LP;
+        bool done = false;
 #pragma unroll
-            for (int q = 0; q < 2; q++)
-#pragma unroll
-                for (int kq = 0; kq < 4; kq++) WB.slot[q][kq][lane] = sl[q][kq];
+        for (int j = 0; j < 4; j++) {
+            if (j < DS) {
+                const u32 bits = (mk[j] >> (g * LP)) & gmask;
+                if (!done && bits != gmask) { h = j * LP + __ffs(~bits) - 1; done = true; }
+            }
         }
-#pragma unroll
-        for (int q = 0; q < 2; q++) {
-            if (!cand[q]) continue;
-            if (hh[q] >= 128) hh[q] = B <= 128 ? B : deep_match(T2[q], P.ckeys + R.a, B, lane);
-            else hh[q] = min(hh[q], B);
-            Inst *sp = st + l0 + s0 + q;
-            if (sp->due <= t) {          // snapshot() flushes every candidate (indicators.py:36-65)
-                __syncwarp();
-                if (lane == 0) flush_view(*sp, t);
-                __syncwarp();
-            }
-            const double sc = score_of(P, *sp, hh[q], in);
-            if (lane == 0) {
-                WB.hit[s0 + q] = hh[q];
-                if (P.scores != nullptr) P.scores[base + l0 + s0 + q] = sc;
-            }
+        if (G == 1 && h >= 128 && B > 128) h = deep_match(T, P.ckeys + R.a, B, lane);   // G == 1: warp-uniform
+        h = min(h, B);
+        u64 bits = ~0ULL;
+        if (cand && li == 0) {
+            Inst *sp = st + l0 + s;
+            if (sp->due <= t) flush_view(*sp, t);        // snapshot() flushes every candidate (indicators.py:36-65)
+            const double sc = score_of(P, *sp, h, in);
+            bits = (u64)__double_as_longlong(sc);
+            WB.hit[s] = h;
+            if (P.scores != nullptr) P.scores[gi] = sc;
             // one 8-B key compare per reference dict lookup + 16 B of view
-            c_bytes += 8ULL * (u64)min(hh[q] + 1, B) + 16ULL;
-            if (lane == s0 + q) mybits = (u64)__double_as_longlong(sc);
+            cb += 8u * (u32)min(h + 1, B) + 16u;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            if (q < G) {
+                const u64 v = __shfl_sync(FULL, bits, q * LP);
+                if (lane == s0 + q) mybits = v;
+            }
         }
     }
-    if (lane == 0) WB.c_bytes += c_bytes;
+    cb = __reduce_add_sync(FULL, cb);
+    if (lane == 0) WB.c_bytes += cb;
     __syncwarp();
     return mybits;
 }
 
-// ---- the argmin with the rotating tie-break (policies.py:160-165, 92-101), by warp 0 of
-// every CTA from all C*W partials; for world > 1 one more level across ranks through
-// peer-mapped mailboxes. Writes the owner warp (or -1) and its local tie index to dec.
 // TieBreaker counter at decision time = c0 + ties, c0 the launch-start value: counter mod T
 // is (c0 mod T + ties mod T) mod T with c0 mod T precomputed per T (modtab, T < RSIM_MODTAB).
 #define RSIM_MODTAB 2048
@@ -563,7 +575,7 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
                 for (int q = 0; q < 4; q++) kk0[q] = (32 * q + lane < R.B) ? R.keys[32 * q + lane] : 0;
                 int cs[4];
 #pragma unroll
-                for (int q = 0; q < 4; q++) cs[q] = s < 2 ? WB.slot[s][q][lane] : -1;
+                for (int q = 0; q < 4; q++) cs[q] = (s < 2 && 32 * q + lane < min(R.B, 128)) ? WB.slot[s][32 * q + lane] : -1;
                 int werr = 0;
                 commit(P, st + l0 + s, base + l0 + s, k, h, R.t, kk0, s < 2 ? cs : nullptr, R.a, R.B, R.in, R.out,
                        R.oa, lane, werr);
@@ -617,27 +629,31 @@ probe_batch_kernel(Params P, i64 r0, i64 nreq, int *out) {
 }
 
 // ---------------------------------------------------------------- cache ops (API)
-// op 0: insert_keys(keys, now) -> evicted ; op 1: match_keys(keys) -> hit
-__global__ void cache_op_kernel(Params P, int gi, int op, const u64 *keys, int n, i64 now, i64 *result) {
+// op 0: insert_keys(keys, now) -> evicted ; op 1: match_keys(keys) -> hit.
+// keys = P.arena + a0 (API keys persist in the arena so eviction runs can name them).
+__global__ void cache_op_kernel(Params P, int gi, int op, i64 a0, int n, i64 now, i64 *result) {
     const int lane = threadIdx.x & 31;
     Table T = table_of(P, gi);
+    const u64 *keys = P.arena + a0;
     int werr = 0;
     if (op == 1) {
         int h = warp_probe(T, keys, n, lane);
         if (lane == 0) result[0] = h;
         return;
     }
-    Inst *sp = P.inst + gi;
-    i64 occ = sp->occ;
-    const i64 occ0 = occ;
-    occ += warp_unpin_insert(T, keys, n, keys, n, 0, now, lane, werr);
-    i64 before_evict = occ;
-    if (occ > P.max_occ) werr = DEV_E_TABLE_FULL;
-    if (P.cap >= 0 && occ > P.cap && !werr) warp_evict(T, P.cap, occ, lane, werr);
-    (void)occ0;
+    Inst s = P.inst[gi];
+    if (n > 0) {
+        Run r; r.T = now; r.a = a0; r.oa = 0; r.B = n; r.dhi = n; r.kind = 1; r.pad = 0;
+        run_add(P, s, gi, r, lane, werr);
+    }
+    s.occ += warp_unpin_insert(T, keys, n, keys, n, 0, now, lane, werr);
+    const i64 before_evict = s.occ;
+    if (s.occ > P.max_occ) werr = DEV_E_TABLE_FULL;
+    evict_to_capacity(P, T, s, gi, lane, werr);
+    __syncwarp();
     if (lane == 0) {
-        sp->occ = occ;
-        result[0] = before_evict - occ;
+        P.inst[gi] = s;
+        result[0] = before_evict - s.occ;
         if (werr) atomicCAS(P.err, 0, werr);
     }
 }

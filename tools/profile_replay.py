@@ -53,4 +53,7 @@ for c, w in shapes:
     cyc = ctr[8:16].astype(float) / len(trace)
     print("   cycles/decision (CTA0 warp0): " + "  ".join(f"{n}={c:.0f}" for n, c in zip(names, cyc))
           + f"  sum={cyc.sum():.0f}", flush=True)
+    if ctr[1]:
+        print(f"   engine: {ctr[1] / len(trace):.2f} steps/decision, {ctr[2] / max(ctr[1], 1):.0f} cycles/step, "
+              f"{ctr[6]} finisher batches at {ctr[3] / max(ctr[6], 1):.0f} cycles each", flush=True)
     h.close()
