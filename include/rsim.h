@@ -154,6 +154,16 @@ rsim_status rsim_mailbox(rsim_t *h, void **dev_ptr);
 rsim_status rsim_mailbox_ipc_handle(rsim_t *h, unsigned char out64[64]);   /* cudaIpcGetMemHandle */
 rsim_status rsim_set_peer(rsim_t *h, int32_t rank, void *peer_mailbox);    /* same-process peer    */
 rsim_status rsim_open_peer_ipc(rsim_t *h, int32_t rank, const unsigned char in64[64]);
+/* Diagnostics: record, for the first capacity_decisions decisions of each replay launch, one
+ * 8 x uint16 record per (decision, instance warp): [0] cycles/16 from the warp's release to its
+ * partial, [1] drain cycles/16, [2] probe+score cycles/16, [3] staging wait cycles/16, [4] engine
+ * steps, [5] finisher batches, [6] instances served by the probe-ahead, [7] instances of the warp.
+ * capacity 0 turns recording off. Read back with rsim_read_phase_records. */
+rsim_status rsim_phase_records(rsim_t *h, int64_t capacity_decisions);
+rsim_status rsim_read_phase_records(rsim_t *h, uint16_t *out, int64_t n_decisions, int32_t *warps_per_decision);
+/* Diagnostics of builds with -DRSIM_STEP_PROFILE: SM cycles summed over engine steps per step
+ * section (setup, plan, cost, apply, pops, decode, finishers, joins+tail); zeros otherwise. */
+rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out8);
 /* Number of kernels librsim launched since create (evidence for bench gpu_launches). */
 int64_t rsim_launch_count(const rsim_t *h);
 

@@ -17,7 +17,8 @@ from .config import (CacheFullError, DuplicateRequestError, InvariantError, NoIn
 from .trace import TraceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librsim.so")
+# RSIM_LIB selects an alternate in-tree build (tools/variants.sh experiments)
+LIB_PATH = os.environ.get("RSIM_LIB") or os.path.join(_HERE, "librsim.so")
 
 RSIM_OK = 0
 E_INVALID, E_TRACE, E_CACHE_FULL, E_DUPLICATE, E_INVARIANT, E_CUDA = 1, 2, 3, 4, 5, 6
@@ -101,6 +102,9 @@ def lib():
         "rsim_set_peer": ([P, I32, P], C.c_int),
         "rsim_open_peer_ipc": ([P, I32, P], C.c_int),
         "rsim_read_counters": ([P, P], C.c_int),
+        "rsim_phase_records": ([P, I64], C.c_int),
+        "rsim_read_phase_records": ([P, P, I64, P], C.c_int),
+        "rsim_read_step_cycles": ([P, P], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -263,6 +267,22 @@ class Handle:
         ms = C.c_double()
         self._ck(self._L.rsim_rerun(self._h, C.byref(ms)))
         return ms.value
+
+    def phase_records(self, capacity: int):
+        """Enable (capacity > 0) per-(decision, warp) phase records of the next replays."""
+        self._ck(self._L.rsim_phase_records(self._h, capacity))
+
+    def read_phase_records(self, n: int) -> np.ndarray:
+        w = C.c_int32()
+        self._ck(self._L.rsim_read_phase_records(self._h, None, 0, C.byref(w)))
+        out = np.zeros((n, w.value, 8), np.uint16)
+        self._ck(self._L.rsim_read_phase_records(self._h, out.ctypes.data, n, None))
+        return out
+
+    def step_cycles(self) -> np.ndarray:
+        out = np.zeros(8, np.int64)
+        self._ck(self._L.rsim_read_step_cycles(self._h, out.ctypes.data))
+        return out
 
     def counters(self) -> np.ndarray:
         out = np.zeros(16, np.int64)

@@ -88,6 +88,8 @@ struct rsim {
     int rlog2 = 0;
     DevArr<u64> arena;             // API-inserted chain keys (named by eviction runs)
     i64 narena = 0;
+    unsigned short *crit = nullptr; // diagnostics: per (decision, warp) phase records
+    i64 crit_cap = 0;
 };
 
 static rsim_status fail(rsim_t *h, rsim_status st, const char *fmt, ...) {
@@ -136,6 +138,7 @@ static Params make_params(rsim_t *h) {
     P.epoch = h->epoch;
     P.runs = h->runs; P.rlog2 = h->rlog2; P.arena = h->arena.p;
     P.timeout_ns = (h->cfg.comm_timeout_ms > 0 ? h->cfg.comm_timeout_ms : 10000) * 1000000LL;
+    P.crit = h->crit; P.crit_cap = h->crit_cap;
     return P;
 }
 
@@ -172,7 +175,7 @@ static rsim_status init_state(rsim_t *h) {
     CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaMemsetAsync(h->errbuf, 0, 4 * sizeof(int), h->stream));
     CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), h->stream));
-    CK(h, cudaMemsetAsync(h->ctr, 0, 16 * sizeof(u64), h->stream));
+    CK(h, cudaMemsetAsync(h->ctr, 0, 32 * sizeof(u64), h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     h->R = 0; h->nblk = 0; h->nout = 0; h->narena = 0;
     // blk_off / ooff hold a leading 0
@@ -235,7 +238,9 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (C <= 0) C = std::min(16, N);       // measured: spreading instances over SMs wins (profiles/)
     C = std::max(1, std::min(16, std::min(C, N)));
     int per_cta = (N + C - 1) / C;
-    int W = c.warps_per_cta > 0 ? c.warps_per_cta : std::min(RSIM_MAX_WARPS, per_cta);
+    // default: the lean kernel (<= 7 instance warps, 255 registers) unless a warp would own > 32 instances
+    int W = c.warps_per_cta > 0 ? c.warps_per_cta : std::min(RSIM_LEAN_WARPS, per_cta);
+    if (c.warps_per_cta <= 0 && (per_cta + W - 1) / W > 32) W = std::min(RSIM_MAX_WARPS, per_cta);
     W = std::max(1, std::min(RSIM_MAX_WARPS, W));
     int ipw = (per_cta + W - 1) / W;
     if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
@@ -246,8 +251,10 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     {   // kernel attributes are process-global: set the ceiling once (handles on other threads launch concurrently)
         static std::once_flag once;
         std::call_once(once, [] {
-            cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaFuncSetAttribute(replay_kernel<RSIM_LEAN_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            cudaFuncSetAttribute(replay_kernel<RSIM_LEAN_WARPS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaFuncSetAttribute(replay_kernel<RSIM_MAX_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            cudaFuncSetAttribute(replay_kernel<RSIM_MAX_WARPS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         });
     }
 
@@ -278,7 +285,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaMalloc(&h->log_n, sizeof(u64)));
     CK(nullptr, cudaMalloc(&h->scores, N * sizeof(double)));
     CK(nullptr, cudaMalloc(&h->scratch_res, 4 * sizeof(i64)));
-    CK(nullptr, cudaMalloc(&h->ctr, 16 * sizeof(u64)));
+    CK(nullptr, cudaMalloc(&h->ctr, 32 * sizeof(u64)));   // [16..23]: RSIM_STEP_PROFILE builds
     CK(nullptr, cudaMalloc(&h->mbox, 2 * 8 * 4 * sizeof(u64)));
     CK(nullptr, cudaMemset(h->mbox, 0, 2 * 8 * 4 * sizeof(u64)));
     h->peer[world > 1 ? c.rank : 0] = h->mbox;
@@ -302,7 +309,7 @@ void rsim_destroy(rsim_t *h) {
     h->rid.free_(); h->blocks.free_(); h->ckeys.free_(); h->okeys.free_();
     h->hit_blocks.free_(); h->chosen.free_();
     void *ps[] = {h->inst, h->qbuf, h->rbuf, h->tkeys, h->tmeta, h->tie, h->errbuf, h->flag, h->log, h->log_n,
-                  h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs};
+                  h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs, h->crit};
     h->arena.free_();
     for (int i = 0; i < 8; i++) if (h->peer_ipc[i] && h->peer[i]) cudaIpcCloseMemHandle(h->peer[i]);
     for (void *p : ps) if (p) cudaFree(p);
@@ -397,7 +404,7 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     cudaLaunchConfig_t lc;
     memset(&lc, 0, sizeof(lc));
     lc.gridDim = dim3(h->C, 1, 1);
-    lc.blockDim = dim3(32 * (h->W + 1), 1, 1);   // + the request-staging warp
+    lc.blockDim = dim3(32 * (h->W + 1), 1, 1);   // + the control warp
     lc.dynamicSmemBytes = h->smem_bytes;
     lc.stream = h->stream;
     cudaLaunchAttribute at[1];
@@ -406,7 +413,10 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     lc.attrs = at;
     lc.numAttrs = 1;
     CK(h, cudaEventRecord(h->ev0, h->stream));
-    CK(h, cudaLaunchKernelEx(&lc, replay_kernel, P, (i64)k0, (i64)k1, (i64)until, mode, target));
+    if (h->W <= RSIM_LEAN_WARPS)
+        CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_LEAN_WARPS>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
+    else
+        CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_MAX_WARPS>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
     h->launches++;
     CK(h, cudaEventRecord(h->ev1, h->stream));
     CK(h, cudaEventSynchronize(h->ev1));
@@ -642,7 +652,7 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
     CK(h, cudaMemsetAsync(h->tmeta, 0, slots * sizeof(Meta), s));
     CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, s));
     CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), s));
-    CK(h, cudaMemsetAsync(h->ctr, 0, 16 * sizeof(u64), s));
+    CK(h, cudaMemsetAsync(h->ctr, 0, 32 * sizeof(u64), s));
     if (h->R > 0) {
         DevArr<i64> *outs[] = {&h->hit_tokens, &h->first_sched, &h->first_token, &h->finish, &h->route_bs, &h->dec_ns};
         for (auto *a : outs) CK(h, cudaMemsetAsync(a->p, 0xff, h->R * sizeof(i64), s));
@@ -673,6 +683,39 @@ rsim_status rsim_read_counters(rsim_t *h, int64_t *out16) {
     CK(h, cudaMemcpy(c, h->ctr, sizeof(c), cudaMemcpyDeviceToHost));
     for (int i = 0; i < 16; i++) out16[i] = (int64_t)c[i];
     out16[4] = h->R; out16[5] = h->nblk; out16[7] = h->N;
+    return RSIM_OK;
+}
+
+rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out8) {
+    if (!h || !out8) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    u64 c[8];
+    CK(h, cudaMemcpy(c, h->ctr + 16, sizeof(c), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 8; i++) out8[i] = (int64_t)c[i];
+    return RSIM_OK;
+}
+
+rsim_status rsim_phase_records(rsim_t *h, int64_t capacity_decisions) {
+    if (!h || capacity_decisions < 0) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    if (h->crit) { cudaFree(h->crit); h->crit = nullptr; }
+    h->crit_cap = 0;
+    if (capacity_decisions == 0) return RSIM_OK;
+    const size_t bytes = (size_t)capacity_decisions * h->C * h->W * 8 * sizeof(unsigned short);
+    CK(h, cudaMalloc(&h->crit, bytes));
+    CK(h, cudaMemset(h->crit, 0, bytes));
+    h->crit_cap = capacity_decisions;
+    return RSIM_OK;
+}
+
+rsim_status rsim_read_phase_records(rsim_t *h, uint16_t *out, int64_t n_decisions, int32_t *warps_per_decision) {
+    if (!h) return RSIM_E_INVALID;
+    if (warps_per_decision) *warps_per_decision = h->C * h->W;
+    if (!out || n_decisions <= 0) return RSIM_OK;
+    if (n_decisions > h->crit_cap) return fail(h, RSIM_E_INVALID, "more decisions than recorded");
+    CK(h, cudaSetDevice(h->cfg.device));
+    CK(h, cudaMemcpy(out, h->crit, (size_t)n_decisions * h->C * h->W * 8 * sizeof(unsigned short),
+                     cudaMemcpyDeviceToHost));
     return RSIM_OK;
 }
 

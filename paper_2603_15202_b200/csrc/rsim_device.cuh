@@ -44,7 +44,8 @@ struct __align__(16) Inst {
     int r, q;         // live running / queued counts
     int v_r, v_q;     // view counts
     int q_head;       // queue ring head index
-    int pad;
+    int tabver;       // bumped whenever the KV$ key set may change (finish inserts / evictions):
+                      // a probe made at version v stays valid while tabver == v
 };
 
 // A request on an instance: one 64-byte record used by the FIFO queue (v =
@@ -106,6 +107,8 @@ struct Params {
     u64 *peer[8];     // every rank's mailbox (peer-mapped), peer[rank] == mbox
     u64 epoch;        // run epoch, distinguishes mailbox contents of successive replays
     i64 timeout_ns;
+    // diagnostics: per (decision, warp) phase record, 8 x u16 (rsim_phase_records); null = off
+    unsigned short *crit; i64 crit_cap;
 };
 
 // ---------------- hashing (hashing.py:15-25) ----------------

@@ -54,6 +54,7 @@ __device__ void finish_one(const Params &P, int gi, Inst &s, i64 a, int B, i64 o
 __device__ void flush_finishers(const Params &P, int gi, Inst &s, FinBuf &F, int nf, i64 end, int lane, int &werr) {
     if (nf == 0 || werr) return;
     const long long c0 = clock64();
+    s.tabver += 1;                                                 // invalidates probes made before this step
     __syncwarp();
     if (P.cap < 0 || s.occ + F.pre[nf] <= P.cap) {
         Table T = table_of(P, gi);
@@ -82,41 +83,92 @@ __device__ __forceinline__ void log_step(const Params &P, int gi, i64 start, i64
     }
 }
 
-// One engine step of instance gi starting at s.next_step. Returns false if
-// the plan was empty (the instance went idle). F is this warp's finisher buffer.
-__device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi, int lane, int &werr, FinBuf &F) {
+// Finisher batch of one step (engine.py:357-361 for every finisher in F): runs
+// on a register copy of the instance and writes back the KV$-side fields only
+// (the step owns the engine-side fields). Out of line: finishes are rare.
+__device__ __noinline__ void finish_batch(const Params &P, Inst *sp, int gi, FinBuf &F, int nf, i64 end, int lane,
+                                          int *werr_sm) {
+    int werr = *werr_sm;
+    __syncwarp();
+    if (lane == 0) werr_sm[1] += 1;                               // WarpBuf.fins (follows werr)
     Inst s = *sp;
-    const i64 t = s.next_step;
-    flush_view(s, t);                                              // form_batch flush, engine.py:293
-    const int ndec = s.r;                                          // running <= max_batch always
+    flush_finishers(P, gi, s, F, nf, end, lane, werr);
+    __syncwarp();
+    if (lane == 0) {
+        sp->occ = s.occ; sp->tabver = s.tabver;
+        sp->r_head = s.r_head; sp->r_tail = s.r_tail; sp->r_tailT = s.r_tailT;
+        if (werr) *werr_sm = werr;
+    }
+    __syncwarp();
+}
+
+// Append the finishers of lane mask fm (lane l's request record at e) to F in
+// lane order -- the reference's order within one ballot -- flushing F first if
+// it would overflow.
+__device__ __forceinline__ void add_finishers(const Params &P, Inst *sp, int gi, FinBuf &F, int &nf, u32 fm,
+                                              const Ent *e, i64 end, int lane, int *werr_sm) {
+    const int cnt = __popc(fm);
+    if (nf + cnt > 32) { finish_batch(P, sp, gi, F, nf, end, lane, werr_sm); nf = 0; }
+    const bool fin = (fm >> lane) & 1u;
+    const int pos = nf + __popc(fm & lanemask_lt());
+    int L = 0;
+    if (fin) {
+        F.a[pos] = e->a; F.oa[pos] = e->oa; F.B[pos] = e->B; F.hb[pos] = e->hb;
+        L = e->L;
+        F.L[pos] = L;
+    }
+    const int prev = nf == 0 ? 0 : F.pre[nf];
+    const int incl = warp_incl_scan(L, lane);
+    __syncwarp();
+    if (lane == 0 && nf == 0) F.pre[0] = 0;
+    if (fin) F.pre[pos + 1] = prev + incl;
+    nf += cnt;
+    __syncwarp();
+}
+
+// One engine step of instance gi starting at its next_step (form_batch +
+// execute_batch, engine.py:291-355). Returns false if the plan was empty (the
+// instance went idle). Queue/running records are read field by field from
+// their (L1-resident) lines instead of being held in registers, so the step
+// needs few registers; lane-uniform engine fields live in registers and go
+// back to shared memory at the end. F is this warp's finisher buffer.
+#ifdef RSIM_STEP_PROFILE
+#define SP_MARK(i) do { const long long _t = clock64(); spc[i] += _t - spt; spt = _t; } while (0)
+#else
+#define SP_MARK(i) do { } while (0)
+#endif
+__device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi, int lane, int *werr_sm, FinBuf &F) {
+#ifdef RSIM_STEP_PROFILE
+    long long spc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, spt = clock64();
+#endif
+    const i64 t = sp->next_step;
+    if (sp->due <= t) {                                            // form_batch flush, engine.py:293
+        __syncwarp();
+        if (lane == 0) flush_view(*sp, t);
+        __syncwarp();
+    }
+    const int ndec = sp->r;                                        // running <= max_batch always
+    const int q = sp->q, qh = sp->q_head;
+    const i64 step_idx = sp->step_idx;
+    const bool fin_step = ndec > 0 && sp->next_finish == step_idx;
     const i64 budget = P.chunk - ndec > 0 ? P.chunk - ndec : 0;   // engine.py:296
     const i64 slots = P.max_batch - ndec;                          // engine.py:297
     QEnt *qb = P.qbuf + ((size_t)gi << P.qlog2);
     REnt *rb = P.rbuf + (size_t)gi * (size_t)P.max_batch;
     const u32 qmask = (1u << P.qlog2) - 1u;
-    const bool fin_step = ndec > 0 && s.next_finish == s.step_idx;
-    // the running list's first 32 records load together with the queue head
-    Ent r0;
-    r0.v = RSIM_NONE;
-    if (fin_step && lane < ndec) r0 = rb[lane];
+    SP_MARK(0);
 
     // pass 1: FIFO plan (_plan_allocations, engine.py:174-184). Entry j is
     // allocated iff j < slots and the budget left before it is positive.
-    // The first 32 entries stay in registers for pass 2.
-    i64 ptok = 0;
+    i64 ptok = 0, v0 = 0;
     int nalloc = 0;
-    Ent e0;
-    e0.v = 0;
     {
         i64 cum = 0;
-        for (int j0 = 0; j0 < s.q && j0 < slots && cum < budget; j0 += 32) {
+        for (int j0 = 0; j0 < q && j0 < slots && cum < budget; j0 += 32) {
             const int j = j0 + lane;
-            const bool valid = j < s.q && j < slots;
-            Ent e;
-            e.v = 0;
-            if (valid) e = qb[(s.q_head + j) & qmask];
-            if (j0 == 0) e0 = e;
-            const i64 p = valid ? e.v : 0;
+            const bool valid = j < q && j < slots;
+            const i64 p = valid ? qb[(qh + j) & qmask].v : 0;
+            if (j0 == 0) v0 = p;
             const i64 incl = warp_incl_scan(p, lane);
             const i64 excl = cum + incl - p;
             const bool alloc = valid && excl < budget;
@@ -129,14 +181,16 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         }
     }
     if (nalloc == 0 && ndec == 0) {                                // empty plan: instance goes idle
-        s.next_step = RSIM_NONE;
         __syncwarp();
-        if (lane == 0) *sp = s;
+        if (lane == 0) sp->next_step = RSIM_NONE;
         __syncwarp();
         return false;
     }
+    SP_MARK(1);
+    i64 dcs = sp->dcs;
     const i64 pre = prefill_cost_us(P, ptok);
-    const i64 end = t + pre + decode_cost_us(P, ndec, s.dcs);      // ctx = sum(in+gen) over decode = dcs
+    const i64 end = t + pre + decode_cost_us(P, ndec, dcs);       // ctx = sum(in+gen) over decode = dcs
+    SP_MARK(2);
 
     // pass 2: apply allocations (engine.py:314-319); pops = allocated entries
     // left with pending == 0 (a prefix of the allocation)
@@ -146,143 +200,146 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         for (int j0 = 0; j0 < nalloc; j0 += 32) {
             const int j = j0 + lane;
             const bool alloc = j < nalloc;
-            Ent e = e0;
-            if (j0 > 0 && alloc) e = qb[(s.q_head + j) & qmask];
-            const i64 p = alloc ? e.v : 0;
+            QEnt *e = qb + ((qh + j) & qmask);
+            const i64 p = alloc ? (j0 == 0 ? v0 : e->v) : 0;
             const i64 incl = warp_incl_scan(p, lane);
             const i64 excl = cum + incl - p;
             const i64 take = alloc ? min(budget - excl, p) : 0;
             if (alloc) {
-                if (!(e.flags & 1)) P.first_sched[e.req] = t;
-                if (p - take != 0) {                        // a popped record is consumed below as is
-                    Ent u = e;
-                    u.v = p - take;
-                    u.flags |= 1;
-                    qb[(s.q_head + j) & qmask] = u;
-                }
+                const int flags = e->flags;
+                if (!(flags & 1)) P.first_sched[e->req] = t;
+                if (p - take != 0) { e->v = p - take; e->flags = flags | 1; }   // a popped record is consumed as is
             }
             npop += __popc(__ballot_sync(FULL, alloc && p - take == 0));
             cum += __shfl_sync(FULL, incl, 31);
         }
     }
-    s.pend -= ptok;
-    __syncwarp();
-
+    i64 total = sp->total + npop;
     int nf = 0;
-    auto add_fin = [&](const Ent &f) {
-        if (nf == 32) { flush_finishers(P, gi, s, F, nf, end, lane, werr); nf = 0; }
-        if (lane == 0) {
-            if (nf == 0) F.pre[0] = 0;
-            F.a[nf] = f.a; F.oa[nf] = f.oa; F.B[nf] = f.B; F.L[nf] = f.L; F.hb[nf] = f.hb;
-            F.pre[nf + 1] = F.pre[nf] + f.L;
-        }
-        nf++;
-    };
+    SP_MARK(3);
 
     // queue heads with pending == 0 get their first token (engine.py:321-331);
     // out == 1 finishes right away, in pop order.
-    const int head0 = s.q_head;
-    s.total += npop;
     for (int j0 = 0; j0 < npop; j0 += 32) {
         const int j = j0 + lane;
         const bool pop = j < npop;
-        Ent e = e0;
-        if (j0 > 0 && pop) e = qb[(head0 + j) & qmask];
-        if (pop) P.first_token[e.req] = end;
-        u32 fm = __ballot_sync(FULL, pop && e.out == 1);
-        while (fm) {
-            const int l = __ffs(fm) - 1;
-            fm &= fm - 1;
-            const Ent f = shfl_ent(e, l);
-            if (lane == 0) P.finish[f.req] = end;
-            s.total -= f.in + 1;
-            add_fin(f);
+        const QEnt *e = qb + ((qh + j) & qmask);
+        bool fin = false;
+        if (pop) {
+            const int req = e->req;
+            P.first_token[req] = end;
+            fin = e->out == 1;
+            if (fin) P.finish[req] = end;
+        }
+        const u32 fm = __ballot_sync(FULL, fin);
+        if (fm) {
+            total -= warp_sum(fin ? e->in + 1 : (i64)0);
+            add_finishers(P, sp, gi, F, nf, fm, e, end, lane, werr_sm);
         }
     }
-    s.q_head = (s.q_head + npop) & (int)qmask;
-    s.q -= npop;
 
+    SP_MARK(4);
     // decode (engine.py:333-347): every running request gains a token; those
     // whose finish step is now leave in running order.
-    s.total += ndec;
-    s.dcs += ndec;
+    total += ndec;
+    dcs += ndec;
+    int r = ndec;
+    i64 nfin = sp->next_finish;
     if (fin_step) {
         int w = 0;
         i64 nf_step = RSIM_NONE;
         for (int j0 = 0; j0 < ndec; j0 += 32) {
             const int j = j0 + lane;
             const bool valid = j < ndec;
-            Ent e = r0;
-            if (j0 > 0) { e.v = RSIM_NONE; if (valid) e = rb[j]; }
-            __syncwarp();
-            const bool fin = valid && e.v == s.step_idx;
+            REnt *e = rb + j;
+            const i64 v = valid ? e->v : RSIM_NONE;
+            const bool fin = valid && v == step_idx;
             const bool keep = valid && !fin;
             const u32 km = __ballot_sync(FULL, keep);
-            if (keep) {
-                const int dst = w + __popc(km & lanemask_lt());
-                if (dst != j) rb[dst] = e;
-                nf_step = e.v < nf_step ? e.v : nf_step;
+            const int dst = w + __popc(km & lanemask_lt());
+            const bool move = keep && dst != j;
+            if (keep) nf_step = v < nf_step ? v : nf_step;
+            const u32 fm = __ballot_sync(FULL, fin);
+            if (fm) {
+                i64 gone = 0;
+                if (fin) { gone = e->in + e->out; P.finish[e->req] = end; }   // generated == out at finish
+                gone = warp_sum(gone);
+                dcs -= gone;
+                total -= gone;
+                add_finishers(P, sp, gi, F, nf, fm, e, end, lane, werr_sm);
             }
-            w += __popc(km);
-            u32 fm = __ballot_sync(FULL, fin);
-            while (fm) {
-                const int l = __ffs(fm) - 1;
-                fm &= fm - 1;
-                const Ent f = shfl_ent(e, l);
-                const i64 gone = f.in + f.out;                     // generated == out at finish
-                if (lane == 0) P.finish[f.req] = end;
-                s.dcs -= gone;
-                s.total -= gone;
-                add_fin(f);
+            if (__any_sync(FULL, move)) {                  // compact: all reads of this chunk before any write
+                ulonglong2 c0, c1, c2, c3;
+                const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(e);
+                if (move) { c0 = src[0]; c1 = src[1]; c2 = src[2]; c3 = src[3]; }
+                __syncwarp();
+                if (move) {
+                    ulonglong2 *d = reinterpret_cast<ulonglong2 *>(rb + dst);
+                    d[0] = c0; d[1] = c1; d[2] = c2; d[3] = c3;
+                }
             }
             __syncwarp();
+            w += __popc(km);
         }
-        s.r = w;
-        s.next_finish = warp_min_i64(nf_step);
+        r = w;
+        nfin = warp_min_i64(nf_step);
     }
-    flush_finishers(P, gi, s, F, nf, end, lane, werr);
+    SP_MARK(5);
+    if (nf) finish_batch(P, sp, gi, F, nf, end, lane, werr_sm);
+    SP_MARK(6);
 
     // popped requests with out > 1 join the running list (after the removals)
-    {
-        i64 nfin = s.next_finish;
-        for (int j0 = 0; j0 < npop; j0 += 32) {
-            const int j = j0 + lane;
-            const bool pop = j < npop;
-            Ent e = e0;
-            if (j0 > 0 && pop) e = qb[(head0 + j) & qmask];
-            const bool join = pop && e.out > 1;
-            const u32 jm = __ballot_sync(FULL, join);
-            if (join) {
-                e.v = s.step_idx + e.out - 1;
-                rb[s.r + __popc(jm & lanemask_lt())] = e;
-                nfin = e.v < nfin ? e.v : nfin;
-            }
-            s.dcs += warp_sum(join ? e.in + 1 : (i64)0);
-            s.r += __popc(jm);
+    for (int j0 = 0; j0 < npop; j0 += 32) {
+        const int j = j0 + lane;
+        const bool pop = j < npop;
+        const QEnt *e = qb + ((qh + j) & qmask);
+        const int out = pop ? e->out : 0;
+        const bool join = pop && out > 1;
+        const u32 jm = __ballot_sync(FULL, join);
+        i64 din = 0;
+        if (join) {
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(e);
+            ulonglong2 c0 = src[0], c1 = src[1], c2 = src[2], c3 = src[3];
+            const i64 fstep = step_idx + out - 1;
+            din = (i64)c0.y + 1;                           // in + 1
+            c0.x = (u64)fstep;                             // v = finish step
+            ulonglong2 *d = reinterpret_cast<ulonglong2 *>(rb + r + __popc(jm & lanemask_lt()));
+            d[0] = c0; d[1] = c1; d[2] = c2; d[3] = c3;
+            nfin = fstep < nfin ? fstep : nfin;
         }
-        s.next_finish = warp_min_i64(nfin);
+        dcs += warp_sum(din);
+        r += __popc(jm);
     }
+    if (npop) nfin = warp_min_i64(nfin);
 
-    s.busy_until = end;                                            // engine.py:349-352
-    s.due = end;
-    s.next_step = end;
-    log_step(P, gi, t, end, pre, (i64)s.q + s.r, s.step_idx, lane);
-    s.step_idx += 1;
     __syncwarp();
-    if (lane == 0) *sp = s;
+    if (lane == 0) {
+        sp->q_head = (qh + npop) & (int)qmask;
+        sp->q = q - npop;
+        sp->r = r;
+        sp->pend -= ptok;
+        sp->total = total;
+        sp->dcs = dcs;
+        sp->next_finish = nfin;
+        sp->busy_until = end;                                      // engine.py:349-352
+        sp->due = end;
+        sp->next_step = end;
+        sp->step_idx = step_idx + 1;
+    }
+    log_step(P, gi, t, end, pre, (i64)(q - npop) + r, step_idx, lane);
     __syncwarp();
+    SP_MARK(7);
+#ifdef RSIM_STEP_PROFILE
+    if (P.ctr != nullptr && lane == 0)
+        for (int i = 0; i < 8; i++) atomicAdd(P.ctr + 16 + i, (u64)spc[i]);
+#endif
     return true;
 }
 
-// Non-inlined entry used by the replay loop: the error word lives in shared
-// memory so no caller register has its address taken.
-__device__ __noinline__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int *werr_sm, FinBuf &F) {
-    int werr = *werr_sm;
+// Entry used by the replay loop (counts SM cycles in engine steps when profiling).
+__device__ __forceinline__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int *werr_sm, FinBuf &F) {
     const long long c0 = clock64();
-    const bool ran = inst_step_body(P, sp, gi, lane, werr, F);
+    const bool ran = inst_step_body(P, sp, gi, lane, werr_sm, F);
     if (P.ctr != nullptr && lane == 0) atomicAdd(P.ctr + 2, (u64)(clock64() - c0));   // SM cycles in engine steps
-    __syncwarp();
-    if (lane == 0 && werr) *werr_sm = werr;
-    __syncwarp();
     return ran;
 }

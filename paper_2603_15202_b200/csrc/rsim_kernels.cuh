@@ -86,7 +86,7 @@ __device__ __forceinline__ void mbar_arrive_expect(u64 *mb, u32 bytes) {
 }
 __device__ __forceinline__ bool mbar_try_wait(u64 *mb, u32 parity) {
     u32 ok;
-    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_addr(mb)), "r"(parity) : "memory");
     return ok != 0;
 }
@@ -175,7 +175,7 @@ __device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, c
 enum { MODE_REPLAY = 0, MODE_DRAIN = 1, MODE_ROUTE = 2, MODE_ENQUEUE = 3 };
 
 // One decision's request, staged once per CTA in shared memory by the CTA's
-// loader warp, two decisions ahead (slot k % 4).
+// control warp, up to RSIM_SLOTS-1 decisions ahead (slot k % RSIM_SLOTS).
 struct __align__(16) ReqStage {
     i64 t, a, in, oa;
     int B, out;
@@ -186,11 +186,15 @@ struct __align__(16) Dec { int owner_warp; int kk; int err; int pad; };
 
 // Per-warp hand-off state between the phases of a decision.
 struct __align__(16) WarpBuf {
-    int slot[2][128];      // probe-found table slot per depth of the warp's first two instances (commit reuses them)
-    int hit[32];           // hit blocks of each of the warp's instances
+    int slot[2][2][128];   // [decision parity][instance 0/1][depth]: probe-found table slots of the
+                           // warp's first two instances (the commit reuses them instead of a lookup)
+    int hit[32];           // hit blocks of each of the warp's instances for the current decision
+    int sph[32];           // probe-ahead: hit blocks for decision spk, made at table version spver
+    int spver[32];
+    i64 spk;               // decision the probe-ahead results belong to (-1: none)
     FinBuf fin;            // finishers of one engine step
     u64 c_bytes, c_steps;  // algorithmic probe bytes / engine steps of this warp
-    int werr, pad;         // first device error seen by this warp
+    int werr, fins;        // first device error seen by this warp; finisher batches run
 };
 
 // counter mod T for the 128-bit TieBreaker counter (hi:lo) without a 128-bit
@@ -206,10 +210,12 @@ __device__ __forceinline__ u32 mod_counter(u64 lo, u64 hi, u32 T) {
     return (u32)r;
 }
 
-#define RSIM_SLOTS 8            // request staging ring depth (loader runs up to 6 decisions ahead)
-#define RSIM_MAX_WARPS 8
+#define RSIM_SLOTS 8            // request staging ring depth
+#define RSIM_MAX_WARPS 8        // instance warps per CTA (+1 control warp)
+#define RSIM_LEAN_WARPS 7       // up to 7 instance warps: 8 warps per CTA = 2 per SM sub-partition,
+                                // which lifts the register budget from 168 to 255 per thread
 
-// ---- loader: stage decision k's request (scalars + first 128 chain keys)
+// ---- control warp: stage decision k's request (scalars + first 128 chain keys)
 __device__ __noinline__ void stage_request(const Params &P, ReqStage &R, i64 k, int mode, i64 until, int lane) {
     const i64 a = P.blk_off[k], e = P.blk_off[k + 1];
     const i64 t = (mode == MODE_REPLAY) ? P.arrival[k] : until;
@@ -239,21 +245,27 @@ __device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base,
     }
 }
 
-// ---- probe + score this warp's instances (cluster.py:106-128, policies.py:117-139).
-// Short prompts are probed several instances at a time: the warp splits into G
-// lane groups of LP = 32/G lanes, lane li of group g probing depths j*LP+li
-// (j < 4) of instance s0+g, so one round trip and one instruction stream
-// cover G instances. Lane s returns instance s's score bits (~0 = not a
-// candidate); hit blocks go to WB.hit, found slots of instances 0/1 to WB.slot.
-__device__ __forceinline__ u64 probe_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
-                                           int mode, int target, int lane, WarpBuf &WB) {
-    const i64 t = R.t, in = R.in;
+// ---- probe this warp's instances (cluster.py:106-128 -> kvcache.py:65-74): longest
+// present prefix of request R in each instance's table, for instances not in
+// `skip`. Short prompts are probed several instances at a time: the warp splits
+// into G lane groups of LP = 32/G lanes, lane li of group g probing depths
+// j*LP+li (j < 4) of instance s0+g, so one round trip and one instruction
+// stream cover G instances. Hit blocks go to hout[s]; found slots of
+// instances 0/1 to slot[s][depth].
+__device__ __forceinline__ void probe_hits(const Params &P, int base, int l0, int n, const ReqStage &R, int mode,
+                                           int target, u32 skip, int lane, int *hout, int (*slot)[128]) {
     const int B = R.B;
     const int Bc = min(B, 128);
     const int G = Bc <= 32 ? 4 : (Bc <= 64 ? 2 : 1);       // instances per round (warp-uniform)
     const int LP = 32 / G, DS = (Bc + LP - 1) / LP;         // lanes per instance, depth slots per lane
     const int g = lane / LP, li = lane - g * LP;
     const u32 gmask = LP == 32 ? FULL : ((1u << LP) - 1u);
+    u32 need = (n >= 32 ? FULL : ((1u << n) - 1u)) & ~skip;
+    if (mode == MODE_ENQUEUE) {
+        const int tl = target - base - l0;
+        need &= (tl >= 0 && tl < n) ? (1u << tl) : 0u;
+    }
+    if (need == 0) return;
     u64 kk[4];
     u32 hm[4];
     bool vd[4];
@@ -264,14 +276,11 @@ __device__ __forceinline__ u64 probe_phase(const Params &P, Inst *st, int base, 
         kk[j] = vd[j] ? R.keys[d] : 0;
         hm[j] = vd[j] ? R.home[d] : 0;
     }
-    u64 mybits = ~0ULL;
-    u32 cb = 0;                       // algorithmic probe bytes of my group's instances
     for (int s0 = 0; s0 < n; s0 += G) {
+        if (((need >> s0) & ((1u << G) - 1u)) == 0) continue;          // warp-uniform
         const int s = s0 + g;
-        const bool have = s < n;
-        const int gi = base + l0 + (have ? s : s0);
-        const bool cand = have && ((mode != MODE_ENQUEUE) || gi == target);
-        const Table T = table_of(P, gi);
+        const bool cand = s < n && ((need >> s) & 1u);
+        const Table T = table_of(P, base + l0 + (s < n ? s : s0));
         ulonglong2 pr[4];
 #pragma unroll
         for (int j = 0; j < 4; j++)
@@ -292,7 +301,7 @@ __device__ __forceinline__ u64 probe_phase(const Params &P, Inst *st, int base, 
                 } else if (f) {
                     sl = (int)((hm[j] & 1u) == 0 && pr[j].x == kk[j] ? hm[j] : hm[j] | 1u);
                 }
-                if (s < 2 && vd[j]) WB.slot[s][j * LP + li] = sl;
+                if (cand && s < 2 && vd[j]) slot[s][j * LP + li] = sl;
                 mk[j] = __ballot_sync(FULL, f);
             }
         }
@@ -308,29 +317,32 @@ __device__ __forceinline__ u64 probe_phase(const Params &P, Inst *st, int base, 
         }
         if (G == 1 && h >= 128 && B > 128) h = deep_match(T, P.ckeys + R.a, B, lane);   // G == 1: warp-uniform
         h = min(h, B);
-        u64 bits = ~0ULL;
-        if (cand && li == 0) {
-            Inst *sp = st + l0 + s;
-            if (sp->due <= t) flush_view(*sp, t);        // snapshot() flushes every candidate (indicators.py:36-65)
-            const double sc = score_of(P, *sp, h, in);
-            bits = (u64)__double_as_longlong(sc);
-            WB.hit[s] = h;
-            if (P.scores != nullptr) P.scores[gi] = sc;
-            // one 8-B key compare per reference dict lookup + 16 B of view
-            cb += 8u * (u32)min(h + 1, B) + 16u;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            if (q < G) {
-                const u64 v = __shfl_sync(FULL, bits, q * LP);
-                if (lane == s0 + q) mybits = v;
-            }
-        }
+        if (cand && li == 0) hout[s] = h;
+    }
+    __syncwarp();
+}
+
+// ---- score this warp's instances from their hit blocks (policies.py:117-139); lane s
+// handles instance s and returns its score bits (~0 = not a candidate).
+__device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
+                                           int mode, int target, int lane, WarpBuf &WB) {
+    const int gi = base + l0 + lane;
+    const bool cand = lane < n && ((mode != MODE_ENQUEUE) || gi == target);
+    u64 bits = ~0ULL;
+    u32 cb = 0;
+    if (cand) {
+        Inst *sp = st + l0 + lane;
+        if (sp->due <= R.t) flush_view(*sp, R.t);        // snapshot() flushes every candidate (indicators.py:36-65)
+        const int h = WB.hit[lane];
+        const double sc = score_of(P, *sp, h, R.in);
+        bits = (u64)__double_as_longlong(sc);
+        if (P.scores != nullptr) P.scores[gi] = sc;
+        // one 8-B key compare per reference dict lookup + 16 B of view
+        cb = 8u * (u32)min(h + 1, R.B) + 16u;
     }
     cb = __reduce_add_sync(FULL, cb);
     if (lane == 0) WB.c_bytes += cb;
-    __syncwarp();
-    return mybits;
+    return bits;
 }
 
 // TieBreaker counter at decision time = c0 + ties, c0 the launch-start value: counter mod T
@@ -442,21 +454,30 @@ __device__ __forceinline__ void bar_warps(int nthreads) {       // named barrier
 // ---------------------------------------------------------------- replay
 // Persistent launch over a cluster of C CTAs (C <= 16, one instance shard per
 // CTA, engine state in shared memory, warps 0..W-1 own ipw instances each).
-// Warp W of every CTA is a decoupled request loader: it stages requests into a
-// shared-memory ring up to RSIM_SLOTS-1 decisions ahead and never joins the
-// decision barriers. Per decision: every instance warp drains and probes its
-// instances and pushes one (min score, tie count) partial into every CTA of
-// the cluster with st.async (completing tx-bytes on the receiver's mbarrier);
-// non-candidate instances are drained to the next arrival while the partials
-// are in flight; warp 0 of every CTA derives the same winner; one named
-// barrier releases the owning warp, which commits. No host round trip.
-__global__ void __launch_bounds__(32 * (RSIM_MAX_WARPS + 1), 1)
-replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
+// Warp W of every CTA is the control warp: it stages requests into a
+// shared-memory ring up to RSIM_SLOTS-1 decisions ahead and decides. Per
+// decision k every instance warp
+//   1. advances its instances through the engine steps starting before t_k,
+//   2. takes each instance's hit blocks from the probe-ahead made during
+//      decision k-1 when the instance's KV$ key set is unchanged since
+//      (tabver), and probes the rest,
+//   3. scores its instances and pushes one (min score, tie count) partial into
+//      every CTA of the cluster with st.async (completing tx-bytes on the
+//      receiver's mbarrier),
+//   4. while the partials are in flight: advances instances that cannot win
+//      k to t_{k+1}, then probes request k+1 against every instance
+//      (probe-ahead; a commit only touches/pins, it never changes the key set),
+// and the control warp of every CTA waits for the C*W partials, derives the
+// same winner and releases the CTA through one barrier; the owning warp
+// commits. No host round trip.
+template <int MAXW>
+__global__ void __launch_bounds__(32 * (MAXW + 1), 1)
+replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = P.C, W = P.W, ipw = P.ipw, CW = P.C * P.W;
     const int cta = (C > 1) ? (int)cluster_ctarank() : 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool loader = warp == W;
+    const bool control = warp == W;
     const int base = cta * P.per_cta;
     const int nloc = max(0, min(P.per_cta, P.N - base));
     Inst *st = (Inst *)smem;
@@ -464,10 +485,10 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
     ReqStage *rq = (ReqStage *)(part + 2 * CW);            // [RSIM_SLOTS] request ring (k % RSIM_SLOTS)
     Dec *dec = (Dec *)(rq + RSIM_SLOTS);                   // [2]
     u64 *mb = (u64 *)(dec + 2);                            // [2] partial-exchange mbarriers
-    volatile i64 *ctl = (volatile i64 *)(mb + 2);          // [0] staged_upto [1] freed_upto [2] abort
+    volatile i64 *ctl = (volatile i64 *)(mb + 2);          // [0] staged_upto
     u32 *modtab = (u32 *)(mb + 6);                         // [RSIM_MODTAB] launch counter mod T
     WarpBuf *wbuf = (WarpBuf *)(modtab + RSIM_MODTAB);     // [W]
-    WarpBuf &WB = wbuf[loader ? 0 : warp];
+    WarpBuf &WB = wbuf[control ? 0 : warp];
 
     {   // load this CTA's instance shard
         const u64 *src = (const u64 *)(P.inst + base);
@@ -476,56 +497,86 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     }
     const u64 c0_lo = P.tie[0], c0_hi = P.tie[1];          // TieBreaker counter at launch
-    u32 ties = 0;                                          // ties resolved in this launch (warp 0)
+    u32 ties = 0;                                          // ties resolved in this launch (control warp)
     const int l0 = warp * ipw;
-    const int nmine = loader ? 0 : max(0, min(ipw, nloc - l0));
-    if (!loader && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; }
+    const int nmine = control ? 0 : max(0, min(ipw, nloc - l0));
+    if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; }
     if (threadIdx.x == 0) {
         mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_fence_init();
-        ctl[0] = k0; ctl[1] = k0; ctl[2] = 0;
+        ctl[0] = k0;
     }
-    u32 mb_phase[2] = {0u, 0u};                            // tracked by warp 0
     if (mode != MODE_DRAIN)
         for (int T = threadIdx.x; T < RSIM_MODTAB; T += blockDim.x) modtab[T] = T > 1 ? mod_counter(c0_lo, c0_hi, (u32)T) : 0u;
     __syncthreads();
     if (C > 1) cluster_sync_all();
 
+    // per-phase SM-cycle accounting of CTA 0 (ctr[8..15]): warp 0: staging wait, drain,
+    // probe + score, publish + advance + probe-ahead, -, -, decision wait, commit;
+    // control warp: exchange wait (4), decide (5)
+    const bool prof = P.ctr != nullptr && cta == 0 && (warp == 0 || control);
+    u64 ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tc = clock64();
+#define PHASE(i) do { if (prof) { const long long t2 = clock64(); ph[i] += (u64)(t2 - tc); tc = t2; } } while (0)
     if (mode == MODE_DRAIN) {
-        if (!loader) drain_phase(P, st, base, l0, nmine, until, 0u, lane, WB);
-    } else if (loader) {
-        // ---- decoupled loader: keep the ring filled ahead of the decisions
-        i64 kk = k0;
-        while (kk < k1 && ctl[2] == 0) {
-            const i64 lim = min(k1, ctl[1] + RSIM_SLOTS);  // slot of decision j is reused once j-SLOTS is freed
-            if (kk >= lim) { __nanosleep(64); continue; }
-            stage_request(P, rq[kk % RSIM_SLOTS], kk, mode, until, lane);
+        if (!control) drain_phase(P, st, base, l0, nmine, until, 0u, lane, WB);
+    } else if (control) {
+        // ---- control warp: stage ahead, then per decision wait for the partials and decide
+        u32 mb_phase[2] = {0u, 0u};
+        i64 staged = k0;
+        auto stage_upto = [&](i64 lim) {
+            lim = min(lim, k1);
+            if (staged >= lim) return;
+            while (staged < lim) { stage_request(P, rq[staged % RSIM_SLOTS], staged, mode, until, lane); staged++; }
             __threadfence_block();
             __syncwarp();
-            kk += 1;
-            if (lane == 0) ctl[0] = kk;
-        }
-    } else {
-        // per-phase SM-cycle accounting of CTA 0 / warp 0 (ctr[8..15]): staging wait,
-        // drain, probe, publish + speculative drain, exchange wait, decide, barrier, commit
-        const bool prof = P.ctr != nullptr && cta == 0 && warp == 0;
-        u64 ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        long long tc = clock64();
-#define PHASE(i) do { if (prof) { const long long t2 = clock64(); ph[i] += (u64)(t2 - tc); tc = t2; } } while (0)
-        i64 staged_seen = k0;
+            if (lane == 0) ctl[0] = staged;
+            __syncwarp();
+        };
+        stage_upto(k0 + RSIM_SLOTS - 1);
         for (i64 k = k0; k < k1; k++) {
             const int par = (int)(k & 1);
-            if (staged_seen <= k + 1) {                     // request k (and k+1) staged? normally long done
+            tc = clock64();
+            if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * 16));
+            while (!mbar_try_wait(&mb[par], mb_phase[par])) { }
+            mb_phase[par] ^= 1u;
+            PHASE(4);
+            decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane);
+            PHASE(5);
+            bar_warps(32 * (W + 1));
+            if (dec[par].err) break;
+            // decisions < k are committed (their warps reached this barrier): their slots are free
+            stage_upto(k - 1 + RSIM_SLOTS);
+        }
+    } else {
+        i64 staged_seen = k0;
+        long long t_rel = clock64();                        // release of this warp for decision k
+        for (i64 k = k0; k < k1; k++) {
+            const int par = (int)(k & 1);
+            const u64 steps0 = WB.c_steps;
+            const int fins0 = WB.fins;
+            if (staged_seen <= k) {                         // request k staged? normally long done
                 while ((staged_seen = ctl[0]) <= k) { }
                 __threadfence_block();
             }
             const ReqStage &R = rq[k % RSIM_SLOTS];
             PHASE(0);
+            const long long t_a = clock64();
             // ---- K4: advance my instances through steps starting before t
             if (mode == MODE_REPLAY) drain_phase(P, st, base, l0, nmine, R.t, 0u, lane, WB);
             PHASE(1);
-            // ---- K2: probe + score
-            const u64 mybits = probe_phase(P, st, base, l0, nmine, R, mode, target, lane, WB);
+            const long long t_b = clock64();
+            // ---- K2: hit blocks (probe-ahead where still valid) + score
+            u32 skip = 0;
+            if (WB.spk == k) {
+                const bool ok = lane < nmine && st[l0 + lane].tabver == WB.spver[lane];
+                if (ok) WB.hit[lane] = WB.sph[lane];
+                skip = __ballot_sync(FULL, ok);
+            }
+            __syncwarp();
+            probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
+            const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB);
             PHASE(2);
+            const long long t_c = clock64();
             if (cta == 0 && warp == 0 && lane == 0) WB.c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once
             const u32 whi = __reduce_min_sync(FULL, (u32)(mybits >> 32));
             const u64 wmin = ((u64)whi << 32) | __reduce_min_sync(FULL, (u32)(mybits >> 32) == whi ? (u32)mybits : ~0u);
@@ -533,38 +584,37 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
             {   // publish this warp's partial to every CTA of the cluster
                 const u64 w1 = ((u64)(u32)WB.werr << 32) | (u32)__popc(tmask);
                 Part *dst = part + par * CW + cta * W + warp;
-                if (C == 1) {
-                    if (lane == 0) { Part q; q.minb = wmin; q.cnt = (u32)w1; q.err = (u32)(w1 >> 32); *dst = q; }
-                } else if (lane < C) {
-                    st_async_16(dst, &mb[par], (u32)lane, wmin, w1);
-                }
+                if (lane < C) st_async_16(dst, &mb[par], (u32)lane, wmin, w1);
             }
-            if (C == 1) bar_warps(32 * W);
-            // instances that cannot win this decision advance to the next arrival meanwhile
-            if (mode == MODE_REPLAY && k + 1 < k1 && staged_seen > k + 1) {
-                u32 skip = 0;
-                for (int s = 0; s < nmine; s++)
-                    if (__shfl_sync(FULL, mybits, s) == wmin) skip |= 1u << s;
-                drain_phase(P, st, base, l0, nmine, rq[(k + 1) % RSIM_SLOTS].t, skip, lane, WB);
+            if (P.crit != nullptr && lane == 0 && k - k0 < P.crit_cap) {   // diagnostics: where this warp's latency went
+                const long long t_d = clock64();
+                auto q16 = [](long long c) { c >>= 4; return (unsigned short)(c > 65535 ? 65535 : (c < 0 ? 0 : c)); };
+                unsigned short *rec = P.crit + ((size_t)(k - k0) * CW + cta * W + warp) * 8;
+                rec[0] = q16(t_d - t_rel); rec[1] = q16(t_b - t_a); rec[2] = q16(t_c - t_b); rec[3] = q16(t_a - t_rel);
+                rec[4] = (unsigned short)min((u64)65535, WB.c_steps - steps0); rec[5] = (unsigned short)(WB.fins - fins0);
+                rec[6] = (unsigned short)__popc(skip); rec[7] = (unsigned short)nmine;
+            }
+            if (mode == MODE_REPLAY && k + 1 < k1) {
+                if (staged_seen <= k + 1) { staged_seen = ctl[0]; __threadfence_block(); }
+                if (staged_seen > k + 1) {
+                    const ReqStage &R1 = rq[(k + 1) % RSIM_SLOTS];
+                    // instances that cannot win this decision advance to the next arrival meanwhile
+                    const u32 adv = __ballot_sync(FULL, lane < nmine && mybits != wmin);
+                    if (adv) drain_phase(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
+                    // probe-ahead of request k+1 (valid while the instance's tabver holds)
+                    probe_hits(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph, WB.slot[par ^ 1]);
+                    if (lane < nmine) WB.spver[lane] = st[l0 + lane].tabver;
+                    if (lane == 0) WB.spk = k + 1;
+                    __syncwarp();
+                }
             }
             PHASE(3);
-            if (warp == 0) {
-                if (C > 1) {            // all C*W partials of decision k have landed in this CTA
-                    if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * 16));
-                    while (!mbar_try_wait(&mb[par], mb_phase[par])) { }
-                    mb_phase[par] ^= 1u;
-                }
-                PHASE(4);
-                decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane);
-                PHASE(5);
-            }
-            bar_warps(32 * W);
+            bar_warps(32 * (W + 1));
             PHASE(6);
-            if (warp == 0 && lane == 0) ctl[1] = k;         // decision k-1's slot is free again
+            t_rel = clock64();
             const Dec d = dec[par];
             if (d.err) {
                 if (lane == 0 && WB.werr == 0) WB.werr = d.err;
-                if (warp == 0 && lane == 0) ctl[2] = 1;     // release the loader
                 break;
             }
             if (warp == d.owner_warp) {
@@ -575,7 +625,7 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
                 for (int q = 0; q < 4; q++) kk0[q] = (32 * q + lane < R.B) ? R.keys[32 * q + lane] : 0;
                 int cs[4];
 #pragma unroll
-                for (int q = 0; q < 4; q++) cs[q] = (s < 2 && 32 * q + lane < min(R.B, 128)) ? WB.slot[s][32 * q + lane] : -1;
+                for (int q = 0; q < 4; q++) cs[q] = (s < 2 && 32 * q + lane < min(R.B, 128)) ? WB.slot[par][s][32 * q + lane] : -1;
                 int werr = 0;
                 commit(P, st + l0 + s, base + l0 + s, k, h, R.t, kk0, s < 2 ? cs : nullptr, R.a, R.B, R.in, R.out,
                        R.oa, lane, werr);
@@ -584,10 +634,10 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
             }
             PHASE(7);
         }
-#undef PHASE
-        if (prof && lane == 0)
-            for (int i = 0; i < 8; i++) atomicAdd(P.ctr + 8 + i, ph[i]);
     }
+#undef PHASE
+    if (prof && lane == 0)
+        for (int i = 0; i < 8; i++) if (ph[i]) atomicAdd(P.ctr + 8 + i, ph[i]);
     // write back
     __syncthreads();
     {
@@ -596,14 +646,14 @@ replay_kernel(Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
         const int words = nloc * (int)(sizeof(Inst) / 8);
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     }
-    if (!loader && lane == 0) {
+    if (!control && lane == 0) {
         if (WB.werr) atomicCAS(P.err, 0, WB.werr);
         if (P.ctr != nullptr) {
             if (WB.c_bytes) atomicAdd(P.ctr + 0, WB.c_bytes);
             if (WB.c_steps) atomicAdd(P.ctr + 1, WB.c_steps);
         }
     }
-    if (cta == 0 && threadIdx.x == 0 && mode != MODE_DRAIN) {
+    if (cta == 0 && control && lane == 0 && mode != MODE_DRAIN) {
         const u64 lo = c0_lo + ties;
         P.tie[0] = lo;
         P.tie[1] = c0_hi + (lo < c0_lo);
@@ -642,6 +692,7 @@ __global__ void cache_op_kernel(Params P, int gi, int op, i64 a0, int n, i64 now
         return;
     }
     Inst s = P.inst[gi];
+    s.tabver += 1;
     if (n > 0) {
         Run r; r.T = now; r.a = a0; r.oa = 0; r.B = n; r.dhi = n; r.kind = 1; r.pad = 0;
         run_add(P, s, gi, r, lane, werr);

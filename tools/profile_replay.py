@@ -34,6 +34,32 @@ if world > 1:
         print(f"{name} R={len(trace)} world={world} ctas={c} warps={w}: total {best:.2f} ms "
               f"({1000 * best / len(trace):.2f} us/decision)", flush=True)
     sys.exit(0)
+def critpath(h, n):
+    """Per decision: the warp whose partial came last (largest release->publish latency) and why."""
+    import numpy as np
+    h.phase_records(n)
+    h.rerun()
+    rec = h.read_phase_records(n).astype(np.float64)          # [n, warps, 8]
+    lat = rec[:, :, 0]
+    mx = lat.argmax(axis=1)
+    top = rec[np.arange(n), mx]                                # record of the slowest warp
+    med = np.median(lat, axis=1)
+    print(f"   critical warp (cycles): latency {16 * top[:, 0].mean():.0f} (median warp {16 * med.mean():.0f})"
+          f"  stage-wait {16 * top[:, 3].mean():.0f}  drain {16 * top[:, 1].mean():.0f}  probe+score {16 * top[:, 2].mean():.0f}"
+          f"  rest {16 * (top[:, 0] - top[:, 1] - top[:, 2] - top[:, 3]).mean():.0f}", flush=True)
+    print(f"   critical warp: steps {top[:, 4].mean():.2f}/decision, finisher batches {top[:, 5].mean():.2f}, "
+          f"probe-ahead used {top[:, 6].sum() / max(top[:, 7].sum(), 1):.2f}; all warps: steps {rec[:, :, 4].sum(1).mean():.2f}, "
+          f"finisher batches {rec[:, :, 5].sum(1).mean():.2f}, probe-ahead used {rec[:, :, 6].sum() / max(rec[:, :, 7].sum(), 1):.2f}",
+          flush=True)
+    for lo, hi in ((0, 1), (1, 2), (2, 99)):
+        m = (top[:, 5] >= lo) & (top[:, 5] < hi)
+        if m.any():
+            print(f"     critical warp with {lo}{'+' if hi > 2 else ''} finisher batches: {m.mean():.2f} of decisions, latency "
+                  f"{16 * top[m, 0].mean():.0f}, drain {16 * top[m, 1].mean():.0f}, probe {16 * top[m, 2].mean():.0f}, "
+                  f"steps {top[m, 4].mean():.2f}", flush=True)
+    h.phase_records(0)
+
+
 for c, w in shapes:
     if c and c > cfg.n_instances:
         continue
@@ -45,6 +71,8 @@ for c, w in shapes:
     h.load(trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.request_id, trace.blk_off, trace.blocks)
     h.rerun()
     best = min(h.rerun() for _ in range(3))
+    if os.environ.get("RSIM_CRIT"):
+        critpath(h, len(trace))
     rep, k1, dr = h.timings()
     print(f"{name} R={len(trace)} ctas={c} warps={w}: total {best:.2f} ms  replay {rep:.2f} ms "
           f"({1000 * rep / len(trace):.2f} us/decision)  k1 {k1:.3f} ms  drain {dr:.2f} ms", flush=True)
@@ -56,4 +84,8 @@ for c, w in shapes:
     if ctr[1]:
         print(f"   engine: {ctr[1] / len(trace):.2f} steps/decision, {ctr[2] / max(ctr[1], 1):.0f} cycles/step, "
               f"{ctr[6]} finisher batches at {ctr[3] / max(ctr[6], 1):.0f} cycles each", flush=True)
+    sc = h.step_cycles()
+    if sc.any() and ctr[1]:
+        names = ["setup", "plan", "cost", "apply", "pops", "decode", "finish", "joins+tail"]
+        print("   step sections (cycles/step): " + "  ".join(f"{n}={c / ctr[1]:.0f}" for n, c in zip(names, sc)), flush=True)
     h.close()
