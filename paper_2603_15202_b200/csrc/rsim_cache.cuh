@@ -324,6 +324,11 @@ __device__ int warp_unpin_insert(const Table &T, const u64 *pk, int B, const u64
 struct FinBuf {
     i64 a[32], oa[32];
     int B[32], L[32], hb[32], pre[33];
+    // a batch whose cache work was deferred past the current decision's publish
+    // (rsim_engine.cuh: finish_or_defer): dnf finishers of local instance dsp / gi dgi, stamped dend
+    int dnf, dgi, dsi, npark;   // ..., local index of that instance, batches parked (diagnostics)
+    i64 dend;
+    struct Inst *dsp;
 };
 
 __device__ int warp_finish_many(const Table &T, const u64 *ckeys, const u64 *okeys, const FinBuf &F, int nf, i64 now,

@@ -105,8 +105,37 @@ __device__ __noinline__ void finish_batch(const Params &P, Inst *sp, int gi, Fin
 // Append the finishers of lane mask fm (lane l's request record at e) to F in
 // lane order -- the reference's order within one ballot -- flushing F first if
 // it would overflow.
+// Deferral of finisher cache work past the publish of the decision being
+// scored. The probe only needs the key *set* of the instance's table, and
+// inserting whole chains (no eviction) changes the longest present prefix of
+// the scored request R in a closed form: the table is prefix-closed along R's
+// chain, a finished chain X contributes exactly its common prefix with R, so
+//     h' = max(h, LCP(X, R))          (chain keys are equal iff prefixes are).
+// So when no eviction can follow (occupancy + inserted keys <= capacity) and
+// the instance's probe-ahead hit h is valid, the batch is parked in F and only
+// h is raised; the caller applies the batch right after publishing.
+struct Defer {
+    const u64 *rkeys;    // the scored request's first 128 chain keys (shared memory)
+    int rB;              // its prefix blocks
+    int *hit;            // per local instance: probe-ahead hit blocks of the scored request
+    u32 valid;           // instances whose probe-ahead hit is valid
+    u32 moved;           // out: instances whose hit a parked batch raised (their probe slots are stale)
+};
+
+__device__ __forceinline__ void apply_deferred(const Params &P, FinBuf &F, int lane, int *werr_sm, Defer *df = nullptr) {
+    if (F.dnf) {
+        // the instance's probe-ahead hit no longer matches its table version: no more parking for it
+        if (df != nullptr) df->valid &= ~(1u << F.dsi);
+        finish_batch(P, F.dsp, F.dgi, F, F.dnf, F.dend, lane, werr_sm);
+        __syncwarp();
+        if (lane == 0) F.dnf = 0;
+        __syncwarp();
+    }
+}
+
 __device__ __forceinline__ void add_finishers(const Params &P, Inst *sp, int gi, FinBuf &F, int &nf, u32 fm,
-                                              const Ent *e, i64 end, int lane, int *werr_sm) {
+                                              const Ent *e, i64 end, int lane, int *werr_sm, Defer *df) {
+    if (nf == 0) apply_deferred(P, F, lane, werr_sm, df);         // F is about to be reused
     const int cnt = __popc(fm);
     if (nf + cnt > 32) { finish_batch(P, sp, gi, F, nf, end, lane, werr_sm); nf = 0; }
     const bool fin = (fm >> lane) & 1u;
@@ -126,6 +155,53 @@ __device__ __forceinline__ void add_finishers(const Params &P, Inst *sp, int gi,
     __syncwarp();
 }
 
+// LCP of finisher f's full chain with the scored request, or -1 if it is not
+// decidable from the first 128 depths.
+__device__ __forceinline__ int chain_lcp(const Params &P, const FinBuf &F, int f, const Defer &df, int lane) {
+    const int B = F.B[f], L = F.L[f];
+    const int m = min(L, df.rB), mc = min(m, 128);
+    int lcp = mc;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int j = 32 * q + lane;
+        bool ne = false;
+        if (j < mc) {
+            const u64 xk = j < B ? P.ckeys[F.a[f] + j] : P.okeys[F.oa[f] + j - B];
+            ne = xk != df.rkeys[j];
+        }
+        const u32 nm = __ballot_sync(FULL, ne);
+        if (nm && lcp == mc) lcp = 32 * q + __ffs(nm) - 1;
+    }
+    if (lcp == 128 && m > 128) return -1;
+    return lcp;
+}
+
+__device__ __forceinline__ void finish_or_defer(const Params &P, Inst *sp, int gi, int s, FinBuf &F, int nf, i64 end,
+                                                int lane, int *werr_sm, Defer *df) {
+    if (df != nullptr && ((df->valid >> s) & 1u) && F.dnf == 0 && (P.cap < 0 || sp->occ + F.pre[nf] <= P.cap)) {
+        int h = df->hit[s];
+        bool ok = true;
+        for (int f = 0; f < nf && ok; f++) {
+            if (min(F.L[f], df->rB) <= h) continue;                // cannot raise h
+            const int l = chain_lcp(P, F, f, *df, lane);
+            if (l < 0) ok = false;
+            else if (l > h) h = l;
+        }
+        if (ok) {
+            const bool raised = h != df->hit[s];                   // lane-uniform
+            if (raised) df->moved |= 1u << s;                       // (df is per-lane: every lane updates)
+            __syncwarp();
+            if (lane == 0) {
+                if (raised) df->hit[s] = h;
+                F.dnf = nf; F.dgi = gi; F.dsi = s; F.dend = end; F.dsp = sp; F.npark += 1;
+            }
+            __syncwarp();
+            return;
+        }
+    }
+    finish_batch(P, sp, gi, F, nf, end, lane, werr_sm);
+}
+
 // One engine step of instance gi starting at its next_step (form_batch +
 // execute_batch, engine.py:291-355). Returns false if the plan was empty (the
 // instance went idle). Queue/running records are read field by field from
@@ -137,7 +213,8 @@ __device__ __forceinline__ void add_finishers(const Params &P, Inst *sp, int gi,
 #else
 #define SP_MARK(i) do { } while (0)
 #endif
-__device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi, int lane, int *werr_sm, FinBuf &F) {
+__device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi, int s, int lane, int *werr_sm,
+                                               FinBuf &F, Defer *df) {
 #ifdef RSIM_STEP_PROFILE
     long long spc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, spt = clock64();
 #endif
@@ -157,6 +234,28 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
     REnt *rb = P.rbuf + (size_t)gi * (size_t)P.max_batch;
     const u32 qmask = (1u << P.qlog2) - 1u;
     SP_MARK(0);
+    if (q == 0 && !fin_step && ndec > 0) {
+        // pure decode step: no prefill, no pop, no finish (the general path below reduces to this)
+        const i64 dcs0 = sp->dcs;
+        const i64 end = t + decode_cost_us(P, ndec, dcs0);
+        __syncwarp();
+        if (lane == 0) {
+            sp->total += ndec;
+            sp->dcs = dcs0 + ndec;
+            sp->busy_until = end;                                  // engine.py:349-352
+            sp->due = end;
+            sp->next_step = end;
+            sp->step_idx = step_idx + 1;
+        }
+        log_step(P, gi, t, end, 0, (i64)ndec, step_idx, lane);
+        __syncwarp();
+        SP_MARK(7);
+#ifdef RSIM_STEP_PROFILE
+        if (P.ctr != nullptr && lane == 0)
+            for (int i = 0; i < 8; i++) atomicAdd(P.ctr + 16 + i, (u64)spc[i]);
+#endif
+        return true;
+    }
 
     // pass 1: FIFO plan (_plan_allocations, engine.py:174-184). Entry j is
     // allocated iff j < slots and the budget left before it is positive.
@@ -234,7 +333,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         const u32 fm = __ballot_sync(FULL, fin);
         if (fm) {
             total -= warp_sum(fin ? e->in + 1 : (i64)0);
-            add_finishers(P, sp, gi, F, nf, fm, e, end, lane, werr_sm);
+            add_finishers(P, sp, gi, F, nf, fm, e, end, lane, werr_sm, df);
         }
     }
 
@@ -266,7 +365,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
                 gone = warp_sum(gone);
                 dcs -= gone;
                 total -= gone;
-                add_finishers(P, sp, gi, F, nf, fm, e, end, lane, werr_sm);
+                add_finishers(P, sp, gi, F, nf, fm, e, end, lane, werr_sm, df);
             }
             if (__any_sync(FULL, move)) {                  // compact: all reads of this chunk before any write
                 ulonglong2 c0, c1, c2, c3;
@@ -285,7 +384,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         nfin = warp_min_i64(nf_step);
     }
     SP_MARK(5);
-    if (nf) finish_batch(P, sp, gi, F, nf, end, lane, werr_sm);
+    if (nf) finish_or_defer(P, sp, gi, s, F, nf, end, lane, werr_sm, df);
     SP_MARK(6);
 
     // popped requests with out > 1 join the running list (after the removals)
@@ -337,9 +436,10 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
 }
 
 // Entry used by the replay loop (counts SM cycles in engine steps when profiling).
-__device__ __forceinline__ bool inst_step(const Params &P, Inst *sp, int gi, int lane, int *werr_sm, FinBuf &F) {
+__device__ __forceinline__ bool inst_step(const Params &P, Inst *sp, int gi, int s, int lane, int *werr_sm, FinBuf &F,
+                                          Defer *df) {
     const long long c0 = clock64();
-    const bool ran = inst_step_body(P, sp, gi, lane, werr_sm, F);
+    const bool ran = inst_step_body(P, sp, gi, s, lane, werr_sm, F, df);
     if (P.ctr != nullptr && lane == 0) atomicAdd(P.ctr + 2, (u64)(clock64() - c0));   // SM cycles in engine steps
     return ran;
 }

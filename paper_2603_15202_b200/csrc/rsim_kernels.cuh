@@ -234,13 +234,15 @@ __device__ __noinline__ void stage_request(const Params &P, ReqStage &R, i64 k, 
 //      (cluster.py:250-273); skip_mask marks instances that must not move yet. The check is
 //      inline; the (noinline) step function is only called when a step is due.
 __device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base, int l0, int n, i64 until,
-                                            u32 skip_mask, int lane, WarpBuf &WB) {
-    for (int s = 0; s < n; s++) {
-        if ((skip_mask >> s) & 1u) continue;
+                                            u32 skip_mask, int lane, WarpBuf &WB, Defer *df = nullptr) {
+    u32 due = __ballot_sync(FULL, lane < n && !((skip_mask >> lane) & 1u) && st[l0 + lane].next_step < until);
+    while (due) {                                       // ascending instance order
+        const int s = __ffs(due) - 1;
+        due &= due - 1;
         Inst *sp = st + l0 + s;
-        if (sp->next_step >= until) continue;
         u64 steps = 0;
-        while (sp->next_step < until && !WB.werr) steps += inst_step(P, sp, base + l0 + s, lane, &WB.werr, WB.fin);
+        while (sp->next_step < until && !WB.werr)
+            steps += inst_step(P, sp, base + l0 + s, s, lane, &WB.werr, WB.fin, df);
         if (lane == 0) WB.c_steps += steps;
     }
 }
@@ -357,19 +359,21 @@ __device__ __forceinline__ u32 tie_index(const u32 *modtab, u64 c0_lo, u64 c0_hi
     return mod_counter(lo, c0_hi + (lo < c0_lo), T);
 }
 
-__device__ __noinline__ void decide_phase(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
-                                          Dec &dec, const u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane) {
-    // lane-major: lane holds flat partials [8*lane, 8*lane+8) (ascending instance id order)
+__device__ __forceinline__ void decide_phase(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
+                                             Dec &dec, const u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane) {
+    // round-major: lane holds flat partials r*32 + lane (conflict-free 16-byte loads); flat
+    // order = ascending instance id
     u64 pm[8];
     u32 pc[8];
     u64 mn = ~0ULL;
     u32 er = 0;
     const Part *pp = part + par * CW;
+    const int NR = (CW + 31) >> 5;
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-        const int idx = lane * 8 + j;
-        pm[j] = ~0ULL; pc[j] = 0;
-        if (idx < CW) { const Part q = pp[idx]; pm[j] = q.minb; pc[j] = q.cnt; er |= q.err; mn = min(mn, q.minb); }
+    for (int r = 0; r < 8; r++) {
+        const int idx = r * 32 + lane;
+        pm[r] = ~0ULL; pc[r] = 0;
+        if (r < NR && idx < CW) { const Part q = pp[idx]; pm[r] = q.minb; pc[r] = q.cnt; er |= q.err; mn = min(mn, q.minb); }
     }
     // 64-bit min with two 32-bit redux ops
     const u32 hmin = __reduce_min_sync(FULL, (u32)(mn >> 32));
@@ -378,7 +382,7 @@ __device__ __noinline__ void decide_phase(const Params &P, const Part *part, int
     er = __reduce_or_sync(FULL, er);
     u32 lc = 0;
 #pragma unroll
-    for (int j = 0; j < 8; j++) { pc[j] = pm[j] == gmin ? pc[j] : 0u; lc += pc[j]; }
+    for (int r = 0; r < 8; r++) { pc[r] = pm[r] == gmin ? pc[r] : 0u; lc += pc[r]; }
     const u32 T = __reduce_add_sync(FULL, lc);
     Dec d; d.owner_warp = -1; d.kk = 0; d.err = (int)er; d.pad = 0;
     u32 kk = 0;
@@ -426,22 +430,22 @@ __device__ __noinline__ void decide_phase(const Params &P, const Part *part, int
     }
     if (!d.err && Tg == 0) d.err = 11;            // NoInstancesError
     if (!d.err && mine) {
-        const u32 incl = warp_incl_scan(lc, lane);
-        const u32 ge = __ballot_sync(FULL, lc > 0 && incl > kk && incl - lc <= kk);
-        const int L = __ffs(ge) - 1;
-        int owner = -1;
-        u32 okk = 0;
-        if (lane == L) {
-            u32 c = incl - lc;
+        // the round holding the kk-th tie, then the lane inside it
+        u32 pre = 0, kr = 0, c = 0;
+        int rb = -1;
 #pragma unroll
-            for (int j = 0; j < 8; j++)
-                if (owner < 0 && pc[j] > 0) {
-                    if (kk < c + pc[j]) { owner = lane * 8 + j; okk = kk - c; }
-                    c += pc[j];
-                }
+        for (int r = 0; r < 8; r++) {
+            if (r < NR) {
+                const u32 S = __reduce_add_sync(FULL, pc[r]);
+                if (rb < 0 && kk < pre + S) { rb = r; kr = kk - pre; c = pc[r]; }
+                pre += S;
+            }
         }
-        owner = __shfl_sync(FULL, owner, L);
-        okk = __shfl_sync(FULL, okk, L);
+        const u32 incl = warp_incl_scan(c, lane);
+        const u32 ge = __ballot_sync(FULL, c > 0 && incl > kr && incl - c <= kr);
+        const int L = __ffs(ge) - 1;
+        const u32 okk = __shfl_sync(FULL, kr - (incl - c), L);
+        const int owner = rb * 32 + L;
         if (owner / W == cta) { d.owner_warp = owner % W; d.kk = (int)okk; }
     }
     if (lane == 0) dec = d;
@@ -500,7 +504,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     u32 ties = 0;                                          // ties resolved in this launch (control warp)
     const int l0 = warp * ipw;
     const int nmine = control ? 0 : max(0, min(ipw, nloc - l0));
-    if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; }
+    if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; WB.fin.dnf = 0; WB.fin.npark = 0; }
     if (threadIdx.x == 0) {
         mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_fence_init();
         ctl[0] = k0;
@@ -550,10 +554,11 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     } else {
         i64 staged_seen = k0;
         long long t_rel = clock64();                        // release of this warp for decision k
+        bool was_owner = false;                             // this warp committed the previous decision
         for (i64 k = k0; k < k1; k++) {
             const int par = (int)(k & 1);
             const u64 steps0 = WB.c_steps;
-            const int fins0 = WB.fins;
+            const int fins0 = WB.fins, park0 = WB.fin.npark;
             if (staged_seen <= k) {                         // request k staged? normally long done
                 while ((staged_seen = ctl[0]) <= k) { }
                 __threadfence_block();
@@ -561,8 +566,12 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             const ReqStage &R = rq[k % RSIM_SLOTS];
             PHASE(0);
             const long long t_a = clock64();
-            // ---- K4: advance my instances through steps starting before t
-            if (mode == MODE_REPLAY) drain_phase(P, st, base, l0, nmine, R.t, 0u, lane, WB);
+            // ---- K4: advance my instances through steps starting before t; finisher cache work
+            //      that cannot change this decision's probe beyond a closed-form update is parked
+            Defer df;
+            df.rkeys = R.keys; df.rB = R.B; df.hit = WB.sph; df.moved = 0u;
+            df.valid = __ballot_sync(FULL, WB.spk == k && lane < nmine && st[l0 + lane].tabver == WB.spver[lane]);
+            if (mode == MODE_REPLAY) drain_phase(P, st, base, l0, nmine, R.t, 0u, lane, WB, &df);
             PHASE(1);
             const long long t_b = clock64();
             // ---- K2: hit blocks (probe-ahead where still valid) + score
@@ -572,6 +581,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 if (ok) WB.hit[lane] = WB.sph[lane];
                 skip = __ballot_sync(FULL, ok);
             }
+            const u32 stale_slots = df.moved & skip;     // hits raised by a parked batch: no probe slots
             __syncwarp();
             probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
             const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB);
@@ -592,8 +602,9 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 unsigned short *rec = P.crit + ((size_t)(k - k0) * CW + cta * W + warp) * 8;
                 rec[0] = q16(t_d - t_rel); rec[1] = q16(t_b - t_a); rec[2] = q16(t_c - t_b); rec[3] = q16(t_a - t_rel);
                 rec[4] = (unsigned short)min((u64)65535, WB.c_steps - steps0); rec[5] = (unsigned short)(WB.fins - fins0);
-                rec[6] = (unsigned short)__popc(skip); rec[7] = (unsigned short)nmine;
+                rec[6] = (unsigned short)(was_owner ? 1 : 0); rec[7] = (unsigned short)(WB.fin.npark - park0);
             }
+            apply_deferred(P, WB.fin, lane, &WB.werr);      // parked finisher cache work (before any commit)
             if (mode == MODE_REPLAY && k + 1 < k1) {
                 if (staged_seen <= k + 1) { staged_seen = ctl[0]; __threadfence_block(); }
                 if (staged_seen > k + 1) {
@@ -617,6 +628,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 if (lane == 0 && WB.werr == 0) WB.werr = d.err;
                 break;
             }
+            was_owner = warp == d.owner_warp;
             if (warp == d.owner_warp) {
                 const int s = nth_set_bit(tmask, d.kk);
                 const int h = WB.hit[s];
@@ -627,8 +639,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
 #pragma unroll
                 for (int q = 0; q < 4; q++) cs[q] = (s < 2 && 32 * q + lane < min(R.B, 128)) ? WB.slot[par][s][32 * q + lane] : -1;
                 int werr = 0;
-                commit(P, st + l0 + s, base + l0 + s, k, h, R.t, kk0, s < 2 ? cs : nullptr, R.a, R.B, R.in, R.out,
-                       R.oa, lane, werr);
+                commit(P, st + l0 + s, base + l0 + s, k, h, R.t, kk0, (s < 2 && !((stale_slots >> s) & 1u)) ? cs : nullptr,
+                       R.a, R.B, R.in, R.out, R.oa, lane, werr);
                 if (lane == 0 && werr) WB.werr = werr;
                 if (P.dec_ns != nullptr && lane == 0) P.dec_ns[k] = (i64)globaltimer();
             }

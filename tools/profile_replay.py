@@ -48,9 +48,15 @@ def critpath(h, n):
           f"  stage-wait {16 * top[:, 3].mean():.0f}  drain {16 * top[:, 1].mean():.0f}  probe+score {16 * top[:, 2].mean():.0f}"
           f"  rest {16 * (top[:, 0] - top[:, 1] - top[:, 2] - top[:, 3]).mean():.0f}", flush=True)
     print(f"   critical warp: steps {top[:, 4].mean():.2f}/decision, finisher batches {top[:, 5].mean():.2f}, "
-          f"probe-ahead used {top[:, 6].sum() / max(top[:, 7].sum(), 1):.2f}; all warps: steps {rec[:, :, 4].sum(1).mean():.2f}, "
-          f"finisher batches {rec[:, :, 5].sum(1).mean():.2f}, probe-ahead used {rec[:, :, 6].sum() / max(rec[:, :, 7].sum(), 1):.2f}",
-          flush=True)
+          f"parked batches {top[:, 7].mean():.2f}, previous owner {top[:, 6].mean():.2f}; all warps: steps "
+          f"{rec[:, :, 4].sum(1).mean():.2f}, finisher batches {rec[:, :, 5].sum(1).mean():.2f}, parked "
+          f"{rec[:, :, 7].sum(1).mean():.2f}", flush=True)
+    for own in (0, 1):
+        m = top[:, 6] == own
+        if m.any():
+            print(f"     critical warp {'is' if own else 'is not'} the previous owner: {m.mean():.2f} of decisions, latency "
+                  f"{16 * top[m, 0].mean():.0f}, stage-wait {16 * top[m, 3].mean():.0f}, drain {16 * top[m, 1].mean():.0f}, "
+                  f"probe {16 * top[m, 2].mean():.0f}, steps {top[m, 4].mean():.2f}, parked {top[m, 7].mean():.2f}", flush=True)
     for lo, hi in ((0, 1), (1, 2), (2, 99)):
         m = (top[:, 5] >= lo) & (top[:, 5] < hi)
         if m.any():
