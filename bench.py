@@ -283,7 +283,7 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
         "lat_p50_us": float(np.percentile(lat, 50)) if lat.size else None,
         "lat_p99_us": float(np.percentile(lat, 99)) if lat.size else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic_for(name),
                      "kernel": "replay_kernel", "algorithmic_bytes_per_launch": int(ctr[0]),
                      "avg_launch_ms": avg_replay_s * 1000.0, "peak_source": f"{peak_src} hbm_gbs (burst copy)",
                      "engine_steps_per_launch": int(ctr[1])},
@@ -301,6 +301,63 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
         out["cpu_port"] = {"value": port, "unit": "decisions/s", "cores": 1, "kind": "port",
                            "sample": f"all {R} requests, oracle/rsim_oracle.c (1 thread)"}
     return out
+
+
+def traffic_for(name):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one replay launch of this workload, from the
+    committed ncu capture (profiles/replay_traffic.json); None if not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "replay_traffic.json")) as fh:
+            t = json.load(fh).get(name)
+        return None if t is None else int(t["dram_bytes"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def measure_sharded(name, args, dev_index, rank, world):
+    """Instances of one cluster sharded over `world` GPUs (one process each); per decision every
+    rank publishes its (min score, tie count) partial into every peer's mailbox over NVLink
+    (device-initiated, distributed.py). Strong scaling: the total work is the one trace."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_15202_b200.distributed import ShardedRouter
+
+    trace, cfg = build_workload(name)
+    R = len(trace)
+    dev = torch.device("cuda", dev_index)
+    router = ShardedRouter(cfg, trace, rank=rank, world=world, device=dev_index)
+    for _ in range(args.warmup):
+        router.rerun()
+    launches0 = router.h.launch_count()
+    dev_ms = []
+    with ClockSampler(dev_index) as clk:
+        for _ in range(args.steps):
+            flush_l2(dev)
+            dist.barrier()
+            dev_ms.append(router.rerun())
+    launches = router.h.launch_count() - launches0
+    ctr = router.h.counters()
+    replay_ms = router.h.timings()[0]
+    e2e_s = []
+    for _ in range(args.steps):
+        flush_l2(dev)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        router.run_trace(trace)
+        e2e_s.append(time.perf_counter() - t0)
+    router.close()
+    h2d = int(trace.arrival_us.nbytes + trace.in_tokens.nbytes + trace.out_tokens.nbytes +
+              trace.request_id.nbytes + trace.blk_off.nbytes + trace.blocks.nbytes)
+    peaks, peak_src = measured_peaks()
+    achieved = ctr[0] / (replay_ms / 1000.0) / 1e9 if replay_ms else 0.0
+    return {"R": R, "cfg": cfg, "trace": trace, "ms_per_step": statistics.mean(dev_ms),
+            "e2e_s": statistics.mean(e2e_s), "h2d": h2d, "d2h": R * 12, "launches": launches,
+            "clocks": clk.summary(), "lat_p50_us": None, "lat_p99_us": None,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": "replay_kernel",
+                         "algorithmic_bytes_per_launch": int(ctr[0]), "avg_launch_ms": replay_ms,
+                         "peak_source": f"{peak_src} hbm_gbs (burst copy)", "scope": f"rank {rank} shard"}}
 
 
 def main():
@@ -331,14 +388,17 @@ def main():
     if pg:
         pg.barrier()
     torch.cuda.synchronize()
-    res = measure_workload(args.workload, args, local, with_cpu=(rank == 0 and world == 1 and not args.no_cpu),
-                           rank=rank)
+    if world > 1:
+        res = measure_sharded(args.workload, args, local, rank, world)
+    else:
+        res = measure_workload(args.workload, args, local, with_cpu=(rank == 0 and not args.no_cpu), rank=rank)
     torch.cuda.synchronize()
     if pg:
         pg.barrier()
-        t = torch.tensor([res["ms_per_step"]], device="cuda")
+        t = torch.tensor([res["ms_per_step"], res["e2e_s"]], device="cuda", dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        res["ms_per_step"] = float(t.item())
+        res["ms_per_step"], res["e2e_s"] = float(t[0].item()), float(t[1].item())
+        res["e2e"] = res["R"] / res["e2e_s"]
     extras = {}
     if rank == 0 and world == 1:
         for name in [x for x in args.extra.split(",") if x and x != args.workload]:
@@ -355,20 +415,21 @@ def main():
             pg.destroy_process_group()
         return
     R = res["R"]
-    value = R * world / (res["ms_per_step"] / 1000.0)
+    value = R / (res["ms_per_step"] / 1000.0)          # decisions of the one (sharded) cluster per second
     line = {
         "metric": METRIC, "value": value, "unit": "decisions/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": args.workload, "description": WORKLOADS[args.workload][1],
                    "n_instances": res["cfg"].n_instances, "requests": R, "block_size": res["cfg"].cache.block_size,
                    "capacity_blocks": res["cfg"].cache.capacity_blocks, "policy": res["cfg"].policy.kind,
-                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "parallelism": f"instances sharded over {world} GPUs, per-decision NVLink mailbox exchange" if world > 1 else "single-gpu",
                    "l2": "512 MB flush between timed steps; trace + tables exceed L2"},
         "decision_latency_us": {"p50": res["lat_p50_us"], "p99": res["lat_p99_us"],
                                 "source": "%globaltimer at each commit, consecutive differences"},
         "roofline": res["roofline"],
-        "e2e": {"value": res["e2e"] * world, "unit": "decisions/s", "h2d_bytes_per_step": res["h2d"],
+        "e2e": {"value": res["e2e"], "unit": "decisions/s", "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": res["d2h"]},
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],

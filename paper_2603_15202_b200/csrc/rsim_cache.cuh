@@ -54,14 +54,24 @@ __device__ __forceinline__ u32 eval_pair(const Table &T, ulonglong2 pr, u32 i, u
     return (j + 1) & T.mask;
 }
 
-// Finish a probe that did not resolve in its first pair.
-__device__ __noinline__ u32 probe_rest(const Table &T, u32 i, u64 key, int &st) {
+// Finish a probe that did not resolve in its first pair. Out of line and with
+// scalar arguments only (no caller object has its address taken, so callers
+// keep the table and the status in registers); returns (status << 32) | slot.
+__device__ __noinline__ u64 probe_rest_v(u64 *tk, u32 mask, u64 empty, u32 i, u64 key) {
+    Table T;
+    T.k = tk; T.m = nullptr; T.mask = mask; T.slog2 = 0; T.empty = empty;
     for (;;) {
+        int st;
         ulonglong2 pr = ld_pair(T, i);
         u32 r = eval_pair(T, pr, i, key, st);
-        if (st != 2) return r;
+        if (st != 2) return ((u64)(u32)st << 32) | r;
         i = r;
     }
+}
+__device__ __forceinline__ u32 probe_rest(const Table &T, u32 i, u64 key, int &st) {
+    const u64 v = probe_rest_v(T.k, T.mask, T.empty, i, key);
+    st = (int)(v >> 32);
+    return (u32)v;
 }
 
 __device__ __forceinline__ int tab_find(const Table &T, u64 key) {
@@ -158,7 +168,9 @@ __device__ __forceinline__ int lead_hits(const u32 m[4]) {   // leading present 
 // Longest present prefix beyond the first 128 depths: 128-ary search over
 // depth (presence is monotone in depth by prefix closure, kvcache.py:4-7),
 // ~3 rounds for a 2048-block prompt. keys = the request's chain keys.
-__device__ __noinline__ int deep_match(const Table &T, const u64 *keys, int B, int lane) {
+__device__ __noinline__ int deep_match_v(u64 *tk, u32 mask, int slog2, u64 empty, const u64 *keys, int B, int lane) {
+    Table T;
+    T.k = tk; T.m = nullptr; T.mask = mask; T.slog2 = slog2; T.empty = empty;
     int lo = 128, hi = B;
     while (lo < hi) {
         const int span = hi - lo;
@@ -194,6 +206,9 @@ __device__ __noinline__ int deep_match(const Table &T, const u64 *keys, int B, i
         lo = d_ok + 1;
     }
     return lo;
+}
+__device__ __forceinline__ int deep_match(const Table &T, const u64 *keys, int B, int lane) {
+    return deep_match_v(T.k, T.mask, T.slog2, T.empty, keys, B, lane);
 }
 
 // Longest present prefix of one instance (match_keys) -- the API / batch path.
@@ -329,6 +344,13 @@ struct FinBuf {
     int dnf, dgi, dsi, npark;   // ..., local index of that instance, batches parked (diagnostics)
     i64 dend;
     struct Inst *dsp;
+    // the last commit's touch + pin of the hit chain (engine.py:275-276), run off the critical
+    // path: before any finisher cache work of that instance and before the next commit
+    int tpn, tpgi, tph, tpver;  // pending?, instance, hit blocks, instance tabver at commit
+    i64 tpa, tpt;               // request chain key offset, touch time
+    const u64 *tpkeys;          // the request's first 128 chain keys (its staging slot)
+    const int *tpsl;            // their probe-found slots, or null
+    struct Inst *tpsp;
 };
 
 __device__ int warp_finish_many(const Table &T, const u64 *ckeys, const u64 *okeys, const FinBuf &F, int nf, i64 now,

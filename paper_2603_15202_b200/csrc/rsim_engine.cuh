@@ -83,11 +83,39 @@ __device__ __forceinline__ void log_step(const Params &P, int gi, i64 start, i64
     }
 }
 
+// Run the pending commit touch + pin of F (if any).
+__device__ __noinline__ void run_touch_pin(const Params &P, FinBuf &F, int lane, int *werr_sm) {
+    __syncwarp();
+    const Table T = table_of(P, F.tpgi);
+    u64 kk0[4];
+    int sl[4];
+    const bool slots = F.tpsl != nullptr && F.tpsp->tabver == F.tpver;   // no key moved since the probe
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int j = 32 * q + lane;
+        kk0[q] = j < min(F.tph, 128) ? F.tpkeys[j] : 0;
+        sl[q] = (slots && j < min(F.tph, 128)) ? F.tpsl[j] : -1;
+    }
+    int werr = 0;
+    warp_touch_pin(T, P.ckeys + F.tpa, kk0, slots ? sl : nullptr, F.tph, F.tpt, lane, werr);
+    __syncwarp();
+    if (lane == 0) {
+        F.tpn = 0;
+        if (werr && *werr_sm == 0) *werr_sm = werr;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void flush_touch_pin(const Params &P, FinBuf &F, int lane, int *werr_sm, int gi = -1) {
+    if (F.tpn && (gi < 0 || gi == F.tpgi)) run_touch_pin(P, F, lane, werr_sm);
+}
+
 // Finisher batch of one step (engine.py:357-361 for every finisher in F): runs
 // on a register copy of the instance and writes back the KV$-side fields only
 // (the step owns the engine-side fields). Out of line: finishes are rare.
 __device__ __noinline__ void finish_batch(const Params &P, Inst *sp, int gi, FinBuf &F, int nf, i64 end, int lane,
                                           int *werr_sm) {
+    flush_touch_pin(P, F, lane, werr_sm, gi);                      // eviction reads touch and pins
     int werr = *werr_sm;
     __syncwarp();
     if (lane == 0) werr_sm[1] += 1;                               // WarpBuf.fins (follows werr)

@@ -84,6 +84,10 @@ __device__ __forceinline__ void mbar_arrive_expect(u64 *mb, u32 bytes) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1;\n\t}"
                  :: "r"(smem_addr(mb)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(u64 *mb) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}"
+                 :: "r"(smem_addr(mb)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(u64 *mb, u32 parity) {
     u32 ok;
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
@@ -145,10 +149,16 @@ __device__ __forceinline__ double score_of(const Params &P, const Inst &s, int h
 }
 
 // enqueue on the winner (InstanceSim.enqueue, engine.py:262-289) + route bookkeeping
-__device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, const u64 kk0[4], const int *slot0,
-                       i64 a, int B, i64 in, int out, i64 oa, int lane, int &werr) {
-    Table T = table_of(P, gi);
-    warp_touch_pin(T, P.ckeys + a, kk0, slot0, h, t, lane, werr);
+// The touch + pin of the hit chain is parked in F (run_touch_pin) and runs after
+// this warp's next publish, or earlier before cache work on the same instance.
+__device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, const u64 *keys128, const int *slot0,
+                       i64 a, int B, i64 in, int out, i64 oa, int lane, int &werr, FinBuf &F) {
+    __syncwarp();
+    if (lane == 0) {
+        F.tpn = h > 0; F.tpgi = gi; F.tph = h; F.tpver = sp->tabver; F.tpa = a; F.tpt = t;
+        F.tpkeys = keys128; F.tpsl = slot0; F.tpsp = sp;
+    }
+    __syncwarp();
     Inst s = *sp;
     i64 ht = (i64)h * P.bs; if (ht > in) ht = in;
     i64 pending = in - ht; if (pending < 1) pending = 1;
@@ -490,6 +500,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     Dec *dec = (Dec *)(rq + RSIM_SLOTS);                   // [2]
     u64 *mb = (u64 *)(dec + 2);                            // [2] partial-exchange mbarriers
     volatile i64 *ctl = (volatile i64 *)(mb + 2);          // [0] staged_upto
+    u64 *dmb = mb + 4;                                     // [2] decision-release mbarriers (control -> CTA)
     u32 *modtab = (u32 *)(mb + 6);                         // [RSIM_MODTAB] launch counter mod T
     WarpBuf *wbuf = (WarpBuf *)(modtab + RSIM_MODTAB);     // [W]
     WarpBuf &WB = wbuf[control ? 0 : warp];
@@ -504,9 +515,9 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     u32 ties = 0;                                          // ties resolved in this launch (control warp)
     const int l0 = warp * ipw;
     const int nmine = control ? 0 : max(0, min(ipw, nloc - l0));
-    if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; WB.fin.dnf = 0; WB.fin.npark = 0; }
+    if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; WB.fin.dnf = 0; WB.fin.npark = 0; WB.fin.tpn = 0; }
     if (threadIdx.x == 0) {
-        mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_fence_init();
+        mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_init(&dmb[0], 1); mbar_init(&dmb[1], 1); mbar_fence_init();
         ctl[0] = k0;
     }
     if (mode != MODE_DRAIN)
@@ -525,7 +536,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         if (!control) drain_phase(P, st, base, l0, nmine, until, 0u, lane, WB);
     } else if (control) {
         // ---- control warp: stage ahead, then per decision wait for the partials and decide
-        u32 mb_phase[2] = {0u, 0u};
+        u32 mb_phase = 0u;                                  // bit p: phase of mbarrier mb[p]
         i64 staged = k0;
         auto stage_upto = [&](i64 lim) {
             lim = min(lim, k1);
@@ -541,18 +552,21 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             const int par = (int)(k & 1);
             tc = clock64();
             if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * 16));
-            while (!mbar_try_wait(&mb[par], mb_phase[par])) { }
-            mb_phase[par] ^= 1u;
+            while (!mbar_try_wait(&mb[par], (mb_phase >> par) & 1u)) { }
+            mb_phase ^= 1u << par;
             PHASE(4);
             decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane);
             PHASE(5);
-            bar_warps(32 * (W + 1));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dmb[par]);          // release decision k to the instance warps
             if (dec[par].err) break;
-            // decisions < k are committed (their warps reached this barrier): their slots are free
-            stage_upto(k - 1 + RSIM_SLOTS);
+            // every warp published k, so it committed k-1 and ran the touch + pin of k-2
+            // (which reads its request's staged keys): slots of decisions < k-1 are free
+            stage_upto(k - 2 + RSIM_SLOTS);
         }
     } else {
         i64 staged_seen = k0;
+        u32 dph = 0u;                                       // bit p: phase of decision-release mbarrier dmb[p]
         long long t_rel = clock64();                        // release of this warp for decision k
         bool was_owner = false;                             // this warp committed the previous decision
         for (i64 k = k0; k < k1; k++) {
@@ -605,6 +619,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 rec[6] = (unsigned short)(was_owner ? 1 : 0); rec[7] = (unsigned short)(WB.fin.npark - park0);
             }
             apply_deferred(P, WB.fin, lane, &WB.werr);      // parked finisher cache work (before any commit)
+            flush_touch_pin(P, WB.fin, lane, &WB.werr);     // the previous commit's touch + pin
             if (mode == MODE_REPLAY && k + 1 < k1) {
                 if (staged_seen <= k + 1) { staged_seen = ctl[0]; __threadfence_block(); }
                 if (staged_seen > k + 1) {
@@ -620,7 +635,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 }
             }
             PHASE(3);
-            bar_warps(32 * (W + 1));
+            while (!mbar_try_wait(&dmb[par], (dph >> par) & 1u)) { }   // decision k released by the control warp
+            dph ^= 1u << par;
             PHASE(6);
             t_rel = clock64();
             const Dec d = dec[par];
@@ -632,15 +648,11 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             if (warp == d.owner_warp) {
                 const int s = nth_set_bit(tmask, d.kk);
                 const int h = WB.hit[s];
-                u64 kk0[4];
-#pragma unroll
-                for (int q = 0; q < 4; q++) kk0[q] = (32 * q + lane < R.B) ? R.keys[32 * q + lane] : 0;
-                int cs[4];
-#pragma unroll
-                for (int q = 0; q < 4; q++) cs[q] = (s < 2 && 32 * q + lane < min(R.B, 128)) ? WB.slot[par][s][32 * q + lane] : -1;
                 int werr = 0;
-                commit(P, st + l0 + s, base + l0 + s, k, h, R.t, kk0, (s < 2 && !((stale_slots >> s) & 1u)) ? cs : nullptr,
-                       R.a, R.B, R.in, R.out, R.oa, lane, werr);
+                flush_touch_pin(P, WB.fin, lane, &WB.werr);      // (normally already run after the publish)
+                commit(P, st + l0 + s, base + l0 + s, k, h, R.t, R.keys,
+                       (s < 2 && !((stale_slots >> s) & 1u)) ? WB.slot[par][s] : nullptr,
+                       R.a, R.B, R.in, R.out, R.oa, lane, werr, WB.fin);
                 if (lane == 0 && werr) WB.werr = werr;
                 if (P.dec_ns != nullptr && lane == 0) P.dec_ns[k] = (i64)globaltimer();
             }
@@ -648,6 +660,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         }
     }
 #undef PHASE
+    if (!control && mode != MODE_DRAIN) flush_touch_pin(P, WB.fin, lane, &WB.werr);
     if (prof && lane == 0)
         for (int i = 0; i < 8; i++) if (ph[i]) atomicAdd(P.ctr + 8 + i, ph[i]);
     // write back

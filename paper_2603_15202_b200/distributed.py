@@ -105,10 +105,31 @@ class ShardedRouter:
         dist.barrier()
 
     def rerun(self) -> float:
+        """Resident collective replay (all ranks call it); returns this rank's device ms."""
         return self.h.rerun()
 
     def local_decisions(self):
         return self.h.decisions(0, len(self.trace))
+
+    def run_trace(self, trace: PackedTrace):
+        """Collective end-to-end replay of host arrays: reset, H2D load, replay, drain, D2H of this
+        rank's decisions, merged over ranks (each decision is committed by exactly one rank).
+        Returns (chosen int32[n], hit_tokens int64[n]) on every rank."""
+        import torch
+        import torch.distributed as dist
+        h = self.h
+        h.reset()
+        n = len(trace)
+        _load(h, trace)
+        h.replay(0, n)
+        h.drain()
+        ch, ht = h.decisions(0, n)
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+        t = torch.from_numpy(np.stack([ch.astype(np.int64), ht.astype(np.int64)])).to(dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = t.cpu().numpy()
+        self.trace = trace
+        return t[0].astype(np.int32), t[1]
 
     def close(self):
         self.h.close()

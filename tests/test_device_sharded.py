@@ -19,3 +19,22 @@ def test_sharded_matches_reference(name, world):
     got = run_sharded_local(trace, cfg, world)
     for key in ("chosen", "hit_tokens", "first_sched_us", "first_token_us", "finish_us"):
         assert np.array_equal(got[key], want[key]), key
+
+
+@pytest.mark.parametrize("name,world,n", [("adv_mixed_n33", 2, 120), ("cfg1_chatbot_full", 2, 150)])
+def test_sharded_processes_match_reference(name, world, n):
+    """One process per shard (torchrun), mailboxes shared through CUDA IPC handles."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "tools", "sharded_check.py"), name, str(n)]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+    assert "OK" in p.stdout
