@@ -528,10 +528,17 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     // per-phase SM-cycle accounting of CTA 0 (ctr[8..15]): warp 0: staging wait, drain,
     // probe + score, publish + advance + probe-ahead, -, -, decision wait, commit;
     // control warp: exchange wait (4), decide (5)
+    // (diagnostics builds only: -DRSIM_DIAG; they cost registers the production path needs)
+#ifdef RSIM_DIAG
     const bool prof = P.ctr != nullptr && cta == 0 && (warp == 0 || control);
     u64 ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tc = clock64();
 #define PHASE(i) do { if (prof) { const long long t2 = clock64(); ph[i] += (u64)(t2 - tc); tc = t2; } } while (0)
+#define DIAG(x) x
+#else
+#define PHASE(i) do { } while (0)
+#define DIAG(x)
+#endif
     if (mode == MODE_DRAIN) {
         if (!control) drain_phase(P, st, base, l0, nmine, until, 0u, lane, WB);
     } else if (control) {
@@ -550,7 +557,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         stage_upto(k0 + RSIM_SLOTS - 1);
         for (i64 k = k0; k < k1; k++) {
             const int par = (int)(k & 1);
-            tc = clock64();
+            DIAG(tc = clock64());
             if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * 16));
             while (!mbar_try_wait(&mb[par], (mb_phase >> par) & 1u)) { }
             mb_phase ^= 1u << par;
@@ -567,19 +574,20 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     } else {
         i64 staged_seen = k0;
         u32 dph = 0u;                                       // bit p: phase of decision-release mbarrier dmb[p]
-        long long t_rel = clock64();                        // release of this warp for decision k
-        bool was_owner = false;                             // this warp committed the previous decision
+        DIAG(long long t_rel = clock64());                  // release of this warp for decision k
+        DIAG(bool was_owner = false);                       // this warp committed the previous decision
         for (i64 k = k0; k < k1; k++) {
             const int par = (int)(k & 1);
-            const u64 steps0 = WB.c_steps;
-            const int fins0 = WB.fins, park0 = WB.fin.npark;
+            DIAG(const u64 steps0 = WB.c_steps);
+            DIAG(const int fins0 = WB.fins);
+            DIAG(const int park0 = WB.fin.npark);
             if (staged_seen <= k) {                         // request k staged? normally long done
                 while ((staged_seen = ctl[0]) <= k) { }
                 __threadfence_block();
             }
             const ReqStage &R = rq[k % RSIM_SLOTS];
             PHASE(0);
-            const long long t_a = clock64();
+            DIAG(const long long t_a = clock64());
             // ---- K4: advance my instances through steps starting before t; finisher cache work
             //      that cannot change this decision's probe beyond a closed-form update is parked
             Defer df;
@@ -587,7 +595,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             df.valid = __ballot_sync(FULL, WB.spk == k && lane < nmine && st[l0 + lane].tabver == WB.spver[lane]);
             if (mode == MODE_REPLAY) drain_phase(P, st, base, l0, nmine, R.t, 0u, lane, WB, &df);
             PHASE(1);
-            const long long t_b = clock64();
+            DIAG(const long long t_b = clock64());
             // ---- K2: hit blocks (probe-ahead where still valid) + score
             u32 skip = 0;
             if (WB.spk == k) {
@@ -600,7 +608,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
             const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB);
             PHASE(2);
-            const long long t_c = clock64();
+            DIAG(const long long t_c = clock64());
             if (cta == 0 && warp == 0 && lane == 0) WB.c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once
             const u32 whi = __reduce_min_sync(FULL, (u32)(mybits >> 32));
             const u64 wmin = ((u64)whi << 32) | __reduce_min_sync(FULL, (u32)(mybits >> 32) == whi ? (u32)mybits : ~0u);
@@ -610,6 +618,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 Part *dst = part + par * CW + cta * W + warp;
                 if (lane < C) st_async_16(dst, &mb[par], (u32)lane, wmin, w1);
             }
+#ifdef RSIM_DIAG
             if (P.crit != nullptr && lane == 0 && k - k0 < P.crit_cap) {   // diagnostics: where this warp's latency went
                 const long long t_d = clock64();
                 auto q16 = [](long long c) { c >>= 4; return (unsigned short)(c > 65535 ? 65535 : (c < 0 ? 0 : c)); };
@@ -618,6 +627,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 rec[4] = (unsigned short)min((u64)65535, WB.c_steps - steps0); rec[5] = (unsigned short)(WB.fins - fins0);
                 rec[6] = (unsigned short)(was_owner ? 1 : 0); rec[7] = (unsigned short)(WB.fin.npark - park0);
             }
+#endif
             apply_deferred(P, WB.fin, lane, &WB.werr);      // parked finisher cache work (before any commit)
             flush_touch_pin(P, WB.fin, lane, &WB.werr);     // the previous commit's touch + pin
             if (mode == MODE_REPLAY && k + 1 < k1) {
@@ -638,13 +648,13 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             while (!mbar_try_wait(&dmb[par], (dph >> par) & 1u)) { }   // decision k released by the control warp
             dph ^= 1u << par;
             PHASE(6);
-            t_rel = clock64();
+            DIAG(t_rel = clock64());
             const Dec d = dec[par];
             if (d.err) {
                 if (lane == 0 && WB.werr == 0) WB.werr = d.err;
                 break;
             }
-            was_owner = warp == d.owner_warp;
+            DIAG(was_owner = warp == d.owner_warp);
             if (warp == d.owner_warp) {
                 const int s = nth_set_bit(tmask, d.kk);
                 const int h = WB.hit[s];
@@ -661,8 +671,11 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     }
 #undef PHASE
     if (!control && mode != MODE_DRAIN) flush_touch_pin(P, WB.fin, lane, &WB.werr);
+#ifdef RSIM_DIAG
     if (prof && lane == 0)
         for (int i = 0; i < 8; i++) if (ph[i]) atomicAdd(P.ctr + 8 + i, ph[i]);
+#endif
+#undef DIAG
     // write back
     __syncthreads();
     {
