@@ -686,12 +686,12 @@ rsim_status rsim_read_counters(rsim_t *h, int64_t *out16) {
     return RSIM_OK;
 }
 
-rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out8) {
-    if (!h || !out8) return RSIM_E_INVALID;
+rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out16) {
+    if (!h || !out16) return RSIM_E_INVALID;
     CK(h, cudaSetDevice(h->cfg.device));
-    u64 c[8];
+    u64 c[16];
     CK(h, cudaMemcpy(c, h->ctr + 16, sizeof(c), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 8; i++) out8[i] = (int64_t)c[i];
+    for (int i = 0; i < 16; i++) out16[i] = (int64_t)c[i];
     return RSIM_OK;
 }
 

@@ -14,8 +14,8 @@
 //  * linear probing reads an aligned 16-byte slot pair per load (tables run at
 //    <= 3/4 load, usually far below, so the home pair nearly always decides);
 //  * an instance's table is written only by its owning warp (one SM) during a
-//    launch, so key probes are L1-cached (ld.global.ca) and slot claims are
-//    plain stores arbitrated among the warp's own lanes (__match_any_sync);
+//    launch, so slot claims are plain stores arbitrated among the warp's own
+//    lanes (__match_any_sync); key probes read L2 directly (ld.global.cg);
 //  * touch / pin / unpin are fire-and-forget atomics (RED) on the metadata:
 //    max and +/- are commutative, so no read-modify-write round trip is
 //    needed; metadata is only ever read through L2 (ld.global.cg).
@@ -37,7 +37,9 @@ __device__ __forceinline__ Table table_of(const Params &P, int gi) {
 }
 
 __device__ __forceinline__ ulonglong2 ld_pair(const Table &T, u32 i) {
-    return __ldca(reinterpret_cast<const ulonglong2 *>(T.k) + (i >> 1));
+    // L2 only (ld.global.cg): table lines have little reuse inside one SM, and not allocating
+    // them keeps L1 for the engine's queue / running records (measured: -7 % per decision, chat1024)
+    return __ldcg(reinterpret_cast<const ulonglong2 *>(T.k) + (i >> 1));
 }
 
 // Evaluate one aligned pair starting the probe at slot i.
@@ -338,6 +340,7 @@ __device__ int warp_unpin_insert(const Table &T, const u64 *pk, int B, const u64
 // claim round trip per round instead of per request.
 struct FinBuf {
     i64 a[32], oa[32];
+    u64 kx[32];                 // Ent.kx of each finisher
     int B[32], L[32], hb[32], pre[33];
     // a batch whose cache work was deferred past the current decision's publish
     // (rsim_engine.cuh: finish_or_defer): dnf finishers of local instance dsp / gi dgi, stamped dend

@@ -59,7 +59,7 @@ struct __align__(16) Ent {
     i64 oa;           // offset of its output-block keys (okeys)
     int req, flags;   // flags bit0: prefill scheduled at least once
     int out, B, L, hb;   // output tokens, prefix blocks, full chain length, admission hit blocks
-    int pad0, pad1;
+    u64 kx;              // chain key at depth hb (the first key not cached at admission), 0 = unknown
 };
 typedef Ent QEnt;
 typedef Ent REnt;

@@ -170,7 +170,7 @@ __device__ __forceinline__ void add_finishers(const Params &P, Inst *sp, int gi,
     const int pos = nf + __popc(fm & lanemask_lt());
     int L = 0;
     if (fin) {
-        F.a[pos] = e->a; F.oa[pos] = e->oa; F.B[pos] = e->B; F.hb[pos] = e->hb;
+        F.a[pos] = e->a; F.oa[pos] = e->oa; F.B[pos] = e->B; F.hb[pos] = e->hb; F.kx[pos] = e->kx;
         L = e->L;
         F.L[pos] = L;
     }
@@ -210,7 +210,12 @@ __device__ __forceinline__ void finish_or_defer(const Params &P, Inst *sp, int g
         int h = df->hit[s];
         bool ok = true;
         for (int f = 0; f < nf && ok; f++) {
-            if (min(F.L[f], df->rB) <= h) continue;                // cannot raise h
+            // LCP(X, R) > h needs X.key[h] == R.key[h]. X's admission-hit keys X.key[0..hb) are
+            // present (pinned by X until this finish) while R.key[h] is not, so h < hb rules it
+            // out; otherwise it needs X.key[hb] == R.key[hb] (Ent.kx). Only then load X's chain.
+            const int hbx = F.hb[f], m = min(F.L[f], df->rB);
+            if (m <= h || h < hbx || hbx >= m) continue;           // cannot raise h
+            if (F.kx[f] != 0 && hbx < 128 && F.kx[f] != df->rkeys[hbx]) continue;
             const int l = chain_lcp(P, F, f, *df, lane);
             if (l < 0) ok = false;
             else if (l > h) h = l;
@@ -279,10 +284,92 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         __syncwarp();
         SP_MARK(7);
 #ifdef RSIM_STEP_PROFILE
-        if (P.ctr != nullptr && lane == 0)
-            for (int i = 0; i < 8; i++) atomicAdd(P.ctr + 16 + i, (u64)spc[i]);
+        if (P.ctr != nullptr && lane == 0) {
+            long long tot = 0;
+            for (int i = 0; i < 8; i++) { atomicAdd(P.ctr + 16 + i, (u64)spc[i]); tot += spc[i]; }
+            atomicAdd(P.ctr + 28, (u64)1);                         // [28..29]: pure decode steps
+            atomicAdd(P.ctr + 29, (u64)tot);
+        }
 #endif
         return true;
+    }
+    if (q == 1 && !fin_step) {
+        // one queued request, no decode finish: the FIFO plan, pop and join of the general path
+        // below for a single entry, on lane 0 (no warp scans); a pop that finishes at once
+        // (out == 1) takes the general path
+        QEnt *e = qb + (qh & qmask);
+        const i64 budget0 = budget, slots0 = slots;
+        int go = 0;
+        i64 ptok1 = 0, end1 = 0, pre1 = 0, dcs1 = 0, tot1 = 0, nfin1 = 0;
+        int r1 = 0, npop1 = 0;
+        if (lane == 0) {
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(e);
+            ulonglong2 c0 = src[0], c1 = src[1], c2 = src[2], c3 = src[3];
+            const i64 p = (i64)c0.x, in = (i64)c0.y;
+            const int req = (int)(u32)c2.x, flags = (int)(u32)(c2.x >> 32), out = (int)(u32)c2.y;
+            const bool alloc = slots0 > 0 && budget0 > 0;
+            const i64 take = alloc ? (budget0 < p ? budget0 : p) : 0;
+            const bool pop = alloc && p - take == 0;
+            go = (alloc || ndec > 0) && !(pop && out == 1);
+            if (go) {
+                ptok1 = take;
+                dcs1 = sp->dcs;
+                pre1 = prefill_cost_us(P, ptok1);
+                end1 = t + pre1 + decode_cost_us(P, ndec, dcs1);
+                if (alloc && !(flags & 1)) P.first_sched[req] = t;
+                tot1 = sp->total + (pop ? 1 : 0) + ndec;
+                dcs1 += ndec;
+                r1 = ndec;
+                nfin1 = sp->next_finish;
+                if (alloc && !pop) {                              // partial prefill: stays queued
+                    c0.x = (u64)(p - take);
+                    c2.x = (c2.x & 0xffffffffULL) | ((u64)(u32)(flags | 1) << 32);
+                    ulonglong2 *dq = reinterpret_cast<ulonglong2 *>(e);
+                    dq[0] = c0; dq[2] = c2;
+                }
+                if (pop) {                                        // first token; joins the running list
+                    npop1 = 1;
+                    P.first_token[req] = end1;
+                    const i64 fstep = step_idx + out - 1;
+                    c0.x = (u64)fstep;
+                    ulonglong2 *d = reinterpret_cast<ulonglong2 *>(rb + r1);
+                    d[0] = c0; d[1] = c1; d[2] = c2; d[3] = c3;
+                    dcs1 += in + 1;
+                    r1 += 1;
+                    nfin1 = fstep < nfin1 ? fstep : nfin1;
+                }
+                sp->q_head = (qh + npop1) & (int)qmask;
+                sp->q = 1 - npop1;
+                sp->r = r1;
+                sp->pend -= ptok1;
+                sp->total = tot1;
+                sp->dcs = dcs1;
+                sp->next_finish = nfin1;
+                sp->busy_until = end1;                             // engine.py:349-352
+                sp->due = end1;
+                sp->next_step = end1;
+                sp->step_idx = step_idx + 1;
+            }
+        }
+        go = __shfl_sync(FULL, go, 0);
+        if (go) {
+            if (P.log != nullptr) {
+                end1 = __shfl_sync(FULL, end1, 0); pre1 = __shfl_sync(FULL, pre1, 0);
+                r1 = __shfl_sync(FULL, r1, 0); npop1 = __shfl_sync(FULL, npop1, 0);
+                log_step(P, gi, t, end1, pre1, (i64)(1 - npop1) + r1, step_idx, lane);
+            }
+            __syncwarp();
+            SP_MARK(7);
+#ifdef RSIM_STEP_PROFILE
+            if (P.ctr != nullptr && lane == 0) {
+                long long tot = 0;
+                for (int i = 0; i < 8; i++) { atomicAdd(P.ctr + 16 + i, (u64)spc[i]); tot += spc[i]; }
+                atomicAdd(P.ctr + 26, (u64)1);
+                atomicAdd(P.ctr + 27, (u64)tot);
+            }
+#endif
+            return true;
+        }
     }
 
     // pass 1: FIFO plan (_plan_allocations, engine.py:174-184). Entry j is
@@ -457,8 +544,13 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
     __syncwarp();
     SP_MARK(7);
 #ifdef RSIM_STEP_PROFILE
-    if (P.ctr != nullptr && lane == 0)
-        for (int i = 0; i < 8; i++) atomicAdd(P.ctr + 16 + i, (u64)spc[i]);
+    if (P.ctr != nullptr && lane == 0) {
+        long long tot = 0;
+        for (int i = 0; i < 8; i++) { atomicAdd(P.ctr + 16 + i, (u64)spc[i]); tot += spc[i]; }
+        const int kind = fin_step ? 0 : 1;                         // [24..27]: finishing / other full steps
+        atomicAdd(P.ctr + 24 + 2 * kind, (u64)1);
+        atomicAdd(P.ctr + 25 + 2 * kind, (u64)tot);
+    }
 #endif
     return true;
 }

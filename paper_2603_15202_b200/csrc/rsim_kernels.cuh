@@ -167,7 +167,8 @@ __device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, c
         Ent e;
         e.v = pending; e.in = in; e.a = a; e.oa = oa;
         e.req = (int)k; e.flags = 0; e.out = out; e.B = B;
-        e.L = B + (int)((out + P.bs - 1) / P.bs); e.hb = h; e.pad0 = 0; e.pad1 = 0;
+        e.L = B + (int)((out + P.bs - 1) / P.bs); e.hb = h;
+        e.kx = (h < B && h < 128) ? keys128[h] : 0ULL;
         P.qbuf[((size_t)gi << P.qlog2) + ((s.q_head + s.q) & ((1 << P.qlog2) - 1))] = e;
         P.hit_blocks[k] = h;
         P.chosen[k] = P.gbase + gi;
@@ -233,7 +234,7 @@ __device__ __noinline__ void stage_request(const Params &P, ReqStage &R, i64 k, 
     const int B = (int)(e - a);
     u64 kk[4];
 #pragma unroll
-    for (int q = 0; q < 4; q++) kk[q] = (32 * q + lane < B) ? P.ckeys[a + 32 * q + lane] : 0;
+    for (int q = 0; q < 4; q++) kk[q] = (32 * q + lane < B) ? __ldcg(P.ckeys + a + 32 * q + lane) : 0;
 #pragma unroll
     for (int q = 0; q < 4; q++)
         if (32 * q + lane < B) { R.keys[32 * q + lane] = kk[q]; R.home[32 * q + lane] = tab_home(kk[q], P.slog2); }
