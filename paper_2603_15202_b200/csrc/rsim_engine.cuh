@@ -293,6 +293,62 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
 #endif
         return true;
     }
+    if (q == 0 && fin_step && ndec <= 32) {
+        // decode step with finishes and at most 32 running (engine.py:333-347): one record per
+        // lane; 32-bit warp reductions (REDUX) replace the 64-bit shuffle trees
+        REnt *e = rb + lane;
+        const bool valid = lane < ndec;
+        const i64 v = valid ? e->v : RSIM_NONE;
+        const i64 dcs0 = sp->dcs;
+        const i64 end = t + decode_cost_us(P, ndec, dcs0);
+        const bool fin = valid && v == step_idx;
+        const bool keep = valid && !fin;
+        const u32 fm = __ballot_sync(FULL, fin), km = __ballot_sync(FULL, keep);
+        u64 g = 0;                                                 // in + out of a finisher (< 2^41)
+        if (fin) { g = (u64)e->in + (u64)(u32)e->out; P.finish[e->req] = end; }
+        const u64 gone = ((u64)__reduce_add_sync(FULL, (u32)(g >> 20)) << 20) + __reduce_add_sync(FULL, (u32)(g & 0xfffffu));
+        int nf = 0;
+        add_finishers(P, sp, gi, F, nf, fm, e, end, lane, werr_sm, df);
+        const int dst = __popc(km & lanemask_lt());
+        const bool move = keep && dst != lane;
+        if (__any_sync(FULL, move)) {                              // compact: all reads before any write
+            ulonglong2 c0, c1, c2, c3;
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(e);
+            if (move) { c0 = src[0]; c1 = src[1]; c2 = src[2]; c3 = src[3]; }
+            __syncwarp();
+            if (move) {
+                ulonglong2 *d = reinterpret_cast<ulonglong2 *>(rb + dst);
+                d[0] = c0; d[1] = c1; d[2] = c2; d[3] = c3;
+            }
+        }
+        const u32 mo = __reduce_min_sync(FULL, keep ? (u32)(v - step_idx) : 0xffffffffu);
+        const i64 nfin = mo == 0xffffffffu ? RSIM_NONE : step_idx + (i64)mo;
+        const int r = __popc(km);
+        if (nf) finish_or_defer(P, sp, gi, s, F, nf, end, lane, werr_sm, df);
+        __syncwarp();
+        if (lane == 0) {
+            sp->r = r;
+            sp->total = sp->total + ndec - (i64)gone;
+            sp->dcs = dcs0 + ndec - (i64)gone;
+            sp->next_finish = nfin;
+            sp->busy_until = end;                                  // engine.py:349-352
+            sp->due = end;
+            sp->next_step = end;
+            sp->step_idx = step_idx + 1;
+        }
+        log_step(P, gi, t, end, 0, (i64)r, step_idx, lane);
+        __syncwarp();
+        SP_MARK(7);
+#ifdef RSIM_STEP_PROFILE
+        if (P.ctr != nullptr && lane == 0) {
+            long long tot = 0;
+            for (int i = 0; i < 8; i++) { atomicAdd(P.ctr + 16 + i, (u64)spc[i]); tot += spc[i]; }
+            atomicAdd(P.ctr + 24, (u64)1);
+            atomicAdd(P.ctr + 25, (u64)tot);
+        }
+#endif
+        return true;
+    }
     if (q == 1 && !fin_step) {
         // one queued request, no decode finish: the FIFO plan, pop and join of the general path
         // below for a single entry, on lane 0 (no warp scans); a pop that finishes at once
