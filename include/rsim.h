@@ -161,9 +161,11 @@ rsim_status rsim_open_peer_ipc(rsim_t *h, int32_t rank, const unsigned char in64
  * capacity 0 turns recording off. Read back with rsim_read_phase_records. */
 rsim_status rsim_phase_records(rsim_t *h, int64_t capacity_decisions);
 rsim_status rsim_read_phase_records(rsim_t *h, uint16_t *out, int64_t n_decisions, int32_t *warps_per_decision);
-/* Diagnostics of builds with -DRSIM_STEP_PROFILE: SM cycles summed over engine steps per step
- * section (setup, plan, cost, apply, pops, decode, finishers, joins+tail); zeros otherwise. */
-rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out8);
+/* Diagnostics of builds with -DRSIM_STEP_PROFILE (16 int64): [0..7] SM cycles summed over engine
+ * steps per step section (setup, plan, cost, apply, pops, decode, finishers, joins+tail);
+ * [8..9] count / cycles of steps where a request finishes, [10..11] of other full steps,
+ * [12..13] of pure decode steps; zeros otherwise. */
+rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out16);
 /* Number of kernels librsim launched since create (evidence for bench gpu_launches). */
 int64_t rsim_launch_count(const rsim_t *h);
 

@@ -126,6 +126,23 @@ __device__ __forceinline__ u64 ld_relaxed_sys(const u64 *p) {
     asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// explicit shared-space loads for pointers the compiler cannot prove to be shared
+// (a generic LD to shared memory takes the L1TEX path and a long scoreboard)
+__device__ __forceinline__ ulonglong2 lds_v2u64(const void *p) {
+    ulonglong2 v;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ u64 lds_u64(const void *p) {
+    u64 v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ u32 lds_u32(const void *p) {
+    u32 v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
 __device__ __forceinline__ u64 globaltimer() { u64 t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 
 struct __align__(16) Part { u64 minb; u32 cnt; u32 err; };
@@ -133,17 +150,17 @@ struct __align__(16) Part { u64 minb; u32 cnt; u32 err; };
 // ---------------------------------------------------------------- score
 // Policy scores (policies.py:104-139) as IEEE doubles, bit-exact with
 // CPython's float arithmetic (each op rounded to nearest, no contraction).
-__device__ __forceinline__ double score_of(const Params &P, const Inst &s, int h, i64 in) {
-    const i64 bsz = (i64)s.v_r + s.v_q;
+__device__ __forceinline__ double score_of(const Params &P, int v_r, int v_q, i64 v_pend, i64 v_total, int h, i64 in) {
+    const i64 bsz = (i64)v_r + v_q;
     if (P.policy == 0) {                                            // multiplicative
         i64 ht = (i64)h * P.bs; if (ht > in) ht = in;
         i64 nw = in - ht; if (nw < 1) nw = 1;
-        double kv = P.kv_ind == 0 ? __ll2double_rn(s.v_pend + nw)
+        double kv = P.kv_ind == 0 ? __ll2double_rn(v_pend + nw)
                                   : __dsub_rn(1.0, __ddiv_rn(__ll2double_rn(ht), __ll2double_rn(in)));
-        i64 bal = P.bal_ind == 0 ? bsz : s.v_total;
+        i64 bal = P.bal_ind == 0 ? bsz : v_total;
         return __dmul_rn(kv, __ll2double_rn(bal > 1 ? bal : 1));
     } else if (P.policy == 1) {                                     // vllm
-        return __dadd_rn(__dmul_rn(P.qw, (double)s.v_q), (double)s.v_r);
+        return __dadd_rn(__dmul_rn(P.qw, (double)v_q), (double)v_r);
     }
     return __ll2double_rn(bsz);                                     // least_bs
 }
@@ -151,35 +168,37 @@ __device__ __forceinline__ double score_of(const Params &P, const Inst &s, int h
 // enqueue on the winner (InstanceSim.enqueue, engine.py:262-289) + route bookkeeping
 // The touch + pin of the hit chain is parked in F (run_touch_pin) and runs after
 // this warp's next publish, or earlier before cache work on the same instance.
-__device__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, const u64 *keys128, const int *slot0,
-                       i64 a, int B, i64 in, int out, i64 oa, int lane, int &werr, FinBuf &F) {
+__device__ __forceinline__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, const u64 *keys128,
+                                       const int *slot0, i64 a, int B, i64 in, int out, i64 oa, int lane, int &werr,
+                                       FinBuf &F) {
+    // scalar work on lane 0: a handful of shared-memory fields and one 64-B queue record
+    int bad = 0;
     __syncwarp();
     if (lane == 0) {
-        F.tpn = h > 0; F.tpgi = gi; F.tph = h; F.tpver = sp->tabver; F.tpa = a; F.tpt = t;
-        F.tpkeys = keys128; F.tpsl = slot0; F.tpsp = sp;
+        const int q = sp->q;
+        if (q >= (1 << P.qlog2)) {
+            bad = 1;
+        } else {
+            F.tpn = h > 0; F.tpgi = gi; F.tph = h; F.tpver = sp->tabver; F.tpa = a; F.tpt = t;
+            F.tpkeys = keys128; F.tpsl = slot0; F.tpsp = sp;
+            i64 ht = (i64)h * P.bs; if (ht > in) ht = in;
+            i64 pending = in - ht; if (pending < 1) pending = 1;
+            Ent e;
+            e.v = pending; e.in = in; e.a = a; e.oa = oa;
+            e.req = (int)k; e.flags = 0; e.out = out; e.B = B;
+            e.L = B + (int)((out + P.bs - 1) / P.bs); e.hb = h;
+            e.kx = (h < B && h < 128) ? keys128[h] : 0ULL;
+            P.qbuf[((size_t)gi << P.qlog2) + ((sp->q_head + q) & ((1 << P.qlog2) - 1))] = e;
+            P.hit_blocks[k] = h;
+            P.chosen[k] = P.gbase + gi;
+            P.hit_tokens[k] = ht;
+            P.route_bs[k] = (i64)q + 1 + sp->r;
+            sp->q = q + 1; sp->pend += pending; sp->total += in;
+            sp->v_q += 1; sp->v_pend += pending; sp->v_total += in;   // view moves incrementally (engine.py:284-285)
+            if (sp->next_step == RSIM_NONE && sp->busy_until <= t) sp->next_step = t;   // cluster.py:284-285
+        }
     }
-    __syncwarp();
-    Inst s = *sp;
-    i64 ht = (i64)h * P.bs; if (ht > in) ht = in;
-    i64 pending = in - ht; if (pending < 1) pending = 1;
-    if (s.q >= (1 << P.qlog2)) { werr = DEV_E_QUEUE_OVERFLOW; return; }
-    if (lane == 0) {
-        Ent e;
-        e.v = pending; e.in = in; e.a = a; e.oa = oa;
-        e.req = (int)k; e.flags = 0; e.out = out; e.B = B;
-        e.L = B + (int)((out + P.bs - 1) / P.bs); e.hb = h;
-        e.kx = (h < B && h < 128) ? keys128[h] : 0ULL;
-        P.qbuf[((size_t)gi << P.qlog2) + ((s.q_head + s.q) & ((1 << P.qlog2) - 1))] = e;
-        P.hit_blocks[k] = h;
-        P.chosen[k] = P.gbase + gi;
-        P.hit_tokens[k] = ht;
-        P.route_bs[k] = (i64)s.q + 1 + s.r;
-    }
-    s.q += 1; s.pend += pending; s.total += in;
-    s.v_q += 1; s.v_pend += pending; s.v_total += in;              // view moves incrementally (engine.py:284-285)
-    if (s.next_step == RSIM_NONE && s.busy_until <= t) s.next_step = t;   // cluster.py:284-285
-    __syncwarp();
-    if (lane == 0) *sp = s;
+    if (__shfl_sync(FULL, bad, 0)) werr = DEV_E_QUEUE_OVERFLOW;
     __syncwarp();
 }
 
@@ -286,8 +305,8 @@ __device__ __forceinline__ void probe_hits(const Params &P, int base, int l0, in
     for (int j = 0; j < 4; j++) {
         const int d = j * LP + li;
         vd[j] = j < DS && d < B;
-        kk[j] = vd[j] ? R.keys[d] : 0;
-        hm[j] = vd[j] ? R.home[d] : 0;
+        kk[j] = vd[j] ? lds_u64(R.keys + d) : 0;
+        hm[j] = vd[j] ? lds_u32(R.home + d) : 0;
     }
     for (int s0 = 0; s0 < n; s0 += G) {
         if (((need >> s0) & ((1u << G) - 1u)) == 0) continue;          // warp-uniform
@@ -345,9 +364,13 @@ __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, 
     u32 cb = 0;
     if (cand) {
         Inst *sp = st + l0 + lane;
-        if (sp->due <= R.t) flush_view(*sp, R.t);        // snapshot() flushes every candidate (indicators.py:36-65)
+        // snapshot() flushes every candidate (indicators.py:36-65): the view is the live state once due
+        const bool fl = sp->due <= R.t;
+        const int vr = fl ? sp->r : sp->v_r, vq = fl ? sp->q : sp->v_q;
+        const i64 vp = fl ? sp->pend : sp->v_pend, vt = fl ? sp->total : sp->v_total;
+        if (fl) { sp->v_r = vr; sp->v_q = vq; sp->v_pend = vp; sp->v_total = vt; sp->v_dc = sp->dcs; sp->due = RSIM_NONE; }
         const int h = WB.hit[lane];
-        const double sc = score_of(P, *sp, h, R.in);
+        const double sc = score_of(P, vr, vq, vp, vt, h, R.in);
         bits = (u64)__double_as_longlong(sc);
         if (P.scores != nullptr) P.scores[gi] = sc;
         // one 8-B key compare per reference dict lookup + 16 B of view
@@ -384,7 +407,10 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
     for (int r = 0; r < 8; r++) {
         const int idx = r * 32 + lane;
         pm[r] = ~0ULL; pc[r] = 0;
-        if (r < NR && idx < CW) { const Part q = pp[idx]; pm[r] = q.minb; pc[r] = q.cnt; er |= q.err; mn = min(mn, q.minb); }
+        if (r < NR && idx < CW) {
+            const ulonglong2 q = lds_v2u64(pp + idx);
+            pm[r] = q.x; pc[r] = (u32)q.y; er |= (u32)(q.y >> 32); mn = min(mn, q.x);
+        }
     }
     // 64-bit min with two 32-bit redux ops
     const u32 hmin = __reduce_min_sync(FULL, (u32)(mn >> 32));
@@ -637,9 +663,12 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     const ReqStage &R1 = rq[(k + 1) % RSIM_SLOTS];
                     // instances that cannot win this decision advance to the next arrival meanwhile
                     const u32 adv = __ballot_sync(FULL, lane < nmine && mybits != wmin);
+                    DIAG(const long long t_s0 = clock64());
                     if (adv) drain_phase(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
+                    DIAG(const long long t_s1 = clock64());
                     // probe-ahead of request k+1 (valid while the instance's tabver holds)
                     probe_hits(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph, WB.slot[par ^ 1]);
+                    DIAG(if (prof && lane == 0) { atomicAdd(P.ctr + 30, (u64)(t_s1 - t_s0)); atomicAdd(P.ctr + 31, (u64)(clock64() - t_s1)); });
                     if (lane < nmine) WB.spver[lane] = st[l0 + lane].tabver;
                     if (lane == 0) WB.spk = k + 1;
                     __syncwarp();

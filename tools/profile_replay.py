@@ -93,5 +93,11 @@ for c, w in shapes:
     sc = h.step_cycles()
     if sc.any() and ctr[1]:
         names = ["setup", "plan", "cost", "apply", "pops", "decode", "finish", "joins+tail"]
-        print("   step sections (cycles/step): " + "  ".join(f"{n}={c / ctr[1]:.0f}" for n, c in zip(names, sc)), flush=True)
+        print("   step sections (cycles/step): " + "  ".join(f"{n}={c / ctr[1]:.0f}" for n, c in zip(names, sc[:8])), flush=True)
+        if sc[14] or sc[15]:
+            print(f"   warp 0 post-publish: advance non-candidates {sc[14] / len(trace):.0f} cyc/decision, "
+                  f"probe-ahead {sc[15] / len(trace):.0f} cyc/decision", flush=True)
+        kinds = ["finishing", "other full", "pure decode"]
+        print("   step kinds: " + "  ".join(f"{kinds[i]} {sc[8 + 2 * i]} x {sc[9 + 2 * i] / max(sc[8 + 2 * i], 1):.0f} cyc"
+                                          for i in range(3)), flush=True)
     h.close()
