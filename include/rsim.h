@@ -161,11 +161,13 @@ rsim_status rsim_open_peer_ipc(rsim_t *h, int32_t rank, const unsigned char in64
  * capacity 0 turns recording off. Read back with rsim_read_phase_records. */
 rsim_status rsim_phase_records(rsim_t *h, int64_t capacity_decisions);
 rsim_status rsim_read_phase_records(rsim_t *h, uint16_t *out, int64_t n_decisions, int32_t *warps_per_decision);
-/* Diagnostics of builds with -DRSIM_STEP_PROFILE (16 int64): [0..7] SM cycles summed over engine
- * steps per step section (setup, plan, cost, apply, pops, decode, finishers, joins+tail);
- * [8..9] count / cycles of steps where a request finishes, [10..11] of other full steps,
- * [12..13] of pure decode steps; zeros otherwise. */
-rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out16);
+/* Diagnostics of builds with -DRSIM_DIAG -DRSIM_STEP_PROFILE (32 int64): [0..7] SM cycles summed
+ * over engine steps per step section (setup, plan, cost, apply, pops, decode, finishers,
+ * joins+tail); [8..9] count / cycles of steps where a request finishes, [10..11] of other full
+ * steps, [12..13] of pure decode steps; [14..15] warp 0 of CTA 0: advancing non-candidates /
+ * probe-ahead cycles; [16..19] its probe-ahead sections (setup, issue, evaluate, tail); zeros
+ * otherwise. */
+rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out32);
 /* Number of kernels librsim launched since create (evidence for bench gpu_launches). */
 int64_t rsim_launch_count(const rsim_t *h);
 

@@ -280,7 +280,7 @@ class Handle:
         return out
 
     def step_cycles(self) -> np.ndarray:
-        out = np.zeros(16, np.int64)
+        out = np.zeros(32, np.int64)
         self._ck(self._L.rsim_read_step_cycles(self._h, out.ctypes.data))
         return out
 

@@ -175,7 +175,7 @@ static rsim_status init_state(rsim_t *h) {
     CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaMemsetAsync(h->errbuf, 0, 4 * sizeof(int), h->stream));
     CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), h->stream));
-    CK(h, cudaMemsetAsync(h->ctr, 0, 32 * sizeof(u64), h->stream));
+    CK(h, cudaMemsetAsync(h->ctr, 0, 48 * sizeof(u64), h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     h->R = 0; h->nblk = 0; h->nout = 0; h->narena = 0;
     // blk_off / ooff hold a leading 0
@@ -285,7 +285,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaMalloc(&h->log_n, sizeof(u64)));
     CK(nullptr, cudaMalloc(&h->scores, N * sizeof(double)));
     CK(nullptr, cudaMalloc(&h->scratch_res, 4 * sizeof(i64)));
-    CK(nullptr, cudaMalloc(&h->ctr, 32 * sizeof(u64)));   // [16..23]: RSIM_STEP_PROFILE builds
+    CK(nullptr, cudaMalloc(&h->ctr, 48 * sizeof(u64)));   // [16..47]: diagnostics builds
     CK(nullptr, cudaMalloc(&h->mbox, 2 * 8 * 4 * sizeof(u64)));
     CK(nullptr, cudaMemset(h->mbox, 0, 2 * 8 * 4 * sizeof(u64)));
     h->peer[world > 1 ? c.rank : 0] = h->mbox;
@@ -652,7 +652,7 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
     CK(h, cudaMemsetAsync(h->tmeta, 0, slots * sizeof(Meta), s));
     CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, s));
     CK(h, cudaMemsetAsync(h->log_n, 0, sizeof(u64), s));
-    CK(h, cudaMemsetAsync(h->ctr, 0, 32 * sizeof(u64), s));
+    CK(h, cudaMemsetAsync(h->ctr, 0, 48 * sizeof(u64), s));
     if (h->R > 0) {
         DevArr<i64> *outs[] = {&h->hit_tokens, &h->first_sched, &h->first_token, &h->finish, &h->route_bs, &h->dec_ns};
         for (auto *a : outs) CK(h, cudaMemsetAsync(a->p, 0xff, h->R * sizeof(i64), s));
@@ -686,12 +686,12 @@ rsim_status rsim_read_counters(rsim_t *h, int64_t *out16) {
     return RSIM_OK;
 }
 
-rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out16) {
-    if (!h || !out16) return RSIM_E_INVALID;
+rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out32) {
+    if (!h || !out32) return RSIM_E_INVALID;
     CK(h, cudaSetDevice(h->cfg.device));
-    u64 c[16];
+    u64 c[32];
     CK(h, cudaMemcpy(c, h->ctr + 16, sizeof(c), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 16; i++) out16[i] = (int64_t)c[i];
+    for (int i = 0; i < 32; i++) out32[i] = (int64_t)c[i];
     return RSIM_OK;
 }
 

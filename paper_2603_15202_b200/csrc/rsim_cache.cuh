@@ -101,7 +101,7 @@ __device__ __forceinline__ void find128(const Table &T, const u64 kk[4], const b
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         home[k] = tab_home(kk[k], T.slog2);
-        if (act[k]) pr[k] = ld_pair(T, home[k]);
+        pr[k] = act[k] ? ld_pair(T, home[k]) : make_ulonglong2(0ULL, 0ULL);   // unconditional: stays in registers
     }
 #pragma unroll
     for (int k = 0; k < 4; k++) {
@@ -136,7 +136,7 @@ __device__ __forceinline__ void probe128(const Table *T, const u64 kk[4], const 
     for (int s = 0; s < NI; s++)
 #pragma unroll
         for (int k = 0; k < 4; k++)
-            if (k < nk && 32 * k + lane < B) pr[s][k] = ld_pair(T[s], hm[k]);
+            pr[s][k] = (k < nk && 32 * k + lane < B) ? ld_pair(T[s], hm[k]) : make_ulonglong2(0ULL, 0ULL);
 #pragma unroll
     for (int s = 0; s < NI; s++)
 #pragma unroll
@@ -369,15 +369,14 @@ __device__ int warp_finish_many(const Table &T, const u64 *ckeys, const u64 *oke
         for (int k = 0; k < 4; k++) {
             const int x = x0 + 32 * k + lane;
             act[k] = x < K;
-            kk[k] = 0; dep[k] = 0; unp[k] = false;
-            if (act[k]) {
-                int f = 0;
+            int f = 0;
+            if (act[k])
                 while (f + 1 < nf && F.pre[f + 1] <= x) f++;
-                const int j = x - F.pre[f];
-                kk[k] = j < F.B[f] ? ckeys[F.a[f] + j] : okeys[F.oa[f] + j - F.B[f]];
-                dep[k] = j + 1;
-                unp[k] = j < F.hb[f];
-            }
+            const int j = x - F.pre[f];
+            // unconditional assignments (a conditionally assigned array goes to local memory)
+            kk[k] = act[k] ? (j < F.B[f] ? ckeys[F.a[f] + j] : okeys[F.oa[f] + j - F.B[f]]) : 0ULL;
+            dep[k] = act[k] ? j + 1 : 0;
+            unp[k] = act[k] && j < F.hb[f];
         }
         int slot[4];
         u32 fp[4];

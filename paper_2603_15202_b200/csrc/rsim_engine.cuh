@@ -312,9 +312,10 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         const int dst = __popc(km & lanemask_lt());
         const bool move = keep && dst != lane;
         if (__any_sync(FULL, move)) {                              // compact: all reads before any write
-            ulonglong2 c0, c1, c2, c3;
             const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(e);
-            if (move) { c0 = src[0]; c1 = src[1]; c2 = src[2]; c3 = src[3]; }
+            const ulonglong2 z = make_ulonglong2(0ULL, 0ULL);
+            const ulonglong2 c0 = move ? src[0] : z, c1 = move ? src[1] : z;   // unconditional: registers
+            const ulonglong2 c2 = move ? src[2] : z, c3 = move ? src[3] : z;
             __syncwarp();
             if (move) {
                 ulonglong2 *d = reinterpret_cast<ulonglong2 *>(rb + dst);
@@ -539,9 +540,10 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
                 add_finishers(P, sp, gi, F, nf, fm, e, end, lane, werr_sm, df);
             }
             if (__any_sync(FULL, move)) {                  // compact: all reads of this chunk before any write
-                ulonglong2 c0, c1, c2, c3;
                 const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(e);
-                if (move) { c0 = src[0]; c1 = src[1]; c2 = src[2]; c3 = src[3]; }
+                const ulonglong2 z = make_ulonglong2(0ULL, 0ULL);
+                const ulonglong2 c0 = move ? src[0] : z, c1 = move ? src[1] : z;
+                const ulonglong2 c2 = move ? src[2] : z, c3 = move ? src[3] : z;
                 __syncwarp();
                 if (move) {
                     ulonglong2 *d = reinterpret_cast<ulonglong2 *>(rb + dst);

@@ -130,17 +130,17 @@ __device__ __forceinline__ u64 ld_relaxed_sys(const u64 *p) {
 // (a generic LD to shared memory takes the L1TEX path and a long scoreboard)
 __device__ __forceinline__ ulonglong2 lds_v2u64(const void *p) {
     ulonglong2 v;
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(smem_addr(p)) : "memory");
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(smem_addr(p)));
     return v;
 }
 __device__ __forceinline__ u64 lds_u64(const void *p) {
     u64 v;
-    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_addr(p)) : "memory");
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_addr(p)));
     return v;
 }
 __device__ __forceinline__ u32 lds_u32(const void *p) {
     u32 v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)));
     return v;
 }
 __device__ __forceinline__ u64 globaltimer() { u64 t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
@@ -284,8 +284,17 @@ __device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base,
 // j*LP+li (j < 4) of instance s0+g, so one round trip and one instruction
 // stream cover G instances. Hit blocks go to hout[s]; found slots of
 // instances 0/1 to slot[s][depth].
-__device__ __forceinline__ void probe_hits(const Params &P, int base, int l0, int n, const ReqStage &R, int mode,
-                                           int target, u32 skip, int lane, int *hout, int (*slot)[128]) {
+// Out of line on purpose: a fresh register budget keeps the batch of loads in registers (inlined
+// into the replay loop, ptxas spilled them and every load serialised on its spill store).
+__device__ __noinline__ void probe_hits(const Params &P, int base, int l0, int n, const ReqStage &R, int mode,
+                                        int target, u32 skip, int lane, int *hout, int (*slot)[128],
+                                        bool diag = false) {
+#ifdef RSIM_DIAG
+    long long pt0 = clock64(), pt1 = 0, pt2 = 0;
+#define PMARK(v) do { if (diag) v = clock64(); } while (0)
+#else
+#define PMARK(v) do { } while (0)
+#endif
     const int B = R.B;
     const int Bc = min(B, 128);
     const int G = Bc <= 32 ? 4 : (Bc <= 64 ? 2 : 1);       // instances per round (warp-uniform)
@@ -308,49 +317,74 @@ __device__ __forceinline__ void probe_hits(const Params &P, int base, int l0, in
         kk[j] = vd[j] ? lds_u64(R.keys + d) : 0;
         hm[j] = vd[j] ? lds_u32(R.home + d) : 0;
     }
-    for (int s0 = 0; s0 < n; s0 += G) {
-        if (((need >> s0) & ((1u << G) - 1u)) == 0) continue;          // warp-uniform
-        const int s = s0 + g;
-        const bool cand = s < n && ((need >> s) & 1u);
-        const Table T = table_of(P, base + l0 + (s < n ? s : s0));
-        ulonglong2 pr[4];
+    // rounds of G instances, issued four rounds at a time: every load of a batch is in flight
+    // before the first is evaluated (one memory round trip per 4 rounds, not per round)
+    const int nr = (n + G - 1) / G;
+    PMARK(pt1);
+    for (int b0 = 0; b0 < nr; b0 += 4) {
+        ulonglong2 pr[4][4];
+        bool cd[4];
 #pragma unroll
-        for (int j = 0; j < 4; j++)
-            if (cand && vd[j]) pr[j] = ld_pair(T, hm[j]);
-        u32 mk[4];
+        for (int q = 0; q < 4; q++) {
+            const int s = (b0 + q) * G + g;
+            cd[q] = b0 + q < nr && s < n && ((need >> s) & 1u);
+            const Table T = table_of(P, base + l0 + (cd[q] ? s : 0));
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            mk[j] = 0;
-            if (j < DS) {
-                bool f = false, c = false;
-                if (cand && vd[j]) eval_first(T, pr[j], hm[j], kk[j], f, c);
-                int sl = -1;
-                if (__any_sync(FULL, c) && c) {          // rare: the home pair is full of other keys
-                    int stt;
-                    const u32 r = probe_rest(T, ((hm[j] | 1u) + 1u) & T.mask, kk[j], stt);
-                    f = stt == 0;
-                    if (f) sl = (int)r;
-                } else if (f) {
-                    sl = (int)((hm[j] & 1u) == 0 && pr[j].x == kk[j] ? hm[j] : hm[j] | 1u);
+            for (int j = 0; j < 4; j++)        // unconditional assignment keeps pr in registers
+                pr[q][j] = (cd[q] && vd[j]) ? ld_pair(T, hm[j]) : make_ulonglong2(0ULL, 0ULL);
+        }
+        PMARK(pt2);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int s0 = (b0 + q) * G;
+            if (b0 + q < nr && ((need >> min(s0, 31)) & ((1u << G) - 1u)) != 0) {   // warp-uniform
+            const int s = s0 + g;
+            const bool cand = cd[q];
+            const Table T = table_of(P, base + l0 + (s < n ? s : s0));
+            u32 mk[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                mk[j] = 0;
+                if (j < DS) {
+                    bool f = false, c = false;
+                    if (cand && vd[j]) eval_first(T, pr[q][j], hm[j], kk[j], f, c);
+                    int sl = -1;
+                    if (__any_sync(FULL, c) && c) {          // rare: the home pair is full of other keys
+                        int stt;
+                        const u32 r = probe_rest(T, ((hm[j] | 1u) + 1u) & T.mask, kk[j], stt);
+                        f = stt == 0;
+                        if (f) sl = (int)r;
+                    } else if (f) {
+                        sl = (int)((hm[j] & 1u) == 0 && pr[q][j].x == kk[j] ? hm[j] : hm[j] | 1u);
+                    }
+                    if (cand && s < 2 && vd[j]) slot[s][j * LP + li] = sl;
+                    mk[j] = __ballot_sync(FULL, f);
                 }
-                if (cand && s < 2 && vd[j]) slot[s][j * LP + li] = sl;
-                mk[j] = __ballot_sync(FULL, f);
             }
-        }
-        // leading present depths of my group's instance
-        int h = DS * LP;
-        bool done = false;
+            // leading present depths of my group's instance
+            int h = DS * LP;
+            bool done = false;
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            if (j < DS) {
-                const u32 bits = (mk[j] >> (g * LP)) & gmask;
-                if (!done && bits != gmask) { h = j * LP + __ffs(~bits) - 1; done = true; }
+            for (int j = 0; j < 4; j++) {
+                if (j < DS) {
+                    const u32 bits = (mk[j] >> (g * LP)) & gmask;
+                    if (!done && bits != gmask) { h = j * LP + __ffs(~bits) - 1; done = true; }
+                }
+            }
+            if (G == 1 && h >= 128 && B > 128) h = deep_match(T, P.ckeys + R.a, B, lane);   // G == 1: warp-uniform
+            h = min(h, B);
+            if (cand && li == 0) hout[s] = h;
             }
         }
-        if (G == 1 && h >= 128 && B > 128) h = deep_match(T, P.ckeys + R.a, B, lane);   // G == 1: warp-uniform
-        h = min(h, B);
-        if (cand && li == 0) hout[s] = h;
     }
+#ifdef RSIM_DIAG
+    if (diag && lane == 0) {
+        const long long pt3 = clock64();
+        atomicAdd(P.ctr + 32, (u64)(pt1 - pt0)); atomicAdd(P.ctr + 33, (u64)(pt2 - pt1));
+        atomicAdd(P.ctr + 34, (u64)(pt3 - pt2));
+    }
+#endif
+#undef PMARK
     __syncwarp();
 }
 
@@ -667,7 +701,11 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     if (adv) drain_phase(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
                     DIAG(const long long t_s1 = clock64());
                     // probe-ahead of request k+1 (valid while the instance's tabver holds)
+#ifdef RSIM_DIAG
+                    probe_hits(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph, WB.slot[par ^ 1], prof && warp == 0);
+#else
                     probe_hits(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph, WB.slot[par ^ 1]);
+#endif
                     DIAG(if (prof && lane == 0) { atomicAdd(P.ctr + 30, (u64)(t_s1 - t_s0)); atomicAdd(P.ctr + 31, (u64)(clock64() - t_s1)); });
                     if (lane < nmine) WB.spver[lane] = st[l0 + lane].tabver;
                     if (lane == 0) WB.spk = k + 1;

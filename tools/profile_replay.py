@@ -97,6 +97,9 @@ for c, w in shapes:
         if sc[14] or sc[15]:
             print(f"   warp 0 post-publish: advance non-candidates {sc[14] / len(trace):.0f} cyc/decision, "
                   f"probe-ahead {sc[15] / len(trace):.0f} cyc/decision", flush=True)
+        if sc[16] or sc[17]:
+            print(f"   warp 0 probe-ahead sections: setup {sc[16] / len(trace):.0f}  issue {sc[17] / len(trace):.0f}  "
+                  f"evaluate {sc[18] / len(trace):.0f} cyc/decision", flush=True)
         kinds = ["finishing", "other full", "pure decode"]
         print("   step kinds: " + "  ".join(f"{kinds[i]} {sc[8 + 2 * i]} x {sc[9 + 2 * i] / max(sc[8 + 2 * i], 1):.0f} cyc"
                                           for i in range(3)), flush=True)
