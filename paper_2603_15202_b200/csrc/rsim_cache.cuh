@@ -41,6 +41,11 @@ __device__ __forceinline__ ulonglong2 ld_pair(const Table &T, u32 i) {
     // them keeps L1 for the engine's queue / running records (measured: -7 % per decision, chat1024)
     return __ldcg(reinterpret_cast<const ulonglong2 *>(T.k) + (i >> 1));
 }
+// L1-allocating pair load for the insert / touch paths, which re-read the lines they just
+// looked up (claims). Safe: an instance's table is written only by its owning warp's SM.
+__device__ __forceinline__ ulonglong2 ld_pair_l1(const Table &T, u32 i) {
+    return __ldca(reinterpret_cast<const ulonglong2 *>(T.k) + (i >> 1));
+}
 
 // Evaluate one aligned pair starting the probe at slot i.
 // st: 0 found (returns slot), 1 absent (returns the first EMPTY slot), 2 continue (returns next i)
@@ -79,7 +84,7 @@ __device__ __forceinline__ u32 probe_rest(const Table &T, u32 i, u64 key, int &s
 __device__ __forceinline__ int tab_find(const Table &T, u64 key) {
     int st;
     u32 i = tab_home(key, T.slog2);
-    u32 r = eval_pair(T, ld_pair(T, i), i, key, st);
+    u32 r = eval_pair(T, ld_pair_l1(T, i), i, key, st);
     if (st == 2) r = probe_rest(T, r, key, st);
     return st == 0 ? (int)r : -1;
 }
@@ -101,7 +106,7 @@ __device__ __forceinline__ void find128(const Table &T, const u64 kk[4], const b
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         home[k] = tab_home(kk[k], T.slog2);
-        pr[k] = act[k] ? ld_pair(T, home[k]) : make_ulonglong2(0ULL, 0ULL);   // unconditional: stays in registers
+        pr[k] = act[k] ? ld_pair_l1(T, home[k]) : make_ulonglong2(0ULL, 0ULL);   // unconditional: stays in registers
     }
 #pragma unroll
     for (int k = 0; k < 4; k++) {
@@ -277,7 +282,7 @@ __device__ __forceinline__ void claim128(const Table &T, const u64 kk[4], const 
             if (pend) {
                 int st;
                 const u32 i = tab_home(kk[k], T.slog2);
-                u32 r = eval_pair(T, ld_pair(T, i), i, kk[k], st);
+                u32 r = eval_pair(T, ld_pair_l1(T, i), i, kk[k], st);
                 if (st == 2) r = probe_rest(T, r, kk[k], st);
                 if (st == 0) { slot[k] = (int)r; pend = false; }
                 else pos = r;

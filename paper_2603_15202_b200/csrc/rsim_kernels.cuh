@@ -446,15 +446,28 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
             pm[r] = q.x; pc[r] = (u32)q.y; er |= (u32)(q.y >> 32); mn = min(mn, q.x);
         }
     }
+    u32 cl = 0;                                   // largest tie count of any partial
+#pragma unroll
+    for (int r = 0; r < 8; r++) cl = max(cl, pc[r]);
     // 64-bit min with two 32-bit redux ops
     const u32 hmin = __reduce_min_sync(FULL, (u32)(mn >> 32));
+    const u32 cmax = __reduce_max_sync(FULL, cl);
+    er = __reduce_or_sync(FULL, er);
     const u32 lmin = __reduce_min_sync(FULL, (u32)(mn >> 32) == hmin ? (u32)mn : 0xffffffffu);
     const u64 gmin = ((u64)hmin << 32) | lmin;
-    er = __reduce_or_sync(FULL, er);
-    u32 lc = 0;
+    // every partial holds at most one tie (one instance per warp, or no intra-warp ties):
+    // the tied partials are ballot bits, the kk-th one is a bit position, no prefix scan
+    const bool single = cmax <= 1;
+    u32 tb[8];
+    u32 lc = 0, T = 0;
 #pragma unroll
-    for (int r = 0; r < 8; r++) { pc[r] = pm[r] == gmin ? pc[r] : 0u; lc += pc[r]; }
-    const u32 T = __reduce_add_sync(FULL, lc);
+    for (int r = 0; r < 8; r++) {
+        pc[r] = pm[r] == gmin ? pc[r] : 0u;
+        lc += pc[r];
+        tb[r] = (single && r < NR) ? __ballot_sync(FULL, pc[r] > 0) : 0u;
+        T += __popc(tb[r]);
+    }
+    if (!single) T = __reduce_add_sync(FULL, lc);
     Dec d; d.owner_warp = -1; d.kk = 0; d.err = (int)er; d.pad = 0;
     u32 kk = 0;
     bool mine = true;
@@ -500,7 +513,18 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         ties += 1;
     }
     if (!d.err && Tg == 0) d.err = 11;            // NoInstancesError
-    if (!d.err && mine) {
+    if (!d.err && mine && single) {
+        u32 pre = 0, kr = 0, bm = 0;
+        int rb = -1;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const u32 S = __popc(tb[r]);
+            if (rb < 0 && kk < pre + S) { rb = r; kr = kk - pre; bm = tb[r]; }
+            pre += S;
+        }
+        const int owner = rb * 32 + nth_set_bit(bm, (int)kr);
+        if (owner / W == cta) { d.owner_warp = owner % W; d.kk = 0; }
+    } else if (!d.err && mine) {
         // the round holding the kk-th tie, then the lane inside it
         u32 pre = 0, kr = 0, c = 0;
         int rb = -1;
@@ -666,7 +690,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             }
             const u32 stale_slots = df.moved & skip;     // hits raised by a parked batch: no probe slots
             __syncwarp();
-            probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
+            if ((~skip & (nmine >= 32 ? FULL : ((1u << nmine) - 1u))) != 0)   // (an out-of-line call: skip when idle)
+                probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
             const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB);
             PHASE(2);
             DIAG(const long long t_c = clock64());
