@@ -161,6 +161,9 @@ rsim_status rsim_open_peer_ipc(rsim_t *h, int32_t rank, const unsigned char in64
  * capacity 0 turns recording off. Read back with rsim_read_phase_records. */
 rsim_status rsim_phase_records(rsim_t *h, int64_t capacity_decisions);
 rsim_status rsim_read_phase_records(rsim_t *h, uint16_t *out, int64_t n_decisions, int32_t *warps_per_decision);
+/* Diagnostics (-DRSIM_DIAG builds): per decision, %globaltimer of every instance warp's publish
+ * ([C*W]), then CTA 0's control warp: partials landed, decided; CTA 0 warp 0: released; 0. */
+rsim_status rsim_read_phase_times(rsim_t *h, uint64_t *out, int64_t n_decisions);
 /* Diagnostics of builds with -DRSIM_DIAG -DRSIM_STEP_PROFILE (32 int64): [0..7] SM cycles summed
  * over engine steps per step section (setup, plan, cost, apply, pops, decode, finishers,
  * joins+tail); [8..9] count / cycles of steps where a request finishes, [10..11] of other full

@@ -105,6 +105,7 @@ def lib():
         "rsim_phase_records": ([P, I64], C.c_int),
         "rsim_read_phase_records": ([P, P, I64, P], C.c_int),
         "rsim_read_step_cycles": ([P, P], C.c_int),
+        "rsim_read_phase_times": ([P, P, I64], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -277,6 +278,11 @@ class Handle:
         self._ck(self._L.rsim_read_phase_records(self._h, None, 0, C.byref(w)))
         out = np.zeros((n, w.value, 8), np.uint16)
         self._ck(self._L.rsim_read_phase_records(self._h, out.ctypes.data, n, None))
+        return out
+
+    def read_phase_times(self, n: int, warps: int) -> np.ndarray:
+        out = np.zeros((n, warps + 4), np.uint64)
+        self._ck(self._L.rsim_read_phase_times(self._h, out.ctypes.data, n))
         return out
 
     def step_cycles(self) -> np.ndarray:

@@ -701,7 +701,9 @@ rsim_status rsim_phase_records(rsim_t *h, int64_t capacity_decisions) {
     if (h->crit) { cudaFree(h->crit); h->crit = nullptr; }
     h->crit_cap = 0;
     if (capacity_decisions == 0) return RSIM_OK;
-    const size_t bytes = (size_t)capacity_decisions * h->C * h->W * 8 * sizeof(unsigned short);
+    // records [n][C*W][8] u16, then the timeline [n][C*W + 4] u64 (%globaltimer)
+    const size_t bytes = (size_t)capacity_decisions * h->C * h->W * 8 * sizeof(unsigned short) +
+                         (size_t)capacity_decisions * (h->C * h->W + 4) * sizeof(u64);
     CK(h, cudaMalloc(&h->crit, bytes));
     CK(h, cudaMemset(h->crit, 0, bytes));
     h->crit_cap = capacity_decisions;
@@ -715,6 +717,16 @@ rsim_status rsim_read_phase_records(rsim_t *h, uint16_t *out, int64_t n_decision
     if (n_decisions > h->crit_cap) return fail(h, RSIM_E_INVALID, "more decisions than recorded");
     CK(h, cudaSetDevice(h->cfg.device));
     CK(h, cudaMemcpy(out, h->crit, (size_t)n_decisions * h->C * h->W * 8 * sizeof(unsigned short),
+                     cudaMemcpyDeviceToHost));
+    return RSIM_OK;
+}
+
+rsim_status rsim_read_phase_times(rsim_t *h, uint64_t *out, int64_t n_decisions) {
+    if (!h || !out) return RSIM_E_INVALID;
+    if (n_decisions > h->crit_cap) return fail(h, RSIM_E_INVALID, "more decisions than recorded");
+    CK(h, cudaSetDevice(h->cfg.device));
+    const size_t off = (size_t)h->crit_cap * h->C * h->W * 8;
+    CK(h, cudaMemcpy(out, h->crit + off, (size_t)n_decisions * (h->C * h->W + 4) * sizeof(u64),
                      cudaMemcpyDeviceToHost));
     return RSIM_OK;
 }

@@ -388,6 +388,97 @@ __device__ __noinline__ void probe_hits(const Params &P, int base, int l0, int n
     __syncwarp();
 }
 
+// ---- two-stage probe for warps that own several instances (prompts of <= 128 blocks). The
+// dense probe costs B lookups per instance and the SM's load unit handles ~1 line per cycle,
+// so with 10 instances per warp the probe-ahead was throughput-bound. Presence is monotone
+// in depth (prefix closure, kvcache.py:4-7): one lookup per lane at stride S = ceil(B/LP)
+// brackets the first miss within S depths, a second lookup of at most S-1 depths pins it:
+// <= LP + S - 1 lookups per instance. Both stages batch up to 8 rounds of G instances.
+__device__ __noinline__ void probe_hits_sparse(const Params &P, int base, int l0, int n, const ReqStage &R, int mode,
+                                               int target, u32 skip, int lane, int *hout) {
+    const int B = R.B;
+    const int G = B <= 32 ? 4 : (B <= 64 ? 2 : 1);
+    const int LP = 32 / G, S = (B + LP - 1) / LP;
+    const int g = lane / LP, li = lane - g * LP;
+    const u32 gmask = LP == 32 ? FULL : ((1u << LP) - 1u);
+    u32 need = (n >= 32 ? FULL : ((1u << n) - 1u)) & ~skip;
+    if (mode == MODE_ENQUEUE) {
+        const int tl = target - base - l0;
+        need &= (tl >= 0 && tl < n) ? (1u << tl) : 0u;
+    }
+    if (need == 0) return;
+    const int d1 = li * S;
+    const bool v1 = d1 < B;
+    const u64 k1 = v1 ? lds_u64(R.keys + d1) : 0ULL;
+    const u32 h1 = v1 ? lds_u32(R.home + d1) : 0u;
+    const int nr = (n + G - 1) / G;
+    for (int b0 = 0; b0 < nr; b0 += 8) {
+        ulonglong2 pr[8];
+        bool cd[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int s = (b0 + q) * G + g;
+            cd[q] = b0 + q < nr && s < n && ((need >> s) & 1u);
+            const Table T = table_of(P, base + l0 + (cd[q] ? s : 0));
+            pr[q] = (cd[q] && v1) ? ld_pair(T, h1) : make_ulonglong2(0ULL, 0ULL);
+        }
+        // stage 1: first miss lane m of each group -> segment of candidate depths
+        int lo[8], cnt[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            lo[q] = 0; cnt[q] = 0;
+            if (b0 + q < nr) {                                            // warp-uniform
+                const int s = (b0 + q) * G + g;
+                const Table T = table_of(P, base + l0 + (cd[q] ? s : 0));
+                bool f = false, c = false;
+                if (cd[q] && v1) eval_first(T, pr[q], h1, k1, f, c);
+                if (__any_sync(FULL, c) && c) {
+                    int stt;
+                    probe_rest(T, ((h1 | 1u) + 1u) & T.mask, k1, stt);
+                    f = stt == 0;
+                }
+                const u32 bits = (__ballot_sync(FULL, f) >> (g * LP)) & gmask;
+                const int m = bits == gmask ? LP : __ffs(~bits) - 1;   // lanes 0..m-1 present
+                lo[q] = m == 0 ? 0 : (m - 1) * S + 1;                     // depth (m-1)*S present
+                cnt[q] = m == 0 ? 0 : min(m * S, B) - lo[q];              // depths lo..lo+cnt-1 unknown
+            }
+        }
+        ulonglong2 p2[8];
+        u64 k2[8];
+        u32 hh2[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int s = (b0 + q) * G + g;
+            const bool v2 = cd[q] && li < cnt[q];
+            const int d2 = lo[q] + li;
+            k2[q] = v2 ? lds_u64(R.keys + d2) : 0ULL;
+            hh2[q] = v2 ? lds_u32(R.home + d2) : 0u;
+            const Table T = table_of(P, base + l0 + (cd[q] ? s : 0));
+            p2[q] = v2 ? ld_pair(T, hh2[q]) : make_ulonglong2(0ULL, 0ULL);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            if (b0 + q < nr) {                                            // warp-uniform
+                const int s = (b0 + q) * G + g;
+                const bool v2 = cd[q] && li < cnt[q];
+                const Table T = table_of(P, base + l0 + (cd[q] ? s : 0));
+                bool f = false, c = false;
+                if (v2) eval_first(T, p2[q], hh2[q], k2[q], f, c);
+                if (__any_sync(FULL, c) && c) {
+                    int stt;
+                    probe_rest(T, ((hh2[q] | 1u) + 1u) & T.mask, k2[q], stt);
+                    f = stt == 0;
+                }
+                const u32 bits = (__ballot_sync(FULL, f) >> (g * LP)) & gmask;
+                const u32 cm = cnt[q] >= LP ? gmask : ((1u << cnt[q]) - 1u);
+                const int h = lo[q] + ((bits & cm) == cm ? cnt[q] : __ffs(~bits) - 1);
+                if (cd[q] && li == 0) hout[s] = min(h, B);
+            }
+        }
+    }
+    __syncwarp();
+}
+
 // ---- score this warp's instances from their hit blocks (policies.py:117-139); lane s
 // handles instance s and returns its score bits (~0 = not a candidate).
 __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
@@ -647,8 +738,17 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             while (!mbar_try_wait(&mb[par], (mb_phase >> par) & 1u)) { }
             mb_phase ^= 1u << par;
             PHASE(4);
+#ifdef RSIM_DIAG
+            u64 *tlc = (P.crit != nullptr && cta == 0 && lane == 0 && k - k0 < P.crit_cap)
+                           ? reinterpret_cast<u64 *>(P.crit + (size_t)P.crit_cap * CW * 8) + (size_t)(k - k0) * (CW + 4) + CW
+                           : nullptr;
+            if (tlc) tlc[0] = globaltimer();
+#endif
             decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane);
             PHASE(5);
+#ifdef RSIM_DIAG
+            if (tlc) tlc[1] = globaltimer();
+#endif
             __syncwarp();
             if (lane == 0) mbar_arrive(&dmb[par]);          // release decision k to the instance warps
             if (dec[par].err) break;
@@ -690,8 +790,13 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             }
             const u32 stale_slots = df.moved & skip;     // hits raised by a parked batch: no probe slots
             __syncwarp();
-            if ((~skip & (nmine >= 32 ? FULL : ((1u << nmine) - 1u))) != 0)   // (an out-of-line call: skip when idle)
-                probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
+            if ((~skip & (nmine >= 32 ? FULL : ((1u << nmine) - 1u))) != 0) {   // (an out-of-line call: skip when idle)
+                if (nmine >= 2 && R.B <= 128)
+                    probe_hits_sparse(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit);
+                else
+                    probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
+            }
+            const u32 sparse_probe = (nmine >= 2 && R.B <= 128) ? ~skip : 0u;   // no probe slots for these
             const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB);
             PHASE(2);
             DIAG(const long long t_c = clock64());
@@ -712,6 +817,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 rec[0] = q16(t_d - t_rel); rec[1] = q16(t_b - t_a); rec[2] = q16(t_c - t_b); rec[3] = q16(t_a - t_rel);
                 rec[4] = (unsigned short)min((u64)65535, WB.c_steps - steps0); rec[5] = (unsigned short)(WB.fins - fins0);
                 rec[6] = (unsigned short)(was_owner ? 1 : 0); rec[7] = (unsigned short)(WB.fin.npark - park0);
+                u64 *tl = reinterpret_cast<u64 *>(P.crit + (size_t)P.crit_cap * CW * 8);
+                tl[(size_t)(k - k0) * (CW + 4) + cta * W + warp] = globaltimer();
             }
 #endif
             apply_deferred(P, WB.fin, lane, &WB.werr);      // parked finisher cache work (before any commit)
@@ -726,11 +833,15 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     if (adv) drain_phase(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
                     DIAG(const long long t_s1 = clock64());
                     // probe-ahead of request k+1 (valid while the instance's tabver holds)
+                    if (nmine >= 2 && R1.B <= 128) {
+                        probe_hits_sparse(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph);
+                    } else {
 #ifdef RSIM_DIAG
-                    probe_hits(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph, WB.slot[par ^ 1], prof && warp == 0);
+                        probe_hits(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph, WB.slot[par ^ 1], prof && warp == 0);
 #else
-                    probe_hits(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph, WB.slot[par ^ 1]);
+                        probe_hits(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph, WB.slot[par ^ 1]);
 #endif
+                    }
                     DIAG(if (prof && lane == 0) { atomicAdd(P.ctr + 30, (u64)(t_s1 - t_s0)); atomicAdd(P.ctr + 31, (u64)(clock64() - t_s1)); });
                     if (lane < nmine) WB.spver[lane] = st[l0 + lane].tabver;
                     if (lane == 0) WB.spk = k + 1;
@@ -741,6 +852,10 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             while (!mbar_try_wait(&dmb[par], (dph >> par) & 1u)) { }   // decision k released by the control warp
             dph ^= 1u << par;
             PHASE(6);
+#ifdef RSIM_DIAG
+            if (P.crit != nullptr && cta == 0 && warp == 0 && lane == 0 && k - k0 < P.crit_cap)
+                reinterpret_cast<u64 *>(P.crit + (size_t)P.crit_cap * CW * 8)[(size_t)(k - k0) * (CW + 4) + CW + 2] = globaltimer();
+#endif
             DIAG(t_rel = clock64());
             const Dec d = dec[par];
             if (d.err) {
@@ -754,7 +869,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 int werr = 0;
                 flush_touch_pin(P, WB.fin, lane, &WB.werr);      // (normally already run after the publish)
                 commit(P, st + l0 + s, base + l0 + s, k, h, R.t, R.keys,
-                       (s < 2 && !((stale_slots >> s) & 1u)) ? WB.slot[par][s] : nullptr,
+                       (s < 2 && nmine < 2 && !(((stale_slots | sparse_probe) >> s) & 1u)) ? WB.slot[par][s] : nullptr,
                        R.a, R.B, R.in, R.out, R.oa, lane, werr, WB.fin);
                 if (lane == 0 && werr) WB.werr = werr;
                 if (P.dec_ns != nullptr && lane == 0) P.dec_ns[k] = (i64)globaltimer();

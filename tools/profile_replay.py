@@ -63,6 +63,18 @@ def critpath(h, n):
             print(f"     critical warp with {lo}{'+' if hi > 2 else ''} finisher batches: {m.mean():.2f} of decisions, latency "
                   f"{16 * top[m, 0].mean():.0f}, drain {16 * top[m, 1].mean():.0f}, probe {16 * top[m, 2].mean():.0f}, "
                   f"steps {top[m, 4].mean():.2f}", flush=True)
+    tl = h.read_phase_times(n, rec.shape[1]).astype(np.float64)   # ns
+    W = rec.shape[1]
+    pub = tl[:, :W].max(axis=1)
+    land, decided, rel = tl[:, W], tl[:, W + 1], tl[:, W + 2]
+    ok = (land > 0) & (decided > 0) & (rel > 0)
+    ok[1:] &= rel[:-1] > 0
+    idx = np.nonzero(ok[1:])[0] + 1
+    if idx.size:
+        f = lambda x: float(np.median(x))
+        print(f"   timeline (median ns per decision): period {f(rel[idx] - rel[idx - 1]):.0f} = release->last publish "
+              f"{f(pub[idx] - rel[idx - 1]):.0f} + exchange {f(land[idx] - pub[idx]):.0f} + decide {f(decided[idx] - land[idx]):.0f}"
+              f" + release {f(rel[idx] - decided[idx]):.0f}", flush=True)
     h.phase_records(0)
 
 
