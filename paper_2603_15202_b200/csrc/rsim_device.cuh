@@ -26,28 +26,6 @@ typedef unsigned int u32;
 #define DEV_E_TABLE_FULL 8
 #define DEV_E_COMM 10
 
-// Engine + router state of one instance. Live aggregates are the engine's
-// truth (engine.py:219-222); v_* is the router-visible view that only syncs at
-// step end (engine.py:224-246). next_finish caches min(finish_step) over the
-// running list so steps without a finish never touch the list.
-struct __align__(16) Inst {
-    i64 next_step;    // next engine step start (RSIM_NONE = idle)     cluster.py:244-285 next_step[]
-    i64 busy_until;   // engine.py:214
-    i64 due;          // view sync due time (RSIM_NONE = none)         engine.py:227
-    i64 pend, total, dcs;          // live pending / total / decode-context tokens
-    i64 v_pend, v_total, v_dc;     // view
-    i64 step_idx;     // steps executed so far
-    i64 next_finish;  // min finish step among running (RSIM_NONE if none)
-    i64 occ;          // KV$ occupancy (live chains)
-    i64 r_head, r_tail, r_tailT;   // touch-run ring (finite capacity): positions and newest T
-    i64 pad2;
-    int r, q;         // live running / queued counts
-    int v_r, v_q;     // view counts
-    int q_head;       // queue ring head index
-    int tabver;       // bumped whenever the KV$ key set may change (finish inserts / evictions):
-                      // a probe made at version v stays valid while tabver == v
-};
-
 // A request on an instance: one 64-byte record used by the FIFO queue (v =
 // pending prefill tokens) and the running list (v = finish step = join step +
 // out - 1). It carries everything a step needs, so pops and finishes never
@@ -63,6 +41,31 @@ struct __align__(16) Ent {
 };
 typedef Ent QEnt;
 typedef Ent REnt;
+
+// Engine + router state of one instance. Live aggregates are the engine's
+// truth (engine.py:219-222); v_* is the router-visible view that only syncs at
+// step end (engine.py:224-246). next_finish caches min(finish_step) over the
+// running list so steps without a finish never touch the list.
+struct __align__(16) Inst {
+    i64 next_step;    // next engine step start (RSIM_NONE = idle)     cluster.py:244-285 next_step[]
+    i64 busy_until;   // engine.py:214
+    i64 due;          // view sync due time (RSIM_NONE = none)         engine.py:227
+    i64 pend, total, dcs;          // live pending / total / decode-context tokens
+    i64 v_pend, v_total, v_dc;     // view
+    i64 step_idx;     // steps executed so far
+    i64 next_finish;  // min finish step among running (RSIM_NONE if none)
+    i64 occ;          // KV$ occupancy (live chains)
+    i64 r_head, r_tail, r_tailT;   // touch-run ring (finite capacity): positions and newest T
+    i64 qcpos;        // queue ring index whose record qhead caches (-1: none)
+    int r, q;         // live running / queued counts
+    int v_r, v_q;     // view counts
+    int q_head;       // queue ring head index
+    int tabver;       // bumped whenever the KV$ key set may change (finish inserts / evictions):
+                      // a probe made at version v stays valid while tabver == v
+    Ent qhead;        // copy of the FIFO head record (valid while qcpos == q_head): the step that
+                      // prefills a lone queued request reads it from shared memory, not L2
+};
+
 
 __device__ __forceinline__ Ent shfl_ent(const Ent &e, int src) {
     Ent r;

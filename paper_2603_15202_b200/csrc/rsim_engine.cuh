@@ -360,7 +360,8 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         i64 ptok1 = 0, end1 = 0, pre1 = 0, dcs1 = 0, tot1 = 0, nfin1 = 0;
         int r1 = 0, npop1 = 0;
         if (lane == 0) {
-            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(e);
+            const bool cached = sp->qcpos == (i64)qh;
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(cached ? &sp->qhead : e);
             ulonglong2 c0 = src[0], c1 = src[1], c2 = src[2], c3 = src[3];
             const i64 p = (i64)c0.x, in = (i64)c0.y;
             const int req = (int)(u32)c2.x, flags = (int)(u32)(c2.x >> 32), out = (int)(u32)c2.y;
@@ -383,6 +384,9 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
                     c2.x = (c2.x & 0xffffffffULL) | ((u64)(u32)(flags | 1) << 32);
                     ulonglong2 *dq = reinterpret_cast<ulonglong2 *>(e);
                     dq[0] = c0; dq[2] = c2;
+                    ulonglong2 *dc = reinterpret_cast<ulonglong2 *>(&sp->qhead);
+                    dc[0] = c0; dc[1] = c1; dc[2] = c2; dc[3] = c3;
+                    sp->qcpos = qh;
                 }
                 if (pop) {                                        // first token; joins the running list
                     npop1 = 1;
@@ -429,6 +433,11 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         }
     }
 
+    if (q > 0) {                                                   // the general path rewrites heads
+        __syncwarp();
+        if (lane == 0) sp->qcpos = -1;
+        __syncwarp();
+    }
     // pass 1: FIFO plan (_plan_allocations, engine.py:174-184). Entry j is
     // allocated iff j < slots and the budget left before it is positive.
     i64 ptok = 0, v0 = 0;

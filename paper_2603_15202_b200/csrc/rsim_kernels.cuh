@@ -189,6 +189,7 @@ __device__ __forceinline__ void commit(const Params &P, Inst *sp, int gi, i64 k,
             e.L = B + (int)((out + P.bs - 1) / P.bs); e.hb = h;
             e.kx = (h < B && h < 128) ? keys128[h] : 0ULL;
             P.qbuf[((size_t)gi << P.qlog2) + ((sp->q_head + q) & ((1 << P.qlog2) - 1))] = e;
+            if (q == 0) { sp->qhead = e; sp->qcpos = sp->q_head; }     // the new record is the head
             P.hit_blocks[k] = h;
             P.chosen[k] = P.gbase + gi;
             P.hit_tokens[k] = ht;
@@ -687,6 +688,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         const int words = nloc * (int)(sizeof(Inst) / 8);
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nloc; i += blockDim.x) st[i].qcpos = -1;   // head caches start cold
     const u64 c0_lo = P.tie[0], c0_hi = P.tie[1];          // TieBreaker counter at launch
     u32 ties = 0;                                          // ties resolved in this launch (control warp)
     const int l0 = warp * ipw;
