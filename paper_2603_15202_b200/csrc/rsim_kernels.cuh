@@ -577,9 +577,12 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         if (lane < P.world) {
             const u64 *slot = P.mbox + (size_t)((par * 8 + lane) * 4);
             const u64 t0 = globaltimer();
-            while (ld_acquire_sys(slot + 2) != seq) {
+            // relaxed polls (an acquire load at sys scope flushes L1 on every iteration), one
+            // acquire fence once the sequence word matches
+            while (ld_relaxed_sys(slot + 2) != seq) {
                 if ((i64)(globaltimer() - t0) > P.timeout_ns) { rer = DEV_E_COMM; break; }
             }
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
             if (!rer) {
                 rmin = ld_relaxed_sys(slot + 0);
                 const u64 ce = ld_relaxed_sys(slot + 1);
@@ -836,7 +839,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     if (adv) drain_phase(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
                     DIAG(const long long t_s1 = clock64());
                     // probe-ahead of request k+1 (valid while the instance's tabver holds)
-                    if (nmine >= 2 && R1.B <= 128) {
+                    if (nmine >= 2 && R1.B <= 128) {   // (one instance: the dense probe's single round trip wins)
                         probe_hits_sparse(P, base, l0, nmine, R1, mode, target, 0u, lane, WB.sph);
                     } else {
 #ifdef RSIM_DIAG
