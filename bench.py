@@ -253,6 +253,7 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     ns = h.decision_ns(0, R)
     lat = np.diff(ns[ns > 0]) / 1000.0
     chosen_dev, _ = h.decisions(0, R)
+    whatif = measure_whatif(h, trace, cfg, args) if args.whatif else None
     h.close()
 
     # e2e through the public API: host arrays in, results out
@@ -279,7 +280,7 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
         "value": R * len(dev_ms) / (sum(dev_ms) / 1000.0),
         "ms_per_step": statistics.mean(dev_ms),
         "e2e": R * len(e2e_s) / sum(e2e_s), "h2d": h2d, "d2h": d2h,
-        "launches": launches, "clocks": clk.summary(),
+        "launches": launches, "clocks": clk.summary(), "whatif": whatif,
         "lat_p50_us": float(np.percentile(lat, 50)) if lat.size else None,
         "lat_p99_us": float(np.percentile(lat, 99)) if lat.size else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -301,6 +302,30 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
         out["cpu_port"] = {"value": port, "unit": "decisions/s", "cores": 1, "kind": "port",
                            "sample": f"all {R} requests, oracle/rsim_oracle.c (1 thread)"}
     return out
+
+
+def measure_whatif(h, trace, cfg, args):
+    """SURVEY 8d tertiary: the batched what-if probe (M requests x all instances against the
+    replay's final KV$ state, no commits) -- the bandwidth-bound form of the probe.
+    Algorithmic bytes: 8 B per chain key of each request (read once) + 8 B per
+    reference dict lookup, min(h+1, B) per (request, instance)."""
+    M = min(len(trace), args.whatif)
+    hits = h.probe_batch(0, M)                       # warm-up + the hit matrix
+    ms = []
+    for _ in range(3):
+        h.probe_batch(0, M)
+        ms.append(h.timings()[0])
+    B = np.diff(trace.blk_off[:M + 1]).astype(np.int64)
+    look = np.minimum(hits.astype(np.int64) + 1, B[:, None])
+    alg = int(8 * B.sum() + 8 * look.sum())
+    best = min(ms) / 1000.0
+    peaks, _ = measured_peaks()
+    gbs = alg / best / 1e9
+    return {"requests": M, "instances": int(hits.shape[1]), "pairs": int(M * hits.shape[1]),
+            "ms": min(ms), "pairs_per_s": M * hits.shape[1] / best, "algorithmic_bytes": alg,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / peaks["hbm_gbs"],
+                         "kernel": "probe_batch_kernel" if hits.shape[1] >= 256 else "probe_pairs_kernel"}}
 
 
 def traffic_for(name):
@@ -370,6 +395,8 @@ def main():
     ap.add_argument("--extra", default="chat1024", help="comma list of extra workloads reported beside the headline")
     ap.add_argument("--ref-budget-s", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--whatif", type=int, default=20000,
+                    help="requests of the batched what-if probe measured after the replay (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -406,7 +433,8 @@ def main():
             extras[name] = {"value": e["value"], "e2e": e["e2e"], "ms_per_step": e["ms_per_step"],
                             "n_instances": e["cfg"].n_instances, "requests": e["R"],
                             "decision_latency_us": {"p50": e["lat_p50_us"], "p99": e["lat_p99_us"]},
-                            "roofline": e["roofline"], "cpu_baseline": e.get("cpu_baseline"),
+                            "roofline": e["roofline"], "whatif_probe": e.get("whatif"),
+                            "cpu_baseline": e.get("cpu_baseline"),
                             "cpu_port": e.get("cpu_port"),
                             "e2e_vs_cpu_baseline": (e["e2e"] / e["cpu_baseline"]["value"]) if e.get("cpu_baseline") else None,
                             "description": WORKLOADS[name][1]}
@@ -432,6 +460,7 @@ def main():
         "e2e": {"value": res["e2e"], "unit": "decisions/s", "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": res["d2h"]},
         "gpu_launches": res["launches"],
+        "whatif_probe": res.get("whatif"),
         "clocks": res["clocks"],
     }
     if "cpu_baseline" in res:

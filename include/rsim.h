@@ -35,7 +35,8 @@ typedef enum {
     RSIM_E_NO_INSTANCES = 11   /* empty candidate set (reference: NoInstancesError, policies.py:226) */
 } rsim_status;
 
-enum { RSIM_POLICY_MULTIPLICATIVE = 0, RSIM_POLICY_VLLM = 1, RSIM_POLICY_LEAST_BS = 2 };
+enum { RSIM_POLICY_MULTIPLICATIVE = 0, RSIM_POLICY_VLLM = 1, RSIM_POLICY_LEAST_BS = 2,
+       RSIM_POLICY_LINEAR = 3, RSIM_POLICY_FILTER = 4 };   /* policies.py:104-192 */
 enum { RSIM_KV_P_TOKENS = 0, RSIM_KV_ONE_MINUS_HIT = 1 };
 enum { RSIM_BAL_BS = 0, RSIM_BAL_TOTAL_TOKENS = 1 };
 
@@ -70,6 +71,9 @@ typedef struct rsim_config {
     int32_t rank;
     int64_t comm_timeout_ms;        /* a rank waiting longer on a peer fails with RSIM_E_COMM  */
     int64_t runs_capacity;          /* per-instance touch-run ring (finite capacity), 0 = auto */
+    double kv_weight;               /* PolicyConfig.kv_weight (linear)                         */
+    double bs_norm_cap;             /* PolicyConfig.bs_norm_cap (linear); 0 = per-decision max */
+    int64_t range_threshold;        /* PolicyConfig.range_threshold (filter)                   */
 } rsim_config;
 
 typedef struct rsim rsim_t;

@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-POLICY_CODE = {"multiplicative": 0, "vllm": 1, "least_bs": 2}
+POLICY_CODE = {"multiplicative": 0, "vllm": 1, "least_bs": 2, "linear": 3, "filter": 4}
 
 
 class _Cfg(C.Structure):
@@ -34,6 +34,7 @@ class _Cfg(C.Structure):
         ("dc", C.c_double), ("q_weight", C.c_double),
         ("chunk", C.c_int64), ("max_batch", C.c_int64),
         ("tie_lo", C.c_uint64), ("tie_hi", C.c_uint64),
+        ("kv_weight", C.c_double), ("bs_norm_cap", C.c_double), ("range_threshold", C.c_int64),
     ]
 
 
@@ -104,7 +105,10 @@ def make_cfg(config) -> _Cfg:
                 cache.block_size, -1 if cache.capacity_blocks is None else cache.capacity_blocks,
                 cm.prefill_base_ms, cm.prefill_per_token_ms, cm.decode_base_ms,
                 cm.decode_per_seq_ms, cm.decode_per_ctx_token_ms, pol.q_weight,
-                cm.chunk_tokens, cm.max_batch_requests, tie, 0)
+                cm.chunk_tokens, cm.max_batch_requests, tie, 0,
+                float(getattr(pol, "kv_weight", 0.4)),
+                float(pol.bs_norm_cap) if getattr(pol, "bs_norm_cap", None) is not None else 0.0,
+                int(getattr(pol, "range_threshold", 4)))
 
 
 class OracleError(RuntimeError):

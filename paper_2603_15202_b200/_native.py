@@ -57,6 +57,7 @@ class Config(C.Structure):
         ("step_log_capacity", C.c_int64), ("expected_keys", C.c_int64),
         ("world", C.c_int32), ("rank", C.c_int32), ("comm_timeout_ms", C.c_int64),
         ("runs_capacity", C.c_int64),
+        ("kv_weight", C.c_double), ("bs_norm_cap", C.c_double), ("range_threshold", C.c_int64),
     ]
 
 

@@ -30,7 +30,7 @@ from .hashing import MASK64, stable_key
 from .report import RoutingDecision, RunReport
 from .trace import PackedTrace, TraceRecord, validate_against_block_size
 
-_POLICY = {"multiplicative": 0, "vllm": 1, "least_bs": 2}
+_POLICY = {"multiplicative": 0, "vllm": 1, "least_bs": 2, "linear": 3, "filter": 4}
 INT64_MAX = (1 << 63) - 1
 
 
@@ -104,6 +104,9 @@ def native_config(config: ClusterConfig, sizing: Sizing, *, device: int = 0, rec
     c.world = world
     c.rank = rank
     c.comm_timeout_ms = comm_timeout_ms
+    c.kv_weight = pol.kv_weight
+    c.bs_norm_cap = float(pol.bs_norm_cap) if pol.bs_norm_cap is not None else 0.0
+    c.range_threshold = pol.range_threshold
     return c
 
 

@@ -20,7 +20,7 @@ from dataclasses import dataclass, field, replace
 POLICY_KINDS = ("vllm", "linear", "filter", "simulate", "multiplicative", "least_bs")
 # policies the device kernel scores (the north-star score plus the two
 # batch-size-only ones that reuse the same fused argmin)
-DEVICE_POLICY_KINDS = ("multiplicative", "vllm", "least_bs")
+DEVICE_POLICY_KINDS = ("multiplicative", "vllm", "least_bs", "linear", "filter")
 
 
 class CacheFullError(Exception):
@@ -159,3 +159,6 @@ class ClusterConfig:
             raise UnsupportedConfigError(
                 f"policy {self.policy.kind!r} is not on the device path "
                 f"(supported: {', '.join(DEVICE_POLICY_KINDS)})")
+        if self.policy.kind == "linear" and self.policy.bs_norm_cap is None:
+            raise UnsupportedConfigError("linear policy needs bs_norm_cap on the device path "
+                                         "(the per-decision max needs a second exchange round)")

@@ -122,6 +122,7 @@ static Params make_params(rsim_t *h) {
     P.route_bs = h->route_bs.p; P.dec_ns = h->dec_ns.p;
     P.N = h->N; P.C = h->C; P.W = h->W; P.ipw = h->ipw; P.per_cta = h->per_cta;
     P.bs = h->cfg.block_size; P.policy = h->cfg.policy; P.kv_ind = h->cfg.kv_indicator;
+    P.kvw = h->cfg.kv_weight; P.bsn = h->cfg.bs_norm_cap; P.range_thr = h->cfg.range_threshold;
     P.bal_ind = h->cfg.balance_indicator; P.debug = h->cfg.debug_checks;
     P.cap = h->cfg.capacity_blocks; P.chunk = h->cfg.chunk_tokens; P.max_batch = h->cfg.max_batch_requests;
     P.pb = h->cfg.prefill_base_ms; P.pt = h->cfg.prefill_per_token_ms; P.db = h->cfg.decode_base_ms;
@@ -200,7 +201,11 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (c.block_size < 1) return fail(nullptr, RSIM_E_INVALID, "block_size must be >= 1");
     if (c.capacity_blocks == 0 || c.capacity_blocks < -1) return fail(nullptr, RSIM_E_INVALID, "capacity_blocks must be >= 1 or -1");
     if (c.chunk_tokens < 1 || c.max_batch_requests < 1) return fail(nullptr, RSIM_E_INVALID, "chunk_tokens and max_batch_requests must be >= 1");
-    if (c.policy < 0 || c.policy > 2) return fail(nullptr, RSIM_E_UNSUPPORTED, "policy %d not on the device path", c.policy);
+    if (c.policy < 0 || c.policy > 4) return fail(nullptr, RSIM_E_UNSUPPORTED, "policy %d not on the device path", c.policy);
+    if (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0))
+        return fail(nullptr, RSIM_E_UNSUPPORTED, "linear policy needs bs_norm_cap > 0 on the device path");
+    if (c.policy == RSIM_POLICY_FILTER && c.world > 1)
+        return fail(nullptr, RSIM_E_UNSUPPORTED, "filter policy is single-rank on the device path");
     if (c.prefill_base_ms < 0 || c.prefill_per_token_ms < 0 || c.decode_base_ms < 0 || c.decode_per_seq_ms < 0 ||
         c.decode_per_ctx_token_ms < 0)
         return fail(nullptr, RSIM_E_INVALID, "cost model coefficients must be non-negative");
@@ -246,15 +251,17 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
     if (C * W > 256) { delete h; return fail(nullptr, RSIM_E_INVALID, "cluster too large"); }
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
-    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(2 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 6 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf);
+    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(4 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 6 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf);
     if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
     {   // kernel attributes are process-global: set the ceiling once (handles on other threads launch concurrently)
         static std::once_flag once;
         std::call_once(once, [] {
-            cudaFuncSetAttribute(replay_kernel<RSIM_LEAN_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            cudaFuncSetAttribute(replay_kernel<RSIM_LEAN_WARPS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            cudaFuncSetAttribute(replay_kernel<RSIM_MAX_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            cudaFuncSetAttribute(replay_kernel<RSIM_MAX_WARPS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            const void *ks[] = {(const void *)replay_kernel<RSIM_LEAN_WARPS, false>, (const void *)replay_kernel<RSIM_MAX_WARPS, false>,
+                                (const void *)replay_kernel<RSIM_LEAN_WARPS, true>, (const void *)replay_kernel<RSIM_MAX_WARPS, true>};
+            for (const void *k : ks) {
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+                cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            }
         });
     }
 
@@ -283,7 +290,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaMalloc(&h->errbuf, 4 * sizeof(int)));
     CK(nullptr, cudaMalloc(&h->flag, sizeof(int)));
     CK(nullptr, cudaMalloc(&h->log_n, sizeof(u64)));
-    CK(nullptr, cudaMalloc(&h->scores, N * sizeof(double)));
+    CK(nullptr, cudaMalloc(&h->scores, 2 * N * sizeof(double)));   // [N..2N): filter's second branch
     CK(nullptr, cudaMalloc(&h->scratch_res, 4 * sizeof(i64)));
     CK(nullptr, cudaMalloc(&h->ctr, 48 * sizeof(u64)));   // [16..47]: diagnostics builds
     CK(nullptr, cudaMalloc(&h->mbox, 2 * 8 * 4 * sizeof(u64)));
@@ -413,10 +420,15 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     lc.attrs = at;
     lc.numAttrs = 1;
     CK(h, cudaEventRecord(h->ev0, h->stream));
-    if (h->W <= RSIM_LEAN_WARPS)
-        CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_LEAN_WARPS>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
+    const bool filt = h->cfg.policy == RSIM_POLICY_FILTER;
+    if (h->W <= RSIM_LEAN_WARPS && !filt)
+        CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_LEAN_WARPS, false>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
+    else if (!filt)
+        CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_MAX_WARPS, false>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
+    else if (h->W <= RSIM_LEAN_WARPS)
+        CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_LEAN_WARPS, true>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
     else
-        CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_MAX_WARPS>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
+        CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_MAX_WARPS, true>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
     h->launches++;
     CK(h, cudaEventRecord(h->ev1, h->stream));
     CK(h, cudaEventSynchronize(h->ev1));
@@ -446,7 +458,16 @@ rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen
     if (st != RSIM_OK) return st;
     if (chosen) CK(h, cudaMemcpy(chosen, h->chosen.p + r, sizeof(int), cudaMemcpyDeviceToHost));
     if (hit_tokens) CK(h, cudaMemcpy(hit_tokens, h->hit_tokens.p + r, sizeof(i64), cudaMemcpyDeviceToHost));
-    if (scores) CK(h, cudaMemcpy(scores, h->scores, h->N * sizeof(double), cudaMemcpyDeviceToHost));
+    if (scores) {
+        CK(h, cudaMemcpy(scores, h->scores, h->N * sizeof(double), cudaMemcpyDeviceToHost));
+        if (h->cfg.policy == RSIM_POLICY_FILTER) {   // the branch route_filter took (policies.py:180-183)
+            std::vector<double> bsv(h->N);
+            CK(h, cudaMemcpy(bsv.data(), h->scores + h->N, h->N * sizeof(double), cudaMemcpyDeviceToHost));
+            const auto mm = std::minmax_element(bsv.begin(), bsv.end());
+            if ((i64)*mm.second - (i64)*mm.first > h->cfg.range_threshold)
+                memcpy(scores, bsv.data(), h->N * sizeof(double));
+        }
+    }
     return RSIM_OK;
 }
 
@@ -524,10 +545,14 @@ rsim_status rsim_probe_batch(rsim_t *h, int64_t first, int64_t count, int32_t *o
     int *d = nullptr;
     const size_t n = (size_t)count * h->N;
     CK(h, cudaMalloc(&d, std::max<size_t>(n, 1) * sizeof(int)));
-    const i64 warps = (i64)n;
-    const int grid = (int)std::min<i64>((warps * 32 + 255) / 256, 148 * 8);
     CK(h, cudaEventRecord(h->ev0, h->stream));
-    probe_batch_kernel<<<std::max(grid, 1), 256, 0, h->stream>>>(make_params(h), first, count, d);
+    if (h->N >= 256) {                                       // a block per request, grid-stride
+        const int grid = (int)std::min<i64>(count, 148 * 8);
+        probe_batch_kernel<<<std::max(grid, 1), 256, 0, h->stream>>>(make_params(h), first, count, d);
+    } else {                                                 // a warp per (request, instance)
+        const int grid = (int)std::min<i64>(((i64)n * 32 + 255) / 256, 148 * 8);
+        probe_pairs_kernel<<<std::max(grid, 1), 256, 0, h->stream>>>(make_params(h), first, count, d);
+    }
     h->launches++;
     CK(h, cudaGetLastError());
     CK(h, cudaEventRecord(h->ev1, h->stream));

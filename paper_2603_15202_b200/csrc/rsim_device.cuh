@@ -91,6 +91,7 @@ struct Params {
     int bs, policy, kv_ind, bal_ind, debug;
     i64 cap, chunk, max_batch;
     double pb, pt, db, ds, dcc, qw;
+    double kvw, bsn; i64 range_thr;   // linear weight / fixed normaliser, filter range threshold
     // instance state
     Inst *inst;
     QEnt *qbuf; int qlog2;

@@ -161,6 +161,13 @@ __device__ __forceinline__ double score_of(const Params &P, int v_r, int v_q, i6
         return __dmul_rn(kv, __ll2double_rn(bal > 1 ? bal : 1));
     } else if (P.policy == 1) {                                     // vllm
         return __dadd_rn(__dmul_rn(P.qw, (double)v_q), (double)v_r);
+    } else if (P.policy == 3 || P.policy == 4) {
+        i64 ht = (i64)h * P.bs; if (ht > in) ht = in;
+        const double hr = __ddiv_rn(__ll2double_rn(ht), __ll2double_rn(in));   // Candidate.hit_ratio
+        if (P.policy == 4) return __dsub_rn(1.0, hr);               // filter, hit branch (policies.py:183)
+        double load = __ddiv_rn(__ll2double_rn(bsz), P.bsn);        // linear (policies.py:109-114)
+        if (!(load < 1.0)) load = 1.0;
+        return __dadd_rn(__dmul_rn(P.kvw, __dsub_rn(1.0, hr)), __dmul_rn(__dsub_rn(1.0, P.kvw), load));
     }
     return __ll2double_rn(bsz);                                     // least_bs
 }
@@ -483,10 +490,11 @@ __device__ __noinline__ void probe_hits_sparse(const Params &P, int base, int l0
 // ---- score this warp's instances from their hit blocks (policies.py:117-139); lane s
 // handles instance s and returns its score bits (~0 = not a candidate).
 __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
-                                           int mode, int target, int lane, WarpBuf &WB) {
+                                           int mode, int target, int lane, WarpBuf &WB, u64 &bits_bs, bool filter) {
     const int gi = base + l0 + lane;
     const bool cand = lane < n && ((mode != MODE_ENQUEUE) || gi == target);
     u64 bits = ~0ULL;
+    bits_bs = ~0ULL;                                   // filter: the batch-size branch (policies.py:181)
     u32 cb = 0;
     if (cand) {
         Inst *sp = st + l0 + lane;
@@ -499,6 +507,11 @@ __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, 
         const double sc = score_of(P, vr, vq, vp, vt, h, R.in);
         bits = (u64)__double_as_longlong(sc);
         if (P.scores != nullptr) P.scores[gi] = sc;
+        if (filter) {
+            const double sb = __ll2double_rn((i64)vr + vq);
+            bits_bs = (u64)__double_as_longlong(sb);
+            if (P.scores != nullptr) P.scores[P.N + gi] = sb;
+        }
         // one 8-B key compare per reference dict lookup + 16 B of view
         cb = 8u * (u32)min(h + 1, R.B) + 16u;
     }
@@ -520,22 +533,43 @@ __device__ __forceinline__ u32 tie_index(const u32 *modtab, u64 c0_lo, u64 c0_hi
 }
 
 __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
-                                             Dec &dec, const u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane) {
+                                             Dec &dec, const u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane,
+                                             bool filter) {
     // round-major: lane holds flat partials r*32 + lane (conflict-free 16-byte loads); flat
     // order = ascending instance id
     u64 pm[8];
     u32 pc[8];
     u64 mn = ~0ULL;
     u32 er = 0;
-    const Part *pp = part + par * CW;
     const int NR = (CW + 31) >> 5;
+    const Part *pp = part + par * 2 * CW;
+    bool bs_branch = false;
+    if (filter) {              // route_filter (policies.py:168-192): bs range over all candidates
+        u64 bmn = ~0ULL;
+        u32 bmx = 0;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const int idx = r * 32 + lane;
+            if (r < NR && idx < CW) {
+                const ulonglong2 q = lds_v2u64(pp + CW + idx);
+                bmn = min(bmn, q.x); bmx = max(bmx, (u32)(q.y >> 32));
+            }
+        }
+        const u32 bh = __reduce_min_sync(FULL, (u32)(bmn >> 32));
+        const u64 gb = ((u64)bh << 32) | __reduce_min_sync(FULL, (u32)(bmn >> 32) == bh ? (u32)bmn : ~0u);
+        const i64 bs_lo = gb == ~0ULL ? 0 : (i64)__longlong_as_double((long long)gb);
+        const i64 bs_hi = (i64)__reduce_max_sync(FULL, bmx);
+        bs_branch = bs_hi - bs_lo > P.range_thr;
+    }
 #pragma unroll
     for (int r = 0; r < 8; r++) {
         const int idx = r * 32 + lane;
         pm[r] = ~0ULL; pc[r] = 0;
         if (r < NR && idx < CW) {
             const ulonglong2 q = lds_v2u64(pp + idx);
-            pm[r] = q.x; pc[r] = (u32)q.y; er |= (u32)(q.y >> 32); mn = min(mn, q.x);
+            er |= (u32)(q.y >> 32);
+            const ulonglong2 qs = bs_branch ? lds_v2u64(pp + CW + idx) : q;   // the chosen branch
+            pm[r] = qs.x; pc[r] = (u32)qs.y; mn = min(mn, qs.x);
         }
     }
     u32 cl = 0;                                   // largest tie count of any partial
@@ -638,6 +672,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         const int owner = rb * 32 + L;
         if (owner / W == cta) { d.owner_warp = owner % W; d.kk = (int)okk; }
     }
+    d.pad = bs_branch ? 1 : 0;                    // the owner picks its tie among the chosen branch
     if (lane == 0) dec = d;
 }
 
@@ -664,7 +699,7 @@ __device__ __forceinline__ void bar_warps(int nthreads) {       // named barrier
 // and the control warp of every CTA waits for the C*W partials, derives the
 // same winner and releases the CTA through one barrier; the owning warp
 // commits. No host round trip.
-template <int MAXW>
+template <int MAXW, bool FILTER>      // FILTER: the two-branch partials of route_filter (policy 4)
 __global__ void __launch_bounds__(32 * (MAXW + 1), 1)
 replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -675,8 +710,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     const int base = cta * P.per_cta;
     const int nloc = max(0, min(P.per_cta, P.N - base));
     Inst *st = (Inst *)smem;
-    Part *part = (Part *)(st + P.per_cta);                 // [2][C*W], flat index cta*W + warp
-    ReqStage *rq = (ReqStage *)(part + 2 * CW);            // [RSIM_SLOTS] request ring (k % RSIM_SLOTS)
+    Part *part = (Part *)(st + P.per_cta);                 // [2 parity][2 branch][C*W], flat index cta*W + warp
+    ReqStage *rq = (ReqStage *)(part + 4 * CW);            // [RSIM_SLOTS] request ring (k % RSIM_SLOTS)
     Dec *dec = (Dec *)(rq + RSIM_SLOTS);                   // [2]
     u64 *mb = (u64 *)(dec + 2);                            // [2] partial-exchange mbarriers
     volatile i64 *ctl = (volatile i64 *)(mb + 2);          // [0] staged_upto
@@ -740,7 +775,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         for (i64 k = k0; k < k1; k++) {
             const int par = (int)(k & 1);
             DIAG(tc = clock64());
-            if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * 16));
+            if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * (FILTER ? 32 : 16)));
             while (!mbar_try_wait(&mb[par], (mb_phase >> par) & 1u)) { }
             mb_phase ^= 1u << par;
             PHASE(4);
@@ -750,7 +785,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                            : nullptr;
             if (tlc) tlc[0] = globaltimer();
 #endif
-            decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane);
+            decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, FILTER);
             PHASE(5);
 #ifdef RSIM_DIAG
             if (tlc) tlc[1] = globaltimer();
@@ -803,17 +838,30 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
             }
             const u32 sparse_probe = (nmine >= 2 && R.B <= 128) ? ~skip : 0u;   // no probe slots for these
-            const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB);
+            u64 bits_bs;
+            const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB, bits_bs, FILTER);
             PHASE(2);
             DIAG(const long long t_c = clock64());
             if (cta == 0 && warp == 0 && lane == 0) WB.c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once
             const u32 whi = __reduce_min_sync(FULL, (u32)(mybits >> 32));
             const u64 wmin = ((u64)whi << 32) | __reduce_min_sync(FULL, (u32)(mybits >> 32) == whi ? (u32)mybits : ~0u);
             const u32 tmask = __ballot_sync(FULL, lane < nmine && mybits == wmin && wmin != ~0ULL);
-            {   // publish this warp's partial to every CTA of the cluster
+            u64 wmin_bs = ~0ULL;
+            u32 tmask_bs = 0u;
+            if (FILTER) {                                // filter: both branches, decided globally
+                const u32 bhi = __reduce_min_sync(FULL, (u32)(bits_bs >> 32));
+                wmin_bs = ((u64)bhi << 32) | __reduce_min_sync(FULL, (u32)(bits_bs >> 32) == bhi ? (u32)bits_bs : ~0u);
+                tmask_bs = __ballot_sync(FULL, lane < nmine && bits_bs == wmin_bs && wmin_bs != ~0ULL);
+            }
+            {   // publish this warp's partial(s) to every CTA of the cluster
                 const u64 w1 = ((u64)(u32)WB.werr << 32) | (u32)__popc(tmask);
-                Part *dst = part + par * CW + cta * W + warp;
+                Part *dst = part + par * 2 * CW + cta * W + warp;
                 if (lane < C) st_async_16(dst, &mb[par], (u32)lane, wmin, w1);
+                if (FILTER) {                            // second partial: (min bs, ties | max bs << 32)
+                    const u32 bsmax = __reduce_max_sync(FULL, lane < nmine ? (u32)(st[l0 + lane].v_r + st[l0 + lane].v_q) : 0u);
+                    const u64 w2 = ((u64)bsmax << 32) | (u32)__popc(tmask_bs);
+                    if (lane < C) st_async_16(dst + CW, &mb[par], (u32)lane, wmin_bs, w2);
+                }
             }
 #ifdef RSIM_DIAG
             if (P.crit != nullptr && lane == 0 && k - k0 < P.crit_cap) {   // diagnostics: where this warp's latency went
@@ -834,7 +882,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 if (staged_seen > k + 1) {
                     const ReqStage &R1 = rq[(k + 1) % RSIM_SLOTS];
                     // instances that cannot win this decision advance to the next arrival meanwhile
-                    const u32 adv = __ballot_sync(FULL, lane < nmine && mybits != wmin);
+                    const u32 adv = __ballot_sync(FULL, lane < nmine && mybits != wmin &&
+                                                            (!FILTER || bits_bs != wmin_bs));
                     DIAG(const long long t_s0 = clock64());
                     if (adv) drain_phase(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
                     DIAG(const long long t_s1 = clock64());
@@ -870,7 +919,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             }
             DIAG(was_owner = warp == d.owner_warp);
             if (warp == d.owner_warp) {
-                const int s = nth_set_bit(tmask, d.kk);
+                const int s = nth_set_bit(d.pad ? tmask_bs : tmask, d.kk);   // d.pad: filter's bs branch
                 const int h = WB.hit[s];
                 int werr = 0;
                 flush_touch_pin(P, WB.fin, lane, &WB.werr);      // (normally already run after the publish)
@@ -914,9 +963,50 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
 }
 
 // ---------------------------------------------------------------- probe batch
-// What-if probe: warp per (request, instance) pair against the frozen state.
+// What-if probe (SURVEY 8d tertiary): M requests x all instances against the frozen state,
+// no commits -- the bandwidth-bound form of the probe. A block per request: its chain keys
+// and home slots are staged in shared memory once for all instances, and each warp runs the
+// two-stage strided probe over a chunk of instances (<= LP + S - 1 lookups per pair instead
+// of B); prompts longer than 128 blocks use the warp probe with the 128-ary deep search.
 __global__ void __launch_bounds__(256)
-probe_batch_kernel(Params P, i64 r0, i64 nreq, int *out) {
+probe_batch_kernel(const __grid_constant__ Params P, i64 r0, i64 nreq, int *out) {
+    __shared__ ReqStage RS;
+    __shared__ int hbuf[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int N = P.N;
+    const int chunk = min(32, max(4, (N + 7) / 8));
+    for (i64 rr = blockIdx.x; rr < nreq; rr += gridDim.x) {
+        const i64 r = r0 + rr;
+        __syncthreads();                                     // the previous request is done with RS
+        const i64 a = P.blk_off[r];
+        const int B = (int)(P.blk_off[r + 1] - a);
+        if (threadIdx.x < 128 && threadIdx.x < B) {
+            const u64 kk = __ldcg(P.ckeys + a + threadIdx.x);
+            RS.keys[threadIdx.x] = kk;
+            RS.home[threadIdx.x] = tab_home(kk, P.slog2);
+        }
+        if (threadIdx.x == 0) { RS.a = a; RS.B = B; }
+        __syncthreads();
+        if (B > 128) {
+            for (int gi = warp; gi < N; gi += 8) {
+                const int h = warp_probe(table_of(P, gi), P.ckeys + a, B, lane);
+                if (lane == 0) out[rr * N + gi] = h;
+            }
+            continue;
+        }
+        for (int c0 = warp * chunk; c0 < N; c0 += 8 * chunk) {
+            const int n = min(chunk, N - c0);
+            probe_hits_sparse(P, 0, c0, n, RS, MODE_REPLAY, -1, 0u, lane, hbuf[warp]);
+            if (lane < n) out[rr * N + c0 + lane] = hbuf[warp][lane];
+            __syncwarp();
+        }
+    }
+}
+
+// Small clusters (few instances per request): one warp per (request, instance) pair with the
+// dense probe -- no per-request block synchronisation to amortise.
+__global__ void __launch_bounds__(256)
+probe_pairs_kernel(const __grid_constant__ Params P, i64 r0, i64 nreq, int *out) {
     const i64 wid = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const i64 total = nreq * P.N;

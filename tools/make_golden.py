@@ -69,6 +69,10 @@ CASES = {
     "policy_least_bs": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='least_bs'), seed=3))", 1000),
     "policy_omh_total": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kv_indicator='one_minus_hit', balance_indicator='total_tokens'), seed=3))", 1000),
     "policy_omh_bs": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=12, policy=PolicyConfig(kv_indicator='one_minus_hit', tie_break_seed=9), seed=1))", 1000),
+    "policy_linear": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='linear'), seed=4))", 1000),
+    "policy_linear_cap": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=12, policy=PolicyConfig(kind='linear', kv_weight=0.7, bs_norm_cap=6), seed=5))", 1000),
+    "policy_filter": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='filter'), seed=6))", 1000),
+    "policy_filter_r2": ("(W.config2_api()[0], ClusterConfig(n_instances=16, policy=PolicyConfig(kind='filter', range_threshold=2, tie_break_seed=3), seed=7))", 1500),
     "cost_fma_sensitive": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, cost_model=CostModel(3.3, 0.0371, 17.1, 0.77, 0.0013, 512, 16), cache=CacheConfig(16, 2000), seed=4))", 1000),
     "cost_small_batch": ("(W.config2_api()[0], ClusterConfig(n_instances=6, cost_model=CostModel(1.0, 0.2, 4.0, 0.5, 0.01, 300, 3), cache=CacheConfig(16, 5000), seed=7))", 1500),
     "block_size_4": ("W.generate_synthetic_packed(W.SyntheticSpec(60.0, 20.0, (W.ClassSpec(0.5, 6, (1, 5), (1, 30)), W.ClassSpec(0.5, 2, (0, 3), (1, 9))), seed=11, block_size=4)), ClusterConfig(n_instances=5, cache=CacheConfig(4, 500), seed=11)", None),
