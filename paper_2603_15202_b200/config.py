@@ -159,6 +159,4 @@ class ClusterConfig:
             raise UnsupportedConfigError(
                 f"policy {self.policy.kind!r} is not on the device path "
                 f"(supported: {', '.join(DEVICE_POLICY_KINDS)})")
-        if self.policy.kind == "linear" and self.policy.bs_norm_cap is None:
-            raise UnsupportedConfigError("linear policy needs bs_norm_cap on the device path "
-                                         "(the per-decision max needs a second exchange round)")
+

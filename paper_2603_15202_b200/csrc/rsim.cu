@@ -202,10 +202,10 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (c.capacity_blocks == 0 || c.capacity_blocks < -1) return fail(nullptr, RSIM_E_INVALID, "capacity_blocks must be >= 1 or -1");
     if (c.chunk_tokens < 1 || c.max_batch_requests < 1) return fail(nullptr, RSIM_E_INVALID, "chunk_tokens and max_batch_requests must be >= 1");
     if (c.policy < 0 || c.policy > 4) return fail(nullptr, RSIM_E_UNSUPPORTED, "policy %d not on the device path", c.policy);
-    if (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0))
-        return fail(nullptr, RSIM_E_UNSUPPORTED, "linear policy needs bs_norm_cap > 0 on the device path");
     if (c.policy == RSIM_POLICY_FILTER && c.world > 1)
         return fail(nullptr, RSIM_E_UNSUPPORTED, "filter policy is single-rank on the device path");
+    if (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0) && c.world > 1)
+        return fail(nullptr, RSIM_E_UNSUPPORTED, "linear policy without bs_norm_cap is single-rank on the device path");
     if (c.prefill_base_ms < 0 || c.prefill_per_token_ms < 0 || c.decode_base_ms < 0 || c.decode_per_seq_ms < 0 ||
         c.decode_per_ctx_token_ms < 0)
         return fail(nullptr, RSIM_E_INVALID, "cost model coefficients must be non-negative");
@@ -251,7 +251,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
     if (C * W > 256) { delete h; return fail(nullptr, RSIM_E_INVALID, "cluster too large"); }
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
-    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(4 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 6 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf);
+    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(6 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 8 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf);
     if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
     {   // kernel attributes are process-global: set the ceiling once (handles on other threads launch concurrently)
         static std::once_flag once;
@@ -420,7 +420,8 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     lc.attrs = at;
     lc.numAttrs = 1;
     CK(h, cudaEventRecord(h->ev0, h->stream));
-    const bool filt = h->cfg.policy == RSIM_POLICY_FILTER;
+    const bool filt = h->cfg.policy == RSIM_POLICY_FILTER ||            // the extended kernel: two-branch or
+                      (h->cfg.policy == RSIM_POLICY_LINEAR && !(h->cfg.bs_norm_cap > 0));   // two-round decisions
     if (h->W <= RSIM_LEAN_WARPS && !filt)
         CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_LEAN_WARPS, false>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
     else if (!filt)

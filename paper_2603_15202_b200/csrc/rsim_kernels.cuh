@@ -150,7 +150,8 @@ struct __align__(16) Part { u64 minb; u32 cnt; u32 err; };
 // ---------------------------------------------------------------- score
 // Policy scores (policies.py:104-139) as IEEE doubles, bit-exact with
 // CPython's float arithmetic (each op rounded to nearest, no contraction).
-__device__ __forceinline__ double score_of(const Params &P, int v_r, int v_q, i64 v_pend, i64 v_total, int h, i64 in) {
+__device__ __forceinline__ double score_of(const Params &P, int v_r, int v_q, i64 v_pend, i64 v_total, int h, i64 in,
+                                           double bsn = 1.0) {
     const i64 bsz = (i64)v_r + v_q;
     if (P.policy == 0) {                                            // multiplicative
         i64 ht = (i64)h * P.bs; if (ht > in) ht = in;
@@ -165,7 +166,7 @@ __device__ __forceinline__ double score_of(const Params &P, int v_r, int v_q, i6
         i64 ht = (i64)h * P.bs; if (ht > in) ht = in;
         const double hr = __ddiv_rn(__ll2double_rn(ht), __ll2double_rn(in));   // Candidate.hit_ratio
         if (P.policy == 4) return __dsub_rn(1.0, hr);               // filter, hit branch (policies.py:183)
-        double load = __ddiv_rn(__ll2double_rn(bsz), P.bsn);        // linear (policies.py:109-114)
+        double load = __ddiv_rn(__ll2double_rn(bsz), bsn);          // linear (policies.py:109-114)
         if (!(load < 1.0)) load = 1.0;
         return __dadd_rn(__dmul_rn(P.kvw, __dsub_rn(1.0, hr)), __dmul_rn(__dsub_rn(1.0, P.kvw), load));
     }
@@ -490,7 +491,8 @@ __device__ __noinline__ void probe_hits_sparse(const Params &P, int base, int l0
 // ---- score this warp's instances from their hit blocks (policies.py:117-139); lane s
 // handles instance s and returns its score bits (~0 = not a candidate).
 __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
-                                           int mode, int target, int lane, WarpBuf &WB, u64 &bits_bs, bool filter) {
+                                           int mode, int target, int lane, WarpBuf &WB, u64 &bits_bs, bool filter,
+                                           double bsn) {
     const int gi = base + l0 + lane;
     const bool cand = lane < n && ((mode != MODE_ENQUEUE) || gi == target);
     u64 bits = ~0ULL;
@@ -504,7 +506,7 @@ __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, 
         const i64 vp = fl ? sp->pend : sp->v_pend, vt = fl ? sp->total : sp->v_total;
         if (fl) { sp->v_r = vr; sp->v_q = vq; sp->v_pend = vp; sp->v_total = vt; sp->v_dc = sp->dcs; sp->due = RSIM_NONE; }
         const int h = WB.hit[lane];
-        const double sc = score_of(P, vr, vq, vp, vt, h, R.in);
+        const double sc = score_of(P, vr, vq, vp, vt, h, R.in, bsn);
         bits = (u64)__double_as_longlong(sc);
         if (P.scores != nullptr) P.scores[gi] = sc;
         if (filter) {
@@ -711,12 +713,14 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     const int nloc = max(0, min(P.per_cta, P.N - base));
     Inst *st = (Inst *)smem;
     Part *part = (Part *)(st + P.per_cta);                 // [2 parity][2 branch][C*W], flat index cta*W + warp
-    ReqStage *rq = (ReqStage *)(part + 4 * CW);            // [RSIM_SLOTS] request ring (k % RSIM_SLOTS)
+    Part *part0 = part + 4 * CW;                           // [2 parity][C*W] round-0 partials (linear)
+    ReqStage *rq = (ReqStage *)(part + 6 * CW);            // [RSIM_SLOTS] request ring (k % RSIM_SLOTS)
     Dec *dec = (Dec *)(rq + RSIM_SLOTS);                   // [2]
     u64 *mb = (u64 *)(dec + 2);                            // [2] partial-exchange mbarriers
     volatile i64 *ctl = (volatile i64 *)(mb + 2);          // [0] staged_upto
     u64 *dmb = mb + 4;                                     // [2] decision-release mbarriers (control -> CTA)
-    u32 *modtab = (u32 *)(mb + 6);                         // [RSIM_MODTAB] launch counter mod T
+    u64 *mb0 = mb + 6;                                     // [2] round-0 mbarriers (linear, per-decision bs max)
+    u32 *modtab = (u32 *)(mb + 8);                         // [RSIM_MODTAB] launch counter mod T
     WarpBuf *wbuf = (WarpBuf *)(modtab + RSIM_MODTAB);     // [W]
     WarpBuf &WB = wbuf[control ? 0 : warp];
 
@@ -734,7 +738,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     const int nmine = control ? 0 : max(0, min(ipw, nloc - l0));
     if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; WB.fin.dnf = 0; WB.fin.npark = 0; WB.fin.tpn = 0; }
     if (threadIdx.x == 0) {
-        mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_init(&dmb[0], 1); mbar_init(&dmb[1], 1); mbar_fence_init();
+        mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_init(&dmb[0], 1); mbar_init(&dmb[1], 1);
+        mbar_init(&mb0[0], 1); mbar_init(&mb0[1], 1); mbar_fence_init();
         ctl[0] = k0;
     }
     if (mode != MODE_DRAIN)
@@ -775,7 +780,11 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         for (i64 k = k0; k < k1; k++) {
             const int par = (int)(k & 1);
             DIAG(tc = clock64());
-            if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * (FILTER ? 32 : 16)));
+            const bool lin_dyn = FILTER && P.policy == 3;           // linear with the per-decision bs max
+            if (lane == 0) {
+                if (lin_dyn) mbar_arrive_expect(&mb0[par], (u32)(CW * 16));
+                mbar_arrive_expect(&mb[par], (u32)(CW * (FILTER && P.policy == 4 ? 32 : 16)));
+            }
             while (!mbar_try_wait(&mb[par], (mb_phase >> par) & 1u)) { }
             mb_phase ^= 1u << par;
             PHASE(4);
@@ -785,7 +794,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                            : nullptr;
             if (tlc) tlc[0] = globaltimer();
 #endif
-            decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, FILTER);
+            decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, FILTER && P.policy == 4);
             PHASE(5);
 #ifdef RSIM_DIAG
             if (tlc) tlc[1] = globaltimer();
@@ -800,6 +809,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     } else {
         i64 staged_seen = k0;
         u32 dph = 0u;                                       // bit p: phase of decision-release mbarrier dmb[p]
+        u32 d0ph = 0u;                                      // bit p: phase of round-0 mbarrier mb0[p]
         DIAG(long long t_rel = clock64());                  // release of this warp for decision k
         DIAG(bool was_owner = false);                       // this warp committed the previous decision
         for (i64 k = k0; k < k1; k++) {
@@ -838,8 +848,26 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
             }
             const u32 sparse_probe = (nmine >= 2 && R.B <= 128) ? ~skip : 0u;   // no probe slots for these
+            double bsn = P.bsn;
+            if (FILTER && P.policy == 3) {      // linear without a cap: bs_norm = max(max bs, 1) over ALL
+                                                // instances (policies.py:250-255) -- one extra exchange round
+                u32 lb = 0u;
+                if (lane < nmine) {
+                    const Inst *sp = st + l0 + lane;
+                    lb = sp->due <= R.t ? (u32)(sp->r + sp->q) : (u32)(sp->v_r + sp->v_q);
+                }
+                lb = __reduce_max_sync(FULL, lb);
+                if (lane < C) st_async_16(part0 + par * CW + cta * W + warp, &mb0[par], (u32)lane, (u64)lb, 0ULL);
+                while (!mbar_try_wait(&mb0[par], (d0ph >> par) & 1u)) { }
+                d0ph ^= 1u << par;
+                u32 gm = 0u;
+                for (int i = lane; i < CW; i += 32) gm = max(gm, (u32)lds_v2u64(part0 + par * CW + i).x);
+                gm = __reduce_max_sync(FULL, gm);
+                bsn = (double)(gm > 1u ? gm : 1u);
+            }
             u64 bits_bs;
-            const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB, bits_bs, FILTER);
+            const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB, bits_bs,
+                                           FILTER && P.policy == 4, bsn);
             PHASE(2);
             DIAG(const long long t_c = clock64());
             if (cta == 0 && warp == 0 && lane == 0) WB.c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once
@@ -848,7 +876,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             const u32 tmask = __ballot_sync(FULL, lane < nmine && mybits == wmin && wmin != ~0ULL);
             u64 wmin_bs = ~0ULL;
             u32 tmask_bs = 0u;
-            if (FILTER) {                                // filter: both branches, decided globally
+            if (FILTER && P.policy == 4) {               // filter: both branches, decided globally
                 const u32 bhi = __reduce_min_sync(FULL, (u32)(bits_bs >> 32));
                 wmin_bs = ((u64)bhi << 32) | __reduce_min_sync(FULL, (u32)(bits_bs >> 32) == bhi ? (u32)bits_bs : ~0u);
                 tmask_bs = __ballot_sync(FULL, lane < nmine && bits_bs == wmin_bs && wmin_bs != ~0ULL);
@@ -857,7 +885,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 const u64 w1 = ((u64)(u32)WB.werr << 32) | (u32)__popc(tmask);
                 Part *dst = part + par * 2 * CW + cta * W + warp;
                 if (lane < C) st_async_16(dst, &mb[par], (u32)lane, wmin, w1);
-                if (FILTER) {                            // second partial: (min bs, ties | max bs << 32)
+                if (FILTER && P.policy == 4) {           // second partial: (min bs, ties | max bs << 32)
                     const u32 bsmax = __reduce_max_sync(FULL, lane < nmine ? (u32)(st[l0 + lane].v_r + st[l0 + lane].v_q) : 0u);
                     const u64 w2 = ((u64)bsmax << 32) | (u32)__popc(tmask_bs);
                     if (lane < C) st_async_16(dst + CW, &mb[par], (u32)lane, wmin_bs, w2);
@@ -883,7 +911,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     const ReqStage &R1 = rq[(k + 1) % RSIM_SLOTS];
                     // instances that cannot win this decision advance to the next arrival meanwhile
                     const u32 adv = __ballot_sync(FULL, lane < nmine && mybits != wmin &&
-                                                            (!FILTER || bits_bs != wmin_bs));
+                                                            (!(FILTER && P.policy == 4) || bits_bs != wmin_bs));
                     DIAG(const long long t_s0 = clock64());
                     if (adv) drain_phase(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
                     DIAG(const long long t_s1 = clock64());
