@@ -150,7 +150,7 @@ class ClusterConfig:
 
     def check_device_supported(self) -> None:
         """Reject the reference features that are outside the device path
-        (detector, staleness > 0, other score kinds)."""
+        (detector, staleness > 0, the simulate policy)."""
         if self.detector is not None:
             raise UnsupportedConfigError("hotspot detector is not on the device path")
         if self.staleness_ms != 0:
