@@ -539,6 +539,10 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
                                              bool filter) {
     // round-major: lane holds flat partials r*32 + lane (conflict-free 16-byte loads); flat
     // order = ascending instance id
+#ifdef RSIM_DIAG
+    const bool dg = P.ctr != nullptr && cta == 0 && lane == 0;
+    long long dt0 = clock64(), dt1 = 0, dt2 = 0, dt3 = 0;
+#endif
     u64 pm[8];
     u32 pc[8];
     u64 mn = ~0ULL;
@@ -596,6 +600,9 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         T += __popc(tb[r]);
     }
     if (!single) T = __reduce_add_sync(FULL, lc);
+#ifdef RSIM_DIAG
+    dt1 = clock64();
+#endif
     Dec d; d.owner_warp = -1; d.kk = 0; d.err = (int)er; d.pad = 0;
     u32 kk = 0;
     bool mine = true;
@@ -644,6 +651,9 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         ties += 1;
     }
     if (!d.err && Tg == 0) d.err = 11;            // NoInstancesError
+#ifdef RSIM_DIAG
+    dt2 = clock64();
+#endif
     if (!d.err && mine && single) {
         u32 pre = 0, kr = 0, bm = 0;
         int rb = -1;
@@ -675,6 +685,10 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         if (owner / W == cta) { d.owner_warp = owner % W; d.kk = (int)okk; }
     }
     d.pad = bs_branch ? 1 : 0;                    // the owner picks its tie among the chosen branch
+#ifdef RSIM_DIAG
+    dt3 = clock64();
+    if (dg) { atomicAdd(P.ctr + 35, (u64)(dt1 - dt0)); atomicAdd(P.ctr + 36, (u64)(dt2 - dt1)); atomicAdd(P.ctr + 37, (u64)(dt3 - dt2)); }
+#endif
     if (lane == 0) dec = d;
 }
 

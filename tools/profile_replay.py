@@ -112,6 +112,9 @@ for c, w in shapes:
         if sc[16] or sc[17]:
             print(f"   warp 0 probe-ahead sections: setup {sc[16] / len(trace):.0f}  issue {sc[17] / len(trace):.0f}  "
                   f"evaluate {sc[18] / len(trace):.0f} cyc/decision", flush=True)
+        if sc[19] or sc[20]:
+            print(f"   decide sections (CTA 0 control warp, cyc/decision): load+min {sc[19] / len(trace):.0f}  "
+                  f"ties+index {sc[20] / len(trace):.0f}  owner {sc[21] / len(trace):.0f}", flush=True)
         kinds = ["finishing", "other full", "pure decode"]
         print("   step kinds: " + "  ".join(f"{kinds[i]} {sc[8 + 2 * i]} x {sc[9 + 2 * i] / max(sc[8 + 2 * i], 1):.0f} cyc"
                                           for i in range(3)), flush=True)
