@@ -35,6 +35,7 @@ class _Cfg(C.Structure):
         ("chunk", C.c_int64), ("max_batch", C.c_int64),
         ("tie_lo", C.c_uint64), ("tie_hi", C.c_uint64),
         ("kv_weight", C.c_double), ("bs_norm_cap", C.c_double), ("range_threshold", C.c_int64),
+        ("staleness_us", C.c_int64),
     ]
 
 
@@ -96,8 +97,8 @@ def make_cfg(config) -> _Cfg:
     cm, cache, pol = config.cost_model, config.cache, config.policy
     if pol.kind not in POLICY_CODE:
         raise ValueError(f"oracle covers policies {sorted(POLICY_CODE)}, not {pol.kind!r}")
-    if getattr(config, "staleness_ms", 0) != 0 or getattr(config, "detector", None) is not None:
-        raise ValueError("oracle covers staleness 0 without detector")
+    if getattr(config, "detector", None) is not None:
+        raise ValueError("oracle covers runs without a detector")
     tie = _stable_key(config.seed, pol.tie_break_seed)
     return _Cfg(config.n_instances, POLICY_CODE[pol.kind],
                 0 if pol.kv_indicator == "p_tokens" else 1,
@@ -108,7 +109,8 @@ def make_cfg(config) -> _Cfg:
                 cm.chunk_tokens, cm.max_batch_requests, tie, 0,
                 float(getattr(pol, "kv_weight", 0.4)),
                 float(pol.bs_norm_cap) if getattr(pol, "bs_norm_cap", None) is not None else 0.0,
-                int(getattr(pol, "range_threshold", 4)))
+                int(getattr(pol, "range_threshold", 4)),
+                int(round(float(getattr(config, "staleness_ms", 0.0)) * 1000.0)))   # cluster.py:77
 
 
 class OracleError(RuntimeError):

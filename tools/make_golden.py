@@ -73,6 +73,11 @@ CASES = {
     "policy_linear_cap": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=12, policy=PolicyConfig(kind='linear', kv_weight=0.7, bs_norm_cap=6), seed=5))", 1000),
     "policy_filter": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='filter'), seed=6))", 1000),
     "policy_filter_r2": ("(W.config2_api()[0], ClusterConfig(n_instances=16, policy=PolicyConfig(kind='filter', range_threshold=2, tie_break_seed=3), seed=7))", 1500),
+    "stale_5ms": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, staleness_ms=5.0, seed=8))", 1000),
+    "stale_50ms_n16": ("(W.config2_api()[0], ClusterConfig(n_instances=16, staleness_ms=50.0, seed=9))", 1500),
+    "stale_frac_vllm": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='vllm'), staleness_ms=12.3456, seed=10))", 1000),
+    "stale_linear": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='linear'), staleness_ms=20.0, seed=11))", 1000),
+    "stale_filter_evict": ("(W.config3_agent(1500, n_instances=16, capacity=4096, rate_per_instance=1.0)[0], ClusterConfig(n_instances=16, cache=CacheConfig(16, 4096), policy=PolicyConfig(kind='filter'), staleness_ms=100.0, seed=12))", None),
     "cost_fma_sensitive": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, cost_model=CostModel(3.3, 0.0371, 17.1, 0.77, 0.0013, 512, 16), cache=CacheConfig(16, 2000), seed=4))", 1000),
     "cost_small_batch": ("(W.config2_api()[0], ClusterConfig(n_instances=6, cost_model=CostModel(1.0, 0.2, 4.0, 0.5, 0.01, 300, 3), cache=CacheConfig(16, 5000), seed=7))", 1500),
     "block_size_4": ("W.generate_synthetic_packed(W.SyntheticSpec(60.0, 20.0, (W.ClassSpec(0.5, 6, (1, 5), (1, 30)), W.ClassSpec(0.5, 2, (0, 3), (1, 9))), seed=11, block_size=4)), ClusterConfig(n_instances=5, cache=CacheConfig(4, 500), seed=11)", None),
