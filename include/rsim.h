@@ -32,7 +32,8 @@ typedef enum {
     RSIM_E_TABLE_FULL = 8,     /* per-instance KV$ hash table too small: recreate with larger table */
     RSIM_E_UNSUPPORTED = 9,    /* feature outside the device path (detector, staleness > 0, ...)  */
     RSIM_E_COMM = 10,          /* multi-GPU exchange failure                                        */
-    RSIM_E_NO_INSTANCES = 11   /* empty candidate set (reference: NoInstancesError, policies.py:226) */
+    RSIM_E_NO_INSTANCES = 11,  /* empty candidate set (reference: NoInstancesError, policies.py:226) */
+    RSIM_E_HISTORY_OVERFLOW = 12 /* view-history ring full (staleness > 0): recreate with larger history_capacity */
 } rsim_status;
 
 enum { RSIM_POLICY_MULTIPLICATIVE = 0, RSIM_POLICY_VLLM = 1, RSIM_POLICY_LEAST_BS = 2,
@@ -74,6 +75,10 @@ typedef struct rsim_config {
     double kv_weight;               /* PolicyConfig.kv_weight (linear)                         */
     double bs_norm_cap;             /* PolicyConfig.bs_norm_cap (linear); 0 = per-decision max */
     int64_t range_threshold;        /* PolicyConfig.range_threshold (filter)                   */
+    int64_t staleness_us;           /* ClusterSim.staleness_us = round(staleness_ms * 1000), cluster.py:77;
+                                       scores see each instance's view as of now - staleness      */
+    int32_t history_capacity;       /* per-instance view-history ring entries (staleness > 0), 0 = auto */
+    int32_t reserved0;
 } rsim_config;
 
 typedef struct rsim rsim_t;

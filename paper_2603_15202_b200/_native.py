@@ -23,6 +23,7 @@ LIB_PATH = os.environ.get("RSIM_LIB") or os.path.join(_HERE, "librsim.so")
 RSIM_OK = 0
 E_INVALID, E_TRACE, E_CACHE_FULL, E_DUPLICATE, E_INVARIANT, E_CUDA = 1, 2, 3, 4, 5, 6
 E_QUEUE_OVERFLOW, E_TABLE_FULL, E_UNSUPPORTED, E_COMM, E_NO_INSTANCES = 7, 8, 9, 10, 11
+E_HISTORY_OVERFLOW = 12
 
 
 class RsimError(RuntimeError):
@@ -58,6 +59,7 @@ class Config(C.Structure):
         ("world", C.c_int32), ("rank", C.c_int32), ("comm_timeout_ms", C.c_int64),
         ("runs_capacity", C.c_int64),
         ("kv_weight", C.c_double), ("bs_norm_cap", C.c_double), ("range_threshold", C.c_int64),
+        ("staleness_us", C.c_int64), ("history_capacity", C.c_int32), ("reserved0", C.c_int32),
     ]
 
 
@@ -159,7 +161,7 @@ class Handle:
     def _raise(self, st: int, msg: str | None = None):
         if msg is None:
             msg = self._L.rsim_last_error(self._h).decode()
-        if st in (E_QUEUE_OVERFLOW, E_TABLE_FULL):
+        if st in (E_QUEUE_OVERFLOW, E_TABLE_FULL, E_HISTORY_OVERFLOW):
             raise CapacityError(st, msg)
         exc = _EXC.get(st)
         if exc is not None:

@@ -43,9 +43,10 @@ class Sizing:
     """Per-instance device capacities (queue ring, KV$ table)."""
     queue_capacity: int
     expected_keys: int
+    history_capacity: int = 0      # view-history ring entries (staleness > 0), 0 = library default
 
     def grown(self) -> "Sizing":
-        return Sizing(self.queue_capacity * 4, self.expected_keys * 4)
+        return Sizing(self.queue_capacity * 4, self.expected_keys * 4, max(self.history_capacity, 256) * 4)
 
 
 def sizing_for(trace: PackedTrace | None, config: ClusterConfig) -> Sizing:
@@ -67,7 +68,28 @@ def sizing_for(trace: PackedTrace | None, config: ClusterConfig) -> Sizing:
     est = min(est, total + 64)
     n = len(trace)
     q = min(n + 16, max(256, 4 * n // N + 256))
-    return Sizing(q, est)
+    return Sizing(q, est, history_capacity(trace, config))
+
+
+def history_capacity(trace: PackedTrace, config: ClusterConfig) -> int:
+    """Live view-history entries one instance may hold (staleness > 0): everything
+    appended within one staleness window -- its enqueues (4x the per-instance
+    share of the busiest window's arrivals) and its steps (one per minimum step
+    cost) -- plus slack. Older entries are dropped on device once no later
+    snapshot can see them."""
+    stal = staleness_us(config)
+    if stal <= 0:
+        return 0
+    arr = trace.arrival_us
+    win = int((np.searchsorted(arr, arr + stal, side="right") - np.arange(len(arr))).max())
+    cm = config.cost_model
+    min_step = max(1.0, 1000.0 * min(cm.prefill_base_ms + cm.prefill_per_token_ms,
+                                     cm.decode_base_ms + cm.decode_per_seq_ms))
+    return int(min(win, 4 * win // config.n_instances + 64) + stal / min_step + 64)
+
+
+def staleness_us(config: ClusterConfig) -> int:
+    return int(round(config.staleness_ms * 1000.0))         # cluster.py:77
 
 
 def native_config(config: ClusterConfig, sizing: Sizing, *, device: int = 0, record_steps: bool = False,
@@ -107,6 +129,8 @@ def native_config(config: ClusterConfig, sizing: Sizing, *, device: int = 0, rec
     c.kv_weight = pol.kv_weight
     c.bs_norm_cap = float(pol.bs_norm_cap) if pol.bs_norm_cap is not None else 0.0
     c.range_threshold = pol.range_threshold
+    c.staleness_us = staleness_us(config)
+    c.history_capacity = sizing.history_capacity
     return c
 
 

@@ -150,11 +150,9 @@ class ClusterConfig:
 
     def check_device_supported(self) -> None:
         """Reject the reference features that are outside the device path
-        (detector, staleness > 0, the simulate policy)."""
+        (the detector, the simulate policy)."""
         if self.detector is not None:
             raise UnsupportedConfigError("hotspot detector is not on the device path")
-        if self.staleness_ms != 0:
-            raise UnsupportedConfigError("staleness_ms > 0 is not on the device path")
         if self.policy.kind not in DEVICE_POLICY_KINDS:
             raise UnsupportedConfigError(
                 f"policy {self.policy.kind!r} is not on the device path "

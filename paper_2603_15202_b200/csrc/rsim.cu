@@ -86,6 +86,8 @@ struct rsim {
     u64 epoch = 1;
     Run *runs = nullptr;
     int rlog2 = 0;
+    HEnt *hring = nullptr;   // view-history rings (staleness > 0)
+    int hlog2 = 0;
     DevArr<u64> arena;             // API-inserted chain keys (named by eviction runs)
     i64 narena = 0;
     unsigned short *crit = nullptr; // diagnostics: per (decision, warp) phase records
@@ -138,6 +140,7 @@ static Params make_params(rsim_t *h) {
     for (int i = 0; i < 8; i++) P.peer[i] = h->peer[i];
     P.epoch = h->epoch;
     P.runs = h->runs; P.rlog2 = h->rlog2; P.arena = h->arena.p;
+    P.stal = h->cfg.staleness_us; P.hring = h->hring; P.hlog2 = h->hlog2;
     P.timeout_ns = (h->cfg.comm_timeout_ms > 0 ? h->cfg.comm_timeout_ms : 10000) * 1000000LL;
     P.crit = h->crit; P.crit_cap = h->crit_cap;
     return P;
@@ -155,19 +158,25 @@ static rsim_status check_device_error(rsim_t *h) {
         case DEV_E_QUEUE_OVERFLOW: return fail(h, RSIM_E_QUEUE_OVERFLOW, "instance queue ring full (queue_capacity=%d)", 1 << h->qlog2);
         case DEV_E_TABLE_FULL: return fail(h, RSIM_E_TABLE_FULL, "instance KV$ table over 3/4 load (slots=%d)", 1 << h->slog2);
         case 11: return fail(h, RSIM_E_NO_INSTANCES, "no instances to route to");
+        case DEV_E_HISTORY_OVERFLOW: return fail(h, RSIM_E_HISTORY_OVERFLOW, "instance view-history ring full (history_capacity=%d)", 1 << h->hlog2);
         case DEV_E_COMM: return fail(h, RSIM_E_COMM, "timed out waiting for a peer rank's decision partial");
         default: return fail(h, RSIM_E_INVARIANT, "device error %d", e[0]);
     }
+}
+
+static Inst fresh_inst() {
+    Inst s;
+    memset(&s, 0, sizeof(s));
+    s.next_step = RSIM_NONE; s.due = RSIM_NONE; s.next_finish = RSIM_NONE;
+    s.hhead = 0; s.htail = 1;   // history = [(-inf, zero view)]
+    return s;
 }
 
 static rsim_status init_state(rsim_t *h) {
     const int N = h->N;
     h->epoch += 1;
     std::vector<Inst> hs(N);
-    for (auto &s : hs) {
-        memset(&s, 0, sizeof(s));
-        s.next_step = RSIM_NONE; s.due = RSIM_NONE; s.next_finish = RSIM_NONE;
-    }
+    for (auto &s : hs) s = fresh_inst();
     CK(h, cudaMemcpyAsync(h->inst, hs.data(), N * sizeof(Inst), cudaMemcpyHostToDevice, h->stream));
     const size_t slots = (size_t)N << h->slog2;
     CK(h, cudaMemsetAsync(h->tkeys, 0, slots * sizeof(u64), h->stream));   // EMPTY = 0
@@ -202,6 +211,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (c.capacity_blocks == 0 || c.capacity_blocks < -1) return fail(nullptr, RSIM_E_INVALID, "capacity_blocks must be >= 1 or -1");
     if (c.chunk_tokens < 1 || c.max_batch_requests < 1) return fail(nullptr, RSIM_E_INVALID, "chunk_tokens and max_batch_requests must be >= 1");
     if (c.policy < 0 || c.policy > 4) return fail(nullptr, RSIM_E_UNSUPPORTED, "policy %d not on the device path", c.policy);
+    if (c.staleness_us < 0) return fail(nullptr, RSIM_E_INVALID, "staleness_us must be >= 0");
     if (c.policy == RSIM_POLICY_FILTER && c.world > 1)
         return fail(nullptr, RSIM_E_UNSUPPORTED, "filter policy is single-rank on the device path");
     if (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0) && c.world > 1)
@@ -251,7 +261,8 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
     if (C * W > 256) { delete h; return fail(nullptr, RSIM_E_INVALID, "cluster too large"); }
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
-    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(6 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 8 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf);
+    h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(6 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 8 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf) +
+                     (c.staleness_us > 0 ? (size_t)per_cta * sizeof(HistHead) : 0);
     if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
     {   // kernel attributes are process-global: set the ceiling once (handles on other threads launch concurrently)
         static std::once_flag once;
@@ -286,6 +297,10 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
         h->rlog2 = std::max(6, std::min(26, ilog2_ceil(want)));
         CK(nullptr, cudaMalloc(&h->runs, ((size_t)N << h->rlog2) * sizeof(Run)));
     }
+    if (c.staleness_us > 0) {   // view-history rings (indicators.py:36-65)
+        h->hlog2 = std::max(4, std::min(24, ilog2_ceil(c.history_capacity > 0 ? c.history_capacity : 1024)));
+        CK(nullptr, cudaMalloc(&h->hring, ((size_t)N << h->hlog2) * sizeof(HEnt)));
+    }
     CK(nullptr, cudaMalloc(&h->tie, 2 * sizeof(u64)));
     CK(nullptr, cudaMalloc(&h->errbuf, 4 * sizeof(int)));
     CK(nullptr, cudaMalloc(&h->flag, sizeof(int)));
@@ -316,7 +331,7 @@ void rsim_destroy(rsim_t *h) {
     h->rid.free_(); h->blocks.free_(); h->ckeys.free_(); h->okeys.free_();
     h->hit_blocks.free_(); h->chosen.free_();
     void *ps[] = {h->inst, h->qbuf, h->rbuf, h->tkeys, h->tmeta, h->tie, h->errbuf, h->flag, h->log, h->log_n,
-                  h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs, h->crit};
+                  h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs, h->crit, h->hring};
     h->arena.free_();
     for (int i = 0; i < 8; i++) if (h->peer_ipc[i] && h->peer[i]) cudaIpcCloseMemHandle(h->peer[i]);
     for (void *p : ps) if (p) cudaFree(p);
@@ -421,7 +436,8 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     lc.numAttrs = 1;
     CK(h, cudaEventRecord(h->ev0, h->stream));
     const bool filt = h->cfg.policy == RSIM_POLICY_FILTER ||            // the extended kernel: two-branch or
-                      (h->cfg.policy == RSIM_POLICY_LINEAR && !(h->cfg.bs_norm_cap > 0));   // two-round decisions
+                      (h->cfg.policy == RSIM_POLICY_LINEAR && !(h->cfg.bs_norm_cap > 0)) ||   // two-round decisions,
+                      h->cfg.staleness_us > 0;                                              // stale snapshots
     if (h->W <= RSIM_LEAN_WARPS && !filt)
         CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_LEAN_WARPS, false>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
     else if (!filt)
@@ -666,7 +682,7 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
     const int N = h->N;
     h->epoch += 1;
     std::vector<Inst> hs(N);
-    for (auto &x : hs) { memset(&x, 0, sizeof(x)); x.next_step = RSIM_NONE; x.due = RSIM_NONE; x.next_finish = RSIM_NONE; }
+    for (auto &x : hs) x = fresh_inst();
     u64 tie[2] = {h->cfg.tie_seed_lo, h->cfg.tie_seed_hi};
     cudaEvent_t e0, e1;
     CK(h, cudaEventCreate(&e0));

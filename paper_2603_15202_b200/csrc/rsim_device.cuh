@@ -25,6 +25,7 @@ typedef unsigned int u32;
 #define DEV_E_QUEUE_OVERFLOW 7
 #define DEV_E_TABLE_FULL 8
 #define DEV_E_COMM 10
+#define DEV_E_HISTORY_OVERFLOW 12
 
 // A request on an instance: one 64-byte record used by the FIFO queue (v =
 // pending prefill tokens) and the running list (v = finish step = join step +
@@ -62,9 +63,16 @@ struct __align__(16) Inst {
     int q_head;       // queue ring head index
     int tabver;       // bumped whenever the KV$ key set may change (finish inserts / evictions):
                       // a probe made at version v stays valid while tabver == v
+    int hhead, htail; // router-observable view history (engine.py:225, staleness > 0 only): a
+                      // deque of (t, view) in the ring P.hring, live entries [hhead, htail);
+                      // entry 0 is an implicit (-inf, zero view), so the deque is never empty
     Ent qhead;        // copy of the FIFO head record (valid while qcpos == q_head): the step that
                       // prefills a lone queued request reads it from shared memory, not L2
 };
+static_assert(sizeof(Inst) == 224, "Inst layout");
+
+// one view-history entry (engine.py:225 history item): 32 B
+struct __align__(16) HEnt { i64 t, pend, total; int r, q; };
 
 
 __device__ __forceinline__ Ent shfl_ent(const Ent &e, int src) {
@@ -113,6 +121,8 @@ struct Params {
     i64 timeout_ns;
     // diagnostics: per (decision, warp) phase record, 8 x u16 (rsim_phase_records); null = off
     unsigned short *crit; i64 crit_cap;
+    i64 stal;         // router staleness in us (cluster.py:77); 0 = the live view
+    HEnt *hring; int hlog2;            // per-instance view-history rings (staleness > 0)
 };
 
 // ---------------- hashing (hashing.py:15-25) ----------------
@@ -162,3 +172,54 @@ __device__ __forceinline__ int nth_set_bit(u32 m, int k) {
 }
 
 __device__ __forceinline__ u64 ldcg_u64(const u64 *p) { return __ldcg(p); }
+
+// ---------------- view history (staleness > 0) ----------------
+// Drop the entries no snapshot with a cutoff >= `cutoff` can see (indicators.py:51-53):
+// advance hhead while entry hhead + 1 exists and is at or before the cutoff.
+__device__ __noinline__ void hist_make_room(const Params &P, Inst &s, int gi, i64 cutoff) {
+    const HEnt *ring = P.hring + ((size_t)gi << P.hlog2);
+    const int mask = (1 << P.hlog2) - 1;
+    int hh = s.hhead;
+    while (hh + 1 < s.htail && ring[(hh + 1) & mask].t <= cutoff) hh++;
+    s.hhead = hh;
+}
+// history.append((t, view)) of instance gi (engine.py:245, 286); view = the v_* fields.
+// now: the current simulated time -- no later snapshot has a cutoff below now - staleness.
+__device__ __noinline__ void hist_append(const Params &P, Inst &s, int gi, i64 t, i64 now) {
+    const int j = s.htail;
+    if (j - s.hhead >= (1 << P.hlog2)) {             // full: drop what no later snapshot can see
+        hist_make_room(P, s, gi, now - P.stal);
+        if (j - s.hhead >= (1 << P.hlog2)) { atomicCAS(P.err, 0, DEV_E_HISTORY_OVERFLOW); return; }
+    }
+    HEnt e;
+    e.t = t; e.pend = s.v_pend; e.total = s.v_total; e.r = s.v_r; e.q = s.v_q;
+    P.hring[((size_t)gi << P.hlog2) + (j & ((1 << P.hlog2) - 1))] = e;
+    s.htail = j + 1;
+}
+
+// Shared-memory cache of one instance's history head (extended kernel, staleness > 0):
+// the view of entry hidx and the time of entry ntidx = hidx + 1 (-1: not cached).
+struct __align__(16) HistHead { i64 pend, total, nt; int r, q, hidx, ntidx; };
+
+// snapshot(now, staleness) of instance gi (indicators.py:36-65), after the caller's
+// flush: pop, then the head is the latest entry at or before the cutoff (times are
+// monotone and cutoffs never decrease). Leaves the stale view in c.
+__device__ __forceinline__ void hist_snapshot(const Params &P, Inst &s, HistHead &c, int gi, i64 cutoff) {
+    const HEnt *ring = P.hring + ((size_t)gi << P.hlog2);
+    const int mask = (1 << P.hlog2) - 1;
+    int hh = s.hhead;
+    const int ht = s.htail;
+    i64 nt = RSIM_NONE;
+    if (hh + 1 < ht) nt = c.ntidx == hh + 1 ? c.nt : ring[(hh + 1) & mask].t;
+    while (nt <= cutoff) {
+        hh++;
+        nt = hh + 1 < ht ? ring[(hh + 1) & mask].t : RSIM_NONE;
+    }
+    s.hhead = hh;
+    if (c.hidx != hh) {
+        if (hh == 0) { c.r = 0; c.q = 0; c.pend = 0; c.total = 0; }
+        else { const HEnt e = ring[hh & mask]; c.r = e.r; c.q = e.q; c.pend = e.pend; c.total = e.total; }
+        c.hidx = hh;
+    }
+    c.nt = nt; c.ntidx = hh + 1 < ht ? hh + 1 : -1;
+}

@@ -29,6 +29,14 @@ __device__ __forceinline__ void flush_view(Inst &s, i64 now) {   // engine.py:24
         s.due = RSIM_NONE;
     }
 }
+// the same, recording the flushed view in the history (engine.py:245; staleness > 0)
+__device__ __forceinline__ void flush_view_hist(const Params &P, Inst &s, int gi, i64 now) {
+    if (s.due <= now) {
+        s.v_r = s.r; s.v_q = s.q; s.v_pend = s.pend; s.v_total = s.total; s.v_dc = s.dcs;
+        hist_append(P, s, gi, s.due, now);
+        s.due = RSIM_NONE;
+    }
+}
 
 // _finish (engine.py:357-372) for one request: unpin the admission hit, insert
 // the full prefix+output chain stamped with the step end, evict to capacity.

@@ -178,7 +178,7 @@ __device__ __forceinline__ double score_of(const Params &P, int v_r, int v_q, i6
 // this warp's next publish, or earlier before cache work on the same instance.
 __device__ __forceinline__ void commit(const Params &P, Inst *sp, int gi, i64 k, int h, i64 t, const u64 *keys128,
                                        const int *slot0, i64 a, int B, i64 in, int out, i64 oa, int lane, int &werr,
-                                       FinBuf &F) {
+                                       FinBuf &F, bool stale) {
     // scalar work on lane 0: a handful of shared-memory fields and one 64-B queue record
     int bad = 0;
     __syncwarp();
@@ -204,6 +204,7 @@ __device__ __forceinline__ void commit(const Params &P, Inst *sp, int gi, i64 k,
             P.route_bs[k] = (i64)q + 1 + sp->r;
             sp->q = q + 1; sp->pend += pending; sp->total += in;
             sp->v_q += 1; sp->v_pend += pending; sp->v_total += in;   // view moves incrementally (engine.py:284-285)
+            if (stale) hist_append(P, *sp, gi, t, t);                      // engine.py:286
             if (sp->next_step == RSIM_NONE && sp->busy_until <= t) sp->next_step = t;   // cluster.py:284-285
         }
     }
@@ -272,6 +273,7 @@ __device__ __noinline__ void stage_request(const Params &P, ReqStage &R, i64 k, 
 // ---- drain: advance instances [l0, l0+n) of this warp through steps starting before `until`
 //      (cluster.py:250-273); skip_mask marks instances that must not move yet. The check is
 //      inline; the (noinline) step function is only called when a step is due.
+template <bool STALE>
 __device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base, int l0, int n, i64 until,
                                             u32 skip_mask, int lane, WarpBuf &WB, Defer *df = nullptr) {
     u32 due = __ballot_sync(FULL, lane < n && !((skip_mask >> lane) & 1u) && st[l0 + lane].next_step < until);
@@ -280,8 +282,14 @@ __device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base,
         due &= due - 1;
         Inst *sp = st + l0 + s;
         u64 steps = 0;
-        while (sp->next_step < until && !WB.werr)
+        while (sp->next_step < until && !WB.werr) {
+            if (STALE && P.stal > 0 && sp->due <= sp->next_step) {   // the step's flush (engine.py:293), recorded
+                __syncwarp();
+                if (lane == 0) flush_view_hist(P, *sp, base + l0 + s, sp->next_step);
+                __syncwarp();
+            }
             steps += inst_step(P, sp, base + l0 + s, s, lane, &WB.werr, WB.fin, df);
+        }
         if (lane == 0) WB.c_steps += steps;
     }
 }
@@ -492,7 +500,7 @@ __device__ __noinline__ void probe_hits_sparse(const Params &P, int base, int l0
 // handles instance s and returns its score bits (~0 = not a candidate).
 __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
                                            int mode, int target, int lane, WarpBuf &WB, u64 &bits_bs, bool filter,
-                                           double bsn) {
+                                           double bsn, bool stale, const HistHead *hc) {
     const int gi = base + l0 + lane;
     const bool cand = lane < n && ((mode != MODE_ENQUEUE) || gi == target);
     u64 bits = ~0ULL;
@@ -501,10 +509,17 @@ __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, 
     if (cand) {
         Inst *sp = st + l0 + lane;
         // snapshot() flushes every candidate (indicators.py:36-65): the view is the live state once due
-        const bool fl = sp->due <= R.t;
-        const int vr = fl ? sp->r : sp->v_r, vq = fl ? sp->q : sp->v_q;
-        const i64 vp = fl ? sp->pend : sp->v_pend, vt = fl ? sp->total : sp->v_total;
-        if (fl) { sp->v_r = vr; sp->v_q = vq; sp->v_pend = vp; sp->v_total = vt; sp->v_dc = sp->dcs; sp->due = RSIM_NONE; }
+        int vr, vq;
+        i64 vp, vt;
+        if (stale) {       // stale_snapshot() ran: the history head is the view as of t - staleness
+            const HistHead &c = hc[l0 + lane];
+            vr = c.r; vq = c.q; vp = c.pend; vt = c.total;
+        } else {
+            const bool fl = sp->due <= R.t;
+            vr = fl ? sp->r : sp->v_r; vq = fl ? sp->q : sp->v_q;
+            vp = fl ? sp->pend : sp->v_pend; vt = fl ? sp->total : sp->v_total;
+            if (fl) { sp->v_r = vr; sp->v_q = vq; sp->v_pend = vp; sp->v_total = vt; sp->v_dc = sp->dcs; sp->due = RSIM_NONE; }
+        }
         const int h = WB.hit[lane];
         const double sc = score_of(P, vr, vq, vp, vt, h, R.in, bsn);
         bits = (u64)__double_as_longlong(sc);
@@ -737,6 +752,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     u32 *modtab = (u32 *)(mb + 8);                         // [RSIM_MODTAB] launch counter mod T
     WarpBuf *wbuf = (WarpBuf *)(modtab + RSIM_MODTAB);     // [W]
     WarpBuf &WB = wbuf[control ? 0 : warp];
+    HistHead *hhc = (HistHead *)(wbuf + W);                // [per_cta] history heads (FILTER, staleness > 0)
 
     {   // load this CTA's instance shard
         const u64 *src = (const u64 *)(P.inst + base);
@@ -745,7 +761,10 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nloc; i += blockDim.x) st[i].qcpos = -1;   // head caches start cold
+    for (int i = threadIdx.x; i < nloc; i += blockDim.x) {   // head caches start cold
+        st[i].qcpos = -1;
+        if (FILTER && P.stal > 0) { hhc[i].hidx = -1; hhc[i].ntidx = -1; }
+    }
     const u64 c0_lo = P.tie[0], c0_hi = P.tie[1];          // TieBreaker counter at launch
     u32 ties = 0;                                          // ties resolved in this launch (control warp)
     const int l0 = warp * ipw;
@@ -776,7 +795,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
 #define DIAG(x)
 #endif
     if (mode == MODE_DRAIN) {
-        if (!control) drain_phase(P, st, base, l0, nmine, until, 0u, lane, WB);
+        if (!control) drain_phase<FILTER>(P, st, base, l0, nmine, until, 0u, lane, WB);
     } else if (control) {
         // ---- control warp: stage ahead, then per decision wait for the partials and decide
         u32 mb_phase = 0u;                                  // bit p: phase of mbarrier mb[p]
@@ -794,7 +813,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         for (i64 k = k0; k < k1; k++) {
             const int par = (int)(k & 1);
             DIAG(tc = clock64());
-            const bool lin_dyn = FILTER && P.policy == 3;           // linear with the per-decision bs max
+            const bool lin_dyn = FILTER && P.policy == 3 && !(P.bsn > 0);   // linear with the per-decision bs max
             if (lane == 0) {
                 if (lin_dyn) mbar_arrive_expect(&mb0[par], (u32)(CW * 16));
                 mbar_arrive_expect(&mb[par], (u32)(CW * (FILTER && P.policy == 4 ? 32 : 16)));
@@ -843,7 +862,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             Defer df;
             df.rkeys = R.keys; df.rB = R.B; df.hit = WB.sph; df.moved = 0u;
             df.valid = __ballot_sync(FULL, WB.spk == k && lane < nmine && st[l0 + lane].tabver == WB.spver[lane]);
-            if (mode == MODE_REPLAY) drain_phase(P, st, base, l0, nmine, R.t, 0u, lane, WB, &df);
+            if (mode == MODE_REPLAY) drain_phase<FILTER>(P, st, base, l0, nmine, R.t, 0u, lane, WB, &df);
             PHASE(1);
             DIAG(const long long t_b = clock64());
             // ---- K2: hit blocks (probe-ahead where still valid) + score
@@ -862,13 +881,24 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     probe_hits(P, base, l0, nmine, R, mode, target, skip, lane, WB.hit, WB.slot[par]);
             }
             const u32 sparse_probe = (nmine >= 2 && R.B <= 128) ? ~skip : 0u;   // no probe slots for these
+            const bool stale = FILTER && P.stal > 0;
+            if (stale) {        // snapshot(now, staleness) of every candidate (indicators.py:36-65)
+                const int gi = base + l0 + lane;
+                if (lane < nmine && (mode != MODE_ENQUEUE || gi == target)) {
+                    Inst &si = st[l0 + lane];
+                    flush_view_hist(P, si, gi, R.t);
+                    hist_snapshot(P, si, hhc[l0 + lane], gi, R.t - P.stal);
+                }
+                __syncwarp();
+            }
             double bsn = P.bsn;
-            if (FILTER && P.policy == 3) {      // linear without a cap: bs_norm = max(max bs, 1) over ALL
+            if (FILTER && P.policy == 3 && !(P.bsn > 0)) {      // linear without a cap: bs_norm = max(max bs, 1) over ALL
                                                 // instances (policies.py:250-255) -- one extra exchange round
                 u32 lb = 0u;
                 if (lane < nmine) {
                     const Inst *sp = st + l0 + lane;
-                    lb = sp->due <= R.t ? (u32)(sp->r + sp->q) : (u32)(sp->v_r + sp->v_q);
+                    lb = stale ? (u32)(hhc[l0 + lane].r + hhc[l0 + lane].q)
+                               : sp->due <= R.t ? (u32)(sp->r + sp->q) : (u32)(sp->v_r + sp->v_q);
                 }
                 lb = __reduce_max_sync(FULL, lb);
                 if (lane < C) st_async_16(part0 + par * CW + cta * W + warp, &mb0[par], (u32)lane, (u64)lb, 0ULL);
@@ -881,7 +911,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             }
             u64 bits_bs;
             const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB, bits_bs,
-                                           FILTER && P.policy == 4, bsn);
+                                           FILTER && P.policy == 4, bsn, stale, hhc);
             PHASE(2);
             DIAG(const long long t_c = clock64());
             if (cta == 0 && warp == 0 && lane == 0) WB.c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once
@@ -900,7 +930,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 Part *dst = part + par * 2 * CW + cta * W + warp;
                 if (lane < C) st_async_16(dst, &mb[par], (u32)lane, wmin, w1);
                 if (FILTER && P.policy == 4) {           // second partial: (min bs, ties | max bs << 32)
-                    const u32 bsmax = __reduce_max_sync(FULL, lane < nmine ? (u32)(st[l0 + lane].v_r + st[l0 + lane].v_q) : 0u);
+                    const Inst &sv = st[l0 + lane];
+                    const u32 bsmax = __reduce_max_sync(FULL, lane < nmine ? (u32)(stale ? hhc[l0 + lane].r + hhc[l0 + lane].q : sv.v_r + sv.v_q) : 0u);
                     const u64 w2 = ((u64)bsmax << 32) | (u32)__popc(tmask_bs);
                     if (lane < C) st_async_16(dst + CW, &mb[par], (u32)lane, wmin_bs, w2);
                 }
@@ -927,7 +958,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     const u32 adv = __ballot_sync(FULL, lane < nmine && mybits != wmin &&
                                                             (!(FILTER && P.policy == 4) || bits_bs != wmin_bs));
                     DIAG(const long long t_s0 = clock64());
-                    if (adv) drain_phase(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
+                    if (adv) drain_phase<FILTER>(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
                     DIAG(const long long t_s1 = clock64());
                     // probe-ahead of request k+1 (valid while the instance's tabver holds)
                     if (nmine >= 2 && R1.B <= 128) {   // (one instance: the dense probe's single round trip wins)
@@ -967,7 +998,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 flush_touch_pin(P, WB.fin, lane, &WB.werr);      // (normally already run after the publish)
                 commit(P, st + l0 + s, base + l0 + s, k, h, R.t, R.keys,
                        (s < 2 && nmine < 2 && !(((stale_slots | sparse_probe) >> s) & 1u)) ? WB.slot[par][s] : nullptr,
-                       R.a, R.B, R.in, R.out, R.oa, lane, werr, WB.fin);
+                       R.a, R.B, R.in, R.out, R.oa, lane, werr, WB.fin, FILTER && P.stal > 0);
                 if (lane == 0 && werr) WB.werr = werr;
                 if (P.dec_ns != nullptr && lane == 0) P.dec_ns[k] = (i64)globaltimer();
             }

@@ -97,16 +97,32 @@ def test_random_configs_match_oracle(native, seed):
                            kv_weight=float(rng.choice([0.0, 0.4, 0.75, 1.0])),
                            bs_norm_cap=[None, 1, 3, 8, 64][int(rng.integers(0, 5))],
                            range_threshold=int(rng.choice([1, 2, 4, 9])))
+        stal = float(rng.choice([0.0, 0.0, 0.5, 3.7, 25.0, 200.0]))
         cfg = ClusterConfig(n_instances=N, cost_model=cm, cache=CacheConfig(bs, cap), policy=pol,
-                            seed=int(rng.integers(0, 99)))
+                            staleness_ms=stal, seed=int(rng.integers(0, 99)))
         ref = run_oracle(trace, cfg)
         rep = run(trace, cfg)
-        tag = f"seed{seed}/trial{trial} N={N} cap={cap} {kind}"
+        tag = f"seed{seed}/trial{trial} N={N} cap={cap} {kind} staleness={stal}"
         assert np.array_equal(rep.chosen, ref.chosen), tag
         assert np.array_equal(rep.hit_tokens, ref.hit_tokens), tag
         assert np.array_equal(rep.columns["first_token_us"], ref.first_token_us), tag
         assert np.array_equal(rep.columns["finish_us"], ref.finish_us), tag
         assert rep.end_us == ref.end_us and rep.queued_at_last_arrival == ref.queued_at_last_arrival, tag
+
+
+@pytest.mark.parametrize("name", ["stale_50ms_n16", "stale_filter_evict"])
+def test_stale_history_ring_small(native, name, monkeypatch):
+    """A view-history ring far below the staleness window: entries no later
+    snapshot can see are dropped on device, and a ring that still overflows is
+    reported (RSIM_E_HISTORY_OVERFLOW) and regrown -- same decisions either way."""
+    import dataclasses
+
+    from paper_2603_15202_b200 import cluster
+    real = cluster.sizing_for
+    monkeypatch.setattr(cluster, "sizing_for", lambda t, c: dataclasses.replace(real(t, c), history_capacity=16))
+    trace, cfg = G.build(name)
+    rep = cluster.run(trace, cfg)
+    _assert_report(rep, G.expected(name), name)
 
 
 @pytest.mark.parametrize("cap", [None, 8, 32, 128])
