@@ -36,6 +36,8 @@ class _Cfg(C.Structure):
         ("tie_lo", C.c_uint64), ("tie_hi", C.c_uint64),
         ("kv_weight", C.c_double), ("bs_norm_cap", C.c_double), ("range_threshold", C.c_int64),
         ("staleness_us", C.c_int64),
+        ("det_on", C.c_int32), ("det_top_k", C.c_int32), ("det_kb", C.c_int32), ("det_force", C.c_int32),
+        ("det_mean", C.c_int32), ("det_pad", C.c_int32), ("det_window_s", C.c_double), ("det_mult", C.c_double),
     ]
 
 
@@ -53,7 +55,7 @@ def lib():
         L = C.CDLL(_LIB)
         P = C.c_void_p
         L.orc_run.restype = C.c_int
-        L.orc_run.argtypes = [C.POINTER(_Cfg), C.c_int64] + [P] * 13 + [C.c_int64, P]
+        L.orc_run.argtypes = [C.POINTER(_Cfg), C.c_int64] + [P] * 13 + [C.c_int64, P, P, C.c_int64]
         L.orc_cache_new.restype = P
         L.orc_cache_new.argtypes = [C.c_int64]
         L.orc_cache_free.argtypes = [P]
@@ -97,9 +99,11 @@ def make_cfg(config) -> _Cfg:
     cm, cache, pol = config.cost_model, config.cache, config.policy
     if pol.kind not in POLICY_CODE:
         raise ValueError(f"oracle covers policies {sorted(POLICY_CODE)}, not {pol.kind!r}")
-    if getattr(config, "detector", None) is not None:
-        raise ValueError("oracle covers runs without a detector")
     tie = _stable_key(config.seed, pol.tie_break_seed)
+    det = getattr(config, "detector", None)
+    dv = (0, 0, 0, 0, 0, 0, 0.0, 0.0) if det is None else (
+        1, int(det.top_k_classes), int(det.class_key_blocks), int(det.mitigation == "force_least_bs"),
+        int(bool(det.compare_mean_non_holder)), 0, float(det.window_s), float(det.consecutive_multiplier))
     return _Cfg(config.n_instances, POLICY_CODE[pol.kind],
                 0 if pol.kv_indicator == "p_tokens" else 1,
                 0 if pol.balance_indicator == "bs" else 1,
@@ -110,7 +114,8 @@ def make_cfg(config) -> _Cfg:
                 float(getattr(pol, "kv_weight", 0.4)),
                 float(pol.bs_norm_cap) if getattr(pol, "bs_norm_cap", None) is not None else 0.0,
                 int(getattr(pol, "range_threshold", 4)),
-                int(round(float(getattr(config, "staleness_ms", 0.0)) * 1000.0)))   # cluster.py:77
+                int(round(float(getattr(config, "staleness_ms", 0.0)) * 1000.0)),   # cluster.py:77
+                *dv)
 
 
 class OracleError(RuntimeError):
@@ -130,10 +135,14 @@ class OracleResult:
     log: np.ndarray | None  # (n, 6): kind, inst, start, end, prefill_us, bs
     route_ns: np.ndarray | None
     evicted: int = 0
+    # detector (None without one): DetectorRow tuples (window_start_s, class_key, fraction,
+    # n_holders, n_others, suspect, phase) and first_violation_us
+    detector_rows: list | None = None
+    first_violation_us: int | None = None
 
 
 def run_oracle(trace, config, *, with_log: bool = False, time_routes: bool = False,
-               _log_cap: int | None = None) -> OracleResult:
+               _log_cap: int | None = None, _rows_cap: int | None = None) -> OracleResult:
     """Replay ``trace`` (a PackedTrace) on the CPU oracle."""
     L = lib()
     cfg = make_cfg(config)
@@ -149,7 +158,10 @@ def run_oracle(trace, config, *, with_log: bool = False, time_routes: bool = Fal
     chosen = np.empty(R, np.int32)
     hit = np.empty(R, np.int64)
     fs, ft, fin = (np.empty(R, np.int64) for _ in range(3))
-    summary = np.zeros(5, np.int64)
+    summary = np.zeros(7, np.int64)
+    det_on = getattr(config, "detector", None) is not None
+    rows_cap = _rows_cap if _rows_cap is not None else (4096 if det_on else 0)
+    rows = np.zeros((max(rows_cap, 1), 7), np.int64)
     log_cap = 0
     log = None
     if with_log:
@@ -158,9 +170,14 @@ def run_oracle(trace, config, *, with_log: bool = False, time_routes: bool = Fal
     rns = np.empty(R, np.int64) if time_routes else None
     rc = L.orc_run(C.byref(cfg), R, _ptr(arr), _ptr(i_in), _ptr(i_out), _ptr(rid), _ptr(off), _ptr(blk),
                    _ptr(chosen), _ptr(hit), _ptr(fs), _ptr(ft), _ptr(fin), _ptr(summary),
-                   _ptr(log) if with_log else None, log_cap, _ptr(rns))
+                   _ptr(log) if with_log else None, log_cap, _ptr(rns), _ptr(rows), rows_cap)
     if rc == -1:
         raise OracleError("CacheFullError")
+    if rc == -4:
+        raise ValueError("class_key needs at least one block")
+    if det_on and summary[5] > rows_cap:
+        return run_oracle(trace, config, with_log=with_log, time_routes=time_routes, _log_cap=_log_cap,
+                          _rows_cap=int(summary[5]))
     if rc != 0:
         raise OracleError(f"oracle error {rc}")
     if with_log:
@@ -168,8 +185,14 @@ def run_oracle(trace, config, *, with_log: bool = False, time_routes: bool = Fal
         if n > log_cap:
             return run_oracle(trace, config, with_log=True, time_routes=time_routes, _log_cap=n)
         log = log[:n].copy()
+    drows = fv = None
+    if det_on:
+        r = rows[:int(summary[5])]
+        drows = [(float(r[i, 0:1].view(np.float64)[0]), int(np.uint64(r[i, 1])), float(r[i, 2:3].view(np.float64)[0]),
+                  int(r[i, 3]), int(r[i, 4]), bool(r[i, 5]), int(r[i, 6])) for i in range(len(r))]
+        fv = None if summary[6] < 0 else int(summary[6])
     return OracleResult(chosen, hit, fs, ft, fin, int(summary[0]), int(summary[1]), int(summary[2]), log, rns,
-                        int(summary[4]))
+                        int(summary[4]), drows, fv)
 
 
 class OracleCache:

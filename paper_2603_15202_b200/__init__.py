@@ -7,7 +7,7 @@ hashing, KV$ prefix probe, multiplicative score, rotating-tie-break argmin,
 engine + cache state updates) executed by librsim's sm_100a kernels.
 """
 
-from .config import (CacheConfig, CacheFullError, ClusterConfig, CostModel, DuplicateRequestError,
+from .config import (CacheConfig, CacheFullError, ClusterConfig, CostModel, DetectorConfig, DuplicateRequestError,
                      InvariantError, NoInstancesError, PolicyConfig, UnsupportedConfigError)
 from .hashing import chain_keys, combine64, splitmix64, stable_key
 from .report import RequestMetrics, RoutingDecision, RunReport, StepRecord, percentile
@@ -28,7 +28,7 @@ def __getattr__(name):
 
 __all__ = [
     "CacheConfig", "CacheFullError", "ClassSpec", "ClusterConfig", "ClusterSim", "CostModel",
-    "DuplicateRequestError", "INFINITE", "InvariantError", "NoInstancesError", "PackedTrace",
+    "DetectorConfig", "DuplicateRequestError", "INFINITE", "InvariantError", "NoInstancesError", "PackedTrace",
     "PolicyConfig", "RequestMetrics", "RoutingDecision", "RunReport", "StepRecord", "SyntheticSpec",
     "TraceError", "TraceRecord", "UnsupportedConfigError", "chain_keys", "class_key", "combine64",
     "generate_synthetic", "generate_synthetic_packed", "load_trace", "percentile", "run", "save_trace",

@@ -128,12 +128,31 @@ class PolicyConfig:
 
 
 @dataclass(frozen=True)
+class DetectorConfig:
+    """Prefix-hotspot detector settings (reference detector.py:104-119)."""
+    window_s: float = 60.0
+    top_k_classes: int = 8
+    class_key_blocks: int = 2
+    consecutive_multiplier: float = 2.0
+    mitigation: str = "exclude_holders"  # or "force_least_bs"
+    compare_mean_non_holder: bool = False
+
+    def validate(self) -> None:
+        if self.window_s <= 0:
+            raise ValueError("window_s must be positive")
+        if self.top_k_classes < 1 or self.class_key_blocks < 1:
+            raise ValueError("top_k_classes and class_key_blocks must be >= 1")
+        if self.mitigation not in ("exclude_holders", "force_least_bs"):
+            raise ValueError(f"unknown mitigation {self.mitigation!r}")
+
+
+@dataclass(frozen=True)
 class ClusterConfig:
     n_instances: int = 16
     cost_model: CostModel = field(default_factory=CostModel)
     cache: CacheConfig = field(default_factory=CacheConfig)
     policy: PolicyConfig = field(default_factory=PolicyConfig)
-    detector: object | None = None
+    detector: DetectorConfig | None = None
     staleness_ms: float = 0.0
     seed: int = 0
     debug_checks: bool = False
@@ -147,6 +166,8 @@ class ClusterConfig:
         self.cost_model.validate()
         self.cache.validate()
         self.policy.validate()
+        if self.detector is not None:
+            self.detector.validate()
 
     def check_device_supported(self) -> None:
         """Reject the reference features that are outside the device path

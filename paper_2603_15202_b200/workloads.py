@@ -47,6 +47,19 @@ def chat_cluster(n_instances: int, n_requests: int, per_instance_rps: float = 3.
     return trace, ClusterConfig(n_instances=n_instances, cache=CacheConfig(16, 40000), seed=0)
 
 
+def hotspot(n_instances: int = 16, n_requests: int = 3000, hot_fraction: float = 0.6, rate_rps: float = 60.0,
+            n_cold: int = 6, seed: int = 0):
+    """One hot system prompt taking ``hot_fraction`` of arrivals next to ``n_cold``
+    cold classes: the prefix-hotspot regime the reference detector watches
+    (detector.py:1-23)."""
+    cold = (1.0 - hot_fraction) / n_cold
+    classes = (ClassSpec(hot_fraction, 16, (1, 3), (16, 96)),) + tuple(
+        ClassSpec(cold, 8, (1, 4), (16, 64)) for _ in range(n_cold))
+    spec = SyntheticSpec(duration_s=n_requests / rate_rps, mean_rate_rps=rate_rps, classes=classes, seed=seed)
+    return generate_synthetic_packed(spec), ClusterConfig(n_instances=n_instances, cache=CacheConfig(16, 40000),
+                                                          seed=seed)
+
+
 def config4_large(n_requests: int = 1_000_000, seed: int = 0):
     """4096 instances, ~1M requests at 3 req/s/instance (SURVEY cfg 4)."""
     return chat_cluster(4096, n_requests, 3.0, seed)

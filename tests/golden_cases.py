@@ -11,7 +11,9 @@ import os
 import numpy as np
 
 from paper_2603_15202_b200 import workloads as W
-from paper_2603_15202_b200.config import CacheConfig, ClusterConfig, CostModel, PolicyConfig
+import dataclasses
+
+from paper_2603_15202_b200.config import CacheConfig, ClusterConfig, CostModel, DetectorConfig, PolicyConfig
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
@@ -30,8 +32,8 @@ def fingerprint(trace) -> str:
 
 def build(name: str):
     meta = index()[name]
-    env = {"W": W, "ClusterConfig": ClusterConfig, "CacheConfig": CacheConfig, "CostModel": CostModel,
-           "PolicyConfig": PolicyConfig}
+    env = {"dataclasses": dataclasses, "W": W, "ClusterConfig": ClusterConfig, "CacheConfig": CacheConfig,
+           "CostModel": CostModel, "PolicyConfig": PolicyConfig, "DetectorConfig": DetectorConfig}
     trace, cfg = eval(meta["expr"], env)
     if meta["prefix"] is not None:
         trace = trace.slice(min(meta["prefix"], len(trace)))
@@ -51,3 +53,16 @@ def names(max_requests: int | None = None):
 def kats() -> dict:
     with open(os.path.join(GOLDEN, "hash_kats.json")) as fh:
         return json.load(fh)
+
+
+def detector_rows(want: dict):
+    """The reference's DetectorRow list of a detector fixture as tuples
+    (window_start_s, class_key, fraction, n_holders, n_others, suspect, phase)."""
+    ints = want["det_ints"]
+    return [(float(want["det_window_start_s"][i]), int(want["det_class_key"][i]), float(want["det_fraction"][i]),
+             int(ints[i, 0]), int(ints[i, 1]), bool(ints[i, 2]), int(ints[i, 3])) for i in range(len(ints))]
+
+
+def first_violation(want: dict):
+    v = int(want["det_first_violation_us"][0])
+    return None if v < 0 else v

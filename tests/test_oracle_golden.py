@@ -38,6 +38,9 @@ def test_oracle_matches_reference(name):
     assert np.array_equal(steps, want["steps"])
     s = want["summary"]
     assert (got.end_us, got.queued_at_last_arrival, got.finished) == (s[0], s[1], s[2])
+    if "det_ints" in want:                         # detector.finalize rows + first violation
+        assert got.detector_rows == G.detector_rows(want)
+        assert got.first_violation_us == G.first_violation(want)
 
 
 def test_oracle_cache_lru_examples():
@@ -53,3 +56,16 @@ def test_oracle_cache_lru_examples():
     c.touch_keys(k, c.match_keys(k), 2)
     c.insert_keys(chain_keys([21, 22]), 3)
     assert c.match_keys(chain_keys([1, 2])) == 2 and c.match_keys(chain_keys([11, 12])) == 0
+
+
+def test_oracle_detector_empty_prefix_raises():
+    """class_key of an empty prefix raises ValueError (reference detector.py:43-44)."""
+    import dataclasses
+    from paper_2603_15202_b200.config import DetectorConfig
+    trace, cfg = G.build("adv_zero_bs")
+    import numpy as np
+    from paper_2603_15202_b200.trace import PackedTrace
+    t = PackedTrace(trace.request_id[:2], trace.arrival_s[:2], trace.in_tokens[:2], trace.out_tokens[:2],
+                    trace.class_key[:2], np.zeros(3, np.int64), np.zeros(0, np.uint64))
+    with pytest.raises(ValueError):
+        run_oracle(t, dataclasses.replace(cfg, detector=DetectorConfig()))

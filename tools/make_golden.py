@@ -15,6 +15,7 @@ instead.
 
 from __future__ import annotations
 
+import dataclasses
 import hashlib
 import json
 import os
@@ -31,7 +32,7 @@ from refcompat import import_reference, to_ref_config, to_ref_records  # noqa: E
 
 from paper_2603_15202_b200 import workloads as W  # noqa: E402
 from paper_2603_15202_b200.config import (CacheConfig, ClusterConfig, CostModel,  # noqa: E402
-                                          PolicyConfig)
+                                          DetectorConfig, PolicyConfig)
 
 OUT = os.path.join(ROOT, "tests", "golden")
 
@@ -78,6 +79,12 @@ CASES = {
     "stale_frac_vllm": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='vllm'), staleness_ms=12.3456, seed=10))", 1000),
     "stale_linear": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='linear'), staleness_ms=20.0, seed=11))", 1000),
     "stale_filter_evict": ("(W.config3_agent(1500, n_instances=16, capacity=4096, rate_per_instance=1.0)[0], ClusterConfig(n_instances=16, cache=CacheConfig(16, 4096), policy=PolicyConfig(kind='filter'), staleness_ms=100.0, seed=12))", None),
+    "det_hot_n16": ("(lambda t, c: (t, dataclasses.replace(c, detector=DetectorConfig(window_s=5.0))))(*W.hotspot(16, 2000))", None),
+    "det_hot_force_mean": ("(lambda t, c: (t, dataclasses.replace(c, detector=DetectorConfig(window_s=3.0, mitigation='force_least_bs', compare_mean_non_holder=True, consecutive_multiplier=1.0))))(*W.hotspot(12, 2000, 0.7, seed=4))", None),
+    "det_hot_vllm_stale": ("(lambda t, c: (t, dataclasses.replace(c, policy=PolicyConfig(kind='vllm'), staleness_ms=20.0, detector=DetectorConfig(window_s=4.0, top_k_classes=2))))(*W.hotspot(8, 1500, 0.5, seed=5))", None),
+    "det_chat_default": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=16, cache=CacheConfig(16, 40000), detector=DetectorConfig(), seed=0))", 1500),
+    "det_api_k1": ("(W.config2_api()[0], ClusterConfig(n_instances=64, cache=CacheConfig(16, 40000), detector=DetectorConfig(window_s=2.0, top_k_classes=4, class_key_blocks=1), seed=0))", 3000),
+    "det_evict_n8": ("(lambda t, c: (t, dataclasses.replace(c, cache=CacheConfig(16, 600), detector=DetectorConfig(window_s=2.0, consecutive_multiplier=0.5))))(*W.hotspot(8, 2000, 0.8, 90.0, seed=6))", None),
     "cost_fma_sensitive": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, cost_model=CostModel(3.3, 0.0371, 17.1, 0.77, 0.0013, 512, 16), cache=CacheConfig(16, 2000), seed=4))", 1000),
     "cost_small_batch": ("(W.config2_api()[0], ClusterConfig(n_instances=6, cost_model=CostModel(1.0, 0.2, 4.0, 0.5, 0.01, 300, 3), cache=CacheConfig(16, 5000), seed=7))", 1500),
     "block_size_4": ("W.generate_synthetic_packed(W.SyntheticSpec(60.0, 20.0, (W.ClassSpec(0.5, 6, (1, 5), (1, 30)), W.ClassSpec(0.5, 2, (0, 3), (1, 9))), seed=11, block_size=4)), ClusterConfig(n_instances=5, cache=CacheConfig(4, 500), seed=11)", None),
@@ -85,8 +92,8 @@ CASES = {
 
 
 def build_case(expr: str, prefix):
-    env = {"W": W, "ClusterConfig": ClusterConfig, "CacheConfig": CacheConfig, "CostModel": CostModel,
-           "PolicyConfig": PolicyConfig}
+    env = {"dataclasses": dataclasses, "W": W, "ClusterConfig": ClusterConfig, "CacheConfig": CacheConfig, "CostModel": CostModel,
+           "PolicyConfig": PolicyConfig, "DetectorConfig": DetectorConfig}
     trace, cfg = eval(expr, env)
     if prefix is not None:
         trace = trace.slice(min(prefix, len(trace)))
@@ -105,7 +112,19 @@ def run_reference(trace, cfg):
 
     steps = np.asarray([(s.instance, s.start_us, s.end_us, s.prefill_us) for s in rep.steps],
                        dtype=np.int64).reshape(-1, 4)
+    det = {}
+    if rep.detector_enabled:
+        rows = rep.detector_rows
+        det = dict(
+            det_window_start_s=np.asarray([r.window_start_s for r in rows], np.float64),
+            det_class_key=np.asarray([r.class_key for r in rows], np.uint64),
+            det_fraction=np.asarray([r.fraction for r in rows], np.float64),
+            det_ints=np.asarray([(r.n_holders, r.n_others, int(r.suspect), r.phase) for r in rows],
+                                np.int64).reshape(-1, 4),
+            det_first_violation_us=np.asarray([-1 if rep.first_violation_us is None else rep.first_violation_us],
+                                              np.int64))
     return dict(
+        **det,
         chosen=np.asarray([r.chosen_instance for r in rep.requests], dtype=np.int32),
         hit_tokens=col("hit_tokens"), first_sched_us=col("first_sched_us"),
         first_token_us=col("first_token_us"), finish_us=col("finish_us"), steps=steps,

@@ -22,6 +22,7 @@ def import_reference():
 def to_ref_config(cfg):
     rs = import_reference()
     from routesim.cluster import CacheConfig, ClusterConfig
+    from routesim.detector import DetectorConfig
     from routesim.engine import CostModel
     from routesim.policies import PolicyConfig
     cm = cfg.cost_model
@@ -33,6 +34,8 @@ def to_ref_config(cfg):
         cache=CacheConfig(cfg.cache.block_size, cfg.cache.capacity_blocks),
         policy=PolicyConfig(**{k: getattr(cfg.policy, k) for k in cfg.policy.__dataclass_fields__}),
         staleness_ms=cfg.staleness_ms, seed=cfg.seed, parallel_instances=cfg.parallel_instances,
+        detector=None if cfg.detector is None else DetectorConfig(
+            **{k: getattr(cfg.detector, k) for k in cfg.detector.__dataclass_fields__}),
     )
 
 
