@@ -33,7 +33,8 @@ typedef enum {
     RSIM_E_UNSUPPORTED = 9,    /* feature outside the device path (detector, staleness > 0, ...)  */
     RSIM_E_COMM = 10,          /* multi-GPU exchange failure                                        */
     RSIM_E_NO_INSTANCES = 11,  /* empty candidate set (reference: NoInstancesError, policies.py:226) */
-    RSIM_E_HISTORY_OVERFLOW = 12 /* view-history ring full (staleness > 0): recreate with larger history_capacity */
+    RSIM_E_HISTORY_OVERFLOW = 12, /* view-history ring full (staleness > 0): recreate with larger history_capacity */
+    RSIM_E_DETECTOR = 13       /* detector capacity exceeded (classes re-evaluated in one decision > 64)  */
 } rsim_status;
 
 enum { RSIM_POLICY_MULTIPLICATIVE = 0, RSIM_POLICY_VLLM = 1, RSIM_POLICY_LEAST_BS = 2,
@@ -79,6 +80,17 @@ typedef struct rsim_config {
                                        scores see each instance's view as of now - staleness      */
     int32_t history_capacity;       /* per-instance view-history ring entries (staleness > 0), 0 = auto */
     int32_t reserved0;
+    /* Prefix-hotspot detector (DetectorConfig, detector.py:104-119; ClusterConfig.detector). Replays
+     * run it on one CTA (n_instances <= 256) with multiplicative / vllm / least_bs / capped linear
+     * scores; classes come from rsim_load_detector. det_on = 0: no detector (None). */
+    int32_t det_on;
+    int32_t det_top_k_classes;
+    int32_t det_class_key_blocks;
+    int32_t det_mitigation;         /* 0 exclude_holders, 1 force_least_bs                    */
+    int32_t det_compare_mean_non_holder;
+    int32_t reserved1;
+    double det_window_s;
+    double det_consecutive_multiplier;
 } rsim_config;
 
 typedef struct rsim rsim_t;
@@ -182,6 +194,24 @@ rsim_status rsim_read_phase_times(rsim_t *h, uint64_t *out, int64_t n_decisions)
 rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out32);
 /* Number of kernels librsim launched since create (evidence for bench gpu_launches). */
 int64_t rsim_launch_count(const rsim_t *h);
+
+/* ---- prefix-hotspot detector (reference detector.py; cluster.py:131-140, 194-201) ---- */
+/* Classes of the loaded trace (all n requests, loaded by one rsim_load_trace after a reset):
+ * track_of_request[r] = dense class id numbered by first arrival; per class the exemplar
+ * (its first request's leading min(class_key_blocks, B) chain keys: offset into the loaded
+ * blocks, length) and its class_key (detector.py:41-45). rows_capacity bounds the DetectorRows
+ * kept (windows x top_k_classes + top_k_classes is always enough). */
+rsim_status rsim_load_detector(rsim_t *h, int64_t n, const int32_t *track_of_request, int32_t n_tracks,
+                               const int64_t *exemplar_offset, const int32_t *exemplar_len,
+                               const uint64_t *class_key, int64_t rows_capacity);
+/* Detector.finalize (detector.py:373-377): the last window's rows, on the tables after the drain. */
+rsim_status rsim_detector_finalize(rsim_t *h);
+/* DetectorRows, 7 int64 each: window_start_s (f64 bits), class_key, fraction (f64 bits),
+ * n_holders, n_others, suspect, phase; first_violation_us = -1 for None. */
+rsim_status rsim_read_detector(rsim_t *h, int64_t *rows, int64_t capacity, int64_t *n_rows,
+                               int64_t *first_violation_us);
+/* Diagnostics: 8 words per decision when RSIM_DET_DEBUG was set at rsim_load_detector. */
+rsim_status rsim_detector_debug(rsim_t *h, int64_t *out, int64_t n);
 
 #ifdef __cplusplus
 }

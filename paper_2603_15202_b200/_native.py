@@ -60,6 +60,9 @@ class Config(C.Structure):
         ("runs_capacity", C.c_int64),
         ("kv_weight", C.c_double), ("bs_norm_cap", C.c_double), ("range_threshold", C.c_int64),
         ("staleness_us", C.c_int64), ("history_capacity", C.c_int32), ("reserved0", C.c_int32),
+        ("det_on", C.c_int32), ("det_top_k_classes", C.c_int32), ("det_class_key_blocks", C.c_int32),
+        ("det_mitigation", C.c_int32), ("det_compare_mean_non_holder", C.c_int32), ("reserved1", C.c_int32),
+        ("det_window_s", C.c_double), ("det_consecutive_multiplier", C.c_double),
     ]
 
 
@@ -109,6 +112,10 @@ def lib():
         "rsim_read_phase_records": ([P, P, I64, P], C.c_int),
         "rsim_read_step_cycles": ([P, P], C.c_int),
         "rsim_read_phase_times": ([P, P, I64], C.c_int),
+        "rsim_load_detector": ([P, I64, P, I32, P, P, P, I64], C.c_int),
+        "rsim_detector_finalize": ([P], C.c_int),
+        "rsim_read_detector": ([P, P, I64, P, P], C.c_int),
+        "rsim_detector_debug": ([P, P, I64], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -124,7 +131,8 @@ EXPORTED = ("rsim_create", "rsim_destroy", "rsim_last_error", "rsim_reset", "rsi
             "rsim_cache_insert_keys", "rsim_cache_match_keys", "rsim_probe_batch", "rsim_chain_keys",
             "rsim_last_timings", "rsim_read_decision_ns", "rsim_launch_count", "rsim_rerun",
             "rsim_read_counters", "rsim_shard_bounds", "rsim_mailbox", "rsim_mailbox_ipc_handle",
-            "rsim_set_peer", "rsim_open_peer_ipc")
+            "rsim_set_peer", "rsim_open_peer_ipc", "rsim_load_detector", "rsim_detector_finalize",
+            "rsim_read_detector", "rsim_detector_debug")
 
 
 def _p(a):
@@ -287,6 +295,31 @@ class Handle:
         out = np.zeros((n, warps + 4), np.uint64)
         self._ck(self._L.rsim_read_phase_times(self._h, out.ctypes.data, n))
         return out
+
+    # -- hotspot detector ----------------------------------------------------------------
+    def load_detector(self, track_of_request, exemplar_offset, exemplar_len, class_key, rows_capacity: int):
+        tid = np.ascontiguousarray(track_of_request, dtype=np.int32)
+        off = np.ascontiguousarray(exemplar_offset, dtype=np.int64)
+        ln = np.ascontiguousarray(exemplar_len, dtype=np.int32)
+        key = np.ascontiguousarray(class_key, dtype=np.uint64)
+        self._ck(self._L.rsim_load_detector(self._h, len(tid), _p(tid), len(off), _p(off), _p(ln), _p(key),
+                                            int(rows_capacity)))
+
+    def detector_finalize(self):
+        self._ck(self._L.rsim_detector_finalize(self._h))
+
+    def read_detector(self):
+        """(rows, first_violation_us): DetectorRow tuples (window_start_s, class_key, fraction,
+        n_holders, n_others, suspect, phase) and None or the first phase-1 time."""
+        n, fv = C.c_int64(), C.c_int64()
+        self._ck(self._L.rsim_read_detector(self._h, None, 0, C.byref(n), C.byref(fv)))
+        raw = np.zeros((max(n.value, 1), 7), np.int64)
+        self._ck(self._L.rsim_read_detector(self._h, _p(raw), n.value, C.byref(n), C.byref(fv)))
+        raw = raw[:n.value]
+        f = raw.view(np.float64)
+        rows = [(float(f[i, 0]), int(np.uint64(raw[i, 1])), float(f[i, 2]), int(raw[i, 3]), int(raw[i, 4]),
+                 bool(raw[i, 5]), int(raw[i, 6])) for i in range(len(raw))]
+        return rows, (None if fv.value < 0 else int(fv.value))
 
     def step_cycles(self) -> np.ndarray:
         out = np.zeros(32, np.int64)

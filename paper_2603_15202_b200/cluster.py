@@ -27,7 +27,7 @@ import numpy as np
 from . import _native
 from .config import ClusterConfig, DuplicateRequestError
 from .hashing import MASK64, stable_key
-from .report import RoutingDecision, RunReport
+from .report import DetectorRow, RoutingDecision, RunReport
 from .trace import PackedTrace, TraceRecord, validate_against_block_size
 
 _POLICY = {"multiplicative": 0, "vllm": 1, "least_bs": 2, "linear": 3, "filter": 4}
@@ -131,7 +131,40 @@ def native_config(config: ClusterConfig, sizing: Sizing, *, device: int = 0, rec
     c.range_threshold = pol.range_threshold
     c.staleness_us = staleness_us(config)
     c.history_capacity = sizing.history_capacity
+    det = config.detector
+    if det is not None:
+        c.det_on = 1
+        c.det_top_k_classes = det.top_k_classes
+        c.det_class_key_blocks = det.class_key_blocks
+        c.det_mitigation = 1 if det.mitigation == "force_least_bs" else 0
+        c.det_compare_mean_non_holder = int(bool(det.compare_mean_non_holder))
+        c.det_window_s = float(det.window_s)
+        c.det_consecutive_multiplier = float(det.consecutive_multiplier)
     return c
+
+
+def detector_classes(trace: PackedTrace, key_blocks: int):
+    """Dense class tracks of a trace for the device detector: per request its track
+    (numbered by first arrival, the order Detector.observe creates them,
+    detector.py:303-307); per track the exemplar -- the first request's leading
+    min(key_blocks, B) chain keys (offset, length) -- and the class key
+    (detector.py:41-45)."""
+    from .hashing import GOLDEN64, combine64, combine64_np
+    from .trace import CLASS_SALT
+    B = np.diff(trace.blk_off)
+    if (B < 1).any():
+        raise ValueError("class_key needs at least one block")
+    acc = np.full(len(trace), combine64(GOLDEN64, CLASS_SALT), np.uint64)
+    for j in range(key_blocks):
+        m = B > j
+        acc[m] = combine64_np(acc[m], trace.blocks[trace.blk_off[:-1][m] + j])
+    keys, first, inv = np.unique(acc, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")              # classes by first arrival
+    rank = np.empty_like(order)
+    rank[order] = np.arange(len(order))
+    tid = rank[inv.ravel()].astype(np.int32)
+    fr = first[order]
+    return tid, trace.blk_off[:-1][fr].astype(np.int64), np.minimum(B[fr], key_blocks).astype(np.int32), keys[order]
 
 
 @dataclass(frozen=True)
@@ -310,6 +343,11 @@ class ClusterSim:
         if n:
             h.load(trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.request_id, trace.blk_off,
                    trace.blocks)
+            det = self.config.detector
+            if det is not None:
+                tid, ex_off, ex_len, ckey = detector_classes(trace, det.class_key_blocks)
+                windows = int(trace.arrival_us[-1] / 1e6 / det.window_s) + 3
+                h.load_detector(tid, ex_off, ex_len, ckey, windows * det.top_k_classes + det.top_k_classes)
             h.replay(0, n)
             queued_last = int(h.instances()[:, 1].sum())
         h.drain(INT64_MAX)
@@ -325,9 +363,16 @@ class ClusterSim:
             log, needed = h.step_log()
             if log is None:
                 raise _StepLogOverflow(needed)
-        return RunReport(self.config.policy.kind, self.config.seed, self.config.n_instances, self.block_size,
-                         trace=trace, columns=cols, step_log=log, end_us=end_us,
-                         queued_at_last_arrival=queued_last)
+        rep = RunReport(self.config.policy.kind, self.config.seed, self.config.n_instances, self.block_size,
+                        trace=trace, columns=cols, step_log=log, end_us=end_us,
+                        queued_at_last_arrival=queued_last)
+        if self.config.detector is not None:              # cluster.py:194-201
+            rep.detector_enabled = True
+            if n:
+                h.detector_finalize()
+                rows, rep.first_violation_us = h.read_detector()
+                rep.detector_rows = [DetectorRow(*r) for r in rows]
+        return rep
 
 
 def run(records, config: ClusterConfig, **kw) -> RunReport:

@@ -171,9 +171,11 @@ class ClusterConfig:
 
     def check_device_supported(self) -> None:
         """Reject the reference features that are outside the device path
-        (the detector, the simulate policy)."""
-        if self.detector is not None:
-            raise UnsupportedConfigError("hotspot detector is not on the device path")
+        (the simulate policy; the detector with set-dependent scores)."""
+        if self.detector is not None and (self.policy.kind == "filter" or
+                                          (self.policy.kind == "linear" and self.policy.bs_norm_cap is None)):
+            raise UnsupportedConfigError("the hotspot detector runs with multiplicative, vllm, least_bs or "
+                                         "capped linear scores on the device path")
         if self.policy.kind not in DEVICE_POLICY_KINDS:
             raise UnsupportedConfigError(
                 f"policy {self.policy.kind!r} is not on the device path "

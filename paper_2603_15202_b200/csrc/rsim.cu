@@ -88,6 +88,16 @@ struct rsim {
     int rlog2 = 0;
     HEnt *hring = nullptr;   // view-history rings (staleness > 0)
     int hlog2 = 0;
+    // hotspot detector (rsim_detector.cuh): classes loaded by rsim_load_detector
+    DevArr<int> dtid, dtw;
+    DevArr<i64> dtex, dbk, drows;
+    DevArr<u64> dtkey;
+    DevArr<DTrack> dtr;
+    i64 *dtot = nullptr, *dglob = nullptr;
+    int dT = 0, dbclog2 = 0;
+    i64 drows_cap = 0;
+    bool det_loaded = false;
+    DevArr<i64> ddbg;
     DevArr<u64> arena;             // API-inserted chain keys (named by eviction runs)
     i64 narena = 0;
     unsigned short *crit = nullptr; // diagnostics: per (decision, warp) phase records
@@ -141,6 +151,14 @@ static Params make_params(rsim_t *h) {
     P.epoch = h->epoch;
     P.runs = h->runs; P.rlog2 = h->rlog2; P.arena = h->arena.p;
     P.stal = h->cfg.staleness_us; P.hring = h->hring; P.hlog2 = h->hlog2;
+    P.dtid = (h->cfg.det_on && h->det_loaded) ? h->dtid.p : nullptr;
+    P.dtw = h->dtw.p; P.dtex = h->dtex.p; P.dtkey = h->dtkey.p; P.dtr = h->dtr.p;
+    P.dbk = h->dbk.p; P.dtot = h->dtot; P.dglob = h->dglob; P.drows = h->drows.p; P.drows_cap = h->drows_cap;
+    P.dwin = h->cfg.det_window_s; P.dmult = h->cfg.det_consecutive_multiplier;
+    P.dwin_i = (i64)h->cfg.det_window_s; P.dcool = (i64)(h->cfg.det_window_s * 1e6);
+    P.dT = h->dT; P.dtopk = h->cfg.det_top_k_classes; P.dforce = h->cfg.det_mitigation == 1;
+    P.dmean = h->cfg.det_compare_mean_non_holder; P.dbclog2 = h->dbclog2;
+    P.ddbg = h->ddbg.p;
     P.timeout_ns = (h->cfg.comm_timeout_ms > 0 ? h->cfg.comm_timeout_ms : 10000) * 1000000LL;
     P.crit = h->crit; P.crit_cap = h->crit_cap;
     return P;
@@ -158,6 +176,7 @@ static rsim_status check_device_error(rsim_t *h) {
         case DEV_E_QUEUE_OVERFLOW: return fail(h, RSIM_E_QUEUE_OVERFLOW, "instance queue ring full (queue_capacity=%d)", 1 << h->qlog2);
         case DEV_E_TABLE_FULL: return fail(h, RSIM_E_TABLE_FULL, "instance KV$ table over 3/4 load (slots=%d)", 1 << h->slog2);
         case 11: return fail(h, RSIM_E_NO_INSTANCES, "no instances to route to");
+        case DEV_E_DETECTOR: return fail(h, RSIM_E_DETECTOR, "detector capacity exceeded (more than %d classes re-evaluated at once, or a window bucket ring overflow)", RSIM_DLMAX);
         case DEV_E_HISTORY_OVERFLOW: return fail(h, RSIM_E_HISTORY_OVERFLOW, "instance view-history ring full (history_capacity=%d)", 1 << h->hlog2);
         case DEV_E_COMM: return fail(h, RSIM_E_COMM, "timed out waiting for a peer rank's decision partial");
         default: return fail(h, RSIM_E_INVARIANT, "device error %d", e[0]);
@@ -172,12 +191,23 @@ static Inst fresh_inst() {
     return s;
 }
 
+static rsim_status det_reset(rsim_t *h, cudaStream_t s) {    // Detector.__init__ state
+    if (!h->cfg.det_on || !h->det_loaded) return RSIM_OK;
+    CK(h, cudaMemsetAsync(h->dtr.p, 0, (size_t)h->dT * sizeof(DTrack), s));
+    const i64 g[DG_N] = {0, 0, 0, -1, 0, 0, 0, INT64_MIN, 0};
+    static_assert(DG_N == 9, "detector scalars");
+    CK(h, cudaMemcpyAsync(h->dglob, g, sizeof(g), cudaMemcpyHostToDevice, s));
+    CK(h, cudaStreamSynchronize(s));
+    return RSIM_OK;
+}
+
 static rsim_status init_state(rsim_t *h) {
     const int N = h->N;
     h->epoch += 1;
     std::vector<Inst> hs(N);
     for (auto &s : hs) s = fresh_inst();
     CK(h, cudaMemcpyAsync(h->inst, hs.data(), N * sizeof(Inst), cudaMemcpyHostToDevice, h->stream));
+    h->det_loaded = false;                          // classes belong to a loaded trace
     const size_t slots = (size_t)N << h->slog2;
     CK(h, cudaMemsetAsync(h->tkeys, 0, slots * sizeof(u64), h->stream));   // EMPTY = 0
     CK(h, cudaMemsetAsync(h->tmeta, 0, slots * sizeof(Meta), h->stream));
@@ -212,6 +242,15 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (c.chunk_tokens < 1 || c.max_batch_requests < 1) return fail(nullptr, RSIM_E_INVALID, "chunk_tokens and max_batch_requests must be >= 1");
     if (c.policy < 0 || c.policy > 4) return fail(nullptr, RSIM_E_UNSUPPORTED, "policy %d not on the device path", c.policy);
     if (c.staleness_us < 0) return fail(nullptr, RSIM_E_INVALID, "staleness_us must be >= 0");
+    if (c.det_on) {
+        if (!(c.det_window_s > 0) || c.det_top_k_classes < 1 || c.det_class_key_blocks < 1 ||
+            c.det_mitigation < 0 || c.det_mitigation > 1)
+            return fail(nullptr, RSIM_E_INVALID, "invalid detector configuration");
+        if (c.world > 1) return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector is single-rank on the device path");
+        if (c.policy == RSIM_POLICY_FILTER || (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0)))
+            return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector runs with multiplicative, vllm, least_bs or capped linear scores");
+        if (c.det_window_s > 1e6) return fail(nullptr, RSIM_E_UNSUPPORTED, "detector window longer than 1e6 s");
+    }
     if (c.policy == RSIM_POLICY_FILTER && c.world > 1)
         return fail(nullptr, RSIM_E_UNSUPPORTED, "filter policy is single-rank on the device path");
     if (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0) && c.world > 1)
@@ -251,6 +290,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     const int N = h->N;
     int C = c.ctas;
     if (C <= 0) C = std::min(16, N);       // measured: spreading instances over SMs wins (profiles/)
+    if (c.det_on) C = 1;                   // the detector's control warp reads every instance warp's state
     C = std::max(1, std::min(16, std::min(C, N)));
     int per_cta = (N + C - 1) / C;
     // default: the lean kernel (<= 7 instance warps, 255 registers) unless a warp would own > 32 instances
@@ -262,7 +302,8 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (C * W > 256) { delete h; return fail(nullptr, RSIM_E_INVALID, "cluster too large"); }
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
     h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(6 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 8 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf) +
-                     (c.staleness_us > 0 ? (size_t)per_cta * sizeof(HistHead) : 0);
+                     (c.staleness_us > 0 ? (size_t)per_cta * sizeof(HistHead) : 0) +
+                     (c.det_on ? sizeof(DetCtl) + (size_t)(6 * W * C) * sizeof(Part) : 0);
     if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
     {   // kernel attributes are process-global: set the ceiling once (handles on other threads launch concurrently)
         static std::once_flag once;
@@ -331,7 +372,9 @@ void rsim_destroy(rsim_t *h) {
     h->rid.free_(); h->blocks.free_(); h->ckeys.free_(); h->okeys.free_();
     h->hit_blocks.free_(); h->chosen.free_();
     void *ps[] = {h->inst, h->qbuf, h->rbuf, h->tkeys, h->tmeta, h->tie, h->errbuf, h->flag, h->log, h->log_n,
-                  h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs, h->crit, h->hring};
+                  h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs, h->crit, h->hring,
+                  h->dtot, h->dglob};
+    h->ddbg.free_(); h->dtid.free_(); h->dtw.free_(); h->dtex.free_(); h->dbk.free_(); h->drows.free_(); h->dtkey.free_(); h->dtr.free_();
     h->arena.free_();
     for (int i = 0; i < 8; i++) if (h->peer_ipc[i] && h->peer[i]) cudaIpcCloseMemHandle(h->peer[i]);
     for (void *p : ps) if (p) cudaFree(p);
@@ -437,7 +480,7 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     CK(h, cudaEventRecord(h->ev0, h->stream));
     const bool filt = h->cfg.policy == RSIM_POLICY_FILTER ||            // the extended kernel: two-branch or
                       (h->cfg.policy == RSIM_POLICY_LINEAR && !(h->cfg.bs_norm_cap > 0)) ||   // two-round decisions,
-                      h->cfg.staleness_us > 0;                                              // stale snapshots
+                      h->cfg.staleness_us > 0 || h->cfg.det_on;                             // stale snapshots, detector
     if (h->W <= RSIM_LEAN_WARPS && !filt)
         CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_LEAN_WARPS, false>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
     else if (!filt)
@@ -469,6 +512,7 @@ rsim_status rsim_drain(rsim_t *h, int64_t until_us) {
 
 rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen, int64_t *hit_tokens, double *scores) {
     if (!h) return RSIM_E_INVALID;
+    if (h->cfg.det_on) return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls with the hotspot detector: use a trace replay");
     if (r < 0 || r >= h->R) return fail(h, RSIM_E_INVALID, "request index out of range");
     CK(h, cudaSetDevice(h->cfg.device));
     rsim_status st = launch_replay(h, r, r + 1, now_us, MODE_ROUTE, -1, scores ? h->scores : nullptr, nullptr);
@@ -490,6 +534,7 @@ rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen
 
 rsim_status rsim_enqueue(rsim_t *h, int32_t instance, int64_t r, int64_t now_us, int64_t *hit_tokens) {
     if (!h) return RSIM_E_INVALID;
+    if (h->cfg.det_on) return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls with the hotspot detector: use a trace replay");
     if (r < 0 || r >= h->R) return fail(h, RSIM_E_INVALID, "request index out of range");
     if (instance < 0 || instance >= h->N) return fail(h, RSIM_E_INVALID, "instance out of range");
     CK(h, cudaSetDevice(h->cfg.device));
@@ -690,6 +735,7 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
     CK(h, cudaEventRecord(e0, s));
     const size_t slots = (size_t)N << h->slog2;
     CK(h, cudaMemcpyAsync(h->inst, hs.data(), N * sizeof(Inst), cudaMemcpyHostToDevice, s));
+    if (det_reset(h, s) != RSIM_OK) return RSIM_E_CUDA;
     CK(h, cudaMemsetAsync(h->tkeys, 0, slots * sizeof(u64), s));
     CK(h, cudaMemsetAsync(h->tmeta, 0, slots * sizeof(Meta), s));
     CK(h, cudaMemcpyAsync(h->tie, tie, sizeof(tie), cudaMemcpyHostToDevice, s));
@@ -822,3 +868,82 @@ rsim_status rsim_last_timings(rsim_t *h, double *replay_ms, double *k1_ms, doubl
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- hotspot detector
+rsim_status rsim_load_detector(rsim_t *h, int64_t n, const int32_t *track_of_request, int32_t n_tracks,
+                               const int64_t *exemplar_offset, const int32_t *exemplar_len, const uint64_t *class_key,
+                               int64_t rows_capacity) {
+    if (!h) return RSIM_E_INVALID;
+    if (!h->cfg.det_on) return fail(h, RSIM_E_INVALID, "handle was created without a detector");
+    if (n != h->R || h->R == 0) return fail(h, RSIM_E_INVALID, "rsim_load_detector needs the loaded trace (%lld requests)", (long long)h->R);
+    if (n_tracks < 1 || !track_of_request || !exemplar_offset || !exemplar_len || !class_key)
+        return fail(h, RSIM_E_INVALID, "null / empty detector classes");
+    int next = 0;
+    for (i64 r = 0; r < n; r++) {                  // dense ids by first arrival
+        if (track_of_request[r] < 0 || track_of_request[r] > next || track_of_request[r] >= n_tracks)
+            return fail(h, RSIM_E_INVALID, "track ids must be numbered by first arrival");
+        if (track_of_request[r] == next) next++;
+    }
+    if (next != n_tracks) return fail(h, RSIM_E_INVALID, "unused detector tracks");
+    for (int t = 0; t < n_tracks; t++)
+        if (exemplar_len[t] < 1 || exemplar_offset[t] < 0 || exemplar_offset[t] + exemplar_len[t] > h->nblk)
+            return fail(h, RSIM_E_INVALID, "bad exemplar of track %d", t);
+    CK(h, cudaSetDevice(h->cfg.device));
+    cudaStream_t s = h->stream;
+    const int T = n_tracks;
+    int bl = 0;
+    while ((1LL << bl) < (i64)h->cfg.det_window_s + 2) bl++;
+    CK(h, h->dtid.reserve(n, 0, s)); CK(h, h->dtw.reserve(T, 0, s)); CK(h, h->dtex.reserve(T, 0, s));
+    CK(h, h->dtkey.reserve(T, 0, s)); CK(h, h->dtr.reserve(T, 0, s));
+    CK(h, h->dbk.reserve((size_t)T * 3 << bl, 0, s));
+    const i64 rc = std::max<i64>(rows_capacity, 16);
+    CK(h, h->drows.reserve((size_t)rc * 7, 0, s));
+    if (!h->dtot || bl > h->dbclog2) {
+        if (h->dtot) cudaFree(h->dtot);
+        CK(h, cudaMalloc(&h->dtot, ((size_t)2 << bl) * sizeof(i64)));
+    }
+    if (!h->dglob) CK(h, cudaMalloc(&h->dglob, DG_N * sizeof(i64)));
+    CK(h, cudaMemcpyAsync(h->dtid.p, track_of_request, n * sizeof(int), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemcpyAsync(h->dtw.p, exemplar_len, T * sizeof(int), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemcpyAsync(h->dtex.p, exemplar_offset, T * sizeof(i64), cudaMemcpyHostToDevice, s));
+    CK(h, cudaMemcpyAsync(h->dtkey.p, class_key, T * sizeof(u64), cudaMemcpyHostToDevice, s));
+    h->dT = T; h->dbclog2 = bl; h->drows_cap = rc;
+    if (getenv("RSIM_DET_DEBUG")) {
+        CK(h, h->ddbg.reserve((size_t)n * (8 + h->N), 0, s));
+        CK(h, cudaMemsetAsync(h->ddbg.p, 0xff, (size_t)n * (8 + h->N) * sizeof(i64), s));
+    }
+    h->det_loaded = true;
+    return det_reset(h, s);
+}
+
+rsim_status rsim_detector_finalize(rsim_t *h) {
+    if (!h) return RSIM_E_INVALID;
+    if (!h->cfg.det_on || !h->det_loaded) return fail(h, RSIM_E_INVALID, "no detector classes loaded");
+    CK(h, cudaSetDevice(h->cfg.device));
+    det_finalize_kernel<<<1, 32, 0, h->stream>>>(make_params(h));
+    CK(h, cudaGetLastError());
+    h->launches += 1;
+    CK(h, cudaStreamSynchronize(h->stream));
+    return check_device_error(h);
+}
+
+rsim_status rsim_read_detector(rsim_t *h, int64_t *rows, int64_t capacity, int64_t *n_rows, int64_t *first_violation_us) {
+    if (!h) return RSIM_E_INVALID;
+    if (!h->cfg.det_on || !h->det_loaded) return fail(h, RSIM_E_INVALID, "no detector classes loaded");
+    CK(h, cudaSetDevice(h->cfg.device));
+    i64 g[DG_N];
+    CK(h, cudaMemcpy(g, h->dglob, sizeof(g), cudaMemcpyDeviceToHost));
+    if (n_rows) *n_rows = g[DG_NROWS];
+    if (first_violation_us) *first_violation_us = g[DG_FIRSTV];
+    const i64 m = std::min(std::min(g[DG_NROWS], h->drows_cap), (i64)capacity);
+    if (rows && m > 0) CK(h, cudaMemcpy(rows, h->drows.p, (size_t)m * 7 * sizeof(i64), cudaMemcpyDeviceToHost));
+    return RSIM_OK;
+}
+
+// diagnostics (RSIM_DET_DEBUG set at rsim_load_detector): per decision code, holders, min / sum
+// holder-free product, chosen hit tokens, chosen product, chosen held, listed tracks
+rsim_status rsim_detector_debug(rsim_t *h, int64_t *out, int64_t n) {
+    if (!h || !h->ddbg.p) return RSIM_E_INVALID;
+    CK(h, cudaMemcpy(out, h->ddbg.p, (size_t)std::min<i64>(n, h->R) * (8 + h->N) * sizeof(i64), cudaMemcpyDeviceToHost));
+    return RSIM_OK;
+}

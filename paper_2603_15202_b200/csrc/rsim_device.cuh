@@ -26,6 +26,7 @@ typedef unsigned int u32;
 #define DEV_E_TABLE_FULL 8
 #define DEV_E_COMM 10
 #define DEV_E_HISTORY_OVERFLOW 12
+#define DEV_E_DETECTOR 13
 
 // A request on an instance: one 64-byte record used by the FIFO queue (v =
 // pending prefill tokens) and the running list (v = finish step = join step +
@@ -123,6 +124,15 @@ struct Params {
     unsigned short *crit; i64 crit_cap;
     i64 stal;         // router staleness in us (cluster.py:77); 0 = the live view
     HEnt *hring; int hlog2;            // per-instance view-history rings (staleness > 0)
+    // prefix-hotspot detector (rsim_detector.cuh; single-CTA replay), dtid == nullptr: off
+    const int *dtid;                   // [R] class track of each request (dense, by first arrival)
+    const int *dtw; const i64 *dtex; const u64 *dtkey;   // [T] exemplar length / chain-key offset / class key
+    struct DTrack *dtr;                // [T] track state
+    i64 *dbk, *dtot, *dglob;           // buckets [T][BC][3], totals [BC][2], scalars (DG_*)
+    i64 *drows; i64 drows_cap;         // emitted DetectorRows, 7 words each
+    double dwin, dmult; i64 dwin_i, dcool;
+    int dT, dtopk, dforce, dmean, dbclog2;
+    i64 *ddbg;                         // diagnostics: 8 words per decision (rsim_detector_debug), null = off
 };
 
 // ---------------- hashing (hashing.py:15-25) ----------------

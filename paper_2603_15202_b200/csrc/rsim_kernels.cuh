@@ -9,6 +9,7 @@
 //   cache_op_kernel  single-instance PrefixCache operations for the API
 #pragma once
 #include "rsim_engine.cuh"
+#include "rsim_detector.cuh"
 
 // ---------------------------------------------------------------- K1
 // One warp per 32 consecutive requests: their blocks are one contiguous CSR
@@ -235,6 +236,10 @@ struct __align__(16) WarpBuf {
     FinBuf fin;            // finishers of one engine step
     u64 c_bytes, c_steps;  // algorithmic probe bytes / engine steps of this warp
     int werr, fins;        // first device error seen by this warp; finisher batches run
+    // detector mode (rsim_detector.cuh): read by the control warp for the chosen instance
+    i64 prod[32];          // p_tokens * max(bs, 1) of each instance (detector.py:312-316)
+    int bsv[32];           // snapshot batch size
+    u32 tm[4];             // tied-instance masks per argmin branch (policy, filter bs, holders excluded, least bs)
 };
 
 // counter mod T for the 128-bit TieBreaker counter (hi:lo) without a 128-bit
@@ -500,7 +505,7 @@ __device__ __noinline__ void probe_hits_sparse(const Params &P, int base, int l0
 // handles instance s and returns its score bits (~0 = not a candidate).
 __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
                                            int mode, int target, int lane, WarpBuf &WB, u64 &bits_bs, bool filter,
-                                           double bsn, bool stale, const HistHead *hc) {
+                                           double bsn, bool stale, const HistHead *hc, bool det = false) {
     const int gi = base + l0 + lane;
     const bool cand = lane < n && ((mode != MODE_ENQUEUE) || gi == target);
     u64 bits = ~0ULL;
@@ -522,6 +527,13 @@ __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, 
         }
         const int h = WB.hit[lane];
         const double sc = score_of(P, vr, vq, vp, vt, h, R.in, bsn);
+        if (det) {                                     // Candidate.p_tokens * max(bs, 1), snapshot bs
+            i64 ht = (i64)h * P.bs; if (ht > R.in) ht = R.in;
+            i64 nw = R.in - ht; if (nw < 1) nw = 1;
+            const i64 bsz = (i64)vr + vq;
+            WB.prod[lane] = (vp + nw) * (bsz > 1 ? bsz : 1);
+            WB.bsv[lane] = (int)bsz;
+        }
         bits = (u64)__double_as_longlong(sc);
         if (P.scores != nullptr) P.scores[gi] = sc;
         if (filter) {
@@ -551,7 +563,7 @@ __device__ __forceinline__ u32 tie_index(const u32 *modtab, u64 c0_lo, u64 c0_hi
 
 __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
                                              Dec &dec, const u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane,
-                                             bool filter) {
+                                             bool filter, const Part *det_branch = nullptr, int det_code = 0) {
     // round-major: lane holds flat partials r*32 + lane (conflict-free 16-byte loads); flat
     // order = ascending instance id
 #ifdef RSIM_DIAG
@@ -589,7 +601,8 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         if (r < NR && idx < CW) {
             const ulonglong2 q = lds_v2u64(pp + idx);
             er |= (u32)(q.y >> 32);
-            const ulonglong2 qs = bs_branch ? lds_v2u64(pp + CW + idx) : q;   // the chosen branch
+            const ulonglong2 qs = det_branch ? lds_v2u64(det_branch + idx)
+                                  : bs_branch ? lds_v2u64(pp + CW + idx) : q;   // the chosen branch
             pm[r] = qs.x; pc[r] = (u32)qs.y; mn = min(mn, qs.x);
         }
     }
@@ -699,7 +712,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         const int owner = rb * 32 + L;
         if (owner / W == cta) { d.owner_warp = owner % W; d.kk = (int)okk; }
     }
-    d.pad = bs_branch ? 1 : 0;                    // the owner picks its tie among the chosen branch
+    d.pad = det_branch ? det_code : (bs_branch ? 1 : 0);   // the owner picks its tie among the chosen branch
 #ifdef RSIM_DIAG
     dt3 = clock64();
     if (dg) { atomicAdd(P.ctr + 35, (u64)(dt1 - dt0)); atomicAdd(P.ctr + 36, (u64)(dt2 - dt1)); atomicAdd(P.ctr + 37, (u64)(dt3 - dt2)); }
@@ -753,6 +766,9 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     WarpBuf *wbuf = (WarpBuf *)(modtab + RSIM_MODTAB);     // [W]
     WarpBuf &WB = wbuf[control ? 0 : warp];
     HistHead *hhc = (HistHead *)(wbuf + W);                // [per_cta] history heads (FILTER, staleness > 0)
+    const bool det = FILTER && P.dtid != nullptr;          // hotspot detector (single CTA)
+    DetCtl *dctl = (DetCtl *)(hhc + (P.stal > 0 ? P.per_cta : 0));
+    Part *dpart = (Part *)(dctl + 1);                      // [2 parity][masked, least bs, products][W]
 
     {   // load this CTA's instance shard
         const u64 *src = (const u64 *)(P.inst + base);
@@ -771,12 +787,19 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     const int nmine = control ? 0 : max(0, min(ipw, nloc - l0));
     if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; WB.fin.dnf = 0; WB.fin.npark = 0; WB.fin.tpn = 0; }
     if (threadIdx.x == 0) {
-        mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_init(&dmb[0], 1); mbar_init(&dmb[1], 1);
-        mbar_init(&mb0[0], 1); mbar_init(&mb0[1], 1); mbar_fence_init();
+        // detector mode: every instance warp also arrives (release) after its plain shared-memory stores
+        mbar_init(&mb[0], det ? 1 + W : 1); mbar_init(&mb[1], det ? 1 + W : 1); mbar_init(&dmb[0], 1); mbar_init(&dmb[1], 1);
+        mbar_init(&mb0[0], 1); mbar_init(&mb0[1], 1);
+        if (det) { mbar_init(&dctl->mbd[0], W); mbar_init(&dctl->mbd[1], W); }
+        mbar_fence_init();
         ctl[0] = k0;
     }
     if (mode != MODE_DRAIN)
         for (int T = threadIdx.x; T < RSIM_MODTAB; T += blockDim.x) modtab[T] = T > 1 ? mod_counter(c0_lo, c0_hi, (u32)T) : 0u;
+    if (det && mode == MODE_REPLAY && k0 < k1) {
+        for (int i = threadIdx.x; i < 2 * RSIM_DLMAX; i += blockDim.x) (&dctl->cnt[0][0])[i] = 0u;
+        if (control) det_prepare(P, *dctl, k0, P.arrival[k0], lane);   // verdict + holder list of k0
+    }
     __syncthreads();
     if (C > 1) cluster_sync_all();
 
@@ -799,6 +822,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     } else if (control) {
         // ---- control warp: stage ahead, then per decision wait for the partials and decide
         u32 mb_phase = 0u;                                  // bit p: phase of mbarrier mb[p]
+        u32 mbd_phase = 0u;                                 // bit p: phase of the detector barrier mbd[p]
         i64 staged = k0;
         auto stage_upto = [&](i64 lim) {
             lim = min(lim, k1);
@@ -827,7 +851,42 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                            : nullptr;
             if (tlc) tlc[0] = globaltimer();
 #endif
-            decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, FILTER && P.policy == 4);
+            if (det) {     // verdict(k) -> argmin branch (policies.py:222-236), then observe(k) before the release
+                const Part *dp = dpart + par * 3 * CW;
+                i64 nh = 0, psum = 0;
+                u64 pmin = ~0ULL;
+                for (int i = lane; i < CW; i += 32) {
+                    const ulonglong2 a = lds_v2u64(dp + i), c = lds_v2u64(dp + 2 * CW + i);
+                    nh += (i64)(a.y >> 32); pmin = min(pmin, c.x); psum += (i64)c.y;
+                }
+                nh = warp_sum(nh); psum = warp_sum(psum); pmin = warp_min_u64(pmin);
+                const int v = dctl->verdict;
+                const int code = v == 2 ? 3 : (v == 1 && nh < P.N ? 2 : 0);   // fail open when all hold
+                decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, false,
+                             code ? dp + (code - 2) * CW : nullptr, code);
+                __syncwarp();
+                while (!mbar_try_wait(&dctl->mbd[par], (mbd_phase >> par) & 1u)) { }   // listed holders counted
+                mbd_phase ^= 1u << par;
+                const Dec d = dec[par];
+                if (!d.err && d.owner_warp >= 0) {
+                    const WarpBuf &OB = wbuf[d.owner_warp];
+                    const int s = nth_set_bit(OB.tm[code], d.kk);
+                    const ReqStage &Rk = rq[k % RSIM_SLOTS];
+                    const int hb = OB.hit[s];
+                    i64 ht = (i64)hb * P.bs; if (ht > Rk.in) ht = Rk.in;
+                    if (P.ddbg != nullptr && lane == 0) {
+                        i64 *g = P.ddbg + (8 + P.N) * k;
+                        g[0] = code; g[1] = nh; g[2] = (i64)pmin; g[3] = psum; g[4] = ht; g[5] = OB.prod[s];
+                        g[6] = hb >= dctl->w; g[7] = dctl->nl;
+                    }
+                    det_observe(P, *dctl, k, Rk.t, lane, ht, hb >= dctl->w, OB.prod[s], nh, pmin, psum, dctl->cnt[par]);
+                    for (int i = lane; i < dctl->nl; i += 32) dctl->cnt[par][i] = 0u;
+                    __syncwarp();
+                    if (k + 1 < k1) det_prepare(P, *dctl, k + 1, P.arrival[k + 1], lane);
+                }
+            } else {
+                decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, FILTER && P.policy == 4);
+            }
             PHASE(5);
 #ifdef RSIM_DIAG
             if (tlc) tlc[1] = globaltimer();
@@ -911,7 +970,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             }
             u64 bits_bs;
             const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB, bits_bs,
-                                           FILTER && P.policy == 4, bsn, stale, hhc);
+                                           FILTER && P.policy == 4, bsn, stale, hhc, det);
             PHASE(2);
             DIAG(const long long t_c = clock64());
             if (cta == 0 && warp == 0 && lane == 0) WB.c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once
@@ -924,6 +983,31 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 const u32 bhi = __reduce_min_sync(FULL, (u32)(bits_bs >> 32));
                 wmin_bs = ((u64)bhi << 32) | __reduce_min_sync(FULL, (u32)(bits_bs >> 32) == bhi ? (u32)bits_bs : ~0u);
                 tmask_bs = __ballot_sync(FULL, lane < nmine && bits_bs == wmin_bs && wmin_bs != ~0ULL);
+            }
+            u32 det_keep = 0u;
+            if (det) {     // detector partials (rsim_detector.cuh): plain stores + a release arrive (C == 1)
+                const DetCtl &dc = *dctl;
+                const bool cand = lane < nmine;
+                const bool held = cand && WB.hit[lane] >= dc.w;          // holders of class(k)
+                const u64 bx = (cand && !held) ? mybits : ~0ULL;
+                const u64 bl = cand ? (u64)__double_as_longlong((double)WB.bsv[lane]) : ~0ULL;
+                const u64 pn = (cand && !held) ? (u64)WB.prod[lane] : ~0ULL;
+                const i64 ps = warp_sum((cand && !held) ? WB.prod[lane] : 0LL);
+                const u64 mx = warp_min_u64(bx), ml = warp_min_u64(bl), mp = warp_min_u64(pn);
+                const u32 tx = __ballot_sync(FULL, cand && bx == mx && mx != ~0ULL);
+                const u32 tl = __ballot_sync(FULL, cand && bl == ml && ml != ~0ULL);
+                const u32 nhw = (u32)__popc(__ballot_sync(FULL, held));
+                det_keep = tx | tl;
+                if (P.ddbg != nullptr && cand) P.ddbg[(8 + P.N) * k + 8 + base + l0 + lane] = held ? -2 : WB.prod[lane];
+                if (lane == 0) {
+                    WB.tm[0] = tmask; WB.tm[1] = tmask_bs; WB.tm[2] = tx; WB.tm[3] = tl;
+                    Part *dp = dpart + par * 3 * CW + warp;
+                    *reinterpret_cast<ulonglong2 *>(dp) = make_ulonglong2(mx, ((u64)nhw << 32) | (u32)__popc(tx));
+                    *reinterpret_cast<ulonglong2 *>(dp + CW) = make_ulonglong2(ml, (u64)(u32)__popc(tl));
+                    *reinterpret_cast<ulonglong2 *>(dp + 2 * CW) = make_ulonglong2(mp, (u64)ps);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&mb[par]);
             }
             {   // publish this warp's partial(s) to every CTA of the cluster
                 const u64 w1 = ((u64)(u32)WB.werr << 32) | (u32)__popc(tmask);
@@ -950,13 +1034,24 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
 #endif
             apply_deferred(P, WB.fin, lane, &WB.werr);      // parked finisher cache work (before any commit)
             flush_touch_pin(P, WB.fin, lane, &WB.werr);     // the previous commit's touch + pin
+            if (det) {     // holders of the listed tracks on the tables as of t_k (before any advance)
+                const DetCtl &dc = *dctl;
+                for (int j = 0; j < dc.nl; j++) {
+                    const bool hd = lane < nmine && det_holds(P, dc.lst[j], base + l0 + lane);
+                    const u32 c = (u32)__popc(__ballot_sync(FULL, hd));
+                    if (lane == 0 && c) atomicAdd(&dctl->cnt[par][j], c);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&dctl->mbd[par]);
+            }
             if (mode == MODE_REPLAY && k + 1 < k1) {
                 if (staged_seen <= k + 1) { staged_seen = ctl[0]; __threadfence_block(); }
                 if (staged_seen > k + 1) {
                     const ReqStage &R1 = rq[(k + 1) % RSIM_SLOTS];
                     // instances that cannot win this decision advance to the next arrival meanwhile
                     const u32 adv = __ballot_sync(FULL, lane < nmine && mybits != wmin &&
-                                                            (!(FILTER && P.policy == 4) || bits_bs != wmin_bs));
+                                                            (!(FILTER && P.policy == 4) || bits_bs != wmin_bs)) &
+                                    ~det_keep;      // detector: the other argmin branches' candidates stay
                     DIAG(const long long t_s0 = clock64());
                     if (adv) drain_phase<FILTER>(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
                     DIAG(const long long t_s1 = clock64());
@@ -992,7 +1087,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             }
             DIAG(was_owner = warp == d.owner_warp);
             if (warp == d.owner_warp) {
-                const int s = nth_set_bit(d.pad ? tmask_bs : tmask, d.kk);   // d.pad: filter's bs branch
+                const int s = nth_set_bit(d.pad == 0 ? tmask : d.pad == 1 ? tmask_bs : WB.tm[d.pad], d.kk);   // d.pad: the branch
                 const int h = WB.hit[s];
                 int werr = 0;
                 flush_touch_pin(P, WB.fin, lane, &WB.werr);      // (normally already run after the publish)

@@ -69,6 +69,18 @@ def _opt(v: int):
     return None if v < 0 else int(v)
 
 
+@dataclass(frozen=True)
+class DetectorRow:
+    """Per-window detector state of one top class (reference detector.py:140-148)."""
+    window_start_s: float
+    class_key: int
+    fraction: float
+    n_holders: int
+    n_others: int
+    suspect: bool
+    phase: int
+
+
 class RunReport:
     """Result of ``run`` / ``ClusterSim.run_trace``."""
 

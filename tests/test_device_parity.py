@@ -31,6 +31,11 @@ def _assert_report(rep, want, name):
     assert np.array_equal(steps, want["steps"]), f"{name}: step log differs"
     s = want["summary"]
     assert (rep.end_us, rep.queued_at_last_arrival, rep.finished, rep.routed) == tuple(int(x) for x in s[:4])
+    if "det_ints" in want:                          # detector rows + first violation (detector.py:340-377)
+        rows = [(r.window_start_s, r.class_key, r.fraction, r.n_holders, r.n_others, r.suspect, r.phase)
+                for r in rep.detector_rows]
+        assert rows == G.detector_rows(want), f"{name}: detector rows differ"
+        assert rep.first_violation_us == G.first_violation(want), f"{name}: first violation differs"
 
 
 @pytest.mark.parametrize("name", G.names())
