@@ -168,11 +168,12 @@ __device__ void det_observe(const Params &P, DetCtl &D, i64 k, i64 now, int lane
         }
     }
     __syncwarp();
-    // _expire (detector.py:177-185): only when the horizon moved
+    // _expire (detector.py:177-185): only when the horizon moved -- or, for windows under one
+    // second (int(window_s) == 0), always: the last bump's bucket is then already at the horizon
     const i64 horizon = now / 1000000 - P.dwin_i;
     const int BC = 1 << P.dbclog2, bm = BC - 1;
     int ntr = (int)P.dglob[DG_NTR];
-    if (horizon > P.dglob[DG_HZ]) {
+    if (horizon > P.dglob[DG_HZ] || P.dwin_i == 0) {
         for (int t = lane; t < ntr; t += 32) {
             DTrack &tr = P.dtr[t];
             const i64 *b = P.dbk + (size_t)t * BC * 3;

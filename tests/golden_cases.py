@@ -66,3 +66,27 @@ def detector_rows(want: dict):
 def first_violation(want: dict):
     v = int(want["det_first_violation_us"][0])
     return None if v < 0 else v
+
+
+def random_detector_case(seed: int, trial: int):
+    """Trial ``trial`` of the random detector parity sweep (test_device_parity.py): a
+    hotspot trace and a random detector / policy / cache / staleness configuration."""
+    rng = np.random.default_rng(500 + seed)
+    for _ in range(trial + 1):
+        N = int(rng.choice([3, 8, 16, 40, 100]))
+        trace, cfg = W.hotspot(N, int(rng.integers(300, 1500)), float(rng.uniform(0.3, 0.9)),
+                               float(rng.uniform(20, 200)), int(rng.integers(1, 12)), seed=int(rng.integers(0, 99)))
+        kind = str(rng.choice(["multiplicative", "multiplicative", "vllm", "least_bs", "linear"]))
+        pol = PolicyConfig(kind=kind, kv_indicator=str(rng.choice(["p_tokens", "one_minus_hit"])),
+                           balance_indicator=str(rng.choice(["bs", "total_tokens"])),
+                           bs_norm_cap=int(rng.integers(1, 9)) if kind == "linear" else None,
+                           tie_break_seed=int(rng.integers(0, 9)))
+        det = DetectorConfig(window_s=float(rng.choice([0.5, 1.0, 2.5, 7.0, 60.0])),
+                             top_k_classes=int(rng.integers(1, 6)), class_key_blocks=int(rng.integers(1, 4)),
+                             consecutive_multiplier=float(rng.choice([0.0, 0.5, 1.0, 2.0])),
+                             mitigation=str(rng.choice(["exclude_holders", "force_least_bs"])),
+                             compare_mean_non_holder=bool(rng.integers(0, 2)))
+        cap = [None, int(rng.integers(200, 2000))][int(rng.integers(0, 2))]
+        cfg = dataclasses.replace(cfg, policy=pol, detector=det, cache=CacheConfig(16, cap),
+                                  staleness_ms=float(rng.choice([0.0, 0.0, 7.5])))
+    return trace, cfg

@@ -115,6 +115,25 @@ def test_random_configs_match_oracle(native, seed):
         assert rep.end_us == ref.end_us and rep.queued_at_last_arrival == ref.queued_at_last_arrival, tag
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_random_detector_configs_match_oracle(native, seed):
+    """Random hotspot traces and detector settings (window, top-k, class key blocks,
+    mitigation, mean comparison, multiplier) under every detector-compatible score,
+    with staleness and eviction, vs the oracle: decisions, rows, first violation."""
+    from paper_2603_15202_b200.cluster import run
+    for trial in range(4):
+        trace, cfg = G.random_detector_case(seed, trial)
+        ref = run_oracle(trace, cfg)
+        rep = run(trace, cfg)
+        tag = f"seed{seed}/trial{trial} {cfg}"
+        assert np.array_equal(rep.chosen, ref.chosen), tag
+        assert np.array_equal(rep.columns["finish_us"], ref.finish_us), tag
+        rows = [(r.window_start_s, r.class_key, r.fraction, r.n_holders, r.n_others, r.suspect, r.phase)
+                for r in rep.detector_rows]
+        assert rows == ref.detector_rows, tag
+        assert rep.first_violation_us == ref.first_violation_us, tag
+
+
 @pytest.mark.parametrize("name", ["stale_50ms_n16", "stale_filter_evict"])
 def test_stale_history_ring_small(native, name, monkeypatch):
     """A view-history ring far below the staleness window: entries no later

@@ -16,7 +16,12 @@ from oracle import oracle as O  # noqa: E402
 from paper_2603_15202_b200.cluster import ClusterSim  # noqa: E402
 
 name = sys.argv[1]
-trace, cfg = G.build(name)
+if name.startswith("random:"):                 # random:<seed>:<trial> of the random detector sweep
+    _, sd, tr_i = name.split(":")
+    trace, cfg = G.random_detector_case(int(sd), int(tr_i))
+    print(cfg)
+else:
+    trace, cfg = G.build(name)
 n = len(trace)
 N = cfg.n_instances
 ob = np.full((n, 8 + N), -1, np.int64)
