@@ -48,6 +48,7 @@ WORKLOADS = {
     "chat16": ("config1_chatbot()", "synthetic chatbot trace, 16 instances, ~10k requests (BASELINE configs[0])"),
     "agent256": ("config3_agent(20_000)", "multi-turn coding-agent trace, 32k-token prompts, 256 instances, capacity 16384 (BASELINE configs[2])"),
     "large4096": ("config4_large(1_000_000)", "4096-instance chat cluster, ~1M requests (BASELINE configs[3])"),
+    "hot64det": ("hotspot_detector(64, 20_000)", "prefix-hotspot trace (one class 60 % of arrivals), 64 instances, reference detector on (SURVEY 8f rank 1)"),
 }
 METRIC = "routing decisions/sec"
 
@@ -154,7 +155,10 @@ def ref_records_and_config(trace, cfg):
                                               cm.decode_per_seq_ms, cm.decode_per_ctx_token_ms, cm.chunk_tokens,
                                               cm.max_batch_requests),
                          cache=CacheConfig(cfg.cache.block_size, cfg.cache.capacity_blocks),
-                         policy=PolicyConfig(kind=cfg.policy.kind), seed=cfg.seed)
+                         policy=PolicyConfig(**{k: getattr(cfg.policy, k) for k in cfg.policy.__dataclass_fields__}),
+                         staleness_ms=cfg.staleness_ms, seed=cfg.seed,
+                         detector=None if cfg.detector is None else __import__("routesim.detector", fromlist=["x"]).DetectorConfig(
+                             **{k: getattr(cfg.detector, k) for k in cfg.detector.__dataclass_fields__}))
     recs = [TraceRecord(r.request_id, r.arrival_s, r.prefix_blocks, r.input_tokens, r.output_tokens, r.class_key)
             for r in trace.records()]
     return routesim, recs, rcfg

@@ -80,9 +80,9 @@ typedef struct rsim_config {
                                        scores see each instance's view as of now - staleness      */
     int32_t history_capacity;       /* per-instance view-history ring entries (staleness > 0), 0 = auto */
     int32_t reserved0;
-    /* Prefix-hotspot detector (DetectorConfig, detector.py:104-119; ClusterConfig.detector). Replays
-     * run it on one CTA (n_instances <= 256) with multiplicative / vllm / least_bs / capped linear
-     * scores; classes come from rsim_load_detector. det_on = 0: no detector (None). */
+    /* Prefix-hotspot detector (DetectorConfig, detector.py:104-119; ClusterConfig.detector). Trace
+     * replays run it on one GPU with multiplicative / vllm / least_bs / capped linear scores;
+     * classes come from rsim_load_detector. det_on = 0: no detector (None). */
     int32_t det_on;
     int32_t det_top_k_classes;
     int32_t det_class_key_blocks;

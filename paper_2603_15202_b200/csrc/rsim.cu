@@ -159,6 +159,8 @@ static Params make_params(rsim_t *h) {
     P.dT = h->dT; P.dtopk = h->cfg.det_top_k_classes; P.dforce = h->cfg.det_mitigation == 1;
     P.dmean = h->cfg.det_compare_mean_non_holder; P.dbclog2 = h->dbclog2;
     P.ddbg = h->ddbg.p;
+    P.dsm = (P.dtid != nullptr && h->dT <= RSIM_DET_SMEM_T &&
+             h->smem_bytes + (size_t)h->dT * (sizeof(DTrack) + sizeof(u64)) <= 220 * 1024) ? 1 : 0;
     P.timeout_ns = (h->cfg.comm_timeout_ms > 0 ? h->cfg.comm_timeout_ms : 10000) * 1000000LL;
     P.crit = h->crit; P.crit_cap = h->crit_cap;
     return P;
@@ -194,8 +196,8 @@ static Inst fresh_inst() {
 static rsim_status det_reset(rsim_t *h, cudaStream_t s) {    // Detector.__init__ state
     if (!h->cfg.det_on || !h->det_loaded) return RSIM_OK;
     CK(h, cudaMemsetAsync(h->dtr.p, 0, (size_t)h->dT * sizeof(DTrack), s));
-    const i64 g[DG_N] = {0, 0, 0, -1, 0, 0, 0, INT64_MIN, 0};
-    static_assert(DG_N == 9, "detector scalars");
+    const i64 g[DG_N] = {0, 0, 0, -1, 0, 0, 0, INT64_MIN, 0, 0, 0};
+    static_assert(DG_N == 11, "detector scalars");
     CK(h, cudaMemcpyAsync(h->dglob, g, sizeof(g), cudaMemcpyHostToDevice, s));
     CK(h, cudaStreamSynchronize(s));
     return RSIM_OK;
@@ -290,7 +292,6 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     const int N = h->N;
     int C = c.ctas;
     if (C <= 0) C = std::min(16, N);       // measured: spreading instances over SMs wins (profiles/)
-    if (c.det_on) C = 1;                   // the detector's control warp reads every instance warp's state
     C = std::max(1, std::min(16, std::min(C, N)));
     int per_cta = (N + C - 1) / C;
     // default: the lean kernel (<= 7 instance warps, 255 registers) unless a warp would own > 32 instances
@@ -303,7 +304,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
     h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(6 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 8 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf) +
                      (c.staleness_us > 0 ? (size_t)per_cta * sizeof(HistHead) : 0) +
-                     (c.det_on ? sizeof(DetCtl) + (size_t)(6 * W * C) * sizeof(Part) : 0);
+                     (c.det_on ? sizeof(DetCtl) + (size_t)(6 * W * C) * sizeof(Part) + (size_t)(2 * W * C) * RSIM_DLMAX : 0);
     if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
     {   // kernel attributes are process-global: set the ceiling once (handles on other threads launch concurrently)
         static std::once_flag once;
@@ -466,11 +467,14 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     }
     Params P = make_params(h);
     P.scores = scores_dev;
+    if (P.dtid != nullptr && !P.dsm && h->C > 1)
+        return fail(h, RSIM_E_DETECTOR, "%d detector classes do not fit in shared memory next to the instance shard; "
+                    "use ctas=1", h->dT);
     cudaLaunchConfig_t lc;
     memset(&lc, 0, sizeof(lc));
     lc.gridDim = dim3(h->C, 1, 1);
     lc.blockDim = dim3(32 * (h->W + 1), 1, 1);   // + the control warp
-    lc.dynamicSmemBytes = h->smem_bytes;
+    lc.dynamicSmemBytes = h->smem_bytes + (P.dsm ? (size_t)h->dT * (sizeof(DTrack) + sizeof(u64)) : 0);
     lc.stream = h->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -895,12 +899,12 @@ rsim_status rsim_load_detector(rsim_t *h, int64_t n, const int32_t *track_of_req
     while ((1LL << bl) < (i64)h->cfg.det_window_s + 2) bl++;
     CK(h, h->dtid.reserve(n, 0, s)); CK(h, h->dtw.reserve(T, 0, s)); CK(h, h->dtex.reserve(T, 0, s));
     CK(h, h->dtkey.reserve(T, 0, s)); CK(h, h->dtr.reserve(T, 0, s));
-    CK(h, h->dbk.reserve((size_t)T * 3 << bl, 0, s));
+    CK(h, h->dbk.reserve(((size_t)T * 3 << bl) * h->C, 0, s));   // one bucket ring set per CTA
     const i64 rc = std::max<i64>(rows_capacity, 16);
     CK(h, h->drows.reserve((size_t)rc * 7, 0, s));
     if (!h->dtot || bl > h->dbclog2) {
         if (h->dtot) cudaFree(h->dtot);
-        CK(h, cudaMalloc(&h->dtot, ((size_t)2 << bl) * sizeof(i64)));
+        CK(h, cudaMalloc(&h->dtot, ((size_t)2 << bl) * h->C * sizeof(i64)));
     }
     if (!h->dglob) CK(h, cudaMalloc(&h->dglob, DG_N * sizeof(i64)));
     CK(h, cudaMemcpyAsync(h->dtid.p, track_of_request, n * sizeof(int), cudaMemcpyHostToDevice, s));

@@ -103,6 +103,21 @@ __device__ __forceinline__ void st_async_16(const void *local_dst, const u64 *lo
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.u64 [%0], {%1, %2}, [%3];"
                  :: "r"(rd), "l"(a), "l"(b), "r"(rm) : "memory");
 }
+// loads from CTA `rank`'s shared memory (the detector's read of the owner warp's buffers)
+__device__ __forceinline__ u32 dsm_ld_u32(const void *local, u32 rank) {
+    u32 ra, v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(local)), "r"(rank));
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+    return v;
+}
+__device__ __forceinline__ u64 dsm_ld_u64(const void *local, u32 rank) {
+    u32 ra;
+    u64 v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(local)), "r"(rank));
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ra) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void st_cluster_u64(u32 local_addr, u32 rank, u64 v) {
@@ -220,10 +235,14 @@ enum { MODE_REPLAY = 0, MODE_DRAIN = 1, MODE_ROUTE = 2, MODE_ENQUEUE = 3 };
 struct __align__(16) ReqStage {
     i64 t, a, in, oa;
     int B, out;
+    int dtid, dw;       // detector: class track and exemplar length
     u64 keys[128];
     u32 home[128];      // table home slot of each key (all instances share slog2)
 };
-struct __align__(16) Dec { int owner_warp; int kk; int err; int pad; };
+struct __align__(16) Dec {
+    int owner_warp; int kk; int err; int pad;   // owner warp in this CTA (-1: another CTA), its tie index, error, branch
+    int oflat, okk, r0, r1;                     // the owner as a flat cluster warp index, its tie index (every CTA)
+};
 
 // Per-warp hand-off state between the phases of a decision.
 struct __align__(16) WarpBuf {
@@ -240,6 +259,7 @@ struct __align__(16) WarpBuf {
     i64 prod[32];          // p_tokens * max(bs, 1) of each instance (detector.py:312-316)
     int bsv[32];           // snapshot batch size
     u32 tm[4];             // tied-instance masks per argmin branch (policy, filter bs, holders excluded, least bs)
+    __align__(16) unsigned char ecs[RSIM_DLMAX];   // holder counts of the listed tracks among this warp's instances
 };
 
 // counter mod T for the 128-bit TieBreaker counter (hi:lo) without a 128-bit
@@ -273,6 +293,7 @@ __device__ __noinline__ void stage_request(const Params &P, ReqStage &R, i64 k, 
     for (int q = 0; q < 4; q++)
         if (32 * q + lane < B) { R.keys[32 * q + lane] = kk[q]; R.home[32 * q + lane] = tab_home(kk[q], P.slog2); }
     if (lane == 0) { R.t = t; R.a = a; R.in = in; R.oa = oa; R.B = B; R.out = (int)out; }
+    if (P.dtid != nullptr && lane == 0) { R.dtid = P.dtid[k]; R.dw = P.dtw[R.dtid]; }
 }
 
 // ---- drain: advance instances [l0, l0+n) of this warp through steps starting before `until`
@@ -631,7 +652,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
 #ifdef RSIM_DIAG
     dt1 = clock64();
 #endif
-    Dec d; d.owner_warp = -1; d.kk = 0; d.err = (int)er; d.pad = 0;
+    Dec d; d.owner_warp = -1; d.kk = 0; d.err = (int)er; d.pad = 0; d.oflat = -1; d.okk = 0; d.r0 = d.r1 = 0;
     u32 kk = 0;
     bool mine = true;
     u32 Tg = T;
@@ -693,6 +714,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         }
         const int owner = rb * 32 + nth_set_bit(bm, (int)kr);
         if (owner / W == cta) { d.owner_warp = owner % W; d.kk = 0; }
+        d.oflat = owner; d.okk = 0;
     } else if (!d.err && mine) {
         // the round holding the kk-th tie, then the lane inside it
         u32 pre = 0, kr = 0, c = 0;
@@ -711,6 +733,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         const u32 okk = __shfl_sync(FULL, kr - (incl - c), L);
         const int owner = rb * 32 + L;
         if (owner / W == cta) { d.owner_warp = owner % W; d.kk = (int)okk; }
+        d.oflat = owner; d.okk = (int)okk;
     }
     d.pad = det_branch ? det_code : (bs_branch ? 1 : 0);   // the owner picks its tie among the chosen branch
 #ifdef RSIM_DIAG
@@ -768,7 +791,14 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     HistHead *hhc = (HistHead *)(wbuf + W);                // [per_cta] history heads (FILTER, staleness > 0)
     const bool det = FILTER && P.dtid != nullptr;          // hotspot detector (single CTA)
     DetCtl *dctl = (DetCtl *)(hhc + (P.stal > 0 ? P.per_cta : 0));
-    Part *dpart = (Part *)(dctl + 1);                      // [2 parity][masked, least bs, products][W]
+    Part *dpart = (Part *)(dctl + 1);                      // [2 parity][masked, least bs, products][C*W]
+    unsigned char *ecnt = (unsigned char *)(dpart + 6 * CW);   // [2 parity][C*W][RSIM_DLMAX] listed holder counts
+    const int BCd = 1 << P.dbclog2;
+    DetView DV{P.dtr, P.dtkey, P.dglob, P.dbk + (size_t)cta * P.dT * BCd * 3, P.dtot + (size_t)cta * BCd * 2, cta == 0};
+    if (det && P.dsm) {                                    // tracks in shared memory (one copy per CTA)
+        DV.tr = (DTrack *)(ecnt + 2 * CW * RSIM_DLMAX); DV.key = (const u64 *)(DV.tr + P.dT); DV.g = dctl->g;
+    }
+    const bool det_run = det && mode == MODE_REPLAY && k0 < k1;
 
     {   // load this CTA's instance shard
         const u64 *src = (const u64 *)(P.inst + base);
@@ -788,17 +818,26 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; WB.fin.dnf = 0; WB.fin.npark = 0; WB.fin.tpn = 0; }
     if (threadIdx.x == 0) {
         // detector mode: every instance warp also arrives (release) after its plain shared-memory stores
-        mbar_init(&mb[0], det ? 1 + W : 1); mbar_init(&mb[1], det ? 1 + W : 1); mbar_init(&dmb[0], 1); mbar_init(&dmb[1], 1);
+        mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_init(&dmb[0], 1); mbar_init(&dmb[1], 1);
         mbar_init(&mb0[0], 1); mbar_init(&mb0[1], 1);
-        if (det) { mbar_init(&dctl->mbd[0], W); mbar_init(&dctl->mbd[1], W); }
+        if (det) { mbar_init(&dctl->mbd[0], 1); mbar_init(&dctl->mbd[1], 1); }
         mbar_fence_init();
         ctl[0] = k0;
     }
     if (mode != MODE_DRAIN)
         for (int T = threadIdx.x; T < RSIM_MODTAB; T += blockDim.x) modtab[T] = T > 1 ? mod_counter(c0_lo, c0_hi, (u32)T) : 0u;
-    if (det && mode == MODE_REPLAY && k0 < k1) {
-        for (int i = threadIdx.x; i < 2 * RSIM_DLMAX; i += blockDim.x) (&dctl->cnt[0][0])[i] = 0u;
-        if (control) det_prepare(P, *dctl, k0, P.arrival[k0], lane);   // verdict + holder list of k0
+    if (det_run) {
+        if (P.dsm) {                                        // detector state -> shared memory
+            const int words = P.dT * (int)(sizeof(DTrack) / 8);
+            for (int i = threadIdx.x; i < words; i += blockDim.x) ((i64 *)DV.tr)[i] = ((const i64 *)P.dtr)[i];
+            for (int i = threadIdx.x; i < P.dT; i += blockDim.x) ((u64 *)DV.key)[i] = P.dtkey[i];
+            for (int i = threadIdx.x; i < DG_N; i += blockDim.x) DV.g[i] = P.dglob[i];
+        }
+        __syncthreads();
+        if (control) {                                      // verdict + list of k0
+            det_prepare(P, DV, *dctl, P.arrival[k0], P.dtid[k0], P.dtw[P.dtid[k0]], lane);
+            if (lane == 0) dctl->list_seq = (k0 << 8) | dctl->nl;
+        }
     }
     __syncthreads();
     if (C > 1) cluster_sync_all();
@@ -823,6 +862,9 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         // ---- control warp: stage ahead, then per decision wait for the partials and decide
         u32 mb_phase = 0u;                                  // bit p: phase of mbarrier mb[p]
         u32 mbd_phase = 0u;                                 // bit p: phase of the detector barrier mbd[p]
+        int det_hb = 0, det_code = 0;                       // decision k's chosen hit blocks, branch
+        i64 det_pc = 0, det_nh = 0, det_psum = 0;           // its product; holders; holder-free product sum
+        u64 det_pmin = ~0ULL;
         i64 staged = k0;
         auto stage_upto = [&](i64 lim) {
             lim = min(lim, k1);
@@ -840,7 +882,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             const bool lin_dyn = FILTER && P.policy == 3 && !(P.bsn > 0);   // linear with the per-decision bs max
             if (lane == 0) {
                 if (lin_dyn) mbar_arrive_expect(&mb0[par], (u32)(CW * 16));
-                mbar_arrive_expect(&mb[par], (u32)(CW * (FILTER && P.policy == 4 ? 32 : 16)));
+                mbar_arrive_expect(&mb[par], (u32)(CW * (FILTER && P.policy == 4 ? 32 : det ? 64 : 16)));
+                if (det) mbar_arrive_expect(&dctl->mbd[par], (u32)(CW * 16 * ((dctl->nl + 15) >> 4)));
             }
             while (!mbar_try_wait(&mb[par], (mb_phase >> par) & 1u)) { }
             mb_phase ^= 1u << par;
@@ -852,6 +895,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             if (tlc) tlc[0] = globaltimer();
 #endif
             if (det) {     // verdict(k) -> argmin branch (policies.py:222-236), then observe(k) before the release
+                fence_cluster();                            // the warps' buffers behind their st.async (release)
                 const Part *dp = dpart + par * 3 * CW;
                 i64 nh = 0, psum = 0;
                 u64 pmin = ~0ULL;
@@ -862,28 +906,19 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 nh = warp_sum(nh); psum = warp_sum(psum); pmin = warp_min_u64(pmin);
                 const int v = dctl->verdict;
                 const int code = v == 2 ? 3 : (v == 1 && nh < P.N ? 2 : 0);   // fail open when all hold
+                det_code = code;
                 decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, false,
                              code ? dp + (code - 2) * CW : nullptr, code);
                 __syncwarp();
-                while (!mbar_try_wait(&dctl->mbd[par], (mbd_phase >> par) & 1u)) { }   // listed holders counted
-                mbd_phase ^= 1u << par;
                 const Dec d = dec[par];
-                if (!d.err && d.owner_warp >= 0) {
-                    const WarpBuf &OB = wbuf[d.owner_warp];
-                    const int s = nth_set_bit(OB.tm[code], d.kk);
-                    const ReqStage &Rk = rq[k % RSIM_SLOTS];
-                    const int hb = OB.hit[s];
-                    i64 ht = (i64)hb * P.bs; if (ht > Rk.in) ht = Rk.in;
-                    if (P.ddbg != nullptr && lane == 0) {
-                        i64 *g = P.ddbg + (8 + P.N) * k;
-                        g[0] = code; g[1] = nh; g[2] = (i64)pmin; g[3] = psum; g[4] = ht; g[5] = OB.prod[s];
-                        g[6] = hb >= dctl->w; g[7] = dctl->nl;
-                    }
-                    det_observe(P, *dctl, k, Rk.t, lane, ht, hb >= dctl->w, OB.prod[s], nh, pmin, psum, dctl->cnt[par]);
-                    for (int i = lane; i < dctl->nl; i += 32) dctl->cnt[par][i] = 0u;
-                    __syncwarp();
-                    if (k + 1 < k1) det_prepare(P, *dctl, k + 1, P.arrival[k + 1], lane);
+                if (!d.err && d.oflat >= 0) {             // the chosen instance, before its warp moves on
+                    const u32 oc = (u32)(d.oflat / W);
+                    const WarpBuf &OB = wbuf[d.oflat % W];   // (the owner CTA's copy, read through DSMEM)
+                    const int s = nth_set_bit(dsm_ld_u32(&OB.tm[code], oc), d.okk);
+                    det_hb = (int)dsm_ld_u32(&OB.hit[s], oc);
+                    det_pc = (i64)dsm_ld_u64(&OB.prod[s], oc);
                 }
+                det_nh = nh; det_pmin = pmin; det_psum = psum;
             } else {
                 decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, FILTER && P.policy == 4);
             }
@@ -894,6 +929,38 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             __syncwarp();
             if (lane == 0) mbar_arrive(&dmb[par]);          // release decision k to the instance warps
             if (dec[par].err) break;
+            if (det) {     // observe(k) and verdict / list of k+1 while the warps work on k+1
+                DIAG(const long long tdw0 = clock64());
+                while (!mbar_try_wait(&dctl->mbd[par], (mbd_phase >> par) & 1u)) { }   // listed holders counted
+                mbd_phase ^= 1u << par;
+                fence_cluster();
+                const ReqStage &Rk = rq[k % RSIM_SLOTS];
+                i64 ht = (i64)det_hb * P.bs; if (ht > Rk.in) ht = Rk.in;
+                const int nl = dctl->nl;
+                for (int j = lane; j < nl; j += 32) {       // listed holders, summed over the cluster's warps
+                    u32 c = 0;
+                    for (int w = 0; w < CW; w++) c += ecnt[((size_t)par * CW + w) * RSIM_DLMAX + j];
+                    dctl->cnt[j] = c;
+                }
+                __syncwarp();
+                if (P.ddbg != nullptr && lane == 0 && cta == 0) {
+                    i64 *g = P.ddbg + (8 + P.N) * k;
+                    g[0] = det_code; g[1] = det_nh; g[2] = (i64)det_pmin; g[3] = det_psum; g[4] = ht; g[5] = det_pc;
+                    g[6] = det_hb >= Rk.dw; g[7] = nl;
+                }
+                DIAG(const long long tdw1 = clock64());
+                det_observe(P, DV, *dctl, Rk.dtid, Rk.t, lane, ht, det_hb >= Rk.dw, det_pc, det_nh, det_pmin, det_psum,
+                            dctl->cnt);
+                DIAG(const long long tdw2 = clock64());
+                if (k + 1 < k1) {
+                    const ReqStage &Rn = rq[(k + 1) % RSIM_SLOTS];   // staged (slots up to k-2+RSIM_SLOTS)
+                    det_prepare(P, DV, *dctl, Rn.t, Rn.dtid, Rn.dw, lane);
+                    __threadfence_block();
+                    if (lane == 0) *(volatile i64 *)&dctl->list_seq = ((k + 1) << 8) | dctl->nl;
+                }
+                DIAG(if (prof && lane == 0) { atomicAdd(P.ctr + 38, (u64)(tdw1 - tdw0)); atomicAdd(P.ctr + 39, (u64)(tdw2 - tdw1));
+                                              atomicAdd(P.ctr + 40, (u64)(clock64() - tdw2)); atomicAdd(P.ctr + 41, (u64)(nl > 0)); });
+            }
             // every warp published k, so it committed k-1 and ran the touch + pin of k-2
             // (which reads its request's staged keys): slots of decisions < k-1 are free
             stage_upto(k - 2 + RSIM_SLOTS);
@@ -985,10 +1052,11 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 tmask_bs = __ballot_sync(FULL, lane < nmine && bits_bs == wmin_bs && wmin_bs != ~0ULL);
             }
             u32 det_keep = 0u;
+            int det_nl = 0;          // |list| of decision k (the control warp rewrites it for k+1 once
+                                     // every warp has sent k's counts)
             if (det) {     // detector partials (rsim_detector.cuh): plain stores + a release arrive (C == 1)
-                const DetCtl &dc = *dctl;
                 const bool cand = lane < nmine;
-                const bool held = cand && WB.hit[lane] >= dc.w;          // holders of class(k)
+                const bool held = cand && WB.hit[lane] >= R.dw;          // holders of class(k)
                 const u64 bx = (cand && !held) ? mybits : ~0ULL;
                 const u64 bl = cand ? (u64)__double_as_longlong((double)WB.bsv[lane]) : ~0ULL;
                 const u64 pn = (cand && !held) ? (u64)WB.prod[lane] : ~0ULL;
@@ -999,15 +1067,15 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 const u32 nhw = (u32)__popc(__ballot_sync(FULL, held));
                 det_keep = tx | tl;
                 if (P.ddbg != nullptr && cand) P.ddbg[(8 + P.N) * k + 8 + base + l0 + lane] = held ? -2 : WB.prod[lane];
-                if (lane == 0) {
-                    WB.tm[0] = tmask; WB.tm[1] = tmask_bs; WB.tm[2] = tx; WB.tm[3] = tl;
-                    Part *dp = dpart + par * 3 * CW + warp;
-                    *reinterpret_cast<ulonglong2 *>(dp) = make_ulonglong2(mx, ((u64)nhw << 32) | (u32)__popc(tx));
-                    *reinterpret_cast<ulonglong2 *>(dp + CW) = make_ulonglong2(ml, (u64)(u32)__popc(tl));
-                    *reinterpret_cast<ulonglong2 *>(dp + 2 * CW) = make_ulonglong2(mp, (u64)ps);
-                }
+                if (lane == 0) { WB.tm[0] = tmask; WB.tm[1] = tmask_bs; WB.tm[2] = tx; WB.tm[3] = tl; }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&mb[par]);
+                fence_cluster();                            // WB.tm / hit / prod before the partials (release)
+                Part *dp = dpart + par * 3 * CW + cta * W + warp;
+                if (lane < C) {
+                    st_async_16(dp, &mb[par], (u32)lane, mx, ((u64)nhw << 32) | (u32)__popc(tx));
+                    st_async_16(dp + CW, &mb[par], (u32)lane, ml, (u64)(u32)__popc(tl));
+                    st_async_16(dp + 2 * CW, &mb[par], (u32)lane, mp, (u64)ps);
+                }
             }
             {   // publish this warp's partial(s) to every CTA of the cluster
                 const u64 w1 = ((u64)(u32)WB.werr << 32) | (u32)__popc(tmask);
@@ -1034,15 +1102,27 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
 #endif
             apply_deferred(P, WB.fin, lane, &WB.werr);      // parked finisher cache work (before any commit)
             flush_touch_pin(P, WB.fin, lane, &WB.werr);     // the previous commit's touch + pin
-            if (det) {     // holders of the listed tracks on the tables as of t_k (before any advance)
+            if (det) {     // the control warp lists decision k's tracks after observe(k-1)
+                i64 lw;
+                while (((lw = *(volatile i64 *)&dctl->list_seq) >> 8) < k) { }
+                __threadfence_block();
+                // past k already: k's list was empty (a listed decision waits for every warp's counts)
+                det_nl = (lw >> 8) == k ? (int)(lw & 0xff) : 0;
+            }
+            if (det && det_nl > 0) {     // holders of the listed tracks on the tables as of t_k (before any advance)
                 const DetCtl &dc = *dctl;
-                for (int j = 0; j < dc.nl; j++) {
-                    const bool hd = lane < nmine && det_holds(P, dc.lst[j], base + l0 + lane);
+                const int nl = det_nl, nch = (nl + 15) >> 4;
+                for (int j = 0; j < nch * 16; j++) {
+                    const bool hd = j < nl && lane < nmine && det_holds(P, dc.lst[j], base + l0 + lane);
                     const u32 c = (u32)__popc(__ballot_sync(FULL, hd));
-                    if (lane == 0 && c) atomicAdd(&dctl->cnt[par][j], c);
+                    if (lane == 0) WB.ecs[j] = (unsigned char)c;
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&dctl->mbd[par]);
+                for (int q = 0; q < nch; q++) {
+                    const ulonglong2 v = lds_v2u64(WB.ecs + 16 * q);
+                    if (lane < C) st_async_16(ecnt + ((size_t)par * CW + cta * W + warp) * RSIM_DLMAX + 16 * q,
+                                              &dctl->mbd[par], (u32)lane, v.x, v.y);
+                }
             }
             if (mode == MODE_REPLAY && k + 1 < k1) {
                 if (staged_seen <= k + 1) { staged_seen = ctl[0]; __threadfence_block(); }
@@ -1109,6 +1189,11 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
 #undef DIAG
     // write back
     __syncthreads();
+    if (det_run && P.dsm && cta == 0) {
+        const int words = P.dT * (int)(sizeof(DTrack) / 8);
+        for (int i = threadIdx.x; i < words; i += blockDim.x) ((i64 *)P.dtr)[i] = ((const i64 *)DV.tr)[i];
+        for (int i = threadIdx.x; i < DG_N; i += blockDim.x) P.dglob[i] = DV.g[i];
+    }
     {
         u64 *dst = (u64 *)(P.inst + base);
         const u64 *src = (const u64 *)st;

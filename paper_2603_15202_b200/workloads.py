@@ -60,6 +60,14 @@ def hotspot(n_instances: int = 16, n_requests: int = 3000, hot_fraction: float =
                                                           seed=seed)
 
 
+def hotspot_detector(n_instances: int = 64, n_requests: int = 20_000, window_s: float = 5.0, seed: int = 0):
+    """``hotspot`` at 2.5 req/s per instance with the reference detector on (detector.py)."""
+    import dataclasses
+    from .config import DetectorConfig
+    trace, cfg = hotspot(n_instances, n_requests, 0.6, 2.5 * n_instances, seed=seed)
+    return trace, dataclasses.replace(cfg, detector=DetectorConfig(window_s=window_s))
+
+
 def config4_large(n_requests: int = 1_000_000, seed: int = 0):
     """4096 instances, ~1M requests at 3 req/s/instance (SURVEY cfg 4)."""
     return chat_cluster(4096, n_requests, 3.0, seed)

@@ -87,6 +87,10 @@ for c, w in shapes:
         print(f"{name} ctas={c} warps={w}: skipped ({exc})")
         continue
     h.load(trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.request_id, trace.blk_off, trace.blocks)
+    if cfg.detector is not None:
+        from paper_2603_15202_b200.cluster import detector_classes
+        tid, off, ln, key = detector_classes(trace, cfg.detector.class_key_blocks)
+        h.load_detector(tid, off, ln, key, 1 << 16)
     h.rerun()
     best = min(h.rerun() for _ in range(3))
     if os.environ.get("RSIM_CRIT"):
@@ -115,6 +119,10 @@ for c, w in shapes:
         if sc[19] or sc[20]:
             print(f"   decide sections (CTA 0 control warp, cyc/decision): load+min {sc[19] / len(trace):.0f}  "
                   f"ties+index {sc[20] / len(trace):.0f}  owner {sc[21] / len(trace):.0f}", flush=True)
+        if sc[22] or sc[23]:
+            print(f"   detector (CTA 0 control warp, cyc/decision): listed-holder wait {sc[22] / len(trace):.0f}  "
+                  f"observe {sc[23] / len(trace):.0f}  prepare {sc[24] / len(trace):.0f}; decisions with a list "
+                  f"{sc[25] / len(trace):.2f}", flush=True)
         kinds = ["finishing", "other full", "pure decode"]
         print("   step kinds: " + "  ".join(f"{kinds[i]} {sc[8 + 2 * i]} x {sc[9 + 2 * i] / max(sc[8 + 2 * i], 1):.0f} cyc"
                                           for i in range(3)), flush=True)
