@@ -44,11 +44,13 @@ struct DetCtl {                        // control warp -> instance warps, decisi
     u64 mbd[2];                        // [parity] the instance warps counted the listed holders
     i64 list_seq;                      // (decision << 8) | nl: the list below belongs to that decision
     i64 pad_;
+    u64 own[2][2];                     // [parity] (hit blocks, product) of the chosen instance, sent by its warp
     int verdict, w, nl, nrow;          // 0 none / 1 exclude holders / 2 force least_bs; w_k; |lst|; rows
     int lst[RSIM_DLMAX];               // tracks whose holders the instance warps count
     u32 cnt[RSIM_DLMAX];               // holder counts of lst, summed over the cluster's warps
     i64 g[DG_N + 1];                   // detector scalars while the replay runs
 };
+static_assert(sizeof(DetCtl) % 16 == 0 && offsetof(DetCtl, own) % 16 == 0, "st.async targets are 16-B aligned");
 
 __device__ __forceinline__ bool det_rank_before(const DTrack &a, u64 ka, const DTrack &b, u64 kb) {
     if (a.wh != b.wh) return a.wh > b.wh;          // sorted by (-hits, -count, key), detector.py:210-213

@@ -103,21 +103,6 @@ __device__ __forceinline__ void st_async_16(const void *local_dst, const u64 *lo
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.u64 [%0], {%1, %2}, [%3];"
                  :: "r"(rd), "l"(a), "l"(b), "r"(rm) : "memory");
 }
-// loads from CTA `rank`'s shared memory (the detector's read of the owner warp's buffers)
-__device__ __forceinline__ u32 dsm_ld_u32(const void *local, u32 rank) {
-    u32 ra, v;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(local)), "r"(rank));
-    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
-    return v;
-}
-__device__ __forceinline__ u64 dsm_ld_u64(const void *local, u32 rank) {
-    u32 ra;
-    u64 v;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(local)), "r"(rank));
-    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ra) : "memory");
-    return v;
-}
-__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void st_cluster_u64(u32 local_addr, u32 rank, u64 v) {
@@ -883,7 +868,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             if (lane == 0) {
                 if (lin_dyn) mbar_arrive_expect(&mb0[par], (u32)(CW * 16));
                 mbar_arrive_expect(&mb[par], (u32)(CW * (FILTER && P.policy == 4 ? 32 : det ? 64 : 16)));
-                if (det) mbar_arrive_expect(&dctl->mbd[par], (u32)(CW * 16 * ((dctl->nl + 15) >> 4)));
+                // the listed holder counts of every warp + the chosen instance's (hit, product) from its warp
+                if (det) mbar_arrive_expect(&dctl->mbd[par], (u32)(CW * 16 * ((dctl->nl + 15) >> 4) + 16));
             }
             while (!mbar_try_wait(&mb[par], (mb_phase >> par) & 1u)) { }
             mb_phase ^= 1u << par;
@@ -895,7 +881,6 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             if (tlc) tlc[0] = globaltimer();
 #endif
             if (det) {     // verdict(k) -> argmin branch (policies.py:222-236), then observe(k) before the release
-                fence_cluster();                            // the warps' buffers behind their st.async (release)
                 const Part *dp = dpart + par * 3 * CW;
                 i64 nh = 0, psum = 0;
                 u64 pmin = ~0ULL;
@@ -910,14 +895,6 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, false,
                              code ? dp + (code - 2) * CW : nullptr, code);
                 __syncwarp();
-                const Dec d = dec[par];
-                if (!d.err && d.oflat >= 0) {             // the chosen instance, before its warp moves on
-                    const u32 oc = (u32)(d.oflat / W);
-                    const WarpBuf &OB = wbuf[d.oflat % W];   // (the owner CTA's copy, read through DSMEM)
-                    const int s = nth_set_bit(dsm_ld_u32(&OB.tm[code], oc), d.okk);
-                    det_hb = (int)dsm_ld_u32(&OB.hit[s], oc);
-                    det_pc = (i64)dsm_ld_u64(&OB.prod[s], oc);
-                }
                 det_nh = nh; det_pmin = pmin; det_psum = psum;
             } else {
                 decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, FILTER && P.policy == 4);
@@ -933,7 +910,10 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 DIAG(const long long tdw0 = clock64());
                 while (!mbar_try_wait(&dctl->mbd[par], (mbd_phase >> par) & 1u)) { }   // listed holders counted
                 mbd_phase ^= 1u << par;
-                fence_cluster();
+                // the chosen instance's hit blocks and product, pushed by its warp after the release (a read of
+                // the owner's buffers from here would race with that warp moving on to k+1)
+                det_hb = (int)dctl->own[par][0];
+                det_pc = (i64)dctl->own[par][1];
                 const ReqStage &Rk = rq[k % RSIM_SLOTS];
                 i64 ht = (i64)det_hb * P.bs; if (ht > Rk.in) ht = Rk.in;
                 const int nl = dctl->nl;
@@ -1069,7 +1049,6 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 if (P.ddbg != nullptr && cand) P.ddbg[(8 + P.N) * k + 8 + base + l0 + lane] = held ? -2 : WB.prod[lane];
                 if (lane == 0) { WB.tm[0] = tmask; WB.tm[1] = tmask_bs; WB.tm[2] = tx; WB.tm[3] = tl; }
                 __syncwarp();
-                fence_cluster();                            // WB.tm / hit / prod before the partials (release)
                 Part *dp = dpart + par * 3 * CW + cta * W + warp;
                 if (lane < C) {
                     st_async_16(dp, &mb[par], (u32)lane, mx, ((u64)nhw << 32) | (u32)__popc(tx));
@@ -1169,6 +1148,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             if (warp == d.owner_warp) {
                 const int s = nth_set_bit(d.pad == 0 ? tmask : d.pad == 1 ? tmask_bs : WB.tm[d.pad], d.kk);   // d.pad: the branch
                 const int h = WB.hit[s];
+                if (det && lane < C)     // (hit, product) of the chosen instance to every CTA's observe(k)
+                    st_async_16(&dctl->own[par][0], &dctl->mbd[par], (u32)lane, (u64)(u32)h, (u64)WB.prod[s]);
                 int werr = 0;
                 flush_touch_pin(P, WB.fin, lane, &WB.werr);      // (normally already run after the publish)
                 commit(P, st + l0 + s, base + l0 + s, k, h, R.t, R.keys,
