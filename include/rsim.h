@@ -38,7 +38,8 @@ typedef enum {
 } rsim_status;
 
 enum { RSIM_POLICY_MULTIPLICATIVE = 0, RSIM_POLICY_VLLM = 1, RSIM_POLICY_LEAST_BS = 2,
-       RSIM_POLICY_LINEAR = 3, RSIM_POLICY_FILTER = 4 };   /* policies.py:104-192 */
+       RSIM_POLICY_LINEAR = 3, RSIM_POLICY_FILTER = 4,
+       RSIM_POLICY_SIMULATE = 5 };   /* policies.py:104-192; simulate: estimate_ttft_us, policies.py:142-157 */
 enum { RSIM_KV_P_TOKENS = 0, RSIM_KV_ONE_MINUS_HIT = 1 };
 enum { RSIM_BAL_BS = 0, RSIM_BAL_TOTAL_TOKENS = 1 };
 
@@ -91,6 +92,10 @@ typedef struct rsim_config {
     int32_t reserved1;
     double det_window_s;
     double det_consecutive_multiplier;
+    /* simulate policy: Policy.sim_cost_model (policies.py:206-211) -- the CostModel coefficients the
+     * TTFT replay uses (CostModel.scaled(mis_tuned_factor) when mis-tuned, else the engine's own) */
+    double sim_prefill_base_ms, sim_prefill_per_token_ms;
+    double sim_decode_base_ms, sim_decode_per_seq_ms, sim_decode_per_ctx_token_ms;
 } rsim_config;
 
 typedef struct rsim rsim_t;

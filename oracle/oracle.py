@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-POLICY_CODE = {"multiplicative": 0, "vllm": 1, "least_bs": 2, "linear": 3, "filter": 4}
+POLICY_CODE = {"multiplicative": 0, "vllm": 1, "least_bs": 2, "linear": 3, "filter": 4, "simulate": 5}
 
 
 class _Cfg(C.Structure):
@@ -38,6 +38,7 @@ class _Cfg(C.Structure):
         ("staleness_us", C.c_int64),
         ("det_on", C.c_int32), ("det_top_k", C.c_int32), ("det_kb", C.c_int32), ("det_force", C.c_int32),
         ("det_mean", C.c_int32), ("det_pad", C.c_int32), ("det_window_s", C.c_double), ("det_mult", C.c_double),
+        ("spb", C.c_double), ("spt", C.c_double), ("sdb", C.c_double), ("sds", C.c_double), ("sdc", C.c_double),
     ]
 
 
@@ -95,6 +96,16 @@ def _stable_key(*vals: int) -> int:
     return acc
 
 
+def sim_cost_coefficients(config) -> tuple:
+    """Policy.sim_cost_model (policies.py:206-211): CostModel.scaled(mis_tuned_factor)
+    (engine.py:70-79) when mis-tuned, else the engine's own coefficients."""
+    cm, pol = config.cost_model, config.policy
+    f = float(pol.mis_tuned_factor) if getattr(pol, "mis_tuned", False) else None
+    c = (cm.prefill_base_ms, cm.prefill_per_token_ms, cm.decode_base_ms, cm.decode_per_seq_ms,
+         cm.decode_per_ctx_token_ms)
+    return tuple(float(x) * f if f is not None else float(x) for x in c)
+
+
 def make_cfg(config) -> _Cfg:
     cm, cache, pol = config.cost_model, config.cache, config.policy
     if pol.kind not in POLICY_CODE:
@@ -115,7 +126,7 @@ def make_cfg(config) -> _Cfg:
                 float(pol.bs_norm_cap) if getattr(pol, "bs_norm_cap", None) is not None else 0.0,
                 int(getattr(pol, "range_threshold", 4)),
                 int(round(float(getattr(config, "staleness_ms", 0.0)) * 1000.0)),   # cluster.py:77
-                *dv)
+                *dv, *sim_cost_coefficients(config))
 
 
 class OracleError(RuntimeError):
@@ -175,6 +186,8 @@ def run_oracle(trace, config, *, with_log: bool = False, time_routes: bool = Fal
         raise OracleError("CacheFullError")
     if rc == -4:
         raise ValueError("class_key needs at least one block")
+    if rc == -5:
+        raise RuntimeError("TTFT replay did not converge")
     if det_on and summary[5] > rows_cap:
         return run_oracle(trace, config, with_log=with_log, time_routes=time_routes, _log_cap=_log_cap,
                           _rows_cap=int(summary[5]))

@@ -63,6 +63,9 @@ class Config(C.Structure):
         ("det_on", C.c_int32), ("det_top_k_classes", C.c_int32), ("det_class_key_blocks", C.c_int32),
         ("det_mitigation", C.c_int32), ("det_compare_mean_non_holder", C.c_int32), ("reserved1", C.c_int32),
         ("det_window_s", C.c_double), ("det_consecutive_multiplier", C.c_double),
+        ("sim_prefill_base_ms", C.c_double), ("sim_prefill_per_token_ms", C.c_double),
+        ("sim_decode_base_ms", C.c_double), ("sim_decode_per_seq_ms", C.c_double),
+        ("sim_decode_per_ctx_token_ms", C.c_double),
     ]
 
 

@@ -30,7 +30,7 @@ from .hashing import MASK64, stable_key
 from .report import DetectorRow, RoutingDecision, RunReport
 from .trace import PackedTrace, TraceRecord, validate_against_block_size
 
-_POLICY = {"multiplicative": 0, "vllm": 1, "least_bs": 2, "linear": 3, "filter": 4}
+_POLICY = {"multiplicative": 0, "vllm": 1, "least_bs": 2, "linear": 3, "filter": 4, "simulate": 5}
 INT64_MAX = (1 << 63) - 1
 
 
@@ -131,6 +131,13 @@ def native_config(config: ClusterConfig, sizing: Sizing, *, device: int = 0, rec
     c.range_threshold = pol.range_threshold
     c.staleness_us = staleness_us(config)
     c.history_capacity = sizing.history_capacity
+    # Policy.sim_cost_model (policies.py:206-211): the TTFT replay's coefficients
+    scm = cm.scaled(pol.mis_tuned_factor) if pol.mis_tuned else cm
+    c.sim_prefill_base_ms = scm.prefill_base_ms
+    c.sim_prefill_per_token_ms = scm.prefill_per_token_ms
+    c.sim_decode_base_ms = scm.decode_base_ms
+    c.sim_decode_per_seq_ms = scm.decode_per_seq_ms
+    c.sim_decode_per_ctx_token_ms = scm.decode_per_ctx_token_ms
     det = config.detector
     if det is not None:
         c.det_on = 1

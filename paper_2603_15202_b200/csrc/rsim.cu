@@ -87,6 +87,7 @@ struct rsim {
     Run *runs = nullptr;
     int rlog2 = 0;
     HEnt *hring = nullptr;   // view-history rings (staleness > 0)
+    int4 *simj = nullptr;    // simulate: per-warp lists of requests joining the TTFT replay's decode set
     int hlog2 = 0;
     // hotspot detector (rsim_detector.cuh): classes loaded by rsim_load_detector
     DevArr<int> dtid, dtw;
@@ -151,6 +152,9 @@ static Params make_params(rsim_t *h) {
     P.epoch = h->epoch;
     P.runs = h->runs; P.rlog2 = h->rlog2; P.arena = h->arena.p;
     P.stal = h->cfg.staleness_us; P.hring = h->hring; P.hlog2 = h->hlog2;
+    P.simj = h->simj;
+    P.spb = h->cfg.sim_prefill_base_ms; P.spt = h->cfg.sim_prefill_per_token_ms; P.sdb = h->cfg.sim_decode_base_ms;
+    P.sds = h->cfg.sim_decode_per_seq_ms; P.sdc = h->cfg.sim_decode_per_ctx_token_ms;
     P.dtid = (h->cfg.det_on && h->det_loaded) ? h->dtid.p : nullptr;
     P.dtw = h->dtw.p; P.dtex = h->dtex.p; P.dtkey = h->dtkey.p; P.dtr = h->dtr.p;
     P.dbk = h->dbk.p; P.dtot = h->dtot; P.dglob = h->dglob; P.drows = h->drows.p; P.drows_cap = h->drows_cap;
@@ -242,14 +246,15 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (c.block_size < 1) return fail(nullptr, RSIM_E_INVALID, "block_size must be >= 1");
     if (c.capacity_blocks == 0 || c.capacity_blocks < -1) return fail(nullptr, RSIM_E_INVALID, "capacity_blocks must be >= 1 or -1");
     if (c.chunk_tokens < 1 || c.max_batch_requests < 1) return fail(nullptr, RSIM_E_INVALID, "chunk_tokens and max_batch_requests must be >= 1");
-    if (c.policy < 0 || c.policy > 4) return fail(nullptr, RSIM_E_UNSUPPORTED, "policy %d not on the device path", c.policy);
+    if (c.policy < 0 || c.policy > 5) return fail(nullptr, RSIM_E_UNSUPPORTED, "policy %d not on the device path", c.policy);
     if (c.staleness_us < 0) return fail(nullptr, RSIM_E_INVALID, "staleness_us must be >= 0");
     if (c.det_on) {
         if (!(c.det_window_s > 0) || c.det_top_k_classes < 1 || c.det_class_key_blocks < 1 ||
             c.det_mitigation < 0 || c.det_mitigation > 1)
             return fail(nullptr, RSIM_E_INVALID, "invalid detector configuration");
         if (c.world > 1) return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector is single-rank on the device path");
-        if (c.policy == RSIM_POLICY_FILTER || (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0)))
+        if (c.policy == RSIM_POLICY_FILTER || c.policy == RSIM_POLICY_SIMULATE ||
+            (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0)))
             return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector runs with multiplicative, vllm, least_bs or capped linear scores");
         if (c.det_window_s > 1e6) return fail(nullptr, RSIM_E_UNSUPPORTED, "detector window longer than 1e6 s");
     }
@@ -343,6 +348,8 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
         h->hlog2 = std::max(4, std::min(24, ilog2_ceil(c.history_capacity > 0 ? c.history_capacity : 1024)));
         CK(nullptr, cudaMalloc(&h->hring, ((size_t)N << h->hlog2) * sizeof(HEnt)));
     }
+    if (c.policy == RSIM_POLICY_SIMULATE)   // <= one joined entry per queued request ahead of the candidate
+        CK(nullptr, cudaMalloc(&h->simj, ((size_t)(h->C * h->W) << h->qlog2) * sizeof(int4)));
     CK(nullptr, cudaMalloc(&h->tie, 2 * sizeof(u64)));
     CK(nullptr, cudaMalloc(&h->errbuf, 4 * sizeof(int)));
     CK(nullptr, cudaMalloc(&h->flag, sizeof(int)));
@@ -374,7 +381,7 @@ void rsim_destroy(rsim_t *h) {
     h->hit_blocks.free_(); h->chosen.free_();
     void *ps[] = {h->inst, h->qbuf, h->rbuf, h->tkeys, h->tmeta, h->tie, h->errbuf, h->flag, h->log, h->log_n,
                   h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs, h->crit, h->hring,
-                  h->dtot, h->dglob};
+                  h->dtot, h->dglob, h->simj};
     h->ddbg.free_(); h->dtid.free_(); h->dtw.free_(); h->dtex.free_(); h->dbk.free_(); h->drows.free_(); h->dtkey.free_(); h->dtr.free_();
     h->arena.free_();
     for (int i = 0; i < 8; i++) if (h->peer_ipc[i] && h->peer[i]) cudaIpcCloseMemHandle(h->peer[i]);
@@ -484,7 +491,8 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     CK(h, cudaEventRecord(h->ev0, h->stream));
     const bool filt = h->cfg.policy == RSIM_POLICY_FILTER ||            // the extended kernel: two-branch or
                       (h->cfg.policy == RSIM_POLICY_LINEAR && !(h->cfg.bs_norm_cap > 0)) ||   // two-round decisions,
-                      h->cfg.staleness_us > 0 || h->cfg.det_on;                             // stale snapshots, detector
+                      h->cfg.staleness_us > 0 || h->cfg.det_on ||                           // stale snapshots, detector,
+                      h->cfg.policy == RSIM_POLICY_SIMULATE;                                // TTFT replays
     if (h->W <= RSIM_LEAN_WARPS && !filt)
         CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_LEAN_WARPS, false>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
     else if (!filt)

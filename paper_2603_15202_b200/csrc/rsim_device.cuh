@@ -134,6 +134,9 @@ struct Params {
     int dT, dtopk, dforce, dmean, dbclog2;
     int dsm;                           // 1: the replay keeps tracks in shared memory
     i64 *ddbg;                         // diagnostics: 8 words per decision (rsim_detector_debug), null = off
+    // simulate policy (policies.py:142-157, engine.py:419-460): the sim cost model and per-warp scratch
+    double spb, spt, sdb, sds, sdc;
+    int4 *simj;                        // [C*W][Qcap] (start step, last step, ctx at start, -) of joined requests
 };
 
 // ---------------- hashing (hashing.py:15-25) ----------------

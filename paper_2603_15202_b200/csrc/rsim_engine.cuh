@@ -23,6 +23,99 @@ __device__ __forceinline__ i64 decode_cost_us(const Params &P, i64 n, i64 ctx) {
     return __double2ll_rn(__dmul_rn(x, 1000.0));
 }
 
+// ---------------- simulate policy: TTFT replay (engine.py:419-460) ----------------
+// estimate_first_token_us over sched_clone (engine.py:376-391) of instance gi, warp-wide:
+// the live queue (ring, pending as of now) and running list replayed forward step by step
+// under the policy's cost model (Policy.sim_cost_model, policies.py:206-211) with the
+// candidate (pending max(cand, 1), in 0, out 1) appended FIFO-last; returns the absolute
+// time of the candidate's first token (-1 past _REPLAY_STEP_CAP). Nothing is written back.
+// Decode set at replay step s (running <= max_batch, so decode == running): a running
+// entry with finish step v decodes in steps 0 .. v - step_idx with context
+// in + out - (v - step_idx + 1) + s; a request popped at step j with out > 1 joins for
+// steps j+1 .. j+out-1 with context in + 1 + (s - j - 1) (kept in the warp's scratch jb).
+__device__ __forceinline__ i64 sim_prefill_us(const Params &P, i64 tok) {
+    if (tok <= 0) return 0;
+    return __double2ll_rn(__dmul_rn(__dadd_rn(P.spb, __dmul_rn(P.spt, __ll2double_rn(tok))), 1000.0));
+}
+__device__ __forceinline__ i64 sim_decode_us(const Params &P, i64 n, i64 ctx) {
+    if (n <= 0) return 0;
+    const double x = __dadd_rn(__dadd_rn(P.sdb, __dmul_rn(P.sds, __ll2double_rn(n))), __dmul_rn(P.sdc, __ll2double_rn(ctx)));
+    return __double2ll_rn(__dmul_rn(x, 1000.0));
+}
+__device__ __noinline__ i64 sim_first_token(const Params &P, const Inst *sp, int gi, i64 now, i64 cand, int lane,
+                                            int4 *jb) {
+    const i64 S = sp->step_idx;
+    const int nr = sp->r, q = sp->q, qh0 = sp->q_head;
+    const QEnt *qb = P.qbuf + ((size_t)gi << P.qlog2);
+    const REnt *rb = P.rbuf + (size_t)gi * (size_t)P.max_batch;
+    const u32 qmask = (1u << P.qlog2) - 1u;
+    const i64 pc = cand > 1 ? cand : 1;
+    i64 t = now > sp->busy_until ? now : sp->busy_until;
+    int qpos = 0;                                   // first queue entry not yet popped (q = the candidate)
+    i64 hrem = q > 0 ? qb[qh0 & qmask].v : pc;      // its pending
+    int nj = 0;                                     // joined requests in jb
+    for (int s = 0; s < 10000000; s++) {            // _REPLAY_STEP_CAP
+        i64 n = 0, ctx = 0;
+        for (int i = lane; i < nr; i += 32) {
+            const i64 er = rb[i].v - S;             // last replay step this entry decodes in
+            if (er >= s) { n++; ctx += rb[i].in + (i64)rb[i].out - (er + 1) + s; }
+        }
+        for (int i = lane; i < nj; i += 32) {
+            const int4 j = jb[i];
+            if (j.x <= s && s <= j.y) { n++; ctx += (i64)j.z + (s - j.x); }
+        }
+        n = warp_sum(n); ctx = warp_sum(ctx);
+        const i64 budget0 = P.chunk - n > 0 ? P.chunk - n : 0;   // engine.py:436-440
+        const i64 slots = P.max_batch - n;
+        // _plan_allocations over entries qpos.. (engine.py:174-184): entry j is allocated iff
+        // j - qpos < slots and the budget left before it is positive; allocations form a prefix,
+        // all popped (take == pending) except possibly the last
+        i64 ptok = 0, spent = 0, nrem = -1;
+        int npop = 0;
+        bool cand_done = false;
+        for (int w0 = qpos; w0 <= q; w0 += 32) {
+            const int j = w0 + lane;
+            const bool ex = j <= q;
+            i64 p = 0;
+            int jin = 0, jout = 1;
+            if (ex) {
+                if (j == q) p = pc;
+                else {
+                    const QEnt &e = qb[(qh0 + j) & qmask];
+                    p = j == qpos ? hrem : e.v; jin = (int)e.in; jout = e.out;
+                }
+                if (j == qpos) p = hrem;
+            }
+            const i64 incl = warp_incl_scan(p, lane);
+            const i64 before = budget0 - (spent + incl - p);
+            const bool alloc = ex && (i64)(j - qpos) < slots && before > 0;
+            const i64 take = alloc ? (before < p ? before : p) : 0;
+            const bool popped = alloc && take == p;
+            const u32 am = __ballot_sync(FULL, alloc), pm = __ballot_sync(FULL, popped);
+            ptok += warp_sum(take);
+            spent += __shfl_sync(FULL, incl, 31);
+            if (__ballot_sync(FULL, popped && j == q)) cand_done = true;
+            // requests that finish prefill join the decode set from the next step (engine.py:452-453)
+            const bool joins = popped && j < q && jout > 1;
+            const u32 jm = __ballot_sync(FULL, joins);
+            if (joins) jb[nj + __popc(jm & lanemask_lt())] = make_int4(s + 1, s + jout - 1, jin + 1, 0);
+            nj += __popc(jm);
+            npop += __popc(pm);
+            const u32 part = am & ~pm;                               // the partially allocated entry
+            if (part) nrem = __shfl_sync(FULL, p - take, __ffs(part) - 1);
+            if (am != FULL) break;                                   // the allocated prefix ended here
+        }
+        const i64 end = t + sim_prefill_us(P, ptok) + sim_decode_us(P, n, ctx);
+        if (cand_done) return end;
+        qpos += npop;
+        if (nrem >= 0) hrem = nrem;
+        else if (npop > 0) hrem = qpos == q ? pc : qb[(qh0 + qpos) & qmask].v;
+        t = end;
+        __syncwarp();
+    }
+    return -1;
+}
+
 __device__ __forceinline__ void flush_view(Inst &s, i64 now) {   // engine.py:240-246
     if (s.due <= now) {
         s.v_r = s.r; s.v_q = s.q; s.v_pend = s.pend; s.v_total = s.total; s.v_dc = s.dcs;

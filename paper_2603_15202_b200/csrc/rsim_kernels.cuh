@@ -511,7 +511,8 @@ __device__ __noinline__ void probe_hits_sparse(const Params &P, int base, int l0
 // handles instance s and returns its score bits (~0 = not a candidate).
 __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, int l0, int n, const ReqStage &R,
                                            int mode, int target, int lane, WarpBuf &WB, u64 &bits_bs, bool filter,
-                                           double bsn, bool stale, const HistHead *hc, bool det = false) {
+                                           double bsn, bool stale, const HistHead *hc, bool det = false,
+                                           int4 *simj = nullptr) {
     const int gi = base + l0 + lane;
     const bool cand = lane < n && ((mode != MODE_ENQUEUE) || gi == target);
     u64 bits = ~0ULL;
@@ -549,6 +550,21 @@ __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, 
         }
         // one 8-B key compare per reference dict lookup + 16 B of view
         cb = 8u * (u32)min(h + 1, R.B) + 16u;
+    }
+    if (simj != nullptr) {     // simulate: float(estimate_first_token_us - now) (policies.py:142-157, 262-267)
+        for (int s = 0; s < n; s++) {
+            const int g = base + l0 + s;
+            if (mode == MODE_ENQUEUE && g != target) continue;          // warp-uniform
+            i64 ht = (i64)WB.hit[s] * P.bs; if (ht > R.in) ht = R.in;
+            const i64 nw = R.in - ht;                                   // Candidate.new_prefill_tokens (>= 1 inside)
+            const i64 ft = sim_first_token(P, st + l0 + s, g, R.t, nw, lane, simj);
+            if (ft < 0 && lane == 0) atomicCAS(P.err, 0, DEV_E_INVARIANT);   // "TTFT replay did not converge"
+            if (lane == s) {
+                const double sc = __ll2double_rn(ft - R.t);
+                bits = (u64)__double_as_longlong(sc);
+                if (P.scores != nullptr) P.scores[g] = sc;
+            }
+        }
     }
     cb = __reduce_add_sync(FULL, cb);
     if (lane == 0) WB.c_bytes += cb;
@@ -1017,7 +1033,9 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             }
             u64 bits_bs;
             const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB, bits_bs,
-                                           FILTER && P.policy == 4, bsn, stale, hhc, det);
+                                           FILTER && P.policy == 4, bsn, stale, hhc, det,
+                                           FILTER && P.policy == 5 ? P.simj + ((size_t)(cta * W + warp) << P.qlog2)
+                                                                   : nullptr);
             PHASE(2);
             DIAG(const long long t_c = clock64());
             if (cta == 0 && warp == 0 && lane == 0) WB.c_bytes += 8ULL * (u64)R.B;   // request chain keys, read once

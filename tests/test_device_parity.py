@@ -69,6 +69,47 @@ def test_chain_keys_kats(native):
     sim.close()
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_random_simulate_configs_match_oracle(native, seed):
+    """The simulate policy (TTFT replay per candidate, policies.py:142-157) on random clusters,
+    cost models (tight chunk / max_batch), capacities and mis-tuned factors vs the oracle
+    (the oracle's simulate is pinned to the reference by the policy_simulate_* fixtures)."""
+    from paper_2603_15202_b200.cluster import run
+    from paper_2603_15202_b200.config import CacheConfig, ClusterConfig, CostModel, PolicyConfig
+    from paper_2603_15202_b200.trace import ClassSpec, SyntheticSpec, generate_synthetic_packed
+    rng = np.random.default_rng(700 + seed)
+    for trial in range(5):
+        n_cls = int(rng.integers(1, 5))
+        w = rng.random(n_cls) + 0.1
+        w = w / w.sum()
+        classes = tuple(ClassSpec(float(x), int(rng.integers(0, 12)),
+                                  (int(a := rng.integers(1, 4)), int(a + rng.integers(0, 6))),
+                                  (1, int(rng.integers(1, 120)))) for x in w)
+        bs = int(rng.choice([4, 16]))
+        spec = SyntheticSpec(float(rng.uniform(5, 30)), float(rng.uniform(5, 90)), classes,
+                             seed=int(rng.integers(0, 1000)), block_size=bs)
+        trace = generate_synthetic_packed(spec)
+        if len(trace) == 0:
+            continue
+        N = int(rng.choice([1, 2, 3, 7, 16, 33, 70]))
+        cap = [None, int(rng.integers(20, 400)), 40000][int(rng.integers(0, 3))]
+        cm = CostModel(float(rng.uniform(0, 8)), float(rng.choice([0.1, 0.0371, 0.05])),
+                       float(rng.uniform(0, 30)), float(rng.uniform(0, 2)), float(rng.choice([0.0, 0.001, 0.0013])),
+                       int(rng.choice([40, 64, 512, 2048])), int(rng.choice([2, 8, 40, 256])))
+        pol = PolicyConfig(kind="simulate", mis_tuned=bool(rng.integers(0, 2)),
+                           mis_tuned_factor=float(rng.choice([4.0, 0.3, 1.7])),
+                           tie_break_seed=int(rng.integers(0, 50)))
+        cfg = ClusterConfig(n_instances=N, cost_model=cm, cache=CacheConfig(bs, cap), policy=pol,
+                            staleness_ms=float(rng.choice([0.0, 3.0])), seed=int(rng.integers(0, 99)))
+        ref = run_oracle(trace, cfg)
+        rep = run(trace, cfg)
+        tag = f"seed{seed}/trial{trial} N={N} cap={cap} chunk={cm.chunk_tokens} mb={cm.max_batch_requests}"
+        assert np.array_equal(rep.chosen, ref.chosen), tag
+        assert np.array_equal(rep.hit_tokens, ref.hit_tokens), tag
+        assert np.array_equal(rep.columns["first_token_us"], ref.first_token_us), tag
+        assert np.array_equal(rep.columns["finish_us"], ref.finish_us), tag
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_random_configs_match_oracle(native, seed):
     """Random cluster sizes, cost models, capacities and policies vs the oracle."""

@@ -74,6 +74,11 @@ CASES = {
     "policy_linear_cap": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=12, policy=PolicyConfig(kind='linear', kv_weight=0.7, bs_norm_cap=6), seed=5))", 1000),
     "policy_filter": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='filter'), seed=6))", 1000),
     "policy_filter_r2": ("(W.config2_api()[0], ClusterConfig(n_instances=16, policy=PolicyConfig(kind='filter', range_threshold=2, tie_break_seed=3), seed=7))", 1500),
+    "policy_simulate": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='simulate'), seed=13))", 1000),
+    "policy_simulate_mistuned": ("(W.config2_api()[0], ClusterConfig(n_instances=16, policy=PolicyConfig(kind='simulate', mis_tuned=True, tie_break_seed=5), seed=14))", 1500),
+    "policy_simulate_factor": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=12, policy=PolicyConfig(kind='simulate', mis_tuned=True, mis_tuned_factor=0.37), staleness_ms=10.0, seed=15))", 1000),
+    "policy_simulate_small_batch": ("(W.config2_api()[0], ClusterConfig(n_instances=4, cost_model=CostModel(1.0, 0.2, 4.0, 0.5, 0.01, 300, 3), cache=CacheConfig(16, 5000), policy=PolicyConfig(kind='simulate'), seed=16))", 800),
+    "policy_simulate_agent_evict": ("(W.config3_agent(600, n_instances=16, capacity=4096, rate_per_instance=1.0)[0], ClusterConfig(n_instances=16, cache=CacheConfig(16, 4096), policy=PolicyConfig(kind='simulate'), seed=17))", None),
     "stale_5ms": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, staleness_ms=5.0, seed=8))", 1000),
     "stale_50ms_n16": ("(W.config2_api()[0], ClusterConfig(n_instances=16, staleness_ms=50.0, seed=9))", 1500),
     "stale_frac_vllm": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, policy=PolicyConfig(kind='vllm'), staleness_ms=12.3456, seed=10))", 1000),
