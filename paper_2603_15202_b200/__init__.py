@@ -20,7 +20,7 @@ INFINITE = None
 def __getattr__(name):
     # the device-backed entry points import librsim lazily so config/trace
     # tooling works on machines without a GPU
-    if name in ("ClusterSim", "run", "AdmissionInfo"):
+    if name in ("ClusterSim", "run", "probe_capacity", "AdmissionInfo"):
         from . import cluster
         return getattr(cluster, name)
     raise AttributeError(name)
@@ -31,6 +31,6 @@ __all__ = [
     "DetectorConfig", "DuplicateRequestError", "INFINITE", "InvariantError", "NoInstancesError", "PackedTrace",
     "PolicyConfig", "RequestMetrics", "RoutingDecision", "RunReport", "StepRecord", "SyntheticSpec",
     "TraceError", "TraceRecord", "UnsupportedConfigError", "chain_keys", "class_key", "combine64",
-    "generate_synthetic", "generate_synthetic_packed", "load_trace", "percentile", "run", "save_trace",
+    "generate_synthetic", "generate_synthetic_packed", "load_trace", "percentile", "probe_capacity", "run", "save_trace",
     "scale_trace", "splitmix64", "stable_key",
 ]

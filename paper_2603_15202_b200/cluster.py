@@ -389,3 +389,31 @@ def run(records, config: ClusterConfig, **kw) -> RunReport:
         return sim.run_trace(records)
     finally:
         sim.close()
+
+
+def probe_capacity(records, config: ClusterConfig, hi_start: float = 8.0, rate_cap: float = 4096.0,
+                   iterations: int = 8, **kw) -> float:
+    """Binary-search the highest arrival rate the cluster sustains (reference
+    cluster.py:295-330, same search and threshold): a rate is sustainable when the
+    queued backlog at the last arrival stays under 2 * n_instances * max_batch_requests.
+    Every probe is a full device replay of the rescaled trace (scale_trace)."""
+    from .trace import scale_packed
+    packed = records if isinstance(records, PackedTrace) else PackedTrace.from_records(list(records))
+    limit = 2 * config.n_instances * config.cost_model.max_batch_requests
+
+    def sustainable(rate: float) -> bool:
+        return run(scale_packed(packed, rate), config, **kw).queued_at_last_arrival < limit
+
+    lo, hi = 0.0, hi_start
+    while sustainable(hi):
+        lo = hi
+        if hi >= rate_cap:
+            return rate_cap
+        hi = min(hi * 2.0, rate_cap)
+    for _ in range(iterations):
+        mid = (lo + hi) / 2.0
+        if sustainable(mid):
+            lo = mid
+        else:
+            hi = mid
+    return lo

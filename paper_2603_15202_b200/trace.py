@@ -245,6 +245,23 @@ def scale_trace(records: Sequence[TraceRecord], target_rate_rps: float) -> list[
     return [dataclasses.replace(r, arrival_s=(r.arrival_s - t0) * factor) for r in records]
 
 
+def scale_packed(trace: "PackedTrace", target_rate_rps: float) -> "PackedTrace":
+    """scale_trace (reference trace.py) on a packed trace: arrival_s' = (arrival_s - t0) * factor
+    with factor = observed rate / target, elementwise in IEEE doubles exactly as the
+    per-record Python arithmetic; arrival_us is re-rounded half-even."""
+    if target_rate_rps <= 0:
+        raise TraceError("target rate must be positive")
+    n = len(trace)
+    if n < 2:
+        raise TraceError("need at least 2 records to measure a rate")
+    span = float(trace.arrival_s[-1]) - float(trace.arrival_s[0])
+    if span <= 0:
+        raise TraceError("trace spans zero time; rate is undefined")
+    factor = ((n - 1) / span) / target_rate_rps
+    arr = (trace.arrival_s - trace.arrival_s[0]) * factor
+    return dataclasses.replace(trace, arrival_s=arr)
+
+
 def validate_against_block_size(trace: PackedTrace, block_size: int) -> None:
     """ceil(in / block_size) must equal the block count (reference trace.py:271-281)."""
     want = -(-trace.in_tokens // block_size)
