@@ -54,3 +54,17 @@ def test_create_without_gpu_fails_loudly():
     with pytest.raises(_native.RsimError) as ei:
         _native.Handle(native_config(ClusterConfig(n_instances=2), Sizing(64, 100)))
     assert ei.value.status == _native.E_CUDA
+
+
+def test_io_library_exports_every_declared_symbol():
+    """librsimio.so (trace codec) exports every entry point include/rsim_io.h declares."""
+    hdr = open(os.path.join(ROOT, "include", "rsim_io.h")).read()
+    names = sorted(set(re.findall(r"^(?:int|void|const char|int64_t)\s*\*?\s*(rsim_\w+)\s*\(", hdr, re.M)))
+    assert "rsim_trace_parse_jsonl" in names and len(names) == 6
+    lib_path = os.path.join(ROOT, "paper_2603_15202_b200", "librsimio.so")
+    if not os.path.exists(lib_path):
+        import __graft_entry__ as g
+        g.build()
+    out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s+(rsim_\w+)", out))
+    assert not [n for n in names if n not in exported]
