@@ -11,8 +11,10 @@ from .config import (CacheConfig, CacheFullError, ClusterConfig, CostModel, Dete
                      InvariantError, NoInstancesError, PolicyConfig, UnsupportedConfigError)
 from .hashing import chain_keys, combine64, splitmix64, stable_key
 from .report import RequestMetrics, RoutingDecision, RunReport, StepRecord, percentile
+from .metrics import export, summarize
 from .trace import (ClassSpec, PackedTrace, SyntheticSpec, TraceError, TraceRecord, class_key,
-                    generate_synthetic, generate_synthetic_packed, load_trace, save_trace, scale_trace)
+                    generate_synthetic, generate_synthetic_packed, load_packed, load_trace, load_trace_packed, save_packed,
+                    save_trace, scale_trace)
 
 INFINITE = None
 
@@ -32,5 +34,5 @@ __all__ = [
     "PolicyConfig", "RequestMetrics", "RoutingDecision", "RunReport", "StepRecord", "SyntheticSpec",
     "TraceError", "TraceRecord", "UnsupportedConfigError", "chain_keys", "class_key", "combine64",
     "generate_synthetic", "generate_synthetic_packed", "load_trace", "percentile", "probe_capacity", "run", "save_trace",
-    "scale_trace", "splitmix64", "stable_key",
+    "scale_trace", "splitmix64", "stable_key", "export", "summarize", "load_trace_packed", "save_packed", "load_packed",
 ]

@@ -69,6 +69,24 @@ def test_chain_keys_kats(native):
     sim.close()
 
 
+@pytest.mark.parametrize("n,ctas", [(600, 0), (1024, 16)])
+def test_detector_large_cluster_matches_oracle(native, n, ctas):
+    """The detector across a whole multi-CTA cluster (> 256 instances) vs the oracle."""
+    import dataclasses
+    from paper_2603_15202_b200 import workloads as W
+    from paper_2603_15202_b200.cluster import run
+    from paper_2603_15202_b200.config import DetectorConfig
+    trace, cfg = W.hotspot(n, 3000, 0.6, 2.5 * n, seed=21)
+    cfg = dataclasses.replace(cfg, detector=DetectorConfig(window_s=1.0, top_k_classes=4, consecutive_multiplier=1.0))
+    ref = run_oracle(trace, cfg)
+    rep = run(trace, cfg, ctas=ctas) if ctas else run(trace, cfg)
+    assert np.array_equal(rep.chosen, ref.chosen)
+    assert np.array_equal(rep.hit_tokens, ref.hit_tokens)
+    rows = [(r.window_start_s, r.class_key, r.fraction, r.n_holders, r.n_others, r.suspect, r.phase)
+            for r in rep.detector_rows]
+    assert len(rows) > 0 and rows == ref.detector_rows
+
+
 @pytest.mark.parametrize("seed", range(3))
 def test_random_simulate_configs_match_oracle(native, seed):
     """The simulate policy (TTFT replay per candidate, policies.py:142-157) on random clusters,
