@@ -307,3 +307,31 @@ def test_probe_batch_matches_oracle_cache(native):
         want = [refs[i].match_keys(keys) for i in range(cfg.n_instances)]
         assert list(got[r]) == want, r
     h.close()
+
+
+_ROUTE_POLICIES = ("simulate", "simulate_mistuned", "multiplicative", "vllm", "linear", "filter")
+
+
+@pytest.mark.parametrize("name", _ROUTE_POLICIES)
+def test_route_api_sequence_matches_reference(native, name):
+    """ClusterSim.route on 80 consecutive records (queues grow, no steps) vs the reference's
+    chosen instance and per-candidate scores (tests/golden/route_api.json,
+    tools/make_route_golden.py)."""
+    import json
+    import os
+    from paper_2603_15202_b200 import workloads as W
+    from paper_2603_15202_b200.cluster import ClusterSim
+    from paper_2603_15202_b200.config import ClusterConfig, CostModel, PolicyConfig
+    want = json.load(open(os.path.join(G.GOLDEN, "route_api.json")))[name]
+    pol = {"simulate": PolicyConfig(kind="simulate"),
+           "simulate_mistuned": PolicyConfig(kind="simulate", mis_tuned=True, mis_tuned_factor=2.5),
+           "multiplicative": PolicyConfig(), "vllm": PolicyConfig(kind="vllm", q_weight=0.5),
+           "linear": PolicyConfig(kind="linear"), "filter": PolicyConfig(kind="filter", range_threshold=2)}[name]
+    cfg = ClusterConfig(n_instances=5, cost_model=CostModel(chunk_tokens=256, max_batch_requests=6), policy=pol, seed=3)
+    trace = W.config1_chatbot()[0].slice(80)
+    sim = ClusterSim(cfg)
+    for r, rec in enumerate(trace.records()):
+        d = sim.route(rec, int(trace.arrival_us[r]))
+        assert d.chosen == want[r][0], f"request {r}"
+        assert [d.scores.get(i) for i in range(5)] == want[r][1], f"request {r}"
+    sim.close()
