@@ -246,12 +246,14 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     for _ in range(max(args.warmup - 1, 0)):
         h.rerun()
     launches0 = h.launch_count()
-    dev_ms, replay_ms = [], []
+    dev_ms, replay_ms, k1_ms = [], [], []
     with ClockSampler(dev_index) as clk:
         for _ in range(args.steps):
             flush_l2(dev)
             dev_ms.append(h.rerun())
-            replay_ms.append(h.timings()[0])
+            tm = h.timings()
+            replay_ms.append(tm[0])
+            k1_ms.append(tm[1])
     launches = h.launch_count() - launches0
     ctr = h.counters()
     ns = h.decision_ns(0, R)
@@ -279,8 +281,18 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     peaks, peak_src = measured_peaks()
     avg_replay_s = statistics.mean(replay_ms) / 1000.0
     achieved = ctr[0] / avg_replay_s / 1e9
+    # K1 chain hashing: 16 B per prefix block (read hash, write key) + 8 B per
+    # output-block key + 40 B of per-request metadata; timed by CUDA events inside each rerun
+    nb = int(trace.blk_off[-1])
+    nob = int(((trace.out_tokens + cfg.cache.block_size - 1) // cfg.cache.block_size).sum())
+    k1_alg = 16 * nb + 8 * nob + 40 * R
+    k1_s = statistics.mean(k1_ms) / 1000.0
+    k1 = {"kernel": "k1_chain_keys", "prefix_blocks": nb, "output_keys": nob, "ms": k1_s * 1000.0,
+          "keys_per_s": (nb + nob) / k1_s, "algorithmic_bytes": k1_alg,
+          "roofline": {"bound": "hbm", "achieved": k1_alg / k1_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                       "frac": k1_alg / k1_s / 1e9 / peaks["hbm_gbs"]}}
     out = {
-        "R": R, "cfg": cfg, "trace": trace,
+        "R": R, "cfg": cfg, "trace": trace, "k1": k1,
         "value": R * len(dev_ms) / (sum(dev_ms) / 1000.0),
         "ms_per_step": statistics.mean(dev_ms),
         "e2e": R * len(e2e_s) / sum(e2e_s), "h2d": h2d, "d2h": d2h,
@@ -437,7 +449,7 @@ def main():
             extras[name] = {"value": e["value"], "e2e": e["e2e"], "ms_per_step": e["ms_per_step"],
                             "n_instances": e["cfg"].n_instances, "requests": e["R"],
                             "decision_latency_us": {"p50": e["lat_p50_us"], "p99": e["lat_p99_us"]},
-                            "roofline": e["roofline"], "whatif_probe": e.get("whatif"),
+                            "roofline": e["roofline"], "whatif_probe": e.get("whatif"), "k1_chain_keys": e["k1"],
                             "cpu_baseline": e.get("cpu_baseline"),
                             "cpu_port": e.get("cpu_port"),
                             "e2e_vs_cpu_baseline": (e["e2e"] / e["cpu_baseline"]["value"]) if e.get("cpu_baseline") else None,
@@ -464,7 +476,7 @@ def main():
         "e2e": {"value": res["e2e"], "unit": "decisions/s", "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": res["d2h"]},
         "gpu_launches": res["launches"],
-        "whatif_probe": res.get("whatif"),
+        "whatif_probe": res.get("whatif"), "k1_chain_keys": res["k1"],
         "clocks": res["clocks"],
     }
     if "cpu_baseline" in res:

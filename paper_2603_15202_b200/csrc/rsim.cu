@@ -741,9 +741,11 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
     std::vector<Inst> hs(N);
     for (auto &x : hs) x = fresh_inst();
     u64 tie[2] = {h->cfg.tie_seed_lo, h->cfg.tie_seed_hi};
-    cudaEvent_t e0, e1;
+    cudaEvent_t e0, e1, ek0, ek1;
     CK(h, cudaEventCreate(&e0));
     CK(h, cudaEventCreate(&e1));
+    CK(h, cudaEventCreate(&ek0));
+    CK(h, cudaEventCreate(&ek1));
     CK(h, cudaEventRecord(e0, s));
     const size_t slots = (size_t)N << h->slog2;
     CK(h, cudaMemcpyAsync(h->inst, hs.data(), N * sizeof(Inst), cudaMemcpyHostToDevice, s));
@@ -758,12 +760,15 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
         for (auto *a : outs) CK(h, cudaMemsetAsync(a->p, 0xff, h->R * sizeof(i64), s));
         CK(h, cudaMemsetAsync(h->chosen.p, 0xff, h->R * sizeof(int), s));
         const i64 nwarps = (h->R + 31) / 32;
+        CK(h, cudaEventRecord(ek0, s));                     // K1 alone (rsim_last_timings' k1_ms)
         k1_chain_keys<<<(int)((nwarps + K1_WARPS - 1) / K1_WARPS), 32 * K1_WARPS, 0, s>>>(
             h->blk_off.p, h->blocks.p, h->ckeys.p, h->ooff.p, h->okeys.p, h->rid.p, 0, h->R, 0ULL, h->flag);
         h->launches++;
         CK(h, cudaGetLastError());
+        CK(h, cudaEventRecord(ek1, s));
         rsim_status st = launch_replay(h, 0, h->R, 0, MODE_REPLAY, -1, nullptr, &h->last_replay_ms);
-        if (st != RSIM_OK) { cudaEventDestroy(e0); cudaEventDestroy(e1); return st; }
+        if (st != RSIM_OK) { cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(ek0); cudaEventDestroy(ek1); return st; }
+        cudaEventElapsedTime(&h->last_k1_ms, ek0, ek1);     // (launch_replay synchronised the stream)
     }
     rsim_status st = launch_replay(h, 0, 0, RSIM_NONE, MODE_DRAIN, -1, nullptr, &h->last_drain_ms);
     CK(h, cudaEventRecord(e1, s));
@@ -773,6 +778,8 @@ rsim_status rsim_rerun(rsim_t *h, double *device_ms) {
     if (device_ms) *device_ms = ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    cudaEventDestroy(ek0);
+    cudaEventDestroy(ek1);
     return st;
 }
 

@@ -12,62 +12,56 @@
 #include "rsim_detector.cuh"
 
 // ---------------------------------------------------------------- K1
-// One warp per 32 consecutive requests: their blocks are one contiguous CSR
-// span, staged through shared memory with coalesced loads/stores; each lane
-// folds its own request's chain (hashing.py:36-47; splitmix64 is not
-// associative, so the chain is sequential per request). Output-block keys
-// extend the chain with stable_key(0x0F0C0DE, rid, idx) (engine.py:363-372).
-#define K1_WIN 256
+// One thread per request: the chain is sequential per request (splitmix64 is not
+// associative, hashing.py:36-47), so every lane folds its own request's blocks
+// at once, a full 32-B sector (4 keys) per iteration with the next sector's load
+// in flight; keys go out as full-sector stores. Output-block keys extend the
+// chain with stable_key(0x0F0C0DE, rid, idx) (engine.py:363-372).
 #define K1_WARPS 8
+__device__ __forceinline__ void k1_fold(u64 &acc, u64 v, u64 empty, bool &bad) {
+    acc = combine64(acc, v);
+    bad |= (acc == empty);
+}
 __global__ void __launch_bounds__(32 * K1_WARPS)
 k1_chain_keys(const i64 *__restrict__ blk_off, const u64 *__restrict__ blocks, u64 *__restrict__ ckeys,
               const i64 *__restrict__ ooff, u64 *__restrict__ okeys, const u64 *__restrict__ rid,
               i64 r0, i64 r1, u64 empty, int *flag) {
-    __shared__ u64 sbuf[K1_WARPS][K1_WIN];
-    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    const i64 wid = (i64)blockIdx.x * K1_WARPS + wl;
-    const i64 base = r0 + wid * 32;
-    if (base >= r1) return;
-    const i64 rlast = min(base + 32, r1);
-    const i64 r = base + lane;
-    const bool mine = r < rlast;
-    const i64 a = mine ? blk_off[r] : 0, b = mine ? blk_off[r + 1] : 0;
-    const i64 span0 = blk_off[base], span1 = blk_off[rlast];
-    u64 acc = RSIM_GOLDEN;
+    const i64 r = r0 + (i64)blockIdx.x * blockDim.x + threadIdx.x;
     bool bad = false;
-    u64 *sb = sbuf[wl];
-    for (i64 ws = span0; ws < span1; ws += K1_WIN) {
-        const i64 we = min(ws + K1_WIN, span1);
-#pragma unroll
-        for (int i = 0; i < K1_WIN / 32; i++) {
-            i64 p = ws + i * 32 + lane;
-            if (p < we) sb[i * 32 + lane] = __ldcs(blocks + p);
+    if (r < r1) {
+        const i64 a = blk_off[r], b = blk_off[r + 1];
+        u64 acc = RSIM_GOLDEN;
+        i64 j = a;
+        for (; j < b && (j & 3); j++) { k1_fold(acc, __ldcs(blocks + j), empty, bad); __stcs(ckeys + j, acc); }
+        if (j + 4 <= b) {
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(blocks + j);
+            ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(ckeys + j);
+            ulonglong2 x0 = __ldcs(src), x1 = __ldcs(src + 1);
+            const i64 nq = (b - j) >> 2;
+            for (i64 q = 0; q < nq; q++) {
+                ulonglong2 n0 = x0, n1 = x1;
+                if (q + 1 < nq) { n0 = __ldcs(src + 2 * q + 2); n1 = __ldcs(src + 2 * q + 3); }
+                u64 k0 = acc, k1, k2, k3;
+                k1_fold(k0, x0.x, empty, bad);
+                k1 = k0; k1_fold(k1, x0.y, empty, bad);
+                k2 = k1; k1_fold(k2, x1.x, empty, bad);
+                k3 = k2; k1_fold(k3, x1.y, empty, bad);
+                acc = k3;
+                __stcs(dst + 2 * q, make_ulonglong2(k0, k1));
+                __stcs(dst + 2 * q + 1, make_ulonglong2(k2, k3));
+                x0 = n0; x1 = n1;
+            }
+            j += nq << 2;
         }
-        __syncwarp();
-        const i64 lo = max(a, ws), hi = min(b, we);
-        for (i64 j = lo; j < hi; j++) {
-            acc = combine64(acc, sb[j - ws]);
-            bad |= (acc == empty);
-            sb[j - ws] = acc;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < K1_WIN / 32; i++) {
-            i64 p = ws + i * 32 + lane;
-            if (p < we) __stcs(ckeys + p, sb[i * 32 + lane]);
-        }
-        __syncwarp();
-    }
-    if (mine) {
+        for (; j < b; j++) { k1_fold(acc, __ldcs(blocks + j), empty, bad); __stcs(ckeys + j, acc); }
         const i64 o0 = ooff[r], o1 = ooff[r + 1];
         const u64 salt = combine64(combine64(RSIM_GOLDEN, RSIM_OUTPUT_SALT), rid[r]);
         for (i64 i = o0; i < o1; i++) {
-            acc = combine64(acc, combine64(salt, (u64)(i - o0)));
-            bad |= (acc == empty);
+            k1_fold(acc, combine64(salt, (u64)(i - o0)), empty, bad);
             okeys[i] = acc;
         }
     }
-    if (__any_sync(FULL, bad) && lane == 0) atomicExch(flag, 1);
+    if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) atomicExch(flag, 1);
 }
 
 // ---------------------------------------------------------------- cluster PTX
