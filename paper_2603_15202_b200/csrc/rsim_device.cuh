@@ -180,6 +180,11 @@ __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
     return v;
 }
 // position of the k-th (0-based) set bit of m
+// warp-wide form (m, k uniform across the warp): one popc + ballot instead of a k-step loop
+__device__ __forceinline__ int nth_set_bit_warp(u32 m, int k, int lane) {
+    const bool hit = ((m >> lane) & 1u) && __popc(m & lanemask_lt()) == k;
+    return __ffs(__ballot_sync(FULL, hit)) - 1;
+}
 __device__ __forceinline__ int nth_set_bit(u32 m, int k) {
     for (int i = 0; i < k; i++) m &= m - 1;
     return __ffs(m) - 1;

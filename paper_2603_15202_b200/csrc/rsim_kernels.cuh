@@ -707,7 +707,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
             if (rb < 0 && kk < pre + S) { rb = r; kr = kk - pre; bm = tb[r]; }
             pre += S;
         }
-        const int owner = rb * 32 + nth_set_bit(bm, (int)kr);
+        const int owner = rb * 32 + nth_set_bit_warp(bm, (int)kr, lane);
         if (owner / W == cta) { d.owner_warp = owner % W; d.kk = 0; }
         d.oflat = owner; d.okk = 0;
     } else if (!d.err && mine) {
@@ -1158,7 +1158,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             }
             DIAG(was_owner = warp == d.owner_warp);
             if (warp == d.owner_warp) {
-                const int s = nth_set_bit(d.pad == 0 ? tmask : d.pad == 1 ? tmask_bs : WB.tm[d.pad], d.kk);   // d.pad: the branch
+                const int s = nth_set_bit_warp(d.pad == 0 ? tmask : d.pad == 1 ? tmask_bs : WB.tm[d.pad], d.kk, lane);   // d.pad: the branch
                 const int h = WB.hit[s];
                 if (det && lane < C)     // (hit, product) of the chosen instance to every CTA's observe(k)
                     st_async_16(&dctl->own[par][0], &dctl->mbd[par], (u32)lane, (u64)(u32)h, (u64)WB.prod[s]);
