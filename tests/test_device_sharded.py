@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("name,world", [("adv_mixed_n33", 2), ("adv_mixed_n33", 3), ("cfg1_chatbot_full", 2),
                                         ("cfg2_api_prefix4000", 4), ("adv_same_time_ties", 4),
                                         ("evict_heavy_n4", 2), ("stale_50ms_n16", 3), ("stale_5ms", 2),
-                                        ("policy_simulate_mistuned", 3), ("policy_simulate_agent_evict", 2)])
+                                        ("policy_simulate_mistuned", 3), ("policy_simulate_agent_evict", 2),
+                                        ("cfg1_chatbot_full", 8), ("adv_mixed_n33", 8), ("cfg2_api_prefix4000", 8)])
 def test_sharded_matches_reference(name, world):
     from paper_2603_15202_b200.distributed import run_sharded_local
     trace, cfg = G.build(name)
