@@ -52,6 +52,7 @@ struct rsim {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int C = 1, W = 1, ipw = 1, per_cta = 1;
     size_t smem_bytes = 0;
+    bool no_rsm = getenv("RSIM_NO_SMEM_RUNNING") != nullptr;   // A/B switch: running lists stay in HBM
     int qlog2 = 0, slog2 = 0;
     i64 max_occ = 0;
     i64 R = 0, nblk = 0, nout = 0;       // loaded requests, blocks, output keys
@@ -482,6 +483,11 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     lc.gridDim = dim3(h->C, 1, 1);
     lc.blockDim = dim3(32 * (h->W + 1), 1, 1);   // + the control warp
     lc.dynamicSmemBytes = h->smem_bytes + (P.dsm ? (size_t)h->dT * (sizeof(DTrack) + sizeof(u64)) : 0);
+    {   // small shards keep their running lists in shared memory for the launch
+        const size_t rs = (size_t)h->per_cta * (size_t)h->cfg.max_batch_requests * sizeof(REnt);
+        const size_t off = (lc.dynamicSmemBytes + 127) & ~(size_t)127;
+        if (!h->no_rsm && off + rs <= 220 * 1024) { P.rsm_off = (int)off; lc.dynamicSmemBytes = off + rs; }
+    }
     lc.stream = h->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;

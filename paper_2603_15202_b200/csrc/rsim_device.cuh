@@ -137,7 +137,17 @@ struct Params {
     // simulate policy (policies.py:142-157, engine.py:419-460): the sim cost model and per-warp scratch
     double spb, spt, sdb, sds, sdc;
     int4 *simj;                        // [C*W][Qcap] (start step, last step, ctx at start, -) of joined requests
+    // small shards: this CTA's running lists live in shared memory during a launch (byte offset of
+    // the region in dynamic shared memory; 0 = global rbuf)
+    int rsm_off;
 };
+
+// running list of instance gi: shared memory (a launch of a small shard) or HBM
+extern __shared__ __align__(16) unsigned char smem[];
+__device__ __forceinline__ REnt *rlist(const Params &P, int gi) {
+    if (P.rsm_off) return reinterpret_cast<REnt *>(smem + P.rsm_off) + (size_t)(gi % P.per_cta) * (size_t)P.max_batch;
+    return P.rbuf + (size_t)gi * (size_t)P.max_batch;
+}
 
 // ---------------- hashing (hashing.py:15-25) ----------------
 __device__ __forceinline__ u64 splitmix64(u64 z) {

@@ -47,7 +47,7 @@ __device__ __noinline__ i64 sim_first_token(const Params &P, const Inst *sp, int
     const i64 S = sp->step_idx;
     const int nr = sp->r, q = sp->q, qh0 = sp->q_head;
     const QEnt *qb = P.qbuf + ((size_t)gi << P.qlog2);
-    const REnt *rb = P.rbuf + (size_t)gi * (size_t)P.max_batch;
+    const REnt *rb = rlist(P, gi);
     const u32 qmask = (1u << P.qlog2) - 1u;
     const i64 pc = cand > 1 ? cand : 1;
     i64 t = now > sp->busy_until ? now : sp->busy_until;
@@ -365,7 +365,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
     const i64 budget = P.chunk - ndec > 0 ? P.chunk - ndec : 0;   // engine.py:296
     const i64 slots = P.max_batch - ndec;                          // engine.py:297
     QEnt *qb = P.qbuf + ((size_t)gi << P.qlog2);
-    REnt *rb = P.rbuf + (size_t)gi * (size_t)P.max_batch;
+    REnt *rb = rlist(P, gi);
     const u32 qmask = (1u << P.qlog2) - 1u;
     SP_MARK(0);
     if (q == 0 && !fin_step && ndec > 0) {

@@ -764,7 +764,6 @@ __device__ __forceinline__ void bar_warps(int nthreads) {       // named barrier
 template <int MAXW, bool FILTER>      // FILTER: the two-branch partials of route_filter (policy 4)
 __global__ void __launch_bounds__(32 * (MAXW + 1), 1)
 replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
-    extern __shared__ __align__(16) unsigned char smem[];
     const int C = P.C, W = P.W, ipw = P.ipw, CW = P.C * P.W;
     const int cta = (C > 1) ? (int)cluster_ctarank() : 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -821,6 +820,12 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     }
     if (mode != MODE_DRAIN)
         for (int T = threadIdx.x; T < RSIM_MODTAB; T += blockDim.x) modtab[T] = T > 1 ? mod_counter(c0_lo, c0_hi, (u32)T) : 0u;
+    if (P.rsm_off) {                                       // running lists of this shard -> shared memory
+        const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(P.rbuf + (size_t)base * P.max_batch);
+        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(smem + P.rsm_off);
+        const int n16 = nloc * (int)P.max_batch * (int)(sizeof(REnt) / 16);
+        for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+    }
     if (det_run) {
         if (P.dsm) {                                        // detector state -> shared memory
             const int words = P.dT * (int)(sizeof(DTrack) / 8);
@@ -1192,6 +1197,12 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         const u64 *src = (const u64 *)st;
         const int words = nloc * (int)(sizeof(Inst) / 8);
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+    }
+    if (P.rsm_off) {
+        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(P.rbuf + (size_t)base * P.max_batch);
+        const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(smem + P.rsm_off);
+        const int n16 = nloc * (int)P.max_batch * (int)(sizeof(REnt) / 16);
+        for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
     }
     if (!control && lane == 0) {
         if (WB.werr) atomicCAS(P.err, 0, WB.werr);
