@@ -335,3 +335,33 @@ def test_route_api_sequence_matches_reference(native, name):
         assert d.chosen == want[r][0], f"request {r}"
         assert [d.scores.get(i) for i in range(5)] == want[r][1], f"request {r}"
     sim.close()
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_random_detector_simulate_match_oracle(native, seed):
+    """The hotspot detector steering the simulate policy (TTFT replay scores): random hotspot
+    traces and detector settings vs the oracle (pinned by the det_simulate_* fixtures)."""
+    import dataclasses
+    from paper_2603_15202_b200 import workloads as W
+    from paper_2603_15202_b200.cluster import run
+    from paper_2603_15202_b200.config import CacheConfig, DetectorConfig, PolicyConfig
+    rng = np.random.default_rng(900 + seed)
+    for trial in range(3):
+        N = int(rng.choice([3, 8, 16, 40]))
+        trace, cfg = W.hotspot(N, int(rng.integers(300, 1200)), float(rng.uniform(0.4, 0.9)),
+                               float(rng.uniform(20, 150)), int(rng.integers(1, 8)), seed=int(rng.integers(0, 99)))
+        det = DetectorConfig(window_s=float(rng.choice([0.5, 1.0, 2.5, 7.0])), top_k_classes=int(rng.integers(1, 5)),
+                             class_key_blocks=int(rng.integers(1, 3)),
+                             consecutive_multiplier=float(rng.choice([0.0, 0.5, 1.0])),
+                             mitigation=str(rng.choice(["exclude_holders", "force_least_bs"])),
+                             compare_mean_non_holder=bool(rng.integers(0, 2)))
+        pol = PolicyConfig(kind="simulate", mis_tuned=bool(rng.integers(0, 2)), tie_break_seed=int(rng.integers(0, 9)))
+        cap = [None, int(rng.integers(200, 2000))][int(rng.integers(0, 2))]
+        cfg = dataclasses.replace(cfg, policy=pol, detector=det, cache=CacheConfig(16, cap))
+        ref = run_oracle(trace, cfg)
+        rep = run(trace, cfg)
+        tag = f"seed{seed}/trial{trial} N={N} {det}"
+        assert np.array_equal(rep.chosen, ref.chosen), tag
+        rows = [(r.window_start_s, r.class_key, r.fraction, r.n_holders, r.n_others, r.suspect, r.phase)
+                for r in rep.detector_rows]
+        assert rows == ref.detector_rows, tag
