@@ -561,16 +561,6 @@ rsim_status rsim_enqueue(rsim_t *h, int32_t instance, int64_t r, int64_t now_us,
     return RSIM_OK;
 }
 
-static rsim_status stage_keys(rsim_t *h, const uint64_t *keys, int64_t n) {
-    if ((size_t)n > h->scratch_cap) {
-        if (h->scratch_keys) cudaFree(h->scratch_keys);
-        h->scratch_cap = std::max<size_t>(n, 1024);
-        CK(h, cudaMalloc(&h->scratch_keys, h->scratch_cap * sizeof(u64)));
-    }
-    if (n) CK(h, cudaMemcpy(h->scratch_keys, keys, n * sizeof(u64), cudaMemcpyHostToDevice));
-    return RSIM_OK;
-}
-
 static rsim_status arena_append(rsim_t *h, const uint64_t *keys, int64_t n, i64 *a0) {
     CK(h, h->arena.reserve(h->narena + n + 1, h->narena, h->stream));
     if (n) CK(h, cudaMemcpy(h->arena.p + h->narena, keys, n * sizeof(u64), cudaMemcpyHostToDevice));
