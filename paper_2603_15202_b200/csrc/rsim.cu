@@ -254,8 +254,8 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
             c.det_mitigation < 0 || c.det_mitigation > 1)
             return fail(nullptr, RSIM_E_INVALID, "invalid detector configuration");
         if (c.world > 1) return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector is single-rank on the device path");
-        if (c.policy == RSIM_POLICY_FILTER || (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0)))
-            return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector runs with multiplicative, vllm, least_bs or capped linear scores");
+        if (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0))
+            return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector does not run with uncapped linear scores (set-dependent normaliser)");
         if (c.det_window_s > 1e6) return fail(nullptr, RSIM_E_UNSUPPORTED, "detector window longer than 1e6 s");
     }
     if (c.policy == RSIM_POLICY_FILTER && c.world > 1)
@@ -309,7 +309,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
     h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(6 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 8 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf) +
                      (c.staleness_us > 0 ? (size_t)per_cta * sizeof(HistHead) : 0) +
-                     (c.det_on ? sizeof(DetCtl) + (size_t)(6 * W * C) * sizeof(Part) + (size_t)(2 * W * C) * RSIM_DLMAX : 0);
+                     (c.det_on ? sizeof(DetCtl) + (size_t)(8 * W * C) * sizeof(Part) + (size_t)(2 * W * C) * RSIM_DLMAX : 0);
     if (h->smem_bytes > 220 * 1024) { delete h; return fail(nullptr, RSIM_E_INVALID, "instance shard does not fit in shared memory"); }
     {   // kernel attributes are process-global: set the ceiling once (handles on other threads launch concurrently)
         static std::once_flag once;

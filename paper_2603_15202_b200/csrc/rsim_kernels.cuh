@@ -237,7 +237,8 @@ struct __align__(16) WarpBuf {
     // detector mode (rsim_detector.cuh): read by the control warp for the chosen instance
     i64 prod[32];          // p_tokens * max(bs, 1) of each instance (detector.py:312-316)
     int bsv[32];           // snapshot batch size
-    u32 tm[4];             // tied-instance masks per argmin branch (policy, filter bs, holders excluded, least bs)
+    u32 tm[6];             // tied-instance masks per argmin branch (policy, filter bs, holders excluded, least bs,
+                           // filter bs among non-holders)
     __align__(16) unsigned char ecs[RSIM_DLMAX];   // holder counts of the listed tracks among this warp's instances
 };
 
@@ -786,7 +787,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     const bool det = FILTER && P.dtid != nullptr;          // hotspot detector (single CTA)
     DetCtl *dctl = (DetCtl *)(hhc + (P.stal > 0 ? P.per_cta : 0));
     Part *dpart = (Part *)(dctl + 1);                      // [2 parity][masked, least bs, products][C*W]
-    unsigned char *ecnt = (unsigned char *)(dpart + 6 * CW);   // [2 parity][C*W][RSIM_DLMAX] listed holder counts
+    unsigned char *ecnt = (unsigned char *)(dpart + 8 * CW);   // [2 parity][C*W][RSIM_DLMAX] listed holder counts
     const int BCd = 1 << P.dbclog2;
     DetView DV{P.dtr, P.dtkey, P.dglob, P.dbk + (size_t)cta * P.dT * BCd * 3, P.dtot + (size_t)cta * BCd * 2, cta == 0};
     if (det && P.dsm) {                                    // tracks in shared memory (one copy per CTA)
@@ -882,7 +883,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             const bool lin_dyn = FILTER && P.policy == 3 && !(P.bsn > 0);   // linear with the per-decision bs max
             if (lane == 0) {
                 if (lin_dyn) mbar_arrive_expect(&mb0[par], (u32)(CW * 16));
-                mbar_arrive_expect(&mb[par], (u32)(CW * (FILTER && P.policy == 4 ? 32 : det ? 64 : 16)));
+                mbar_arrive_expect(&mb[par], (u32)(CW * (16 + (FILTER && P.policy == 4 ? 16 : 0) +
+                                                         (det ? 48 + (FILTER && P.policy == 4 ? 16 : 0) : 0))));
                 // the listed holder counts of every warp + the chosen instance's (hit, product) from its warp
                 if (det) mbar_arrive_expect(&dctl->mbd[par], (u32)(CW * 16 * ((dctl->nl + 15) >> 4) + 16));
             }
@@ -896,7 +898,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             if (tlc) tlc[0] = globaltimer();
 #endif
             if (det) {     // verdict(k) -> argmin branch (policies.py:222-236), then observe(k) before the release
-                const Part *dp = dpart + par * 3 * CW;
+                const Part *dp = dpart + par * 4 * CW;
                 i64 nh = 0, psum = 0;
                 u64 pmin = ~0ULL;
                 for (int i = lane; i < CW; i += 32) {
@@ -905,10 +907,25 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 }
                 nh = warp_sum(nh); psum = warp_sum(psum); pmin = warp_min_u64(pmin);
                 const int v = dctl->verdict;
-                const int code = v == 2 ? 3 : (v == 1 && nh < P.N ? 2 : 0);   // fail open when all hold
+                int code = v == 2 ? 3 : (v == 1 && nh < P.N ? 2 : 0);         // fail open when all hold
+                if (FILTER && P.policy == 4 && code == 2) {
+                    // route_filter over the kept (non-holder) candidates (policies.py:168-192, 229-236):
+                    // their batch-size range picks least bs among them (code 4) or the hit branch (2)
+                    u64 bmn = ~0ULL;
+                    u32 bmx = 0;
+                    for (int i = lane; i < CW; i += 32) {
+                        const ulonglong2 q = lds_v2u64(dp + 3 * CW + i);
+                        bmn = min(bmn, q.x); bmx = max(bmx, (u32)(q.y >> 32));
+                    }
+                    bmn = warp_min_u64(bmn);
+                    bmx = __reduce_max_sync(FULL, bmx);
+                    const i64 lo = bmn == ~0ULL ? 0 : (i64)__longlong_as_double((long long)bmn);
+                    if ((i64)bmx - lo > P.range_thr) code = 4;
+                }
                 det_code = code;
-                decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, false,
-                             code ? dp + (code - 2) * CW : nullptr, code);
+                decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane,
+                             FILTER && P.policy == 4,
+                             code == 2 ? dp : code == 3 ? dp + CW : code == 4 ? dp + 3 * CW : nullptr, code);
                 __syncwarp();
                 det_nh = nh; det_pmin = pmin; det_psum = psum;
             } else {
@@ -1062,11 +1079,20 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 const u32 tx = __ballot_sync(FULL, cand && bx == mx && mx != ~0ULL);
                 const u32 tl = __ballot_sync(FULL, cand && bl == ml && ml != ~0ULL);
                 const u32 nhw = (u32)__popc(__ballot_sync(FULL, held));
-                det_keep = tx | tl;
+                u32 txb = 0u;
+                if (FILTER && P.policy == 4) {           // filter's bs branch among the non-holders
+                    const u64 bb = (cand && !held) ? bits_bs : ~0ULL;
+                    const u64 mb_ = warp_min_u64(bb);
+                    txb = __ballot_sync(FULL, cand && !held && bb == mb_ && mb_ != ~0ULL);
+                    const u32 bmx = __reduce_max_sync(FULL, (cand && !held) ? (u32)WB.bsv[lane] : 0u);
+                    Part *dq = dpart + par * 4 * CW + 3 * CW + cta * W + warp;
+                    if (lane < C) st_async_16(dq, &mb[par], (u32)lane, mb_, ((u64)bmx << 32) | (u32)__popc(txb));
+                }
+                det_keep = tx | tl | txb;
                 if (P.ddbg != nullptr && cand) P.ddbg[(8 + P.N) * k + 8 + base + l0 + lane] = held ? -2 : WB.prod[lane];
-                if (lane == 0) { WB.tm[0] = tmask; WB.tm[1] = tmask_bs; WB.tm[2] = tx; WB.tm[3] = tl; }
+                if (lane == 0) { WB.tm[0] = tmask; WB.tm[1] = tmask_bs; WB.tm[2] = tx; WB.tm[3] = tl; WB.tm[4] = txb; }
                 __syncwarp();
-                Part *dp = dpart + par * 3 * CW + cta * W + warp;
+                Part *dp = dpart + par * 4 * CW + cta * W + warp;
                 if (lane < C) {
                     st_async_16(dp, &mb[par], (u32)lane, mx, ((u64)nhw << 32) | (u32)__popc(tx));
                     st_async_16(dp + CW, &mb[par], (u32)lane, ml, (u64)(u32)__popc(tl));

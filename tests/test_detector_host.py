@@ -38,13 +38,14 @@ def test_empty_prefix_rejected():
         detector_classes(t, 2)
 
 
-@pytest.mark.parametrize("pol", [PolicyConfig(kind="filter"), PolicyConfig(kind="linear")])
-def test_detector_with_set_dependent_scores_is_gated(pol):
+def test_detector_with_set_dependent_scores_is_gated():
+    """Uncapped linear normalises by the max batch size of the (kept) candidate set: gated.
+    filter (kept-set bs range, handled by its own partials), simulate and capped linear run."""
     _, cfg = G.build("det_hot_n16")
-    cfg = dataclasses.replace(cfg, policy=pol)
     with pytest.raises(UnsupportedConfigError):
-        cfg.check_device_supported()
-    dataclasses.replace(cfg, policy=PolicyConfig(kind="linear", bs_norm_cap=4)).check_device_supported()
+        dataclasses.replace(cfg, policy=PolicyConfig(kind="linear")).check_device_supported()
+    for pol in (PolicyConfig(kind="linear", bs_norm_cap=4), PolicyConfig(kind="filter"), PolicyConfig(kind="simulate")):
+        dataclasses.replace(cfg, policy=pol).check_device_supported()
 
 
 def test_detector_config_validation():

@@ -337,15 +337,16 @@ def test_route_api_sequence_matches_reference(native, name):
     sim.close()
 
 
-@pytest.mark.parametrize("seed", range(2))
-def test_random_detector_simulate_match_oracle(native, seed):
-    """The hotspot detector steering the simulate policy (TTFT replay scores): random hotspot
-    traces and detector settings vs the oracle (pinned by the det_simulate_* fixtures)."""
+@pytest.mark.parametrize("kind,seed", [("simulate", 0), ("simulate", 1), ("filter", 0), ("filter", 1), ("filter", 2)])
+def test_random_detector_simulate_match_oracle(native, kind, seed):
+    """The hotspot detector steering the simulate policy (TTFT replay scores) and the filter
+    policy (route_filter over the kept candidates): random hotspot traces and detector settings
+    vs the oracle (pinned by the det_simulate_* / det_filter_* fixtures)."""
     import dataclasses
     from paper_2603_15202_b200 import workloads as W
     from paper_2603_15202_b200.cluster import run
     from paper_2603_15202_b200.config import CacheConfig, DetectorConfig, PolicyConfig
-    rng = np.random.default_rng(900 + seed)
+    rng = np.random.default_rng(900 + seed + (50 if kind == "filter" else 0))
     for trial in range(3):
         N = int(rng.choice([3, 8, 16, 40]))
         trace, cfg = W.hotspot(N, int(rng.integers(300, 1200)), float(rng.uniform(0.4, 0.9)),
@@ -355,7 +356,8 @@ def test_random_detector_simulate_match_oracle(native, seed):
                              consecutive_multiplier=float(rng.choice([0.0, 0.5, 1.0])),
                              mitigation=str(rng.choice(["exclude_holders", "force_least_bs"])),
                              compare_mean_non_holder=bool(rng.integers(0, 2)))
-        pol = PolicyConfig(kind="simulate", mis_tuned=bool(rng.integers(0, 2)), tie_break_seed=int(rng.integers(0, 9)))
+        pol = PolicyConfig(kind=kind, mis_tuned=bool(rng.integers(0, 2)), tie_break_seed=int(rng.integers(0, 9)),
+                           range_threshold=int(rng.choice([1, 2, 4])))
         cap = [None, int(rng.integers(200, 2000))][int(rng.integers(0, 2))]
         cfg = dataclasses.replace(cfg, policy=pol, detector=det, cache=CacheConfig(16, cap))
         ref = run_oracle(trace, cfg)
