@@ -171,10 +171,7 @@ class ClusterConfig:
 
     def check_device_supported(self) -> None:
         """Reject the reference features that are outside the device path
-        (the detector with set-dependent scores)."""
-        if self.detector is not None and self.policy.kind == "linear" and self.policy.bs_norm_cap is None:
-            raise UnsupportedConfigError("the hotspot detector runs with multiplicative, vllm, least_bs or "
-                                         "capped linear, filter or simulate scores on the device path (not uncapped linear)")
+        (SURVEY.md section 8f); every policy, staleness and the detector run on it."""
         if self.policy.kind not in DEVICE_POLICY_KINDS:
             raise UnsupportedConfigError(
                 f"policy {self.policy.kind!r} is not on the device path "

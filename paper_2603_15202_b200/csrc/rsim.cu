@@ -254,8 +254,6 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
             c.det_mitigation < 0 || c.det_mitigation > 1)
             return fail(nullptr, RSIM_E_INVALID, "invalid detector configuration");
         if (c.world > 1) return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector is single-rank on the device path");
-        if (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0))
-            return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector does not run with uncapped linear scores (set-dependent normaliser)");
         if (c.det_window_s > 1e6) return fail(nullptr, RSIM_E_UNSUPPORTED, "detector window longer than 1e6 s");
     }
     if (c.policy == RSIM_POLICY_FILTER && c.world > 1)

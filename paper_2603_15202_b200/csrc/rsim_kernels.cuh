@@ -1029,23 +1029,31 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 }
                 __syncwarp();
             }
-            double bsn = P.bsn;
+            double bsn = P.bsn, bsn_kept = P.bsn;      // linear's normaliser over all / over the kept set
             if (FILTER && P.policy == 3 && !(P.bsn > 0)) {      // linear without a cap: bs_norm = max(max bs, 1) over ALL
                                                 // instances (policies.py:250-255) -- one extra exchange round
-                u32 lb = 0u;
+                u32 lb = 0u, lbk = 0u;
                 if (lane < nmine) {
                     const Inst *sp = st + l0 + lane;
                     lb = stale ? (u32)(hhc[l0 + lane].r + hhc[l0 + lane].q)
                                : sp->due <= R.t ? (u32)(sp->r + sp->q) : (u32)(sp->v_r + sp->v_q);
+                    // detector: also the max over the non-holders of class(k), the set an exclusion keeps
+                    if (!(det && WB.hit[lane] >= R.dw)) lbk = lb;
                 }
                 lb = __reduce_max_sync(FULL, lb);
-                if (lane < C) st_async_16(part0 + par * CW + cta * W + warp, &mb0[par], (u32)lane, (u64)lb, 0ULL);
+                lbk = __reduce_max_sync(FULL, lbk);
+                if (lane < C) st_async_16(part0 + par * CW + cta * W + warp, &mb0[par], (u32)lane, (u64)lb, (u64)lbk);
                 while (!mbar_try_wait(&mb0[par], (d0ph >> par) & 1u)) { }
                 d0ph ^= 1u << par;
-                u32 gm = 0u;
-                for (int i = lane; i < CW; i += 32) gm = max(gm, (u32)lds_v2u64(part0 + par * CW + i).x);
+                u32 gm = 0u, gmk = 0u;
+                for (int i = lane; i < CW; i += 32) {
+                    const ulonglong2 q = lds_v2u64(part0 + par * CW + i);
+                    gm = max(gm, (u32)q.x); gmk = max(gmk, (u32)q.y);
+                }
                 gm = __reduce_max_sync(FULL, gm);
+                gmk = __reduce_max_sync(FULL, gmk);
                 bsn = (double)(gm > 1u ? gm : 1u);
+                bsn_kept = (double)(gmk > 1u ? gmk : 1u);
             }
             u64 bits_bs;
             const u64 mybits = score_phase(P, st, base, l0, nmine, R, mode, target, lane, WB, bits_bs,
@@ -1071,7 +1079,10 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             if (det) {     // detector partials (rsim_detector.cuh): plain stores + a release arrive (C == 1)
                 const bool cand = lane < nmine;
                 const bool held = cand && WB.hit[lane] >= R.dw;          // holders of class(k)
-                const u64 bx = (cand && !held) ? mybits : ~0ULL;
+                u64 kb = mybits;                          // the kept-set score (uncapped linear renormalises)
+                if (FILTER && P.policy == 3 && !(P.bsn > 0) && cand && !held)
+                    kb = (u64)__double_as_longlong(score_of(P, WB.bsv[lane], 0, 0, 0, WB.hit[lane], R.in, bsn_kept));
+                const u64 bx = (cand && !held) ? kb : ~0ULL;
                 const u64 bl = cand ? (u64)__double_as_longlong((double)WB.bsv[lane]) : ~0ULL;
                 const u64 pn = (cand && !held) ? (u64)WB.prod[lane] : ~0ULL;
                 const i64 ps = warp_sum((cand && !held) ? WB.prod[lane] : 0LL);

@@ -38,14 +38,15 @@ def test_empty_prefix_rejected():
         detector_classes(t, 2)
 
 
-def test_detector_with_set_dependent_scores_is_gated():
-    """Uncapped linear normalises by the max batch size of the (kept) candidate set: gated.
-    filter (kept-set bs range, handled by its own partials), simulate and capped linear run."""
+def test_detector_runs_with_every_policy():
+    """Set-dependent scores included: filter (kept-set bs range) and uncapped linear (kept-set
+    max batch size) have their own partials; only a non-device policy name is rejected."""
     _, cfg = G.build("det_hot_n16")
-    with pytest.raises(UnsupportedConfigError):
-        dataclasses.replace(cfg, policy=PolicyConfig(kind="linear")).check_device_supported()
-    for pol in (PolicyConfig(kind="linear", bs_norm_cap=4), PolicyConfig(kind="filter"), PolicyConfig(kind="simulate")):
+    for pol in (PolicyConfig(kind="linear"), PolicyConfig(kind="linear", bs_norm_cap=4), PolicyConfig(kind="filter"),
+                PolicyConfig(kind="simulate"), PolicyConfig(kind="vllm"), PolicyConfig(kind="least_bs")):
         dataclasses.replace(cfg, policy=pol).check_device_supported()
+    with pytest.raises(UnsupportedConfigError):
+        dataclasses.replace(cfg, policy=dataclasses.replace(PolicyConfig(), kind="nope")).check_device_supported()
 
 
 def test_detector_config_validation():

@@ -337,7 +337,8 @@ def test_route_api_sequence_matches_reference(native, name):
     sim.close()
 
 
-@pytest.mark.parametrize("kind,seed", [("simulate", 0), ("simulate", 1), ("filter", 0), ("filter", 1), ("filter", 2)])
+@pytest.mark.parametrize("kind,seed", [("simulate", 0), ("simulate", 1), ("filter", 0), ("filter", 1), ("filter", 2),
+                                       ("linear", 0), ("linear", 1), ("linear", 2)])
 def test_random_detector_simulate_match_oracle(native, kind, seed):
     """The hotspot detector steering the simulate policy (TTFT replay scores) and the filter
     policy (route_filter over the kept candidates): random hotspot traces and detector settings
@@ -346,7 +347,7 @@ def test_random_detector_simulate_match_oracle(native, kind, seed):
     from paper_2603_15202_b200 import workloads as W
     from paper_2603_15202_b200.cluster import run
     from paper_2603_15202_b200.config import CacheConfig, DetectorConfig, PolicyConfig
-    rng = np.random.default_rng(900 + seed + (50 if kind == "filter" else 0))
+    rng = np.random.default_rng(900 + seed + {"simulate": 0, "filter": 50, "linear": 70}[kind])
     for trial in range(3):
         N = int(rng.choice([3, 8, 16, 40]))
         trace, cfg = W.hotspot(N, int(rng.integers(300, 1200)), float(rng.uniform(0.4, 0.9)),

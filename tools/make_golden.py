@@ -93,6 +93,8 @@ CASES = {
     "det_simulate_force": ("(lambda t, c: (t, dataclasses.replace(c, policy=PolicyConfig(kind='simulate', mis_tuned=True), detector=DetectorConfig(window_s=2.0, mitigation='force_least_bs', consecutive_multiplier=1.0))))(*W.hotspot(10, 1500, 0.75, seed=9))", None),
     "det_filter_n12": ("(lambda t, c: (t, dataclasses.replace(c, policy=PolicyConfig(kind='filter', range_threshold=2), detector=DetectorConfig(window_s=3.0, consecutive_multiplier=1.0))))(*W.hotspot(12, 1500, 0.7, 120.0, seed=10))", None),
     "det_filter_force": ("(lambda t, c: (t, dataclasses.replace(c, policy=PolicyConfig(kind='filter'), detector=DetectorConfig(window_s=2.0, mitigation='force_least_bs', consecutive_multiplier=0.5, compare_mean_non_holder=True))))(*W.hotspot(16, 2000, 0.8, 200.0, seed=11))", None),
+    "det_linear_uncapped": ("(lambda t, c: (t, dataclasses.replace(c, policy=PolicyConfig(kind='linear', kv_weight=0.3), detector=DetectorConfig(window_s=3.0, consecutive_multiplier=1.0))))(*W.hotspot(12, 1500, 0.7, 150.0, seed=12))", None),
+    "det_linear_stale": ("(lambda t, c: (t, dataclasses.replace(c, policy=PolicyConfig(kind='linear'), staleness_ms=15.0, detector=DetectorConfig(window_s=2.0, consecutive_multiplier=0.5, compare_mean_non_holder=True))))(*W.hotspot(16, 2000, 0.8, 250.0, seed=13))", None),
     "det_evict_n8": ("(lambda t, c: (t, dataclasses.replace(c, cache=CacheConfig(16, 600), detector=DetectorConfig(window_s=2.0, consecutive_multiplier=0.5))))(*W.hotspot(8, 2000, 0.8, 90.0, seed=6))", None),
     "cost_fma_sensitive": ("(W.config1_chatbot()[0], ClusterConfig(n_instances=8, cost_model=CostModel(3.3, 0.0371, 17.1, 0.77, 0.0013, 512, 16), cache=CacheConfig(16, 2000), seed=4))", 1000),
     "cost_small_batch": ("(W.config2_api()[0], ClusterConfig(n_instances=6, cost_model=CostModel(1.0, 0.2, 4.0, 0.5, 0.01, 300, 3), cache=CacheConfig(16, 5000), seed=7))", 1500),
