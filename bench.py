@@ -408,7 +408,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="api64", choices=sorted(WORKLOADS))
-    ap.add_argument("--extra", default="chat1024", help="comma list of extra workloads reported beside the headline")
+    ap.add_argument("--extra", default="chat1024,agent256", help="comma list of extra workloads reported beside the headline")
     ap.add_argument("--ref-budget-s", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--whatif", type=int, default=20000,
