@@ -181,11 +181,50 @@ def time_reference(trace, cfg, n_sample: int, repeats: int = 1):
 
 
 def time_port(trace, cfg):
-    """The C oracle port (oracle/rsim_oracle.c, 1 thread) over the whole trace."""
+    """The C oracle port (oracle/rsim_oracle.c, 1 thread) over ``trace``: (decisions/s, result).
+    The result is the parity checker of the device replay (parity_vs_oracle)."""
     from oracle.oracle import run_oracle
     t0 = time.perf_counter()
-    run_oracle(trace, cfg)
-    return len(trace) / (time.perf_counter() - t0)
+    res = run_oracle(trace, cfg)
+    return len(trace) / (time.perf_counter() - t0), res
+
+
+def parity_vs_oracle(ref, chosen, hit_tokens, finish_us, n_total):
+    """Decision-by-decision comparison of the device replay with the oracle (which is pinned to
+    the reference's own run(), tests/golden): chosen instance, hit tokens and finish time of every
+    request the oracle replayed (all of them, or a prefix: decision k depends only on records[:k+1],
+    SURVEY 8c)."""
+    n = len(ref.chosen)
+    mism = {"chosen": int((ref.chosen != chosen[:n]).sum()),
+            "hit_tokens": int((ref.hit_tokens != hit_tokens[:n]).sum()),
+            "finish_us": int((ref.finish_us != finish_us[:n]).sum())}
+    first = None
+    bad = (ref.chosen != chosen[:n]) | (ref.hit_tokens != hit_tokens[:n]) | (ref.finish_us != finish_us[:n])
+    if bad.any():
+        first = int(np.argmax(bad))
+    return {"vs": "oracle/rsim_oracle.c (pinned to the reference's run(), tests/golden)",
+            "decisions": n, "of": n_total, "mismatches": sum(mism.values()), "by_field": mism,
+            "first_mismatch": first, "evicted_blocks": int(getattr(ref, "evicted", 0))}
+
+
+def chosen_digest(chosen) -> str:
+    """sha256 (first 16 hex) of the int32 decision log: equal across G = 1, 2, 4, 8."""
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(chosen, dtype=np.int32).tobytes()).hexdigest()[:16]
+
+
+def host_cpu():
+    """lscpu model name and the host's logical core count."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cores": os.cpu_count()}
 
 
 def reference_arm(args):
@@ -218,7 +257,8 @@ def reference_arm(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": {"workload": args.workload, "description": WORKLOADS[args.workload][1],
                                             "n_instances": cfg.n_instances, "requests": n},
-            "cpu_baseline": {"value": value, "unit": "decisions/s", "cores": cores, "kind": kind, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "decisions/s", "cores": cores, "kind": kind, "sample": sample,
+                             "host_cpu": host_cpu()},
             "e2e": {"value": value, "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -258,12 +298,13 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     ctr = h.counters()
     ns = h.decision_ns(0, R)
     lat = np.diff(ns[ns > 0]) / 1000.0
-    chosen_dev, _ = h.decisions(0, R)
+    chosen_dev, hit_dev = h.decisions(0, R)
+    finish_dev = h.request_times(0, R)[2]
     whatif = measure_whatif(h, trace, cfg, args) if args.whatif else None
     h.close()
 
     # e2e through the public API: host arrays in, results out
-    sim = ClusterSim(cfg, device=dev_index, record_steps=False)
+    sim = ClusterSim(cfg, device=dev_index)          # record_steps=True, as the reference's run() reports steps
     for _ in range(args.warmup):
         sim.run_trace(trace)
     e2e_s = []
@@ -273,11 +314,12 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
         rep = sim.run_trace(trace)
         e2e_s.append(time.perf_counter() - t0)
     assert np.array_equal(rep.chosen, chosen_dev), "e2e and resident replays disagree"
+    log_bytes = int(rep._step_log.nbytes) if rep._step_log is not None else 0
     sim.close()
 
     h2d = int(trace.arrival_us.nbytes + trace.in_tokens.nbytes + trace.out_tokens.nbytes +
               trace.request_id.nbytes + trace.blk_off.nbytes + trace.blocks.nbytes)
-    d2h = R * (4 + 8 * 5)   # chosen, hit_tokens, first_sched, first_token, finish, route_bs
+    d2h = R * (4 + 8 * 5) + log_bytes   # chosen, hit_tokens, first_sched, first_token, finish, route_bs + step log
     peaks, peak_src = measured_peaks()
     avg_replay_s = statistics.mean(replay_ms) / 1000.0
     achieved = ctr[0] / avg_replay_s / 1e9
@@ -297,6 +339,7 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
         "ms_per_step": statistics.mean(dev_ms),
         "e2e": R * len(e2e_s) / sum(e2e_s), "h2d": h2d, "d2h": d2h,
         "launches": launches, "clocks": clk.summary(), "whatif": whatif,
+        "decisions_sha256_16": chosen_digest(chosen_dev),
         "lat_p50_us": float(np.percentile(lat, 50)) if lat.size else None,
         "lat_p99_us": float(np.percentile(lat, 99)) if lat.size else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -308,15 +351,22 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     if with_cpu:
         n = reference_samples(trace, cfg, args.ref_budget_s)
         ref = time_reference(trace, cfg, n)
-        port = time_port(trace, cfg)
+        cpu = host_cpu()
         if ref is not None:
             out["cpu_baseline"] = {"value": ref, "unit": "decisions/s", "cores": 1, "kind": "reference",
-                                   "sample": f"first {n} of {R} requests, routesim.run from baseline/_ref (CPython, 1 thread)"}
-        else:
-            out["cpu_baseline"] = {"value": port, "unit": "decisions/s", "cores": 1, "kind": "port",
-                                   "sample": f"all {R} requests, C oracle port (1 thread)"}
+                                   "sample": f"first {n} of {R} requests, routesim.run from baseline/_ref (CPython, 1 thread)",
+                                   "host_cpu": cpu}
+    if args.parity:
+        # the C oracle over the benched trace (or its first --parity-max requests): the timed CPU port
+        # and the decision-by-decision parity check of this step's device replay
+        sample = trace if R <= args.parity_max else trace.slice(args.parity_max)
+        port, oref = time_port(sample, cfg)
+        out["parity"] = parity_vs_oracle(oref, chosen_dev, hit_dev, finish_dev, R)
         out["cpu_port"] = {"value": port, "unit": "decisions/s", "cores": 1, "kind": "port",
-                           "sample": f"all {R} requests, oracle/rsim_oracle.c (1 thread)"}
+                           "sample": f"{'all' if len(sample) == R else 'first'} {len(sample)} of {R} requests, "
+                                     "oracle/rsim_oracle.c (1 thread)", "host_cpu": host_cpu()}
+        if "cpu_baseline" not in out and with_cpu:
+            out["cpu_baseline"] = dict(out["cpu_port"])
     return out
 
 
@@ -355,7 +405,24 @@ def traffic_for(name):
         return None
 
 
-def measure_sharded(name, args, dev_index, rank, world):
+def peer_evidence(rank, world, dev_index, router, backend):
+    """Per-rank device identity and peer-open evidence (the data plane is not NCCL, so the
+    driver's comm_nranks_ok says nothing about it)."""
+    import torch
+    p = torch.cuda.get_device_properties(dev_index)
+    ndev = torch.cuda.device_count()
+    peers = {}
+    for r in range(world):
+        d = r % ndev
+        if r != rank:
+            peers[str(r)] = {"device": d, "same_device": d == dev_index,
+                             "can_access_peer": bool(d == dev_index or torch.cuda.can_device_access_peer(dev_index, d))}
+    return {"rank": rank, "device": dev_index, "name": p.name, "pci_bus_id": getattr(p, "pci_bus_id", None),
+            "uuid": str(getattr(p, "uuid", "")), "shard": list(router.h.shard_bounds()),
+            "ipc_mailboxes_opened": router.peers_opened, "plumbing_backend": backend, "peers": peers}
+
+
+def measure_sharded(name, args, dev_index, rank, world, backend):
     """Instances of one cluster sharded over `world` GPUs (one process each); per decision every
     rank publishes its (min score, tie count) partial into every peer's mailbox over NVLink
     (device-initiated, distributed.py). Strong scaling: the total work is the one trace."""
@@ -364,41 +431,94 @@ def measure_sharded(name, args, dev_index, rank, world):
     from paper_2603_15202_b200.distributed import ShardedRouter
 
     trace, cfg = build_workload(name)
+    if args.requests and args.requests < len(trace):
+        trace = trace.slice(args.requests)
     R = len(trace)
     dev = torch.device("cuda", dev_index)
     router = ShardedRouter(cfg, trace, rank=rank, world=world, device=dev_index)
     for _ in range(args.warmup):
         router.rerun()
     launches0 = router.h.launch_count()
-    dev_ms = []
+    dev_ms, replay_ms, k1_ms = [], [], []
     with ClockSampler(dev_index) as clk:
         for _ in range(args.steps):
             flush_l2(dev)
             dist.barrier()
             dev_ms.append(router.rerun())
+            tm = router.h.timings()
+            replay_ms.append(tm[0])
+            k1_ms.append(tm[1])
     launches = router.h.launch_count() - launches0
     ctr = router.h.counters()
-    replay_ms = router.h.timings()[0]
+    ns = router.h.decision_ns(0, R)                  # this rank's clock, stamped at every decide
+    lat = np.diff(ns[ns > 0]) / 1000.0
+    ch_local, ht_local = router.local_decisions()
+    fin_local = router.h.request_times(0, R)[2]
+    evidence = peer_evidence(rank, world, dev_index, router, backend)
     e2e_s = []
     for _ in range(args.steps):
         flush_l2(dev)
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        router.run_trace(trace)
+        chosen, hit_tokens = router.run_trace(trace)
         e2e_s.append(time.perf_counter() - t0)
     router.close()
+    # merge this rank's owned decisions with its peers' (each decision is committed by exactly one rank)
+    fin = merge_over_ranks(fin_local, backend, dev)
+    assert np.array_equal(merge_over_ranks(ch_local.astype(np.int64), backend, dev).astype(np.int32), chosen), \
+        "resident and e2e sharded replays disagree"
     h2d = int(trace.arrival_us.nbytes + trace.in_tokens.nbytes + trace.out_tokens.nbytes +
               trace.request_id.nbytes + trace.blk_off.nbytes + trace.blocks.nbytes)
     peaks, peak_src = measured_peaks()
-    achieved = ctr[0] / (replay_ms / 1000.0) / 1e9 if replay_ms else 0.0
-    return {"R": R, "cfg": cfg, "trace": trace, "ms_per_step": statistics.mean(dev_ms),
-            "e2e_s": statistics.mean(e2e_s), "h2d": h2d, "d2h": R * 12, "launches": launches,
-            "clocks": clk.summary(), "lat_p50_us": None, "lat_p99_us": None,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": "replay_kernel",
-                         "algorithmic_bytes_per_launch": int(ctr[0]), "avg_launch_ms": replay_ms,
-                         "peak_source": f"{peak_src} hbm_gbs (burst copy)", "scope": f"rank {rank} shard"}}
+    avg_replay_s = statistics.mean(replay_ms) / 1000.0
+    achieved = ctr[0] / avg_replay_s / 1e9 if avg_replay_s else 0.0
+    nb = int(trace.blk_off[-1])
+    nob = int(((trace.out_tokens + cfg.cache.block_size - 1) // cfg.cache.block_size).sum())
+    k1_alg = 16 * nb + 8 * nob + 40 * R
+    k1_s = statistics.mean(k1_ms) / 1000.0
+    k1 = {"kernel": "k1_chain_keys", "prefix_blocks": nb, "output_keys": nob, "ms": k1_s * 1000.0,
+          "keys_per_s": (nb + nob) / k1_s, "algorithmic_bytes": k1_alg, "scope": "replicated on every rank",
+          "roofline": {"bound": "hbm", "achieved": k1_alg / k1_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                       "frac": k1_alg / k1_s / 1e9 / peaks["hbm_gbs"]}}
+    out = {"R": R, "cfg": cfg, "trace": trace, "k1": k1, "ms_per_step": statistics.mean(dev_ms),
+           "e2e_s": statistics.mean(e2e_s), "h2d": h2d, "d2h": R * 12, "launches": launches,
+           "clocks": clk.summary(), "chosen": chosen, "hit_tokens": hit_tokens, "finish_us": fin,
+           "evidence": evidence,
+           "lat_p50_us": float(np.percentile(lat, 50)) if lat.size else None,
+           "lat_p99_us": float(np.percentile(lat, 99)) if lat.size else None,
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": "replay_kernel",
+                        "algorithmic_bytes_per_launch": int(ctr[0]), "avg_launch_ms": avg_replay_s * 1000.0,
+                        "peak_source": f"{peak_src} hbm_gbs (burst copy)", "scope": f"rank {rank} shard"}}
+    return out
+
+
+def merge_over_ranks(a, backend, dev):
+    """Element-wise max over ranks (non-owned entries are -1)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64))
+    t = t.to(dev) if backend == "nccl" else t
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.cpu().numpy()
+
+
+def relaunch_distributed(n):
+    """``bench.py --gpus N`` outside torchrun: re-exec under torch.distributed.run with N ranks."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
+def default_workload(world):
+    """api64 (BASELINE configs[1], where the metric is quoted) on one GPU; the sharded configs[3]
+    cluster (4096 instances over the N GPUs) for N > 1."""
+    return "api64" if world == 1 else "large4096"
 
 
 def main():
@@ -407,48 +527,82 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="api64", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: api64 on 1 GPU, large4096 sharded over N > 1")
+    ap.add_argument("--requests", type=int, default=0, help="sharded runs: replay only the first R requests (0: all)")
     ap.add_argument("--extra", default="chat1024,agent256", help="comma list of extra workloads reported beside the headline")
     ap.add_argument("--ref-budget-s", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", dest="parity", action="store_false",
+                    help="skip the decision-by-decision check of the device replay against the C oracle")
+    ap.add_argument("--parity-max", type=int, default=0,
+                    help="oracle-checked prefix length (decision k depends only on records[:k+1]); "
+                         "default 120k on 1 GPU (every request of api64 / chat1024 / agent256), 50k sharded")
     ap.add_argument("--whatif", type=int, default=20000,
                     help="requests of the batched what-if probe measured after the replay (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args.gpus)
+    if world > 1 and args.gpus not in (1, world):
+        raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE={world}")
+    if args.workload is None:
+        args.workload = default_workload(world)
+    if args.parity_max <= 0:
+        args.parity_max = 120_000 if world == 1 else 50_000
     if args.impl == "reference":
         reference_arm(args)
         return
 
     import torch
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    pg = None
+    ndev = torch.cuda.device_count()
+    dev_index = local % max(ndev, 1)                 # ranks share a GPU only when fewer GPUs than ranks
+    torch.cuda.set_device(dev_index)
+    pg, backend = None, None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = "nccl" if ndev >= world else "gloo"   # NCCL cannot put two ranks on one device
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
         pg = dist
-    if pg:
         pg.barrier()
     torch.cuda.synchronize()
     if world > 1:
-        res = measure_sharded(args.workload, args, local, rank, world)
+        res = measure_sharded(args.workload, args, dev_index, rank, world, backend)
     else:
-        res = measure_workload(args.workload, args, local, with_cpu=(rank == 0 and not args.no_cpu), rank=rank)
+        res = measure_workload(args.workload, args, dev_index, with_cpu=not args.no_cpu, rank=rank)
     torch.cuda.synchronize()
     if pg:
         pg.barrier()
-        t = torch.tensor([res["ms_per_step"], res["e2e_s"]], device="cuda", dtype=torch.float64)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        t = torch.tensor([res["ms_per_step"], res["e2e_s"]], dtype=torch.float64)
+        t = t.cuda() if backend == "nccl" else t
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)          # max over ranks
         res["ms_per_step"], res["e2e_s"] = float(t[0].item()), float(t[1].item())
         res["e2e"] = res["R"] / res["e2e_s"]
+        ev = [None] * world
+        pg.all_gather_object(ev, res["evidence"])
+        res["evidence"] = ev
+        if rank == 0 and args.parity:
+            trace, cfg = res["trace"], res["cfg"]
+            sample = trace if res["R"] <= args.parity_max else trace.slice(args.parity_max)
+            port, oref = time_port(sample, cfg)
+            res["parity"] = parity_vs_oracle(oref, res["chosen"], res["hit_tokens"], res["finish_us"], res["R"])
+            res["cpu_port"] = {"value": port, "unit": "decisions/s", "cores": 1, "kind": "port",
+                               "sample": f"first {len(sample)} of {res['R']} requests, oracle/rsim_oracle.c (1 thread)",
+                               "host_cpu": host_cpu()}
+        res["decisions_sha256_16"] = chosen_digest(res["chosen"])
     extras = {}
-    if rank == 0 and world == 1:
+    if world == 1:
         for name in [x for x in args.extra.split(",") if x and x != args.workload]:
-            e = measure_workload(name, args, local, with_cpu=not args.no_cpu, rank=rank)
+            e = measure_workload(name, args, dev_index, with_cpu=not args.no_cpu, rank=rank)
             extras[name] = {"value": e["value"], "e2e": e["e2e"], "ms_per_step": e["ms_per_step"],
                             "n_instances": e["cfg"].n_instances, "requests": e["R"],
                             "decision_latency_us": {"p50": e["lat_p50_us"], "p99": e["lat_p99_us"]},
+                            "parity": e.get("parity"), "decisions_sha256_16": e.get("decisions_sha256_16"),
                             "roofline": e["roofline"], "whatif_probe": e.get("whatif"), "k1_chain_keys": e["k1"],
                             "cpu_baseline": e.get("cpu_baseline"),
                             "cpu_port": e.get("cpu_port"),
@@ -468,10 +622,13 @@ def main():
         "config": {"workload": args.workload, "description": WORKLOADS[args.workload][1],
                    "n_instances": res["cfg"].n_instances, "requests": R, "block_size": res["cfg"].cache.block_size,
                    "capacity_blocks": res["cfg"].cache.capacity_blocks, "policy": res["cfg"].policy.kind,
-                   "parallelism": f"instances sharded over {world} GPUs, per-decision NVLink mailbox exchange" if world > 1 else "single-gpu",
+                   "parallelism": (f"instances sharded over {world} ranks ({backend} plumbing), per-decision "
+                                   "device-initiated mailbox exchange over peer memory") if world > 1 else "single-gpu",
                    "l2": "512 MB flush between timed steps; trace + tables exceed L2"},
         "decision_latency_us": {"p50": res["lat_p50_us"], "p99": res["lat_p99_us"],
-                                "source": "%globaltimer at each commit, consecutive differences"},
+                                "source": "%globaltimer at each commit (rank 0's decide for N > 1), consecutive differences"},
+        "parity": res.get("parity"),
+        "decisions_sha256_16": res.get("decisions_sha256_16"),
         "roofline": res["roofline"],
         "e2e": {"value": res["e2e"], "unit": "decisions/s", "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": res["d2h"]},
@@ -479,16 +636,18 @@ def main():
         "whatif_probe": res.get("whatif"), "k1_chain_keys": res["k1"],
         "clocks": res["clocks"],
     }
+    if world > 1:
+        line["ranks"] = res["evidence"]
     if "cpu_baseline" in res:
         line["cpu_baseline"] = res["cpu_baseline"]
-        line["cpu_port"] = res["cpu_port"]
         line["e2e_vs_cpu_baseline"] = res["e2e"] / res["cpu_baseline"]["value"]
+    if "cpu_port" in res:
+        line["cpu_port"] = res["cpu_port"]
     if extras:
         line["extra_workloads"] = extras
     print(json.dumps(line), flush=True)
     if pg:
         pg.destroy_process_group()
-
 
 if __name__ == "__main__":
     main()

@@ -691,6 +691,8 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
             mine = owner_rank == P.rank;
             kk -= bef;                            // this rank's local tie index if it owns
         }
+        // sharded: every rank stamps each decision on its own clock (rank 0's series gives p50/p99)
+        if (P.dec_ns != nullptr && cta == 0 && lane == 0) P.dec_ns[k] = (i64)globaltimer();
     } else if (!d.err && T > 1) {                 // TieBreaker.pick: tied[counter % len]; counter += 1
         kk = tie_index(modtab, c0_lo, c0_hi, ties, T);
         ties += 1;
@@ -1210,7 +1212,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                        (s < 2 && nmine < 2 && !(((stale_slots | sparse_probe) >> s) & 1u)) ? WB.slot[par][s] : nullptr,
                        R.a, R.B, R.in, R.out, R.oa, lane, werr, WB.fin, FILTER && P.stal > 0);
                 if (lane == 0 && werr) WB.werr = werr;
-                if (P.dec_ns != nullptr && lane == 0) P.dec_ns[k] = (i64)globaltimer();
+                if (P.dec_ns != nullptr && lane == 0 && P.world == 1) P.dec_ns[k] = (i64)globaltimer();
             }
             PHASE(7);
         }

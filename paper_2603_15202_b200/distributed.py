@@ -98,9 +98,11 @@ class ShardedRouter:
                                               comm_timeout_ms=comm_timeout_ms))
         handles = [None] * world
         dist.all_gather_object(handles, self.h.mailbox_ipc_handle())
+        self.peers_opened = 0
         for r, hd in enumerate(handles):
             if r != rank:
                 self.h.open_peer_ipc(r, hd)
+                self.peers_opened += 1
         _load(self.h, trace)
         dist.barrier()
 
