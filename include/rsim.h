@@ -45,7 +45,11 @@ enum { RSIM_BAL_BS = 0, RSIM_BAL_TOTAL_TOKENS = 1 };
 
 /* Mirrors ClusterConfig + CostModel + CacheConfig + PolicyConfig
  * (reference cluster.py:32-64, engine.py:46-55, policies.py:37-53). */
+#define RSIM_ABI_VERSION 2
 typedef struct rsim_config {
+    uint32_t struct_size;           /* = sizeof(rsim_config) as the caller compiled it: rsim_create
+                                       rejects a mismatch (a binding built against another layout) */
+    uint32_t abi_version;           /* = RSIM_ABI_VERSION                                       */
     int32_t n_instances;            /* ClusterConfig.n_instances                              */
     int32_t block_size;             /* CacheConfig.block_size                                 */
     int64_t capacity_blocks;        /* CacheConfig.capacity_blocks, -1 = infinite (None)      */
@@ -55,7 +59,9 @@ typedef struct rsim_config {
     int32_t policy;                 /* RSIM_POLICY_*                                           */
     int32_t kv_indicator;           /* RSIM_KV_*   (multiplicative)                            */
     int32_t balance_indicator;      /* RSIM_BAL_*  (multiplicative)                            */
-    int32_t debug_checks;           /* ClusterConfig.debug_checks                              */
+    int32_t debug_checks;           /* ClusterConfig.debug_checks: replay one decision per launch and
+                                       check InstanceSim.reconcile + PrefixCache.check_invariants on
+                                       device after each (cluster.py:168-170) -> RSIM_E_INVARIANT   */
     double q_weight;                /* PolicyConfig.q_weight (vllm)                            */
     uint64_t tie_seed_lo, tie_seed_hi; /* TieBreaker counter = stable_key(seed, tie_break_seed), cluster.py:90-94 */
     int32_t device;                 /* CUDA ordinal                                            */
@@ -100,6 +106,9 @@ typedef struct rsim_config {
 
 typedef struct rsim rsim_t;
 
+/* sizeof(rsim_config) of this build: bindings assert it before the first rsim_create. */
+size_t rsim_config_size(void);
+
 /* ClusterSim.__init__ (cluster.py:73-102): allocate device state for N instances. */
 rsim_status rsim_create(const rsim_config *cfg, rsim_t **out);
 void rsim_destroy(rsim_t *h);
@@ -143,6 +152,20 @@ rsim_status rsim_read_route_bs(rsim_t *h, int64_t first, int64_t count, int64_t 
  * (cluster.py:130-154) on loaded request r. scores (N doubles) may be NULL. */
 rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen,
                            int64_t *hit_tokens, double *scores);
+/* route() of a request id already present on some instances (InstanceSim._present, engine.py:266-267):
+ * the decision is made as usual (the TieBreaker counter moves); if the winner is one of
+ * holders[0..n_holders) (global ids) nothing is enqueued and RSIM_E_DUPLICATE is returned. */
+rsim_status rsim_route_one_excl(rsim_t *h, int64_t r, int64_t now_us, const int32_t *holders, int32_t n_holders,
+                                int32_t *chosen, int64_t *hit_tokens, double *scores);
+/* InstanceSim.queue / .running (engine.py:212-213) of a local instance: 8 int64 per slot -- the FIFO
+ * queue in order, then the running list: request index, kind (0 queued / 1 running), pending,
+ * generated, hit blocks, input tokens, output tokens, flags (bit0: prefill scheduled). out may be
+ * NULL to query the counts. */
+rsim_status rsim_read_slots(rsim_t *h, int32_t instance, int64_t *out, int64_t cap, int64_t *n_queued,
+                            int64_t *n_running);
+/* Start of a run_trace on a handle with API state: no instance has a step scheduled
+ * (cluster.py:210-211, 247); queued requests wait for an arrival routed to their instance. */
+rsim_status rsim_unschedule(rsim_t *h);
 /* InstanceSim.enqueue(record r, now_us) on a given instance (engine.py:262-289). */
 rsim_status rsim_enqueue(rsim_t *h, int32_t instance, int64_t r, int64_t now_us, int64_t *hit_tokens);
 
@@ -197,6 +220,15 @@ rsim_status rsim_read_phase_times(rsim_t *h, uint64_t *out, int64_t n_decisions)
  * probe-ahead cycles; [16..19] its probe-ahead sections (setup, issue, evaluate, tail); zeros
  * otherwise. */
 rsim_status rsim_read_step_cycles(rsim_t *h, int64_t *out32);
+/* ClusterConfig.debug_checks' per-step checks, run now over every instance of the handle
+ * (engine.py:248-258 reconcile, kvcache.py:178-194 check_invariants); RSIM_E_INVARIANT with the
+ * instance and the failed check in rsim_last_error. Runs automatically after every decision and
+ * after the drain when cfg.debug_checks is set. */
+rsim_status rsim_check_invariants(rsim_t *h);
+/* Fault injection for the checker's tests: what = 0 pins the deepest KV$ entry of the local
+ * instance once more (its parent no longer covers the pin), 1 breaks the live aggregates,
+ * 2 ages the deepest entry's parent. */
+rsim_status rsim_debug_corrupt(rsim_t *h, int32_t instance, int32_t what);
 /* Number of kernels librsim launched since create (evidence for bench gpu_launches). */
 int64_t rsim_launch_count(const rsim_t *h);
 

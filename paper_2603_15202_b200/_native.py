@@ -43,8 +43,13 @@ _EXC = {
 }
 
 
+RSIM_ABI_VERSION = 2
+
+
 class Config(C.Structure):
+    """rsim_config (include/rsim.h); struct_size / abi_version are filled in on construction."""
     _fields_ = [
+        ("struct_size", C.c_uint32), ("abi_version", C.c_uint32),
         ("n_instances", C.c_int32), ("block_size", C.c_int32), ("capacity_blocks", C.c_int64),
         ("prefill_base_ms", C.c_double), ("prefill_per_token_ms", C.c_double),
         ("decode_base_ms", C.c_double), ("decode_per_seq_ms", C.c_double),
@@ -67,6 +72,11 @@ class Config(C.Structure):
         ("sim_decode_base_ms", C.c_double), ("sim_decode_per_seq_ms", C.c_double),
         ("sim_decode_per_ctx_token_ms", C.c_double),
     ]
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        self.struct_size = C.sizeof(Config)
+        self.abi_version = RSIM_ABI_VERSION
 
 
 _lib = None
@@ -119,11 +129,20 @@ def lib():
         "rsim_detector_finalize": ([P], C.c_int),
         "rsim_read_detector": ([P, P, I64, P, P], C.c_int),
         "rsim_detector_debug": ([P, P, I64], C.c_int),
+        "rsim_config_size": ([], C.c_size_t),
+        "rsim_check_invariants": ([P], C.c_int),
+        "rsim_debug_corrupt": ([P, I32, I32], C.c_int),
+        "rsim_route_one_excl": ([P, I64, I64, P, I32, P, P, P], C.c_int),
+        "rsim_read_slots": ([P, I32, P, I64, P, P], C.c_int),
+        "rsim_unschedule": ([P], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res
+    if L.rsim_config_size() != C.sizeof(Config):
+        raise RuntimeError(f"librsim's rsim_config is {L.rsim_config_size()} bytes, this binding's "
+                           f"{C.sizeof(Config)}: rebuild librsim.so from this tree")
     _lib = L
     return L
 
@@ -135,7 +154,8 @@ EXPORTED = ("rsim_create", "rsim_destroy", "rsim_last_error", "rsim_reset", "rsi
             "rsim_last_timings", "rsim_read_decision_ns", "rsim_launch_count", "rsim_rerun",
             "rsim_read_counters", "rsim_shard_bounds", "rsim_mailbox", "rsim_mailbox_ipc_handle",
             "rsim_set_peer", "rsim_open_peer_ipc", "rsim_load_detector", "rsim_detector_finalize",
-            "rsim_read_detector", "rsim_detector_debug")
+            "rsim_read_detector", "rsim_detector_debug", "rsim_config_size", "rsim_check_invariants",
+            "rsim_debug_corrupt", "rsim_route_one_excl", "rsim_read_slots", "rsim_unschedule")
 
 
 def _p(a):
@@ -237,12 +257,28 @@ class Handle:
         self._ck(self._L.rsim_read_step_log(self._h, _p(out), n.value, C.byref(n)))
         return out[: n.value], n.value
 
-    def route_one(self, r: int, now_us: int, want_scores: bool = True):
+    def route_one(self, r: int, now_us: int, want_scores: bool = True, holders=()):
+        """One route() decision; ``holders``: instances already holding the request id
+        (a decision for one of them raises DuplicateRequestError after the tie-break)."""
         ch = np.zeros(1, np.int32)
         ht = np.zeros(1, np.int64)
         sc = np.empty(self.n_local, np.float64) if want_scores else None
-        self._ck(self._L.rsim_route_one(self._h, r, now_us, _p(ch), _p(ht), _p(sc)))
+        hd = np.asarray(sorted(holders), np.int32)
+        self._ck(self._L.rsim_route_one_excl(self._h, r, now_us, _p(hd) if hd.size else None, int(hd.size),
+                                             _p(ch), _p(ht), _p(sc)))
         return int(ch[0]), int(ht[0]), sc
+
+    def slots(self, instance: int) -> np.ndarray:
+        """(n, 8) int64: the FIFO queue then the running list of a local instance (rsim_read_slots)."""
+        nq, nr = C.c_int64(), C.c_int64()
+        self._ck(self._L.rsim_read_slots(self._h, instance, None, 0, C.byref(nq), C.byref(nr)))
+        n = nq.value + nr.value
+        out = np.empty((max(n, 1), 8), np.int64)
+        self._ck(self._L.rsim_read_slots(self._h, instance, _p(out), n, C.byref(nq), C.byref(nr)))
+        return out[:n]
+
+    def unschedule(self):
+        self._ck(self._L.rsim_unschedule(self._h))
 
     def enqueue(self, instance: int, r: int, now_us: int) -> int:
         ht = np.zeros(1, np.int64)
@@ -355,6 +391,12 @@ class Handle:
     def open_peer_ipc(self, rank: int, handle: bytes):
         buf = (C.c_ubyte * 64).from_buffer_copy(handle)
         self._ck(self._L.rsim_open_peer_ipc(self._h, rank, buf))
+
+    def check_invariants(self):
+        self._ck(self._L.rsim_check_invariants(self._h))
+
+    def debug_corrupt(self, instance: int, what: int):
+        self._ck(self._L.rsim_debug_corrupt(self._h, instance, what))
 
     def launch_count(self) -> int:
         return int(self._L.rsim_launch_count(self._h))

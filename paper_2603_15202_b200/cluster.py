@@ -188,11 +188,10 @@ class _CacheProxy:
         self._sim, self._i = sim, idx
 
     def insert(self, blocks, now_us: int) -> int:
-        h = self._sim._device()
-        return h.cache_insert_keys(self._i, h.chain_keys(np.asarray(blocks, dtype=np.uint64)), now_us)
+        return self.insert_keys(self._sim._device().chain_keys(np.asarray(blocks, dtype=np.uint64)), now_us)
 
     def insert_keys(self, keys, now_us: int) -> int:
-        return self._sim._device().cache_insert_keys(self._i, keys, now_us)
+        return self._sim._do(("insert", self._i, np.asarray(keys, dtype=np.uint64).copy(), int(now_us)))
 
     def match_prefix(self, blocks) -> int:
         h = self._sim._device()
@@ -210,6 +209,25 @@ class _CacheProxy:
         return self._sim.config.cache.capacity_blocks
 
 
+@dataclass(frozen=True)
+class SlotView:
+    """One request on an instance (the reference's ``_Slot``, engine.py:114-145), read from the
+    device queue ring / running list."""
+    record: TraceRecord
+    hit_blocks: int
+    hit_tokens: int
+    pending: int
+    generated: int
+    enqueue_us: int
+    first_sched_us: int | None
+    index: int                       # the request's position among the sim's loaded requests
+
+    @property
+    def keys(self) -> list[int]:
+        from .hashing import chain_keys
+        return chain_keys(self.record.prefix_blocks)
+
+
 class _InstanceProxy:
     """``sim.instances[i]`` -- read/poke one instance's device state."""
 
@@ -221,13 +239,29 @@ class _InstanceProxy:
     def _row(self):
         return self._sim._device().instances()[self.id]
 
-    @property
-    def queue(self):
-        return tuple(range(int(self._row()[1])))
+    def _slots(self, kind: int) -> tuple:
+        sim = self._sim
+        h = sim._device()
+        rows = h.slots(self.id)
+        rows = rows[rows[:, 1] == kind]
+        out = []
+        for r in rows:
+            idx = int(r[0])
+            fs = int(h.request_times(idx, 1)[0][0])
+            ht = int(h.decisions(idx, 1)[1][0])
+            out.append(SlotView(sim._record(idx), int(r[4]), ht, int(r[2]), int(r[3]),
+                                int(sim._arrival_us(idx)), fs if fs >= 0 else None, idx))
+        return tuple(out)
 
     @property
-    def running(self):
-        return tuple(range(int(self._row()[0])))
+    def queue(self) -> tuple:
+        """The FIFO queue (engine.py:212), head first."""
+        return self._slots(0)
+
+    @property
+    def running(self) -> tuple:
+        """The running list (engine.py:213), in order."""
+        return self._slots(1)
 
     @property
     def busy_until_us(self) -> int:
@@ -242,9 +276,14 @@ class _InstanceProxy:
         return tuple(int(x) for x in self._row()[5:10])
 
     def enqueue(self, record: TraceRecord, now_us: int, keys=None) -> AdmissionInfo:
+        """InstanceSim.enqueue (engine.py:262-289): DuplicateRequestError when this instance
+        already holds the request id, before any state changes."""
         sim = self._sim
-        idx = sim._append(record)
-        ht = sim._device().enqueue(self.id, idx, now_us)
+        if self.id in sim._holders(record.request_id):
+            raise DuplicateRequestError(f"request {record.request_id} already present")
+        idx = sim._do(("load", PackedTrace.from_records([record]), np.array([now_us], np.int64)))
+        ht = sim._do(("enqueue", self.id, idx, int(now_us)))
+        sim._by_rid.setdefault(record.request_id, []).append(idx)
         hb = int(sim._read_hit_blocks(idx)) if ht else 0
         return AdmissionInfo(hb, ht, max(record.input_tokens - ht, 1))
 
@@ -255,8 +294,59 @@ class _StepLogOverflow(Exception):
         self.needed = needed
 
 
+def _max_sizing(a: Sizing, b: Sizing) -> Sizing:
+    return Sizing(max(a.queue_capacity, b.queue_capacity), max(a.expected_keys, b.expected_keys),
+                  max(a.history_capacity, b.history_capacity))
+
+
+class _HandlePool:
+    """Device handles of closed ClusterSims, reused (after rsim_reset) by the next ClusterSim with
+    the same native configuration -- the CUDA allocations of a 100k-request replay are not
+    repeated for every ``run()``, like a caching allocator. Bounded: at most ``limit`` idle
+    handles."""
+
+    def __init__(self, limit: int = 2):
+        self.limit = limit
+        self.idle: list[tuple[bytes, _native.Handle]] = []
+
+    def take(self, cfg: _native.Config) -> _native.Handle | None:
+        key = bytes(cfg)
+        for i, (k, h) in enumerate(self.idle):
+            if k == key:
+                del self.idle[i]
+                h.reset()
+                return h
+        return None
+
+    def give(self, h: _native.Handle) -> None:
+        self.idle.append((bytes(h.cfg), h))
+        while len(self.idle) > self.limit:
+            self.idle.pop(0)[1].close()
+
+    def clear(self) -> None:
+        while self.idle:
+            self.idle.pop()[1].close()
+
+
+_POOL = _HandlePool()
+# sizes a ClusterSim had to grow to, keyed by the native config it started from
+_LEARNED: dict[bytes, tuple[Sizing, int]] = {}
+
+
+def release_pool() -> None:
+    """Free the device memory of idle pooled handles."""
+    _POOL.clear()
+
+
 class ClusterSim:
-    """A cluster of instances plus one global routing policy, on the GPU."""
+    """A cluster of instances plus one global routing policy, on the GPU.
+
+    State persists across calls exactly as in the reference: ``route`` / ``enqueue`` /
+    ``cache.insert`` calls and successive ``run_trace`` calls all act on the same instances,
+    caches and TieBreaker counter, and each ``run_trace`` report covers every request routed
+    so far (the reference's Collector, cluster.py:98-101). The state-changing calls are logged
+    so that a device ring or table that turns out too small is regrown by replaying them onto
+    a larger handle (the device state is a pure function of the calls)."""
 
     def __init__(self, config: ClusterConfig, *, device: int = 0, record_steps: bool = True,
                  ctas: int = 0, warps_per_cta: int = 0):
@@ -269,49 +359,189 @@ class ClusterSim:
         self.record_steps = record_steps
         self._shape = (ctas, warps_per_cta)
         self._handle: _native.Handle | None = None
-        self._api_records: list[TraceRecord] = []
-        self._present: dict[int, int] = {}
+        self._sizing = sizing_for(None, config)
+        self._log_cap = 1 << 16 if record_steps else 0
+        self._ops: list = []                  # state-changing calls, replayed onto a regrown handle
+        self._parts: list[PackedTrace] = []   # loaded requests, in load order
+        self._arrival: list[np.ndarray] = []  # their arrival (route / enqueue time) in us
+        self._reported: list[np.ndarray] = []  # which of them the Collector reports (route / trace)
+        self._n = 0
+        self._by_rid: dict[int, list[int]] = {}   # request id -> loaded indices (duplicate checks)
+        self._runs = 0
+        self._first_key: bytes | None = None
         self.instances = [_InstanceProxy(self, i) for i in range(config.n_instances)]
 
     # -- device handle -----------------------------------------------------------------
-    def _make(self, sizing: Sizing, log_cap: int = 0) -> _native.Handle:
-        cfg = native_config(self.config, sizing, device=self.device, record_steps=self.record_steps,
-                            step_log_capacity=log_cap, ctas=self._shape[0], warps_per_cta=self._shape[1])
-        return _native.Handle(cfg)
+    def _native_cfg(self, sizing: Sizing, log_cap: int) -> _native.Config:
+        return native_config(self.config, sizing, device=self.device, record_steps=self.record_steps,
+                             step_log_capacity=log_cap, ctas=self._shape[0], warps_per_cta=self._shape[1])
 
     def _device(self) -> _native.Handle:
         if self._handle is None:
-            self._handle = self._make(sizing_for(None, self.config))
+            cfg = self._native_cfg(self._sizing, self._log_cap)
+            if self._first_key is None:
+                self._first_key = bytes(cfg)
+                if self._first_key in _LEARNED:
+                    self._sizing, self._log_cap = _LEARNED[self._first_key]
+                    cfg = self._native_cfg(self._sizing, self._log_cap)
+            self._handle = _POOL.take(cfg) or _native.Handle(cfg)
         return self._handle
 
     def close(self) -> None:
+        """Release the device state (the handle returns to the pool for the next ClusterSim)."""
+        if self._handle is not None:
+            _POOL.give(self._handle)
+            self._handle = None
+
+    def _rebuild(self, sizing: Sizing | None = None, log_cap: int | None = None) -> None:
+        """A larger handle with every logged call replayed onto it."""
         if self._handle is not None:
             self._handle.close()
             self._handle = None
+        if sizing is not None:
+            self._sizing = _max_sizing(self._sizing, sizing)
+        elif log_cap is None:
+            self._sizing = self._sizing.grown()
+        if log_cap is not None:
+            self._log_cap = max(self._log_cap, log_cap)
+        if self._first_key is not None:          # later sims of this shape start at the grown size
+            _LEARNED[self._first_key] = (self._sizing, self._log_cap)
+        stateful = False
+        for op, raised in self._ops:
+            try:
+                self._exec(op, replaying=True, stateful=stateful)
+            except raised or ():
+                pass
+            stateful = stateful or op[0] != "load"
+
+    def _do(self, op, expected: tuple = ()):
+        """Run a state-changing call, regrowing on a capacity signal; log it (with the exception
+        it raised, when that exception is part of the reference semantics)."""
+        stateful = any(o[0] != "load" for o, _ in self._ops)
+        for _attempt in range(8):
+            try:
+                res = self._exec(op, stateful=stateful)
+            except _native.CapacityError:
+                self._rebuild()
+                continue
+            except _StepLogOverflow as exc:
+                self._rebuild(log_cap=exc.needed + 1024)
+                continue
+            except expected as exc:
+                self._ops.append((op, type(exc)))
+                raise
+            self._ops.append((op, None))
+            return res
+        raise RuntimeError("device capacities kept overflowing")
+
+    def _exec(self, op, *, replaying: bool = False, stateful: bool = False):
+        h = self._device()
+        kind = op[0]
+        if kind == "load":
+            _, tr, arr = op
+            h.load(arr, tr.in_tokens, tr.out_tokens, tr.request_id, tr.blk_off, tr.blocks)
+            if replaying:                 # the bookkeeping of a logged load exists already
+                return None
+            first = self._n
+            self._parts.append(tr)
+            self._arrival.append(np.asarray(arr, np.int64))
+            self._reported.append(np.zeros(len(tr), bool))
+            self._n += len(tr)
+            return first
+        if kind == "route":
+            _, idx, now, holders = op
+            return h.route_one(idx, now, holders=holders)
+        if kind == "enqueue":
+            _, inst, idx, now = op
+            return h.enqueue(inst, idx, now)
+        if kind == "insert":
+            _, inst, keys, now = op
+            return h.cache_insert_keys(inst, keys, now)
+        if kind == "run":
+            # run_trace's loops start with no step scheduled (cluster.py:210-211, 247); a fresh
+            # handle has none anyway
+            _, first, count, det = op
+            if stateful:
+                h.unschedule()
+            if det is not None:
+                h.load_detector(*det)
+            if count:
+                h.replay(first, count)
+            # queued_at_last_arrival (cluster.py:222-223, 277-278): right after the last decision
+            queued = int(h.instances()[:, 1].sum()) if count else 0
+            h.drain(INT64_MAX)
+            if self.record_steps:
+                log, needed = h.step_log()
+                if log is None:
+                    raise _StepLogOverflow(needed)
+            return queued
+        raise ValueError(kind)
 
     # -- API-mode helpers -------------------------------------------------------------------
-    def _append(self, record: TraceRecord) -> int:
+    def _record(self, idx: int) -> TraceRecord:
+        for tr in self._parts:
+            if idx < len(tr):
+                return tr.record(idx)
+            idx -= len(tr)
+        raise IndexError(idx)
+
+    def _arrival_us(self, idx: int) -> int:
+        for a in self._arrival:
+            if idx < len(a):
+                return int(a[idx])
+            idx -= len(a)
+        raise IndexError(idx)
+
+    def _mark_reported(self, idx: int, n: int = 1) -> None:
+        base = 0
+        for m in self._reported:
+            if base <= idx < base + len(m):
+                m[idx - base: idx - base + n] = True
+                return
+            base += len(m)
+
+    def _holders(self, request_id: int) -> set[int]:
+        """Instances where the request id is present (InstanceSim._present: enqueued, not finished)."""
         h = self._device()
-        tr = PackedTrace.from_records([record])
-        h.load(tr.arrival_us, tr.in_tokens, tr.out_tokens, tr.request_id, tr.blk_off, tr.blocks)
-        self._api_records.append(record)
-        return len(self._api_records) - 1
+        out = set()
+        for idx in self._by_rid.get(request_id, ()):
+            ch, _ = h.decisions(idx, 1)
+            fin = h.request_times(idx, 1)[2]
+            if ch[0] >= 0 and fin[0] < 0:
+                out.add(int(ch[0]))
+        return out
 
     def _read_hit_blocks(self, idx: int) -> int:
-        rec = self._api_records[idx]
+        rec = self._record(idx)
         _, ht = self._device().decisions(idx, 1)
         return min(-(-int(ht[0]) // self.block_size), len(rec.prefix_blocks))
 
+    def _grow_for(self, trace: PackedTrace | None) -> None:
+        need = sizing_for(trace, self.config) if trace is not None and len(trace) else None
+        if need is not None and self._handle is None and not self._ops:
+            self._sizing = need                  # a fresh sim sizes from its first trace
+            return
+        if need is not None and (need.queue_capacity > self._sizing.queue_capacity or
+                                 need.expected_keys > self._sizing.expected_keys or
+                                 need.history_capacity > self._sizing.history_capacity):
+            if self._handle is None:
+                self._sizing = _max_sizing(self._sizing, need)
+            else:
+                self._rebuild(need)
+
     # -- one routing decision (cluster.py:130-154) ---------------------------------------
     def route(self, record: TraceRecord, now_us: int) -> RoutingDecision:
-        prior = self._present.get(record.request_id)
-        if prior is not None:
-            _, _, fin = self._device().request_times(prior, 1)
-            if fin[0] < 0:
-                raise DuplicateRequestError(f"request {record.request_id} already present")
-        idx = self._append(record)
-        chosen, _ht, scores = self._device().route_one(idx, now_us)
-        self._present[record.request_id] = idx
+        """Snapshot, score, enqueue on the winner. A request id already present on the chosen
+        instance raises DuplicateRequestError after the decision (the TieBreaker counter moved),
+        as InstanceSim.enqueue does (engine.py:266-267)."""
+        if self.config.detector is not None:
+            from .config import UnsupportedConfigError
+            raise UnsupportedConfigError("route() with the hotspot detector: replay a trace with run_trace")
+        holders = tuple(sorted(self._holders(record.request_id)))
+        idx = self._do(("load", PackedTrace.from_records([record]), np.array([now_us], np.int64)))
+        chosen, _ht, scores = self._do(("route", idx, int(now_us), holders), expected=(DuplicateRequestError,))
+        self._by_rid.setdefault(record.request_id, []).append(idx)
+        self._mark_reported(idx)
         return RoutingDecision(chosen=chosen, scores={i: float(s) for i, s in enumerate(scores)},
                                filtered=frozenset(), kind=self.config.policy.kind, time_us=now_us)
 
@@ -324,62 +554,99 @@ class ClusterSim:
                 raise ValueError("duplicate request id in trace")
             if (np.diff(trace.arrival_s) < 0).any():
                 raise ValueError("trace arrivals are not sorted")
-        if self._api_records:
-            raise NotImplementedError("run_trace after route()/enqueue() API calls on the same ClusterSim")
-        sizing = sizing_for(trace, self.config)
+        det = self.config.detector
+        if det is not None and self._ops:
+            from .config import UnsupportedConfigError
+            raise UnsupportedConfigError("the hotspot detector replays one trace per ClusterSim on the device")
+        if len(trace) and self._by_rid and any(self._holders(int(r)) for r in trace.request_id
+                                               if int(r) in self._by_rid):
+            from .config import UnsupportedConfigError
+            raise UnsupportedConfigError("trace request ids still present from earlier route()/enqueue() calls")
+        fresh = not self._ops
+        self._grow_for(trace if fresh else _concat_all(self._parts + [trace]))
+        if self.record_steps:
+            need = self._log_cap_for(trace)
+            if need > self._log_cap:
+                if self._handle is None:
+                    self._log_cap = need
+                else:
+                    self._rebuild(log_cap=need)
         n = len(trace)
-        log_cap = max(1 << 16, 8 * n + int(trace.out_tokens.sum()) // 2) if self.record_steps else 0
-        for _attempt in range(6):
-            try:
-                return self._replay(trace, sizing, log_cap)
-            except _native.CapacityError:
-                self.close()
-                sizing = sizing.grown()
-            except _StepLogOverflow as exc:
-                self.close()
-                log_cap = exc.needed + 1024
-        raise RuntimeError("device capacities kept overflowing")
+        first = self._do(("load", trace, trace.arrival_us)) if n else self._n
+        if n:
+            self._mark_reported(first, n)
+        dl = None
+        if det is not None and n:
+            tid, ex_off, ex_len, ckey = detector_classes(trace, det.class_key_blocks)
+            windows = int(trace.arrival_us[-1] / 1e6 / det.window_s) + 3
+            dl = (tid, ex_off, ex_len, ckey, windows * det.top_k_classes + det.top_k_classes)
+        queued_last = self._do(("run", first, n, dl))
+        self._runs += 1
+        return self._report(trace, queued_last)
 
-    def _replay(self, trace: PackedTrace, sizing: Sizing, log_cap: int) -> RunReport:
-        n = len(trace)
-        if self._handle is None:
-            self._handle = self._make(sizing, log_cap)
-        h = self._handle
-        h.reset()
-        queued_last = 0
-        if n:
-            h.load(trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.request_id, trace.blk_off,
-                   trace.blocks)
-            det = self.config.detector
-            if det is not None:
-                tid, ex_off, ex_len, ckey = detector_classes(trace, det.class_key_blocks)
-                windows = int(trace.arrival_us[-1] / 1e6 / det.window_s) + 3
-                h.load_detector(tid, ex_off, ex_len, ckey, windows * det.top_k_classes + det.top_k_classes)
-            h.replay(0, n)
-            queued_last = int(h.instances()[:, 1].sum())
-        h.drain(INT64_MAX)
+    def _log_cap_for(self, trace: PackedTrace) -> int:
+        n = self._n + len(trace)
+        out = int(trace.out_tokens.sum()) + sum(int(p.out_tokens.sum()) for p in self._parts)
+        return max(1 << 16, 8 * n + out // 2)
+
+    def _report(self, trace: PackedTrace, queued_last: int) -> RunReport:
+        h = self._device()
+        N = self._n
         inst = h.instances()
-        end_us = int(max(int(trace.arrival_us[-1]) if n else 0, int(inst[:, 10].max()) if n else 0))
+        last = int(trace.arrival_us[-1]) if len(trace) else 0
+        end_us = int(max(last, int(inst[:, 10].max()) if N else 0))
         cols = {}
-        if n:
-            cols["chosen"], cols["hit_tokens"] = h.decisions(0, n)
-            cols["first_sched_us"], cols["first_token_us"], cols["finish_us"] = h.request_times(0, n)
-            cols["route_bs"] = h.route_bs(0, n)
+        rep_mask = np.concatenate(self._reported) if self._reported else np.zeros(0, bool)
+        alltr = _concat_all(self._parts) if self._parts else None
+        if N:
+            ch, ht = h.decisions(0, N)
+            fs, ft, fin = h.request_times(0, N)
+            bs = h.route_bs(0, N)
+            full = {"chosen": ch, "hit_tokens": ht, "first_sched_us": fs, "first_token_us": ft,
+                    "finish_us": fin, "route_bs": bs}
+            cols = {k: v[rep_mask] for k, v in full.items()}
+            alltr = _with_arrival(alltr, np.concatenate(self._arrival))
+            alltr = _take(alltr, np.flatnonzero(rep_mask))
         log = None
         if self.record_steps:
             log, needed = h.step_log()
-            if log is None:
-                raise _StepLogOverflow(needed)
         rep = RunReport(self.config.policy.kind, self.config.seed, self.config.n_instances, self.block_size,
-                        trace=trace, columns=cols, step_log=log, end_us=end_us,
-                        queued_at_last_arrival=queued_last)
+                        trace=alltr, columns=cols, step_log=log, end_us=end_us,
+                        queued_at_last_arrival=queued_last, hash_trace=trace)
         if self.config.detector is not None:              # cluster.py:194-201
             rep.detector_enabled = True
-            if n:
+            if len(trace):
                 h.detector_finalize()
                 rows, rep.first_violation_us = h.read_detector()
                 rep.detector_rows = [DetectorRow(*r) for r in rows]
         return rep
+
+
+def _concat_all(parts: list[PackedTrace]) -> PackedTrace:
+    from .trace import concat_packed
+    return parts[0] if len(parts) == 1 else concat_packed(parts)
+
+
+def _with_arrival(tr: PackedTrace, arrival_us: np.ndarray) -> PackedTrace:
+    """The loaded requests as the Collector saw them: arrival = the route / enqueue time."""
+    if np.array_equal(tr.arrival_us, arrival_us):
+        return tr
+    out = PackedTrace(tr.request_id, tr.arrival_s, tr.in_tokens, tr.out_tokens, tr.class_key, tr.blk_off, tr.blocks)
+    out.arrival_us = np.asarray(arrival_us, np.int64)
+    return out
+
+
+def _take(tr: PackedTrace, idx: np.ndarray) -> PackedTrace:
+    if idx.size == len(tr):
+        return tr
+    B = np.diff(tr.blk_off)[idx]
+    off = np.zeros(idx.size + 1, np.int64)
+    np.cumsum(B, out=off[1:])
+    blocks = np.concatenate([tr.blocks[tr.blk_off[i]:tr.blk_off[i + 1]] for i in idx]) if idx.size else tr.blocks[:0]
+    out = PackedTrace(tr.request_id[idx], tr.arrival_s[idx], tr.in_tokens[idx], tr.out_tokens[idx],
+                      tr.class_key[idx], off, blocks)
+    out.arrival_us = tr.arrival_us[idx]
+    return out
 
 
 def run(records, config: ClusterConfig, **kw) -> RunReport:

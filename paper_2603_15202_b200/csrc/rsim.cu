@@ -15,6 +15,7 @@
 
 #include "../../include/rsim.h"
 #include "rsim_kernels.cuh"
+#include "rsim_check.cuh"
 
 namespace {
 
@@ -103,6 +104,11 @@ struct rsim {
     DevArr<u64> arena;             // API-inserted chain keys (named by eviction runs)
     i64 narena = 0;
     unsigned short *crit = nullptr; // diagnostics: per (decision, warp) phase records
+    std::vector<i64> api_segs;      // debug_checks: API-inserted chains (instance, arena offset, length)
+    DevArr<i64> dsegs;
+    DevArr<u32> seen;               // debug_checks: per-slot "named by a chain" bits
+    DevArr<u32> dupmask;            // route() API: instances holding the request id (bitmap)
+    const u32 *cur_dupmask = nullptr;
     i64 crit_cap = 0;
 };
 
@@ -179,10 +185,21 @@ static rsim_status check_device_error(rsim_t *h) {
     CK(h, cudaMemsetAsync(h->errbuf, 0, 4 * sizeof(int), h->stream));
     switch (e[0]) {
         case DEV_E_CACHE_FULL: return fail(h, RSIM_E_CACHE_FULL, "pinned blocks exceed capacity");
-        case DEV_E_INVARIANT: return fail(h, RSIM_E_INVARIANT, "unpin of a chain that is not pinned / missing chain");
+        case DEV_E_INVARIANT: {
+            static const char *what[] = {"unpin of a chain that is not pinned / missing chain",
+                "aggregates != recount (InstanceSim.reconcile)", "entry with depth < 1 or pin < 0",
+                "occupancy counter != present entries", "occupancy over capacity",
+                "entry depth != its chain position", "prefix closure violated (parent missing)",
+                "parent older than child breaks LRU eviction safety", "pin must cover the path",
+                "present key on no chain of the instance"};
+            const int c = (e[2] >= 1 && e[2] <= 9) ? e[2] : 0;
+            if (c) return fail(h, RSIM_E_INVARIANT, "instance %d: %s", e[1], what[c]);
+            return fail(h, RSIM_E_INVARIANT, "%s", what[0]);
+        }
         case DEV_E_QUEUE_OVERFLOW: return fail(h, RSIM_E_QUEUE_OVERFLOW, "instance queue ring full (queue_capacity=%d)", 1 << h->qlog2);
         case DEV_E_TABLE_FULL: return fail(h, RSIM_E_TABLE_FULL, "instance KV$ table over 3/4 load (slots=%d)", 1 << h->slog2);
         case 11: return fail(h, RSIM_E_NO_INSTANCES, "no instances to route to");
+        case DEV_E_DUPLICATE: return fail(h, RSIM_E_DUPLICATE, "request already present on the chosen instance");
         case DEV_E_DETECTOR: return fail(h, RSIM_E_DETECTOR, "detector capacity exceeded (more than %d classes re-evaluated at once, or a window bucket ring overflow)", RSIM_DLMAX);
         case DEV_E_HISTORY_OVERFLOW: return fail(h, RSIM_E_HISTORY_OVERFLOW, "instance view-history ring full (history_capacity=%d)", 1 << h->hlog2);
         case DEV_E_COMM: return fail(h, RSIM_E_COMM, "timed out waiting for a peer rank's decision partial");
@@ -225,6 +242,7 @@ static rsim_status init_state(rsim_t *h) {
     CK(h, cudaMemsetAsync(h->ctr, 0, 48 * sizeof(u64), h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     h->R = 0; h->nblk = 0; h->nout = 0; h->narena = 0;
+    h->api_segs.clear();
     // blk_off / ooff hold a leading 0
     CK(h, h->blk_off.reserve(1, 0, h->stream));
     CK(h, h->ooff.reserve(1, 0, h->stream));
@@ -237,11 +255,16 @@ static rsim_status init_state(rsim_t *h) {
 extern "C" {
 
 const char *rsim_last_error(const rsim_t *h) { return h ? h->err : g_create_err; }
+size_t rsim_config_size(void) { return sizeof(rsim_config); }
 int64_t rsim_launch_count(const rsim_t *h) { return h ? h->launches : 0; }
 
 rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     if (!cfg || !out) return fail(nullptr, RSIM_E_INVALID, "null argument");
     *out = nullptr;
+    if (cfg->struct_size != sizeof(rsim_config) || cfg->abi_version != RSIM_ABI_VERSION)
+        return fail(nullptr, RSIM_E_INVALID, "rsim_config layout mismatch: struct_size %u / abi_version %u, "
+                    "this librsim expects %zu / %d", cfg->struct_size, cfg->abi_version, sizeof(rsim_config),
+                    RSIM_ABI_VERSION);
     const rsim_config &c = *cfg;
     if (c.n_instances < 1) return fail(nullptr, RSIM_E_INVALID, "n_instances must be >= 1");
     if (c.block_size < 1) return fail(nullptr, RSIM_E_INVALID, "block_size must be >= 1");
@@ -380,6 +403,7 @@ void rsim_destroy(rsim_t *h) {
     void *ps[] = {h->inst, h->qbuf, h->rbuf, h->tkeys, h->tmeta, h->tie, h->errbuf, h->flag, h->log, h->log_n,
                   h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs, h->crit, h->hring,
                   h->dtot, h->dglob, h->simj};
+    h->dsegs.free_(); h->seen.free_(); h->dupmask.free_();
     h->ddbg.free_(); h->dtid.free_(); h->dtw.free_(); h->dtex.free_(); h->dbk.free_(); h->drows.free_(); h->dtkey.free_(); h->dtr.free_();
     h->arena.free_();
     for (int i = 0; i < 8; i++) if (h->peer_ipc[i] && h->peer[i]) cudaIpcCloseMemHandle(h->peer[i]);
@@ -472,6 +496,7 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     }
     Params P = make_params(h);
     P.scores = scores_dev;
+    P.dupmask = h->cur_dupmask;
     if (P.dtid != nullptr && !P.dsm && h->C > 1)
         return fail(h, RSIM_E_DETECTOR, "%d detector classes do not fit in shared memory next to the instance shard; "
                     "use ctas=1", h->dT);
@@ -511,26 +536,88 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     return check_device_error(h);
 }
 
+// debug_checks (cluster.py:168-170): reconcile + check_invariants of every instance on device
+static rsim_status run_checks(rsim_t *h) {
+    const size_t words = (((size_t)h->N << h->slog2) + 31) / 32;
+    CK(h, h->seen.reserve(words, 0, h->stream));
+    CK(h, cudaMemsetAsync(h->seen.p, 0, words * sizeof(u32), h->stream));
+    const i64 nseg = (i64)h->api_segs.size() / 3;
+    CK(h, h->dsegs.reserve(h->api_segs.size() + 3, 0, h->stream));
+    if (nseg) CK(h, cudaMemcpyAsync(h->dsegs.p, h->api_segs.data(), h->api_segs.size() * sizeof(i64),
+                                    cudaMemcpyHostToDevice, h->stream));
+    const int threads = 128, blocks = (h->N * 32 + threads - 1) / threads;
+    check_invariants_kernel<<<blocks, threads, 0, h->stream>>>(make_params(h), h->R, h->dsegs.p, nseg, h->seen.p);
+    h->launches++;
+    CK(h, cudaGetLastError());
+    return check_device_error(h);
+}
+
 rsim_status rsim_replay(rsim_t *h, int64_t first, int64_t count) {
     if (!h) return RSIM_E_INVALID;
     if (first < 0 || count < 0 || first + count > h->R) return fail(h, RSIM_E_INVALID, "decision range out of the loaded trace");
     if (count == 0) return RSIM_OK;
     CK(h, cudaSetDevice(h->cfg.device));
+    if (h->cfg.debug_checks) {      // one decision per launch, the checks after each (its steps ran before it)
+        float tot = 0;
+        for (i64 k = first; k < first + count; k++) {
+            rsim_status st = launch_replay(h, k, k + 1, 0, MODE_REPLAY, -1, nullptr, &h->last_replay_ms);
+            if (st) return st;
+            tot += h->last_replay_ms;
+            if ((st = run_checks(h))) return st;
+        }
+        h->last_replay_ms = tot;
+        return RSIM_OK;
+    }
     return launch_replay(h, first, first + count, 0, MODE_REPLAY, -1, nullptr, &h->last_replay_ms);
 }
 
 rsim_status rsim_drain(rsim_t *h, int64_t until_us) {
     if (!h) return RSIM_E_INVALID;
     CK(h, cudaSetDevice(h->cfg.device));
-    return launch_replay(h, 0, 0, until_us, MODE_DRAIN, -1, nullptr, &h->last_drain_ms);
+    rsim_status st = launch_replay(h, 0, 0, until_us, MODE_DRAIN, -1, nullptr, &h->last_drain_ms);
+    if (st == RSIM_OK && h->cfg.debug_checks) st = run_checks(h);
+    return st;
+}
+rsim_status rsim_check_invariants(rsim_t *h) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    return run_checks(h);
+}
+rsim_status rsim_debug_corrupt(rsim_t *h, int32_t instance, int32_t what) {
+    if (!h) return RSIM_E_INVALID;
+    if (instance < 0 || instance >= h->N || what < 0 || what > 2) return fail(h, RSIM_E_INVALID, "bad fault");
+    CK(h, cudaSetDevice(h->cfg.device));
+    debug_corrupt_kernel<<<1, 32, 0, h->stream>>>(make_params(h), instance, what);
+    h->launches++;
+    CK(h, cudaGetLastError());
+    CK(h, cudaStreamSynchronize(h->stream));
+    return RSIM_OK;
 }
 
 rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen, int64_t *hit_tokens, double *scores) {
+    return rsim_route_one_excl(h, r, now_us, nullptr, 0, chosen, hit_tokens, scores);
+}
+rsim_status rsim_route_one_excl(rsim_t *h, int64_t r, int64_t now_us, const int32_t *holders, int32_t n_holders,
+                                int32_t *chosen, int64_t *hit_tokens, double *scores) {
     if (!h) return RSIM_E_INVALID;
     if (h->cfg.det_on) return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls with the hotspot detector: use a trace replay");
     if (r < 0 || r >= h->R) return fail(h, RSIM_E_INVALID, "request index out of range");
     CK(h, cudaSetDevice(h->cfg.device));
+    const u32 *dm = nullptr;
+    if (n_holders > 0) {
+        const size_t words = ((size_t)h->cfg.n_instances + 31) / 32;
+        std::vector<u32> m(words, 0u);
+        for (int i = 0; i < n_holders; i++) {
+            if (holders[i] < 0 || holders[i] >= h->cfg.n_instances) return fail(h, RSIM_E_INVALID, "holder out of range");
+            m[holders[i] >> 5] |= 1u << (holders[i] & 31);
+        }
+        CK(h, h->dupmask.reserve(words, 0, h->stream));
+        CK(h, cudaMemcpy(h->dupmask.p, m.data(), words * sizeof(u32), cudaMemcpyHostToDevice));
+        dm = h->dupmask.p;
+    }
+    h->cur_dupmask = dm;
     rsim_status st = launch_replay(h, r, r + 1, now_us, MODE_ROUTE, -1, scores ? h->scores : nullptr, nullptr);
+    h->cur_dupmask = nullptr;
     if (st != RSIM_OK) return st;
     if (chosen) CK(h, cudaMemcpy(chosen, h->chosen.p + r, sizeof(int), cudaMemcpyDeviceToHost));
     if (hit_tokens) CK(h, cudaMemcpy(hit_tokens, h->hit_tokens.p + r, sizeof(i64), cudaMemcpyDeviceToHost));
@@ -544,6 +631,52 @@ rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen
                 memcpy(scores, bsv.data(), h->N * sizeof(double));
         }
     }
+    return RSIM_OK;
+}
+
+// InstanceSim.queue / .running of one local instance (engine.py:212-213): 8 int64 per slot, the
+// FIFO queue in order, then the running list in order: request index, kind (0 queued, 1 running),
+// pending prefill tokens, generated tokens, hit blocks, input tokens, output tokens, flags.
+rsim_status rsim_read_slots(rsim_t *h, int32_t instance, int64_t *out, int64_t cap, int64_t *n_queued,
+                            int64_t *n_running) {
+    if (!h) return RSIM_E_INVALID;
+    if (instance < 0 || instance >= h->N) return fail(h, RSIM_E_INVALID, "instance out of range");
+    CK(h, cudaSetDevice(h->cfg.device));
+    CK(h, cudaStreamSynchronize(h->stream));
+    Inst s;
+    CK(h, cudaMemcpy(&s, h->inst + instance, sizeof(Inst), cudaMemcpyDeviceToHost));
+    if (n_queued) *n_queued = s.q;
+    if (n_running) *n_running = s.r;
+    if (!out) return RSIM_OK;
+    if (cap < (i64)s.q + s.r) return fail(h, RSIM_E_INVALID, "slot buffer too small (%d needed)", s.q + s.r);
+    const int qcap = 1 << h->qlog2;
+    std::vector<Ent> ring(qcap), run(std::max(s.r, 1));
+    CK(h, cudaMemcpy(ring.data(), h->qbuf + ((size_t)instance << h->qlog2), qcap * sizeof(Ent), cudaMemcpyDeviceToHost));
+    if (s.r) CK(h, cudaMemcpy(run.data(), h->rbuf + (size_t)instance * h->cfg.max_batch_requests, s.r * sizeof(Ent),
+                              cudaMemcpyDeviceToHost));
+    int64_t *o = out;
+    for (int j = 0; j < s.q; j++, o += 8) {
+        const Ent &e = ring[(s.q_head + j) & (qcap - 1)];
+        o[0] = e.req; o[1] = 0; o[2] = e.v; o[3] = 0; o[4] = e.hb; o[5] = e.in; o[6] = e.out; o[7] = e.flags;
+    }
+    for (int j = 0; j < s.r; j++, o += 8) {      // finish step v = join step + out - 1
+        const Ent &e = run[j];
+        o[0] = e.req; o[1] = 1; o[2] = 0; o[3] = (i64)e.out - 1 - (e.v - s.step_idx); o[4] = e.hb; o[5] = e.in;
+        o[6] = e.out; o[7] = e.flags;
+    }
+    return RSIM_OK;
+}
+
+// run_trace's loops start with no step scheduled (cluster.py:210-211, 247): route()/enqueue() API
+// calls before it leave their instances idle-but-queued until an arrival is routed there.
+rsim_status rsim_unschedule(rsim_t *h) {
+    if (!h) return RSIM_E_INVALID;
+    CK(h, cudaSetDevice(h->cfg.device));
+    CK(h, cudaStreamSynchronize(h->stream));
+    std::vector<Inst> hs(h->N);
+    CK(h, cudaMemcpy(hs.data(), h->inst, h->N * sizeof(Inst), cudaMemcpyDeviceToHost));
+    for (auto &s : hs) s.next_step = RSIM_NONE;
+    CK(h, cudaMemcpy(h->inst, hs.data(), h->N * sizeof(Inst), cudaMemcpyHostToDevice));
     return RSIM_OK;
 }
 
@@ -576,6 +709,7 @@ rsim_status rsim_cache_insert_keys(rsim_t *h, int32_t instance, const uint64_t *
     i64 a0 = 0;
     rsim_status st = arena_append(h, keys, n, &a0);
     if (st) return st;
+    h->api_segs.insert(h->api_segs.end(), {(i64)instance, a0, (i64)n});
     cache_op_kernel<<<1, 32, 0, h->stream>>>(make_params(h), instance, 0, a0, (int)n, now_us, h->scratch_res);
     h->launches++;
     CK(h, cudaGetLastError());

@@ -21,6 +21,7 @@ typedef unsigned int u32;
 
 // Error codes (match rsim_status in include/rsim.h)
 #define DEV_E_CACHE_FULL 3
+#define DEV_E_DUPLICATE 4
 #define DEV_E_INVARIANT 5
 #define DEV_E_QUEUE_OVERFLOW 7
 #define DEV_E_TABLE_FULL 8
@@ -140,6 +141,9 @@ struct Params {
     // small shards: this CTA's running lists live in shared memory during a launch (byte offset of
     // the region in dynamic shared memory; 0 = global rbuf)
     int rsm_off;
+    // route() API: instances (global-id bitmap) already holding the routed request id -- a decision
+    // for one of them raises DuplicateRequestError after the tie-break (engine.py:266-267); null = none
+    const u32 *dupmask;
 };
 
 // running list of instance gi: shared memory (a launch of a small shard) or HBM

@@ -1208,6 +1208,10 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     st_async_16(&dctl->own[par][0], &dctl->mbd[par], (u32)lane, (u64)(u32)h, (u64)WB.prod[s]);
                 int werr = 0;
                 flush_touch_pin(P, WB.fin, lane, &WB.werr);      // (normally already run after the publish)
+                const int gch = P.gbase + base + l0 + s;
+                if (mode == MODE_ROUTE && P.dupmask != nullptr && ((P.dupmask[gch >> 5] >> (gch & 31)) & 1u)) {
+                    if (lane == 0) WB.werr = DEV_E_DUPLICATE;          // chosen (the counter moved), never enqueued
+                } else
                 commit(P, st + l0 + s, base + l0 + s, k, h, R.t, R.keys,
                        (s < 2 && nmine < 2 && !(((stale_slots | sparse_probe) >> s) & 1u)) ? WB.slot[par][s] : nullptr,
                        R.a, R.B, R.in, R.out, R.oa, lane, werr, WB.fin, FILTER && P.stal > 0);

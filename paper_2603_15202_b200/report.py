@@ -86,7 +86,7 @@ class RunReport:
 
     def __init__(self, policy_kind: str, seed: int, n_instances: int, block_size: int, trace=None,
                  columns: dict | None = None, step_log: np.ndarray | None = None,
-                 end_us: int = 0, queued_at_last_arrival: int = 0):
+                 end_us: int = 0, queued_at_last_arrival: int = 0, hash_trace=None):
         self.policy_kind = policy_kind
         self.seed = seed
         self.n_instances = n_instances
@@ -97,6 +97,7 @@ class RunReport:
         self.end_us = end_us
         self.queued_at_last_arrival = queued_at_last_arrival
         self._trace = trace
+        self._hash_trace = trace if hash_trace is None else hash_trace   # run_trace's own records
         self.columns = columns or {}
         self._step_log = step_log
         self._requests = None
@@ -173,7 +174,7 @@ class RunReport:
         """sha256 over ``f"{id}:{arrival_us}\\n"`` (reference cluster.py:184-187)."""
         if self._hash is None:
             d = hashlib.sha256()
-            tr = self._trace
+            tr = self._hash_trace
             if tr is not None:
                 for rid, t in zip(tr.request_id.tolist(), tr.arrival_us.tolist()):
                     d.update(f"{rid}:{t}\n".encode())

@@ -1,0 +1,54 @@
+"""Stateful drop-in API sessions against the reference (tests/golden/api_sessions.json, made by
+tools/make_api_golden.py from the reference's ClusterSim): route() / enqueue() / cache.insert()
+followed by run_trace(), run_trace() twice on one sim (state and Collector persist,
+cluster.py:98-201), duplicate request ids (DuplicateRequestError after the tie-break,
+engine.py:266-267), and the instance queues (engine.py:212-213)."""
+import json
+import os
+import sys
+
+import pytest
+
+import golden_cases as G
+
+pytestmark = pytest.mark.gpu
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+
+
+def _ours():
+    from paper_2603_15202_b200.cluster import ClusterSim
+    from paper_2603_15202_b200.config import DuplicateRequestError
+    return ClusterSim, (lambda tr: tr.records()), DuplicateRequestError
+
+
+@pytest.mark.parametrize("name", ["route_then_run", "run_twice", "duplicates", "enqueue_dup", "small_batch_queues"])
+def test_session_matches_reference(name):
+    import make_api_golden as M
+    from paper_2603_15202_b200 import workloads as W
+    want = json.load(open(os.path.join(G.GOLDEN, "api_sessions.json")))[name]
+    cfg, steps = M.SESSIONS[name]
+    trace = W.config1_chatbot()[0].slice(600)
+    got = M.run_session(cfg, steps, trace, _ours())
+    got = json.loads(json.dumps(got))
+    assert len(got) == len(want)
+    for i, (g, w) in enumerate(zip(got, want)):
+        assert g == w, f"step {i} ({steps[i]}): {str(g)[:300]} != {str(w)[:300]}"
+
+
+def test_session_survives_regrow():
+    """A queue ring too small for the API calls: the sim regrows the handle by replaying its
+    logged calls, and the session still matches the reference."""
+    import make_api_golden as M
+    from paper_2603_15202_b200 import cluster, workloads as W
+    want = json.load(open(os.path.join(G.GOLDEN, "api_sessions.json")))["small_batch_queues"]
+    cfg, steps = M.SESSIONS["small_batch_queues"]
+    trace = W.config1_chatbot()[0].slice(600)
+    real = cluster.sizing_for
+    try:
+        cluster.sizing_for = lambda t, c: cluster.Sizing(16, 64) if t is None else real(t, c)
+        cluster._LEARNED.clear()
+        got = json.loads(json.dumps(M.run_session(cfg, steps, trace, _ours())))
+    finally:
+        cluster.sizing_for = real
+        cluster._LEARNED.clear()
+    assert got == want

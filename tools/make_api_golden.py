@@ -1,0 +1,103 @@
+"""Golden stateful-API sessions from the REFERENCE's ClusterSim: route() / enqueue() /
+cache.insert() calls, run_trace() after them and a second run_trace() on the same sim
+(cluster.py:130-201), duplicate request ids (engine.py:266-267), and the instance queues
+those calls leave behind (engine.py:212-213).
+
+    python tools/make_api_golden.py      # writes tests/golden/api_sessions.json
+
+Each session is a list of steps; tests/test_api_sessions.py replays the same steps on the
+device drop-in and compares every recorded value."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from refcompat import import_reference, to_ref_config, to_ref_records  # noqa: E402
+
+from paper_2603_15202_b200 import workloads as W  # noqa: E402
+from paper_2603_15202_b200.config import CacheConfig, ClusterConfig, CostModel, PolicyConfig  # noqa: E402
+
+SESSIONS = {
+    # name: (config, steps); a step is ("route", i) / ("enqueue", inst, i) / ("insert", inst, i, now) /
+    # ("run", lo, hi) / ("route_dup", i, now) / ("queues",) over records of the chat trace
+    "route_then_run": (ClusterConfig(n_instances=4, seed=1),
+                       [("insert", 0, 0, 0)] + [("route", i) for i in range(1, 27)]
+                       + [("queues",), ("run", 27, 260), ("queues",), ("run", 260, 400)]),
+    # (a bare enqueue() before run_trace makes the reference's Collector raise KeyError on the
+    # request's first step -- metrics.py:132 -- so enqueue() appears only in API-only sessions)
+    "run_twice": (ClusterConfig(n_instances=6, cache=CacheConfig(16, 600), seed=2),
+                  [("run", 0, 250), ("run", 250, 500), ("route", 500), ("run", 501, 600)]),
+    "duplicates": (ClusterConfig(n_instances=3, policy=PolicyConfig(kind="vllm"), seed=0),
+                   [("route", 0), ("route", 1)] + [("route_dup", j % 2, 10 * j) for j in range(2, 26)]
+                   + [("route", 2), ("queues",)]),
+    "enqueue_dup": (ClusterConfig(n_instances=2, seed=0),
+                    [("enqueue", 0, 0), ("enqueue_dup", 0, 0), ("enqueue", 1, 0), ("route", 1), ("queues",)]),
+    "small_batch_queues": (ClusterConfig(n_instances=3, cost_model=CostModel(chunk_tokens=64, max_batch_requests=2), seed=5),
+                           [("route", i) for i in range(40)] + [("queues",), ("run", 40, 120)]),
+}
+
+
+def run_session(cfg, steps, trace, api):
+    """api: (ClusterSim class, record converter, DuplicateRequestError). Returns the observations."""
+    Sim, conv, Dup = api
+    sim = Sim(cfg)
+    recs = conv(trace)
+    obs = []
+    for st in steps:
+        kind = st[0]
+        if kind == "route":
+            r = recs[st[1]]
+            d = sim.route(r, int(trace.arrival_us[st[1]]))
+            obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)]])
+        elif kind == "route_dup":
+            r = recs[st[1]]
+            try:
+                d = sim.route(r, st[2])
+                obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)]])
+            except Dup:
+                obs.append(["dup"])
+        elif kind == "enqueue":
+            a = sim.instances[st[1]].enqueue(recs[st[2]], int(trace.arrival_us[st[2]]))
+            obs.append(["enqueue", a.hit_blocks, a.hit_tokens, a.pending_prefill])
+        elif kind == "enqueue_dup":
+            try:
+                sim.instances[st[1]].enqueue(recs[st[2]], int(trace.arrival_us[st[2]]))
+                obs.append(["enqueue_ok"])
+            except Dup:
+                obs.append(["dup"])
+        elif kind == "insert":
+            sim.instances[st[1]].cache.insert(recs[st[2]].prefix_blocks, st[3])
+            obs.append(["insert"])
+        elif kind == "queues":
+            q = []
+            for inst in sim.instances:
+                q.append([[s.record.request_id, s.pending, s.hit_blocks, s.hit_tokens, s.generated, s.enqueue_us]
+                          for s in inst.queue] + [["running"] + [[s.record.request_id, s.generated] for s in inst.running]])
+            obs.append(["queues", q])
+        elif kind == "run":
+            rep = sim.run_trace(recs[st[1]:st[2]])
+            reqs = [[m.request_id, m.chosen_instance, m.hit_tokens, m.arrival_us, m.first_token_us, m.finish_us]
+                    for m in rep.requests]
+            obs.append(["run", reqs, rep.arrivals_hash, len(rep.steps), rep.queued_at_last_arrival, rep.end_us,
+                        [[s.instance, s.start_us, s.end_us, s.prefill_us] for s in rep.steps[-50:]]])
+    return obs
+
+
+def main():
+    import_reference()
+    from routesim.cluster import ClusterSim
+    from routesim.engine import DuplicateRequestError
+    trace = W.config1_chatbot()[0].slice(600)
+    out = {}
+    for name, (cfg, steps) in SESSIONS.items():
+        out[name] = run_session(to_ref_config(cfg), steps, trace,
+                                (ClusterSim, to_ref_records, DuplicateRequestError))
+        print(name, [o[0] if o[0] != "route" else o[1] for o in out[name]][:40])
+    with open(os.path.join(ROOT, "tests", "golden", "api_sessions.json"), "w") as fh:
+        json.dump(out, fh)
+
+
+if __name__ == "__main__":
+    main()
