@@ -11,7 +11,7 @@ arrivals, then the final drain -- exactly ``run(records, config)``.
 
 * ``value``  : decisions/s with the trace resident in HBM (device time of
                reset + K1 + replay + drain, CUDA events on librsim's stream).
-* ``e2e``    : decisions/s through the public API ``ClusterSim.run_trace``
+* ``e2e``    : decisions/s through the public API ``run(records, config)``
                with host numpy inputs: H2D of the trace, K1, replay, drain and
                D2H of every per-request result are inside the timed region.
 * ``roofline``: the replay kernel's algorithmic bytes per launch
@@ -267,7 +267,7 @@ def reference_arm(args):
 def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     import torch
     from paper_2603_15202_b200 import _native
-    from paper_2603_15202_b200.cluster import ClusterSim, native_config, sizing_for
+    from paper_2603_15202_b200.cluster import native_config, release_pool, run, sizing_for
 
     trace, cfg = build_workload(name)
     R = len(trace)
@@ -303,19 +303,20 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     whatif = measure_whatif(h, trace, cfg, args) if args.whatif else None
     h.close()
 
-    # e2e through the public API: host arrays in, results out
-    sim = ClusterSim(cfg, device=dev_index)          # record_steps=True, as the reference's run() reports steps
+    # e2e through the public API run(records, config) (cluster.py:290-292): a new ClusterSim per
+    # call (its device handle comes from the pool after the first), host arrays in, every
+    # per-request result and the step log (record_steps=True, as the reference reports steps) out
     for _ in range(args.warmup):
-        sim.run_trace(trace)
+        run(trace, cfg, device=dev_index)
     e2e_s = []
     for _ in range(args.steps):
         flush_l2(dev)
         t0 = time.perf_counter()
-        rep = sim.run_trace(trace)
+        rep = run(trace, cfg, device=dev_index)
         e2e_s.append(time.perf_counter() - t0)
     assert np.array_equal(rep.chosen, chosen_dev), "e2e and resident replays disagree"
     log_bytes = int(rep._step_log.nbytes) if rep._step_log is not None else 0
-    sim.close()
+    release_pool()
 
     h2d = int(trace.arrival_us.nbytes + trace.in_tokens.nbytes + trace.out_tokens.nbytes +
               trace.request_id.nbytes + trace.blk_off.nbytes + trace.blocks.nbytes)

@@ -281,6 +281,7 @@ class _InstanceProxy:
         sim = self._sim
         if self.id in sim._holders(record.request_id):
             raise DuplicateRequestError(f"request {record.request_id} already present")
+        sim._advance_clock(int(now_us), "enqueue()")
         idx = sim._do(("load", PackedTrace.from_records([record]), np.array([now_us], np.int64)))
         ht = sim._do(("enqueue", self.id, idx, int(now_us)))
         sim._by_rid.setdefault(record.request_id, []).append(idx)
@@ -369,6 +370,7 @@ class ClusterSim:
         self._by_rid: dict[int, list[int]] = {}   # request id -> loaded indices (duplicate checks)
         self._runs = 0
         self._first_key: bytes | None = None
+        self._clock = 0                       # simulated time reached by the calls so far
         self.instances = [_InstanceProxy(self, i) for i in range(config.n_instances)]
 
     # -- device handle -----------------------------------------------------------------
@@ -516,6 +518,17 @@ class ClusterSim:
         _, ht = self._device().decisions(idx, 1)
         return min(-(-int(ht[0]) // self.block_size), len(rec.prefix_blocks))
 
+    def _advance_clock(self, now_us: int, what: str) -> None:
+        """The device keeps the router view live (indicators.snapshot at staleness 0 equals the
+        flushed view while time does not go backwards); a call earlier than the time the sim has
+        reached would read the reference's view history instead, which the device path does not
+        keep -- refused loudly rather than answered differently."""
+        if now_us < self._clock:
+            from .config import UnsupportedConfigError
+            raise UnsupportedConfigError(f"{what} at {now_us} us precedes the simulated time already reached "
+                                         f"({self._clock} us): the device path needs non-decreasing time across calls")
+        self._clock = now_us
+
     def _grow_for(self, trace: PackedTrace | None) -> None:
         need = sizing_for(trace, self.config) if trace is not None and len(trace) else None
         if need is not None and self._handle is None and not self._ops:
@@ -537,6 +550,7 @@ class ClusterSim:
         if self.config.detector is not None:
             from .config import UnsupportedConfigError
             raise UnsupportedConfigError("route() with the hotspot detector: replay a trace with run_trace")
+        self._advance_clock(int(now_us), "route()")
         holders = tuple(sorted(self._holders(record.request_id)))
         idx = self._do(("load", PackedTrace.from_records([record]), np.array([now_us], np.int64)))
         chosen, _ht, scores = self._do(("route", idx, int(now_us), holders), expected=(DuplicateRequestError,))
@@ -562,6 +576,8 @@ class ClusterSim:
                                                if int(r) in self._by_rid):
             from .config import UnsupportedConfigError
             raise UnsupportedConfigError("trace request ids still present from earlier route()/enqueue() calls")
+        if len(trace) and self._ops:
+            self._advance_clock(int(trace.arrival_us[0]), "run_trace()'s first arrival")
         fresh = not self._ops
         self._grow_for(trace if fresh else _concat_all(self._parts + [trace]))
         if self.record_steps:
@@ -582,7 +598,9 @@ class ClusterSim:
             dl = (tid, ex_off, ex_len, ckey, windows * det.top_k_classes + det.top_k_classes)
         queued_last = self._do(("run", first, n, dl))
         self._runs += 1
-        return self._report(trace, queued_last)
+        rep = self._report(trace, queued_last)
+        self._clock = max(self._clock, rep.end_us)
+        return rep
 
     def _log_cap_for(self, trace: PackedTrace) -> int:
         n = self._n + len(trace)

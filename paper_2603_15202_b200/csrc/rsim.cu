@@ -104,6 +104,8 @@ struct rsim {
     DevArr<u64> arena;             // API-inserted chain keys (named by eviction runs)
     i64 narena = 0;
     unsigned short *crit = nullptr; // diagnostics: per (decision, warp) phase records
+    std::vector<i64> order_breaks;  // loaded request indices whose arrival precedes the previous one
+    i64 last_arrival = 0;
     std::vector<i64> api_segs;      // debug_checks: API-inserted chains (instance, arena offset, length)
     DevArr<i64> dsegs;
     DevArr<u32> seen;               // debug_checks: per-slot "named by a chain" bits
@@ -243,6 +245,8 @@ static rsim_status init_state(rsim_t *h) {
     CK(h, cudaStreamSynchronize(h->stream));
     h->R = 0; h->nblk = 0; h->nout = 0; h->narena = 0;
     h->api_segs.clear();
+    h->order_breaks.clear();
+    h->last_arrival = 0;
     // blk_off / ooff hold a leading 0
     CK(h, h->blk_off.reserve(1, 0, h->stream));
     CK(h, h->ooff.reserve(1, 0, h->stream));
@@ -443,11 +447,10 @@ rsim_status rsim_load_trace(rsim_t *h, int64_t n, const int64_t *arrival_us, con
         oo[i + 1] = oo[i] + (output_tokens[i] + bs - 1) / bs;
     }
     off[n] = h->nblk + blk_off[n];
-    if (h->R > 0) {
-        i64 last = 0;
-        CK(h, cudaMemcpy(&last, h->arrival.p + h->R - 1, sizeof(i64), cudaMemcpyDeviceToHost));
-        if (arrival_us[0] < last) return fail(h, RSIM_E_TRACE, "appended arrivals precede the loaded trace");
-    }
+    // route()/enqueue() API requests may arrive at any time; a replay range must not span an
+    // arrival that precedes its predecessor (rsim_replay checks against these breaks)
+    if (h->R > 0 && arrival_us[0] < h->last_arrival) h->order_breaks.push_back(h->R);
+    h->last_arrival = arrival_us[n - 1];
     const i64 R0 = h->R, R1 = h->R + n, nb = blk_off[n], no = oo[n] - h->nout;
     cudaStream_t s = h->stream;
     CK(h, h->arrival.reserve(R1, R0, s)); CK(h, h->in_tok.reserve(R1, R0, s)); CK(h, h->out_tok.reserve(R1, R0, s));
@@ -556,6 +559,8 @@ rsim_status rsim_replay(rsim_t *h, int64_t first, int64_t count) {
     if (!h) return RSIM_E_INVALID;
     if (first < 0 || count < 0 || first + count > h->R) return fail(h, RSIM_E_INVALID, "decision range out of the loaded trace");
     if (count == 0) return RSIM_OK;
+    for (i64 b : h->order_breaks)
+        if (b > first && b < first + count) return fail(h, RSIM_E_TRACE, "replay range spans unsorted arrivals");
     CK(h, cudaSetDevice(h->cfg.device));
     if (h->cfg.debug_checks) {      // one decision per launch, the checks after each (its steps ran before it)
         float tot = 0;

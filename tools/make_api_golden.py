@@ -24,14 +24,14 @@ SESSIONS = {
     # ("run", lo, hi) / ("route_dup", i, now) / ("queues",) over records of the chat trace
     "route_then_run": (ClusterConfig(n_instances=4, seed=1),
                        [("insert", 0, 0, 0)] + [("route", i) for i in range(1, 27)]
-                       + [("queues",), ("run", 27, 260), ("queues",), ("run", 260, 400)]),
+                       + [("queues",), ("run", 27, 260), ("queues",), ("run_after", 260, 400)]),
     # (a bare enqueue() before run_trace makes the reference's Collector raise KeyError on the
     # request's first step -- metrics.py:132 -- so enqueue() appears only in API-only sessions)
     "run_twice": (ClusterConfig(n_instances=6, cache=CacheConfig(16, 600), seed=2),
-                  [("run", 0, 250), ("run", 250, 500), ("route", 500), ("run", 501, 600)]),
+                  [("run", 0, 250), ("run_after", 250, 500), ("route_after", 500), ("run_after", 501, 600)]),
     "duplicates": (ClusterConfig(n_instances=3, policy=PolicyConfig(kind="vllm"), seed=0),
-                   [("route", 0), ("route", 1)] + [("route_dup", j % 2, 10 * j) for j in range(2, 26)]
-                   + [("route", 2), ("queues",)]),
+                   [("route", 0), ("route", 1)] + [("route_dup", j % 2, 70_000 + 10 * j) for j in range(2, 26)]
+                   + [("route_after", 2), ("queues",)]),
     "enqueue_dup": (ClusterConfig(n_instances=2, seed=0),
                     [("enqueue", 0, 0), ("enqueue_dup", 0, 0), ("enqueue", 1, 0), ("route", 1), ("queues",)]),
     "small_batch_queues": (ClusterConfig(n_instances=3, cost_model=CostModel(chunk_tokens=64, max_batch_requests=2), seed=5),
@@ -42,17 +42,35 @@ SESSIONS = {
 def run_session(cfg, steps, trace, api):
     """api: (ClusterSim class, record converter, DuplicateRequestError). Returns the observations."""
     Sim, conv, Dup = api
+    import dataclasses
     sim = Sim(cfg)
     recs = conv(trace)
     obs = []
-    for st in steps:
+    clock = 0              # simulated time reached so far: "_after" steps start past it (the device
+    for st in steps:       # path needs non-decreasing time across calls, see ClusterSim)
         kind = st[0]
+        if kind == "run_after":
+            shift = (clock + 1_000_000 - int(trace.arrival_us[st[1]])) / 1e6
+            rs = [dataclasses.replace(r, arrival_s=r.arrival_s + shift) for r in recs[st[1]:st[2]]]
+            rep = sim.run_trace(rs)
+            clock = max(clock, rep.end_us)
+            obs.append(["run", [[m.request_id, m.chosen_instance, m.hit_tokens, m.arrival_us, m.first_token_us,
+                                 m.finish_us] for m in rep.requests], rep.arrivals_hash, len(rep.steps),
+                        rep.queued_at_last_arrival, rep.end_us])
+            continue
+        if kind == "route_after":
+            clock += 1000
+            d = sim.route(recs[st[1]], clock)
+            obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)]])
+            continue
         if kind == "route":
             r = recs[st[1]]
             d = sim.route(r, int(trace.arrival_us[st[1]]))
+            clock = max(clock, int(trace.arrival_us[st[1]]))
             obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)]])
         elif kind == "route_dup":
             r = recs[st[1]]
+            clock = max(clock, st[2])
             try:
                 d = sim.route(r, st[2])
                 obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)]])
@@ -78,6 +96,7 @@ def run_session(cfg, steps, trace, api):
             obs.append(["queues", q])
         elif kind == "run":
             rep = sim.run_trace(recs[st[1]:st[2]])
+            clock = max(clock, rep.end_us)
             reqs = [[m.request_id, m.chosen_instance, m.hit_tokens, m.arrival_us, m.first_token_us, m.finish_us]
                     for m in rep.requests]
             obs.append(["run", reqs, rep.arrivals_hash, len(rep.steps), rep.queued_at_last_arrival, rep.end_us,
