@@ -61,7 +61,10 @@ def sizing_for(trace: PackedTrace | None, config: ClusterConfig) -> Sizing:
     chain = trace.n_blocks + (trace.out_tokens + bs - 1) // bs
     total = int(chain.sum())
     maxchain = int(chain.max())
-    est = 4 * total // N + 4 * maxchain + 1024
+    # the tables hold DISTINCT keys: 1.15x the estimated mean per instance (measured max/mean:
+    # 1.04 api64, 1.15 chat1024) -- sizing from non-distinct keys made chat1024's tables 10x
+    # too large for L2
+    est = int(1.15 * distinct_keys_per_instance(trace, N, bs)) + maxchain + 128
     cap = config.cache.capacity_blocks
     if cap is not None:
         est = min(est, cap + maxchain + 64)
@@ -69,6 +72,29 @@ def sizing_for(trace: PackedTrace | None, config: ClusterConfig) -> Sizing:
     n = len(trace)
     q = min(n + 16, max(256, 4 * n // N + 256))
     return Sizing(q, est, history_capacity(trace, config))
+
+
+def distinct_keys_per_instance(trace: PackedTrace, n_instances: int, block_size: int,
+                               sample: int = 2048) -> float:
+    """Mean distinct KV$ keys one instance ends up holding (no eviction), estimated from an evenly
+    spaced sample of requests. A chain key lives on every instance a request carrying it was
+    routed to, so the (key, instance) pairs are bounded by sum_k min(count_k, N): block hashes
+    seen once in the sample are extrapolated as request-private, repeated ones by their scaled
+    count (block values stand in for chain keys: equal chain keys have equal blocks). Output-block
+    keys are salted by request id (engine.py:363-372), so always private. An underestimate is
+    caught on device (RSIM_E_TABLE_FULL) and regrown."""
+    R = len(trace)
+    off = trace.blk_off
+    nb = np.diff(off)
+    idx = np.unique(np.linspace(0, R - 1, min(R, sample)).astype(np.int64))
+    frac = len(idx) / R
+    lens = nb[idx]
+    pos = np.repeat(off[idx] - np.concatenate(([0], np.cumsum(lens[:-1]))), lens) + np.arange(int(lens.sum()))
+    _, counts = np.unique(trace.blocks[pos], return_counts=True)
+    private = int((counts == 1).sum()) / frac
+    shared = float(np.minimum(counts[counts > 1] / frac, n_instances).sum())
+    out_keys = int(((trace.out_tokens + block_size - 1) // block_size).sum())
+    return (private + shared + out_keys) / n_instances
 
 
 def history_capacity(trace: PackedTrace, config: ClusterConfig) -> int:

@@ -200,6 +200,7 @@ static rsim_status check_device_error(rsim_t *h) {
         }
         case DEV_E_QUEUE_OVERFLOW: return fail(h, RSIM_E_QUEUE_OVERFLOW, "instance queue ring full (queue_capacity=%d)", 1 << h->qlog2);
         case DEV_E_TABLE_FULL: return fail(h, RSIM_E_TABLE_FULL, "instance KV$ table over 3/4 load (slots=%d)", 1 << h->slog2);
+        case DEV_E_RUNS_FULL: return fail(h, RSIM_E_TABLE_FULL, "instance LRU touch-run ring full (runs=%d)", 1 << h->rlog2);
         case 11: return fail(h, RSIM_E_NO_INSTANCES, "no instances to route to");
         case DEV_E_DUPLICATE: return fail(h, RSIM_E_DUPLICATE, "request already present on the chosen instance");
         case DEV_E_DETECTOR: return fail(h, RSIM_E_DETECTOR, "detector capacity exceeded (more than %d classes re-evaluated at once, or a window bucket ring overflow)", RSIM_DLMAX);

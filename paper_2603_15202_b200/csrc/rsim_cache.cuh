@@ -427,6 +427,89 @@ __device__ void tab_delete(const Table &T, u32 i) {
     T.k[i] = T.empty;
 }
 
+// Delete up to 32 present entries at once (lane l deletes key kv at slot v when del): the
+// same key set as backward-shift deleting them one by one and again a table with no hole on
+// any probe path, in a few round trips instead of ~4 dependent ones per key. Victims are
+// first marked (a transient TOMB key); then every maximal run of slots from a victim to the
+// next EMPTY is rebuilt by one lane: its live entries are re-inserted in slot order, each
+// into the first free slot at or after its home (homes before the run count as its start),
+// which never moves an entry forward; the rest of the run becomes EMPTY. Runs of different
+// lanes are disjoint (each ends at an EMPTY slot); a victim inside another victim's run is
+// left to that run's lane. A run longer than 64 slots (a bitmap) sends the whole batch to
+// the one-at-a-time path. Only the owning warp touches the table: plain stores suffice.
+#define RSIM_TOMB (~0ULL)
+__device__ __forceinline__ void tab_place(u64 *tk, Meta *tm, u32 mask, int slog2, u32 v, u32 off, u64 k, u64 &occ) {
+    if (k == RSIM_TOMB) return;
+    const u32 u = (tab_home(k, slog2) - v) & mask;      // home offset; > off: home before v
+    const u32 st = u <= off ? u : 0;
+    const u32 t = (u32)(__ffsll((long long)(~occ & (~0ULL << st))) - 1);   // <= off
+    occ |= 1ULL << t;
+    if (t != off) {
+        const u32 x = (v + off) & mask, y = (v + t) & mask;
+        const ulonglong2 m = __ldcg(reinterpret_cast<const ulonglong2 *>(tm + x));
+        tk[y] = k;
+        *reinterpret_cast<ulonglong2 *>(tm + y) = m;
+    }
+}
+
+__device__ __forceinline__ void tab_delete32(u64 *tk, Meta *tm, u32 mask, int slog2, u32 v, u64 kv, bool del, int lane) {
+    if (!__any_sync(FULL, del)) return;
+    if (del) tk[v] = RSIM_TOMB;
+    __syncwarp();
+    // the run [v, v + len): len = distance to the first EMPTY after v (8 slots per round trip;
+    // the first window stays in registers for the rebuild)
+    u32 len = 0;
+    u64 w[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) w[i] = del ? __ldcg(tk + ((v + 1 + i) & mask)) : 0ULL;
+    if (del) {
+#pragma unroll
+        for (int i = 7; i >= 0; i--) if (w[i] == 0ULL) len = 1 + (u32)i;
+        for (u32 base = 9; len == 0 && base <= 64; base += 8) {
+            u64 x[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) x[i] = __ldcg(tk + ((v + base + i) & mask));
+#pragma unroll
+            for (int i = 7; i >= 0; i--) if (x[i] == 0ULL) len = base + (u32)i;
+        }
+    }
+    if (__any_sync(FULL, del && (len == 0 || len > 64))) {     // a long run: one key at a time
+        if (del) tk[v] = kv;
+        __syncwarp();
+        Table T;
+        T.k = tk; T.m = tm; T.mask = mask; T.slog2 = slog2; T.empty = 0ULL;
+        for (u32 b = __ballot_sync(FULL, del); b; b &= b - 1) {
+            const u64 key = __shfl_sync(FULL, kv, __ffs(b) - 1);
+            if (lane == 0) {
+                const int slot = tab_find(T, key);
+                if (slot >= 0) tab_delete(T, (u32)slot);
+            }
+            __syncwarp();
+        }
+        return;
+    }
+    // a victim inside another victim's run belongs to that run
+    bool lead = del;
+    for (u32 b = __ballot_sync(FULL, del); b; b &= b - 1) {     // warp-uniform loop over the victims
+        const int o = __ffs(b) - 1;
+        const u32 vo = __shfl_sync(FULL, v, o), lo = __shfl_sync(FULL, len, o);
+        const u32 dist = (v - vo) & mask;
+        if (o != lane && dist != 0 && dist < lo) lead = false;
+    }
+    if (lead) {
+        u64 occ = 0;                                    // offsets of the run already re-filled
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const u32 off = (u32)i + 1;
+            if (off < len) tab_place(tk, tm, mask, slog2, v, off, w[i], occ);
+        }
+        for (u32 off = 9; off < len; off++) tab_place(tk, tm, mask, slog2, v, off, __ldcg(tk + ((v + off) & mask)), occ);
+        for (u32 g = 0; g < len; g++)
+            if (!((occ >> g) & 1ULL)) tk[(v + g) & mask] = 0ULL;
+    }
+    __syncwarp();
+}
+
 __device__ __forceinline__ bool lru_before(i64 t, int d, u64 k, i64 bt, int bd, u64 bk) {
     return t < bt || (t == bt && (d > bd || (d == bd && k < bk)));
 }

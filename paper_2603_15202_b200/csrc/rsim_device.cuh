@@ -28,6 +28,7 @@ typedef unsigned int u32;
 #define DEV_E_COMM 10
 #define DEV_E_HISTORY_OVERFLOW 12
 #define DEV_E_DETECTOR 13
+#define DEV_E_RUNS_FULL 14
 
 // A request on an instance: one 64-byte record used by the FIFO queue (v =
 // pending prefill tokens) and the running list (v = finish step = join step +

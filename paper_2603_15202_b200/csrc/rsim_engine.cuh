@@ -144,9 +144,18 @@ __device__ void finish_one(const Params &P, int gi, Inst &s, i64 a, int B, i64 o
     Table T = table_of(P, gi);
     Run r; r.T = end; r.a = a; r.oa = oa; r.B = B; r.dhi = L; r.kind = 0; r.pad = 0;
     run_add(P, s, gi, r, lane, werr);
+#ifdef RSIM_STEP_PROFILE
+    const long long c0 = clock64();
+#endif
     s.occ += warp_unpin_insert(T, P.ckeys + a, B, P.okeys + oa, L, hb, end, lane, werr);
     if (s.occ > P.max_occ) werr = DEV_E_TABLE_FULL;
+#ifdef RSIM_STEP_PROFILE
+    const long long c1 = clock64();
+#endif
     evict_to_capacity(P, T, s, gi, lane, werr);
+#ifdef RSIM_STEP_PROFILE
+    if (P.ctr != nullptr && lane == 0) { atomicAdd(P.ctr + 42, (u64)(c1 - c0)); atomicAdd(P.ctr + 43, (u64)(clock64() - c1)); }
+#endif
 }
 
 // Process the finishers collected in F, in collection order (= the reference's:

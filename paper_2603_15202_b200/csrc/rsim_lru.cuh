@@ -40,7 +40,7 @@ __device__ void run_add(const Params &P, Inst &s, int gi, const Run &r, int lane
     Run *R = P.runs + ((size_t)gi << P.rlog2);
     const i64 mask = (1LL << P.rlog2) - 1;
     const i64 head = s.r_head, tail = s.r_tail;
-    if (tail - head > mask) { werr = DEV_E_TABLE_FULL; return; }
+    if (tail - head > mask) { werr = DEV_E_RUNS_FULL; return; }
     if (tail == head || r.T >= s.r_tailT) {
         if (lane == 0) R[tail & mask] = r;
         s.r_tail = tail + 1;
@@ -77,9 +77,114 @@ __device__ __forceinline__ void delete_key(const Table &T, u64 key) {
     if (slot >= 0) tab_delete(T, (u32)slot);
 }
 
+// Evict from the single run r (the oldest touch group, no other run shares its T), deepest
+// depth first: the reference's (touch asc, depth desc, key asc) order restricted to one
+// chain. Every event touches or pins a whole chain PREFIX (kvcache.py:81-138), so along the
+// chain touch and pin never increase with depth (prefix closure, kvcache.py:4-7, keeps the
+// present items a prefix too). Walking up from the deepest depth the items are therefore:
+// absent or re-touched older than T (skipped: not live in this run), then live (touch == T)
+// and unpinned -- the victims, in order --, then a first item that is pinned or newer, above
+// which nothing in this run is evictable. 128 depths per round trip (plus one for the
+// metadata); the victims go in batches of 32 (tab_delete32). Returns the run's new depth
+// bound: everything deeper is known dead for this run.
+__device__ __forceinline__ int evict_chain_body(const Params &P, const Table &T, const Run &r, i64 &need, int lane,
+                                                bool &alive) {
+    int d0 = r.dhi;
+    while (d0 >= 1 && need > 0) {
+        u64 kk[4];
+        bool act[4];
+        int slot[4];
+        u32 fp[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int d = d0 - (32 * k + lane);
+            act[k] = d >= 1;
+            kk[k] = act[k] ? run_key(P, r, d) : 0ULL;
+        }
+        find128(T, kk, act, slot, fp);
+        // 0 skip, 1 victim, 2 newer (stop), 3 live but pinned (stop; the run stays)
+        int cls[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            cls[k] = 0;
+            if (slot[k] >= 0) {
+                const Meta m = load_meta(T.m + slot[k]);
+                const int d = d0 - (32 * k + lane);
+                if (m.touch > r.T) cls[k] = 2;
+                else if (m.touch == r.T && m.depth == d) cls[k] = m.pin > 0 ? 3 : 1;
+            }
+        }
+        // first stop in depth order (k major, lane minor), and the victims before it
+        int stop = 128;
+#pragma unroll
+        for (int k = 3; k >= 0; k--) {
+            const u32 sm = __ballot_sync(FULL, cls[k] >= 2);
+            if (sm) stop = 32 * k + __ffs(sm) - 1;
+        }
+        const int ncand = __reduce_add_sync(FULL, (cls[0] == 1 && lane < stop) + (cls[1] == 1 && 32 + lane < stop) +
+                                                      (cls[2] == 1 && 64 + lane < stop) + (cls[3] == 1 && 96 + lane < stop));
+        const i64 ntake = ncand < need ? ncand : need;
+        int taken = 0, last = -1;                      // victims taken so far in depth order; index of the last
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int idx = 32 * k + lane;
+            const bool cand = cls[k] == 1 && idx < stop;
+            const u32 cm = __ballot_sync(FULL, cand);
+            const bool take = cand && taken + __popc(cm & lanemask_lt()) < ntake;
+            const u32 tm = __ballot_sync(FULL, take);
+            if (tm) last = 32 * k + 31 - __clz(tm);
+            taken += __popc(tm);
+#ifdef RSIM_STEP_PROFILE
+            const long long cd = clock64();
+            if (P.ctr != nullptr && lane == 0 && tm) { atomicAdd(P.ctr + 44, (u64)1); atomicAdd(P.ctr + 45, (u64)__popc(tm)); }
+#endif
+            // an earlier deletion of this batch may have shifted the slot (backward shifts)
+            int sl = slot[k];
+            if (taken > __popc(tm) && take) sl = tab_find(T, kk[k]);
+            tab_delete32(T.k, T.m, T.mask, T.slog2, (u32)sl, kk[k], take, lane);
+#ifdef RSIM_STEP_PROFILE
+            if (P.ctr != nullptr && lane == 0 && tm) atomicAdd(P.ctr + 46, (u64)(clock64() - cd));
+#endif
+        }
+        need -= ntake;
+        if (ntake < ncand) {                           // capacity reached: victims remain live
+            alive = true;
+            return d0 - last - 1;
+        }
+        if (stop < 128) {                              // nothing above is evictable in this run
+            int cs = cls[0];
+#pragma unroll
+            for (int k = 1; k < 4; k++) if ((stop >> 5) == k) cs = cls[k];
+            alive = __shfl_sync(FULL, cs, stop & 31) == 3;
+            return d0 - stop;
+        }
+        if (need == 0) {                               // done; what lies above is unknown
+            alive = true;
+            return d0 > 128 ? d0 - 128 : 0;
+        }
+        d0 -= 128;
+    }
+    return 0;
+}
+
+// Out of line with scalar arguments only (no caller object has its address taken); returns
+// (victims << 32) | (alive << 31) | new depth bound.
+__device__ __forceinline__ u64 evict_chain_v(const Params &P, u64 *tk, Meta *tmeta, u32 tmask, int slog2, i64 rT, i64 ra,
+                                          i64 roa, int rB, int rkind, int rdhi, i64 need0, int lane) {
+    Table T;
+    T.k = tk; T.m = tmeta; T.mask = tmask; T.slog2 = slog2; T.empty = 0;
+    Run r;
+    r.T = rT; r.a = ra; r.oa = roa; r.B = rB; r.kind = rkind; r.dhi = rdhi; r.pad = 0;
+    i64 need = need0;
+    bool alive = false;
+    const int nd = evict_chain_body(P, T, r, need, lane, alive);
+    return ((u64)(need0 - need) << 32) | ((u64)alive << 31) | (u64)(u32)nd;
+}
+
 // Evict down to capacity in exact reference order. Returns false when a group
 // is too large for the run walk (the caller then uses the table scan).
-__device__ bool evict_runs(const Params &P, const Table &T, Inst &s, int gi, i64 &occ, int lane, int &werr) {
+__device__ bool evict_runs(const Params &P, const Table &T, Inst &s, int gi, i64 &occ, int lane,
+                                                int &werr) {
     Run *R = P.runs + ((size_t)gi << P.rlog2);
     const i64 mask = (1LL << P.rlog2) - 1;
     i64 need = occ - P.cap;
@@ -95,7 +200,26 @@ __device__ bool evict_runs(const Params &P, const Table &T, Inst &s, int gi, i64
         const i64 T0 = __shfl_sync(FULL, rr.T, 0);
         const u32 gm = __ballot_sync(FULL, p < s.r_tail && rr.T == T0);
         if (gm == FULL) return false;                  // > 31 runs share T: fall back to the scan
+#ifdef RSIM_STEP_PROFILE
+        if (P.ctr != nullptr && lane == 0) atomicAdd(P.ctr + 47, (u64)1);
+#endif
         const int ng = __ffs(~gm) - 1;
+        if (ng == 1) {                                 // one run: its live items are one depth range
+            bool alive = false;
+            const int dhi = __shfl_sync(FULL, rr.dhi, 0);
+            const u64 res = evict_chain_v(P, T.k, T.m, T.mask, T.slog2, T0, __shfl_sync(FULL, rr.a, 0),
+                                          __shfl_sync(FULL, rr.oa, 0), __shfl_sync(FULL, rr.B, 0),
+                                          __shfl_sync(FULL, rr.kind, 0), dhi, need, lane);
+            const int ndhi = (int)(res & 0x7fffffffu);
+            alive = (res >> 31) & 1u;
+            need -= (i64)(res >> 32);
+            occ -= (i64)(res >> 32);
+            if (lane == 0 && ndhi != dhi) R[pos & mask].dhi = ndhi;
+            if (!alive && head_clean && pos == s.r_head) s.r_head = pos + 1;
+            else head_clean = false;
+            pos += 1;
+            continue;
+        }
         int maxd = __reduce_max_sync(FULL, lane < ng ? rr.dhi : 0);
         bool alive = false;                            // live items of the group left in place
         // K depth levels per batch, lanes = (run r, level l); order (depth desc, key asc)
@@ -117,8 +241,9 @@ __device__ bool evict_runs(const Params &P, const Table &T, Inst &s, int gi, i64
             bool lead = false;
             if (act) { const u32 peers = __match_any_sync(am, key); lead = (__ffs(peers) - 1) == lane; }
             bool live = false, evictable = false;
+            int slot = -1;
             if (lead) {
-                const int slot = tab_find(T, key);
+                slot = tab_find(T, key);
                 if (slot >= 0) {
                     const Meta m = load_meta(T.m + slot);
                     live = m.touch == T0 && m.depth == d;
@@ -143,14 +268,14 @@ __device__ bool evict_runs(const Params &P, const Table &T, Inst &s, int gi, i64
             const i64 ntake = ncand < need ? ncand : need;
             alive = alive || __any_sync(FULL, live && !take);
             // delete the victims (order among them is irrelevant once chosen)
-            u32 tm = __ballot_sync(FULL, take);
-            while (tm) {
-                const int l2 = __ffs(tm) - 1;
-                tm &= tm - 1;
-                const u64 vk = __shfl_sync(FULL, key, l2);
-                if (lane == 0) delete_key(T, vk);
-                __syncwarp();
-            }
+#ifdef RSIM_STEP_PROFILE
+            const long long cd = clock64();
+            if (P.ctr != nullptr && lane == 0) { atomicAdd(P.ctr + 44, (u64)1); atomicAdd(P.ctr + 45, (u64)ntake); }
+#endif
+            tab_delete32(T.k, T.m, T.mask, T.slog2, (u32)slot, key, take, lane);
+#ifdef RSIM_STEP_PROFILE
+            if (P.ctr != nullptr && lane == 0) atomicAdd(P.ctr + 46, (u64)(clock64() - cd));
+#endif
             occ -= ntake;
             need -= ntake;
         }

@@ -123,6 +123,10 @@ for c, w in shapes:
             print(f"   detector (CTA 0 control warp, cyc/decision): listed-holder wait {sc[22] / len(trace):.0f}  "
                   f"observe {sc[23] / len(trace):.0f}  prepare {sc[24] / len(trace):.0f}; decisions with a list "
                   f"{sc[25] / len(trace):.2f}", flush=True)
+        if sc[26] or sc[27]:
+            print(f"   inline finishes (finish_one): insert {sc[26] / max(ctr[6], 1):.0f} cyc/batch, evict {sc[27] / max(ctr[6], 1):.0f} "
+                  f"cyc/batch; evict walk: {sc[31]} groups, {sc[28]} batches, {sc[29]} victims, delete {sc[30] / max(sc[29], 1):.0f} cyc/victim",
+                  flush=True)
         kinds = ["finishing", "other full", "pure decode"]
         print("   step kinds: " + "  ".join(f"{kinds[i]} {sc[8 + 2 * i]} x {sc[9 + 2 * i] / max(sc[8 + 2 * i], 1):.0f} cyc"
                                           for i in range(3)), flush=True)
