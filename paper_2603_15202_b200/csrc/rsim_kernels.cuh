@@ -300,6 +300,99 @@ __device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base,
     }
 }
 
+// ---- longest present prefix beyond the first 128 depths for up to 4 instances at once
+// (instances gi0 + q for the bits q of dm), all of whose first 128 depths are present.
+// Presence is monotone in depth (prefix closure, kvcache.py:4-7), so lane li first probes depth
+// 128 + li*S (S = ceil((B-128)/32)); the first missing lane brackets the boundary within S
+// depths, which a second lookup of <= 64 depths (two per lane) pins. The stage-1 keys are the
+// request's and shared by all instances: two round trips of table loads for all four
+// instances instead of ~3 rounds of (key load, table load) per instance (deep_match). Longer
+// prompts (S > 65) take deep_match.
+__device__ __noinline__ void deep_hits(const Params &P, int gi0, u32 dm, const u64 *keys, int B, int lane, int *hout) {
+    const int span = B - 128, S = (span + 31) / 32;
+    if (S > 65) {
+        for (u32 b = dm; b; b &= b - 1) {
+            const int q = __ffs(b) - 1;
+            const int h = deep_match(table_of(P, gi0 + q), keys, B, lane);
+            if (lane == 0) hout[q] = min(h, B);
+        }
+        __syncwarp();
+        return;
+    }
+    const int d1 = 128 + lane * S;
+    const bool v1 = d1 < B;
+    const u64 k1 = v1 ? keys[d1] : 0ULL;
+    ulonglong2 pr[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const Table T = table_of(P, gi0 + (((dm >> q) & 1u) ? q : 0));
+        pr[q] = (((dm >> q) & 1u) && v1) ? ld_pair(T, tab_home(k1, T.slog2)) : make_ulonglong2(0ULL, 0ULL);
+    }
+    int lo[4], cnt[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        lo[q] = 128; cnt[q] = 0;
+        if ((dm >> q) & 1u) {                                    // warp-uniform
+            const Table T = table_of(P, gi0 + q);
+            bool f = false, c = false;
+            if (v1) eval_first(T, pr[q], tab_home(k1, T.slog2), k1, f, c);
+            if (__any_sync(FULL, c) && c) {
+                int stt;
+                probe_rest(T, ((tab_home(k1, T.slog2) | 1u) + 1u) & T.mask, k1, stt);
+                f = stt == 0;
+            }
+            const u32 bits = __ballot_sync(FULL, f);
+            const int m = bits == FULL ? 32 : __ffs(~bits) - 1;  // lanes 0..m-1 present
+            if (m > 0) {
+                lo[q] = 128 + (m - 1) * S + 1;                  // depth 128+(m-1)S present
+                cnt[q] = min(128 + m * S, B) - lo[q];            // depths lo..lo+cnt-1 unknown
+            }
+        }
+    }
+    u64 k2[4][2];
+    ulonglong2 p2[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            const bool v2 = ((dm >> q) & 1u) && 32 * j + lane < cnt[q];
+            k2[q][j] = v2 ? keys[lo[q] + 32 * j + lane] : 0ULL;
+        }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const Table T = table_of(P, gi0 + (((dm >> q) & 1u) ? q : 0));
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            const bool v2 = ((dm >> q) & 1u) && 32 * j + lane < cnt[q];
+            p2[q][j] = v2 ? ld_pair(T, tab_home(k2[q][j], T.slog2)) : make_ulonglong2(0ULL, 0ULL);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        if ((dm >> q) & 1u) {                                    // warp-uniform
+            const Table T = table_of(P, gi0 + q);
+            int miss = 64;
+#pragma unroll
+            for (int j = 1; j >= 0; j--) {
+                const bool v2 = 32 * j + lane < cnt[q];
+                bool f = false, c = false;
+                const u32 hm2 = tab_home(k2[q][j], T.slog2);
+                if (v2) eval_first(T, p2[q][j], hm2, k2[q][j], f, c);
+                if (__any_sync(FULL, c) && c) {
+                    int stt;
+                    probe_rest(T, ((hm2 | 1u) + 1u) & T.mask, k2[q][j], stt);
+                    f = stt == 0;
+                }
+                const u32 mb = __ballot_sync(FULL, v2 && !f);
+                if (mb) miss = 32 * j + __ffs(mb) - 1;
+            }
+            const int h = lo[q] + min(miss, cnt[q]);
+            if (lane == 0) hout[q] = min(h, B);
+        }
+    }
+    __syncwarp();
+}
+
 // ---- probe this warp's instances (cluster.py:106-128 -> kvcache.py:65-74): longest
 // present prefix of request R in each instance's table, for instances not in
 // `skip`. Short prompts are probed several instances at a time: the warp splits
@@ -394,10 +487,17 @@ __device__ __noinline__ void probe_hits(const Params &P, int base, int l0, int n
                     if (!done && bits != gmask) { h = j * LP + __ffs(~bits) - 1; done = true; }
                 }
             }
-            if (G == 1 && h >= 128 && B > 128) h = deep_match(T, P.ckeys + R.a, B, lane);   // G == 1: warp-uniform
             h = min(h, B);
-            if (cand && li == 0) hout[s] = h;
+            if (cand && li == 0) hout[s] = h;                    // 128 of > 128: refined below
             }
+        }
+        if (G == 1 && B > 128) {                                 // warp-uniform
+            __syncwarp();
+            u32 dm = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (b0 + q < nr && ((need >> min(b0 + q, 31)) & 1u) && hout[b0 + q] == 128) dm |= 1u << q;
+            if (dm) deep_hits(P, base + l0 + b0, dm, P.ckeys + R.a, B, lane, hout + b0);
         }
     }
 #ifdef RSIM_DIAG

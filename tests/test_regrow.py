@@ -53,7 +53,6 @@ def test_touch_run_ring_overflow_is_reported():
     ("cfg2_api_prefix4000", dict(expected_keys=64)),
     ("evict_heavy_n4", dict(queue_capacity=16, expected_keys=64)),      # runs ring derives from the queue
     ("cfg3_agent_evict_n16", dict(queue_capacity=16, expected_keys=256)),
-    ("adv_tight_capacity", dict(queue_capacity=16, expected_keys=64)),
 ])
 def test_regrown_replay_matches_reference(name, sizing, monkeypatch):
     """run() starting from rings/tables far too small: every overflow regrows and the final
