@@ -300,7 +300,7 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     lat = np.diff(ns[ns > 0]) / 1000.0
     chosen_dev, hit_dev = h.decisions(0, R)
     finish_dev = h.request_times(0, R)[2]
-    whatif = measure_whatif(h, trace, cfg, args) if args.whatif else None
+    whatif = measure_whatif(h, trace, cfg, args, name) if args.whatif else None
     h.close()
 
     # e2e through the public API run(records, config) (cluster.py:290-292): a new ClusterSim per
@@ -333,7 +333,8 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     k1 = {"kernel": "k1_chain_keys", "prefix_blocks": nb, "output_keys": nob, "ms": k1_s * 1000.0,
           "keys_per_s": (nb + nob) / k1_s, "algorithmic_bytes": k1_alg,
           "roofline": {"bound": "hbm", "achieved": k1_alg / k1_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                       "frac": k1_alg / k1_s / 1e9 / peaks["hbm_gbs"]}}
+                       "frac": k1_alg / k1_s / 1e9 / peaks["hbm_gbs"], "traffic": traffic_for(name, "k1_chain_keys"),
+                       "l2": l2_for(name, "k1_chain_keys")}}
     out = {
         "R": R, "cfg": cfg, "trace": trace, "k1": k1,
         "value": R * len(dev_ms) / (sum(dev_ms) / 1000.0),
@@ -345,6 +346,7 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
         "lat_p99_us": float(np.percentile(lat, 99)) if lat.size else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic_for(name),
+                     "l2": l2_for(name, "replay_kernel"),
                      "kernel": "replay_kernel", "algorithmic_bytes_per_launch": int(ctr[0]),
                      "avg_launch_ms": avg_replay_s * 1000.0, "peak_source": f"{peak_src} hbm_gbs (burst copy)",
                      "engine_steps_per_launch": int(ctr[1])},
@@ -371,7 +373,68 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     return out
 
 
-def measure_whatif(h, trace, cfg, args):
+def measure_route_api(name, n_calls, dev_index, with_ref: bool):
+    """The online router use case (BASELINE.md section 2 route p50/p99): ``ClusterSim.route(record,
+    now_us)`` called once per request in arrival order, each call timed with perf_counter_ns around
+    the public API (host record in, RoutingDecision with every instance's score out); the reference's
+    ``ClusterSim.route`` on the same records beside it, and the two decision sequences compared."""
+    from paper_2603_15202_b200.cluster import ClusterSim
+    trace, cfg = build_workload(name)
+    recs = trace.slice(min(n_calls, len(trace))).records()
+    arr = [int(x) for x in trace.arrival_us[:len(recs)]]
+    warm = ClusterSim(cfg, device=dev_index)
+    for r, t in zip(recs[:32], arr[:32]):
+        warm.route(r, t)
+    warm.close()
+    sim = ClusterSim(cfg, device=dev_index)
+    ns, chosen = [], []
+    for r, t in zip(recs, arr):
+        t0 = time.perf_counter_ns()
+        d = sim.route(r, t)
+        ns.append(time.perf_counter_ns() - t0)
+        chosen.append(d.chosen)
+    sim.close()
+    us = np.asarray(ns) / 1000.0
+    # the same calls straight through the C ABI (rsim_route_request): the boundary's own cost
+    from paper_2603_15202_b200 import _native
+    from paper_2603_15202_b200.cluster import native_config, sizing_for
+    h = _native.Handle(native_config(cfg, sizing_for(trace.slice(len(recs)), cfg), device=dev_index))
+    blk = [np.asarray(r.prefix_blocks, np.uint64) for r in recs]
+    cns = []
+    for r, b, t in zip(recs, blk, arr):
+        t0 = time.perf_counter_ns()
+        h.route_request(t, r.input_tokens, r.output_tokens, r.request_id, b)
+        cns.append(time.perf_counter_ns() - t0)
+    h.close()
+    cus = np.asarray(cns) / 1000.0
+    out = {"instances": cfg.n_instances, "calls": len(recs), "workload": name,
+           "c_abi": {"p50_us": float(np.percentile(cus, 50)), "p99_us": float(np.percentile(cus, 99)),
+                     "entry": "rsim_route_request"},
+           "ours": {"p50_us": float(np.percentile(us, 50)), "p99_us": float(np.percentile(us, 99)),
+                    "mean_us": float(us.mean()), "calls_per_s": len(us) / (us.sum() / 1e6)},
+           "timed": "perf_counter_ns around each ClusterSim.route(record, now_us) call (no engine steps between "
+                    "calls, as in the reference's route()); ours: host record -> RoutingDecision incl. scores"}
+    if with_ref and import_reference() is not None:
+        routesim, rrecs, rcfg = ref_records_and_config(trace.slice(len(recs)), cfg)
+        from routesim.cluster import ClusterSim as RefSim
+        ref = RefSim(rcfg)
+        rns, rchosen = [], []
+        for r, t in zip(rrecs, arr):
+            t0 = time.perf_counter_ns()
+            d = ref.route(r, t)
+            rns.append(time.perf_counter_ns() - t0)
+            rchosen.append(d.chosen)
+        rus = np.asarray(rns) / 1000.0
+        out["reference"] = {"p50_us": float(np.percentile(rus, 50)), "p99_us": float(np.percentile(rus, 99)),
+                            "mean_us": float(rus.mean()), "calls_per_s": len(rus) / (rus.sum() / 1e6),
+                            "impl": "routesim ClusterSim.route from baseline/_ref (CPython, 1 thread)"}
+        out["parity"] = {"vs": "reference ClusterSim.route", "calls": len(recs),
+                         "mismatches": int(sum(a != b for a, b in zip(chosen, rchosen)))}
+        out["p50_speedup"] = out["reference"]["p50_us"] / out["ours"]["p50_us"]
+    return out
+
+
+def measure_whatif(h, trace, cfg, args, name):
     """SURVEY 8d tertiary: the batched what-if probe (M requests x all instances against the
     replay's final KV$ state, no commits) -- the bandwidth-bound form of the probe.
     Algorithmic bytes: 8 B per chain key of each request (read once) + 8 B per
@@ -388,20 +451,31 @@ def measure_whatif(h, trace, cfg, args):
     best = min(ms) / 1000.0
     peaks, _ = measured_peaks()
     gbs = alg / best / 1e9
+    kern = "probe_batch_kernel" if hits.shape[1] >= 256 else "probe_pairs_kernel"
     return {"requests": M, "instances": int(hits.shape[1]), "pairs": int(M * hits.shape[1]),
             "ms": min(ms), "pairs_per_s": M * hits.shape[1] / best, "algorithmic_bytes": alg,
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": gbs / peaks["hbm_gbs"],
-                         "kernel": "probe_batch_kernel" if hits.shape[1] >= 256 else "probe_pairs_kernel"}}
+                         "frac": gbs / peaks["hbm_gbs"], "kernel": kern, "traffic": traffic_for(name, kern),
+                         "l2": l2_for(name, kern)}}
 
 
-def traffic_for(name):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one replay launch of this workload, from the
-    committed ncu capture (profiles/replay_traffic.json); None if not captured."""
+def traffic_for(name, kernel="replay_kernel"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of ``kernel`` on this workload, from
+    the committed ncu capture (profiles/kernel_traffic.json, tools/profile_r2.sh +
+    tools/update_traffic.py); None if not captured."""
     try:
-        with open(os.path.join(ROOT, "profiles", "replay_traffic.json")) as fh:
-            t = json.load(fh).get(name)
+        with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as fh:
+            t = json.load(fh).get(name, {}).get(kernel)
         return None if t is None else int(t["dram_bytes"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def l2_for(name, kernel):
+    try:
+        with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as fh:
+            t = json.load(fh).get(name, {}).get(kernel)
+        return None if t is None else {"l2_sector_bytes": 32 * int(t["l2_sectors"]), "l2_hit_pct": t["l2_hit_pct"]}
     except (OSError, ValueError, KeyError):
         return None
 
@@ -481,7 +555,8 @@ def measure_sharded(name, args, dev_index, rank, world, backend):
     k1 = {"kernel": "k1_chain_keys", "prefix_blocks": nb, "output_keys": nob, "ms": k1_s * 1000.0,
           "keys_per_s": (nb + nob) / k1_s, "algorithmic_bytes": k1_alg, "scope": "replicated on every rank",
           "roofline": {"bound": "hbm", "achieved": k1_alg / k1_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                       "frac": k1_alg / k1_s / 1e9 / peaks["hbm_gbs"]}}
+                       "frac": k1_alg / k1_s / 1e9 / peaks["hbm_gbs"], "traffic": traffic_for(name, "k1_chain_keys"),
+                       "l2": l2_for(name, "k1_chain_keys")}}
     out = {"R": R, "cfg": cfg, "trace": trace, "k1": k1, "ms_per_step": statistics.mean(dev_ms),
            "e2e_s": statistics.mean(e2e_s), "h2d": h2d, "d2h": R * 12, "launches": launches,
            "clocks": clk.summary(), "chosen": chosen, "hit_tokens": hit_tokens, "finish_us": fin,
@@ -539,6 +614,8 @@ def main():
     ap.add_argument("--parity-max", type=int, default=0,
                     help="oracle-checked prefix length (decision k depends only on records[:k+1]); "
                          "default 120k on 1 GPU (every request of api64 / chat1024 / agent256), 50k sharded")
+    ap.add_argument("--route-api", default="api64:2000,chat1024:500",
+                    help="online route() API latency, workload:calls list ('' to skip)")
     ap.add_argument("--whatif", type=int, default=20000,
                     help="requests of the batched what-if probe measured after the replay (0: skip)")
     args = ap.parse_args()
@@ -597,6 +674,10 @@ def main():
                                "host_cpu": host_cpu()}
         res["decisions_sha256_16"] = chosen_digest(res["chosen"])
     extras = {}
+    route_api = None
+    if world == 1 and args.route_api:
+        route_api = [measure_route_api(spec.split(":")[0], int(spec.split(":")[1]), dev_index, with_ref=not args.no_cpu)
+                     for spec in args.route_api.split(",") if spec]
     if world == 1:
         for name in [x for x in args.extra.split(",") if x and x != args.workload]:
             e = measure_workload(name, args, dev_index, with_cpu=not args.no_cpu, rank=rank)
@@ -635,6 +716,7 @@ def main():
                 "d2h_bytes_per_step": res["d2h"]},
         "gpu_launches": res["launches"],
         "whatif_probe": res.get("whatif"), "k1_chain_keys": res["k1"],
+        "route_api": route_api,
         "clocks": res["clocks"],
     }
     if world > 1:

@@ -157,6 +157,14 @@ rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen
  * holders[0..n_holders) (global ids) nothing is enqueued and RSIM_E_DUPLICATE is returned. */
 rsim_status rsim_route_one_excl(rsim_t *h, int64_t r, int64_t now_us, const int32_t *holders, int32_t n_holders,
                                 int32_t *chosen, int64_t *hit_tokens, double *scores);
+/* ClusterSim.route(record, now_us) of a request that is not loaded yet (cluster.py:130-154):
+ * appends it to the loaded trace (as rsim_load_trace of one request would) and decides it, with
+ * the holders semantics of rsim_route_one_excl -- one fused call (the request goes in and the
+ * decision comes out through mapped pinned memory, three launches, one stream synchronisation). */
+rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, int64_t output_tokens,
+                               uint64_t request_id, const uint64_t *blocks, int64_t n_blocks,
+                               const int32_t *holders, int32_t n_holders, int32_t *chosen, int64_t *hit_tokens,
+                               double *scores);
 /* InstanceSim.queue / .running (engine.py:212-213) of a local instance: 8 int64 per slot -- the FIFO
  * queue in order, then the running list: request index, kind (0 queued / 1 running), pending,
  * generated, hit blocks, input tokens, output tokens, flags (bit0: prefill scheduled). out may be

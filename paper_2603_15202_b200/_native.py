@@ -135,6 +135,7 @@ def lib():
         "rsim_route_one_excl": ([P, I64, I64, P, I32, P, P, P], C.c_int),
         "rsim_read_slots": ([P, I32, P, I64, P, P], C.c_int),
         "rsim_unschedule": ([P], C.c_int),
+        "rsim_route_request": ([P, I64, I64, I64, C.c_uint64, P, I64, P, I32, P, P, P], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -155,7 +156,8 @@ EXPORTED = ("rsim_create", "rsim_destroy", "rsim_last_error", "rsim_reset", "rsi
             "rsim_read_counters", "rsim_shard_bounds", "rsim_mailbox", "rsim_mailbox_ipc_handle",
             "rsim_set_peer", "rsim_open_peer_ipc", "rsim_load_detector", "rsim_detector_finalize",
             "rsim_read_detector", "rsim_detector_debug", "rsim_config_size", "rsim_check_invariants",
-            "rsim_debug_corrupt", "rsim_route_one_excl", "rsim_read_slots", "rsim_unschedule")
+            "rsim_debug_corrupt", "rsim_route_one_excl", "rsim_read_slots", "rsim_unschedule",
+            "rsim_route_request")
 
 
 def _p(a):
@@ -267,6 +269,30 @@ class Handle:
         self._ck(self._L.rsim_route_one_excl(self._h, r, now_us, _p(hd) if hd.size else None, int(hd.size),
                                              _p(ch), _p(ht), _p(sc)))
         return int(ch[0]), int(ht[0]), sc
+
+    def route_request(self, now_us: int, input_tokens: int, output_tokens: int, request_id: int, blocks,
+                      holders=(), want_scores: bool = True):
+        """ClusterSim.route of a request not loaded yet: rsim_route_request appends it to the device
+        trace and decides it in one call. ``blocks``: u64 array (or sequence) of its block hashes."""
+        b = blocks if isinstance(blocks, np.ndarray) and blocks.dtype == np.uint64 else \
+            np.fromiter((x & 0xFFFFFFFFFFFFFFFF for x in blocks), np.uint64)
+        b = np.ascontiguousarray(b)
+        out = self._rr_out
+        sc = np.empty(self.n_local, np.float64) if want_scores else None
+        hd = np.asarray(sorted(holders), np.int32) if holders else None
+        self._ck(self._L.rsim_route_request(self._h, now_us, input_tokens, output_tokens,
+                                            request_id & 0xFFFFFFFFFFFFFFFF, _p(b) if b.size else None, b.size,
+                                            _p(hd), 0 if hd is None else int(hd.size), self._rr_ch_p, self._rr_ht_p,
+                                            _p(sc)))
+        return int(out[0][0]), int(out[1][0]), sc
+
+    @property
+    def _rr_out(self):
+        o = getattr(self, "_rr", None)
+        if o is None:
+            o = self._rr = (np.zeros(1, np.int32), np.zeros(1, np.int64))
+            self._rr_ch_p, self._rr_ht_p = _p(o[0]), _p(o[1])
+        return o
 
     def slots(self, instance: int) -> np.ndarray:
         """(n, 8) int64: the FIFO queue then the running list of a local instance (rsim_read_slots)."""

@@ -389,9 +389,11 @@ class ClusterSim:
         self._sizing = sizing_for(None, config)
         self._log_cap = 1 << 16 if record_steps else 0
         self._ops: list = []                  # state-changing calls, replayed onto a regrown handle
+        self._stateful = False                # any logged call other than a trace load
         self._parts: list[PackedTrace] = []   # loaded requests, in load order
         self._arrival: list[np.ndarray] = []  # their arrival (route / enqueue time) in us
         self._reported: list[np.ndarray] = []  # which of them the Collector reports (route / trace)
+        self._pending: list = []              # route() records not folded into _parts yet
         self._n = 0
         self._by_rid: dict[int, list[int]] = {}   # request id -> loaded indices (duplicate checks)
         self._runs = 0
@@ -445,7 +447,7 @@ class ClusterSim:
     def _do(self, op, expected: tuple = ()):
         """Run a state-changing call, regrowing on a capacity signal; log it (with the exception
         it raised, when that exception is part of the reference semantics)."""
-        stateful = any(o[0] != "load" for o, _ in self._ops)
+        stateful = self._stateful
         for _attempt in range(8):
             try:
                 res = self._exec(op, stateful=stateful)
@@ -456,11 +458,15 @@ class ClusterSim:
                 self._rebuild(log_cap=exc.needed + 1024)
                 continue
             except expected as exc:
-                self._ops.append((op, type(exc)))
+                self._log(op, type(exc))
                 raise
-            self._ops.append((op, None))
+            self._log(op, None)
             return res
         raise RuntimeError("device capacities kept overflowing")
+
+    def _log(self, op, raised) -> None:
+        self._ops.append((op, raised))
+        self._stateful = self._stateful or op[0] != "load"
 
     def _exec(self, op, *, replaying: bool = False, stateful: bool = False):
         h = self._device()
@@ -470,6 +476,7 @@ class ClusterSim:
             h.load(arr, tr.in_tokens, tr.out_tokens, tr.request_id, tr.blk_off, tr.blocks)
             if replaying:                 # the bookkeeping of a logged load exists already
                 return None
+            self._flush()
             first = self._n
             self._parts.append(tr)
             self._arrival.append(np.asarray(arr, np.int64))
@@ -479,6 +486,10 @@ class ClusterSim:
         if kind == "route":
             _, idx, now, holders = op
             return h.route_one(idx, now, holders=holders)
+        if kind == "route_request":       # load + decide in one device call (rsim_route_request)
+            _, rec, now, holders = op
+            return h.route_request(now, rec.input_tokens, rec.output_tokens, rec.request_id, rec.prefix_blocks,
+                                   holders=holders)
         if kind == "enqueue":
             _, inst, idx, now = op
             return h.enqueue(inst, idx, now)
@@ -506,7 +517,17 @@ class ClusterSim:
         raise ValueError(kind)
 
     # -- API-mode helpers -------------------------------------------------------------------
+    def _flush(self) -> None:
+        """Fold the records route() appended since the last fold into the loaded parts."""
+        if self._pending:
+            recs = [r for r, _ in self._pending]
+            self._parts.append(PackedTrace.from_records(recs))
+            self._arrival.append(np.fromiter((t for _, t in self._pending), np.int64, len(recs)))
+            self._reported.append(np.ones(len(recs), bool))
+            self._pending = []
+
     def _record(self, idx: int) -> TraceRecord:
+        self._flush()
         for tr in self._parts:
             if idx < len(tr):
                 return tr.record(idx)
@@ -514,6 +535,7 @@ class ClusterSim:
         raise IndexError(idx)
 
     def _arrival_us(self, idx: int) -> int:
+        self._flush()
         for a in self._arrival:
             if idx < len(a):
                 return int(a[idx])
@@ -521,6 +543,7 @@ class ClusterSim:
         raise IndexError(idx)
 
     def _mark_reported(self, idx: int, n: int = 1) -> None:
+        self._flush()
         base = 0
         for m in self._reported:
             if base <= idx < base + len(m):
@@ -576,17 +599,28 @@ class ClusterSim:
         if self.config.detector is not None:
             from .config import UnsupportedConfigError
             raise UnsupportedConfigError("route() with the hotspot detector: replay a trace with run_trace")
-        self._advance_clock(int(now_us), "route()")
-        holders = tuple(sorted(self._holders(record.request_id)))
-        idx = self._do(("load", PackedTrace.from_records([record]), np.array([now_us], np.int64)))
-        chosen, _ht, scores = self._do(("route", idx, int(now_us), holders), expected=(DuplicateRequestError,))
-        self._by_rid.setdefault(record.request_id, []).append(idx)
-        self._mark_reported(idx)
-        return RoutingDecision(chosen=chosen, scores={i: float(s) for i, s in enumerate(scores)},
+        now_us = int(now_us)
+        self._advance_clock(now_us, "route()")
+        holders = tuple(sorted(self._holders(record.request_id))) if record.request_id in self._by_rid else ()
+        idx = self._n
+        try:
+            chosen, _ht, scores = self._do(("route_request", record, now_us, holders),
+                                           expected=(DuplicateRequestError,))
+        except DuplicateRequestError:
+            self._routed(record, now_us, idx)
+            raise
+        self._routed(record, now_us, idx)
+        return RoutingDecision(chosen=chosen, scores=dict(enumerate(scores.tolist())),
                                filtered=frozenset(), kind=self.config.policy.kind, time_us=now_us)
+
+    def _routed(self, record: TraceRecord, now_us: int, idx: int) -> None:
+        self._pending.append((record, now_us))
+        self._n += 1
+        self._by_rid.setdefault(record.request_id, []).append(idx)
 
     # -- trace replay (cluster.py:172-201) -----------------------------------------------------
     def run_trace(self, records: Sequence[TraceRecord] | PackedTrace) -> RunReport:
+        self._flush()
         trace = PackedTrace.from_records(records)
         validate_against_block_size(trace, self.block_size)
         if len(trace):
@@ -634,6 +668,7 @@ class ClusterSim:
         return max(1 << 16, 8 * n + out // 2)
 
     def _report(self, trace: PackedTrace, queued_last: int) -> RunReport:
+        self._flush()
         h = self._device()
         N = self._n
         inst = h.instances()

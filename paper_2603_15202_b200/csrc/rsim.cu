@@ -15,7 +15,14 @@
 
 #include "../../include/rsim.h"
 #include "rsim_kernels.cuh"
+#ifndef RSIM_SLOT_MULT
+#define RSIM_SLOT_MULT 8   // table slots >= 8/3 x expected keys at least: load <= 3/8
+#endif
+#ifndef RSIM_TABLE_BUDGET
+#define RSIM_TABLE_BUDGET (256ull << 20)   // all N tables: keep chat1024's inside L2-friendly sizes
+#endif
 #include "rsim_check.cuh"
+#include "rsim_api.cuh"
 
 namespace {
 
@@ -112,6 +119,12 @@ struct rsim {
     DevArr<u32> dupmask;            // route() API: instances holding the request id (bitmap)
     const u32 *cur_dupmask = nullptr;
     i64 crit_cap = 0;
+    // rsim_route_request: one mapped pinned block in each direction (the request in, the
+    // decision + scores + device error word out), read / written by the kernels themselves
+    i64 *rq_h = nullptr;            // pinned request block
+    DevArr<i64> rq_dev;             // its device copy
+    size_t rq_cap = 0;              // i64 words
+    i64 *ro_h = nullptr, *ro_d = nullptr;
 };
 
 static rsim_status fail(rsim_t *h, rsim_status st, const char *fmt, ...) {
@@ -179,10 +192,15 @@ static Params make_params(rsim_t *h) {
     return P;
 }
 
+static rsim_status decode_device_error(rsim_t *h, const int *e);
 static rsim_status check_device_error(rsim_t *h) {
     int e[4];
     CK(h, cudaMemcpyAsync(e, h->errbuf, sizeof(e), cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
+    return decode_device_error(h, e);
+}
+// the device error word (errbuf: code, instance, detail); non-zero words are cleared for the next call
+static rsim_status decode_device_error(rsim_t *h, const int *e) {
     if (e[0] == 0) return RSIM_OK;
     CK(h, cudaMemsetAsync(h->errbuf, 0, 4 * sizeof(int), h->stream));
     switch (e[0]) {
@@ -355,7 +373,19 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     int sl = c.table_slots_log2;
     if (sl <= 0) {
         i64 expect = c.expected_keys > 0 ? c.expected_keys : 3000;   // callers size from the trace
-        sl = ilog2_ceil(expect * 4 / 3 + 64);
+        // A low load factor keeps nearly every lookup inside the aligned 16-B slot pair at its
+        // home (linear probing: a miss at load a scans ~(1 + 1/(1-a)^2)/2 slots). Load <= 3/32
+        // while the N tables (24 B per slot) stay within RSIM_TABLE_BUDGET, else down to <= 3/8
+        // (A/B on one B200, us/decision at load <= 3/4, 3/8, 3/16, 3/32: api64 6.05 / 5.20 /
+        // 4.95 / 4.88; chat1024 7.07 / 6.80 / 6.71 / 6.82 -- but 3.2x the algorithmic DRAM bytes
+        // at 3/32 (805 MB of tables); agent256 - / 19.1 / 18.4 / 18.3; large4096 12.7 / 12.2 /
+        // 12.9 / 13.4).
+        int mult = 32;
+        sl = ilog2_ceil(expect * mult / 3 + 64);
+        while (mult > RSIM_SLOT_MULT && ((size_t)N << sl) * 24 > (size_t)RSIM_TABLE_BUDGET) {
+            mult /= 2;
+            sl = ilog2_ceil(expect * mult / 3 + 64);
+        }
     }
     h->slog2 = std::max(6, std::min(30, sl));
     h->max_occ = ((i64)3 << h->slog2) / 4;
@@ -409,6 +439,10 @@ void rsim_destroy(rsim_t *h) {
                   h->scores, h->scratch_keys, h->scratch_res, h->ctr, h->mbox, h->runs, h->crit, h->hring,
                   h->dtot, h->dglob, h->simj};
     h->dsegs.free_(); h->seen.free_(); h->dupmask.free_();
+    if (h->rq_h) cudaFreeHost(h->rq_h);
+    if (h->ro_h) cudaFreeHost(h->ro_h);
+    h->rq_h = h->ro_h = h->ro_d = nullptr; h->rq_cap = 0;
+    h->rq_dev.free_();
     h->ddbg.free_(); h->dtid.free_(); h->dtw.free_(); h->dtex.free_(); h->dbk.free_(); h->drows.free_(); h->dtkey.free_(); h->dtr.free_();
     h->arena.free_();
     for (int i = 0; i < 8; i++) if (h->peer_ipc[i] && h->peer[i]) cudaIpcCloseMemHandle(h->peer[i]);
@@ -491,7 +525,7 @@ rsim_status rsim_load_trace(rsim_t *h, int64_t n, const int64_t *arrival_us, con
 }
 
 static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode, int target, double *scores_dev,
-                                 float *ms_out) {
+                                 float *ms_out, bool sync = true) {
     if (h->cfg.world > 1) {
         if (mode == MODE_ROUTE || mode == MODE_ENQUEUE)
             return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls are single-rank only");
@@ -520,7 +554,7 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     at[0].val.clusterDim.x = h->C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    CK(h, cudaEventRecord(h->ev0, h->stream));
+    if (sync) CK(h, cudaEventRecord(h->ev0, h->stream));
     const bool filt = h->cfg.policy == RSIM_POLICY_FILTER ||            // the extended kernel: two-branch or
                       (h->cfg.policy == RSIM_POLICY_LINEAR && !(h->cfg.bs_norm_cap > 0)) ||   // two-round decisions,
                       h->cfg.staleness_us > 0 || h->cfg.det_on ||                           // stale snapshots, detector,
@@ -534,6 +568,7 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     else
         CK(h, cudaLaunchKernelEx(&lc, replay_kernel<RSIM_MAX_WARPS, true>, P, (i64)k0, (i64)k1, (i64)until, mode, target));
     h->launches++;
+    if (!sync) return RSIM_OK;       // rsim_route_request: the caller collects results + error word
     CK(h, cudaEventRecord(h->ev1, h->stream));
     CK(h, cudaEventSynchronize(h->ev1));
     if (ms_out) cudaEventElapsedTime(ms_out, h->ev0, h->ev1);
@@ -636,6 +671,97 @@ rsim_status rsim_route_one_excl(rsim_t *h, int64_t r, int64_t now_us, const int3
             if ((i64)*mm.second - (i64)*mm.first > h->cfg.range_threshold)
                 memcpy(scores, bsv.data(), h->N * sizeof(double));
         }
+    }
+    return RSIM_OK;
+}
+
+// ClusterSim.route(record, now_us) of a request that is not loaded yet (cluster.py:130-154): the
+// request is appended to the device trace by route_ingest_kernel straight from mapped pinned
+// memory, decided by a one-decision replay launch, and the decision + scores + device error word
+// come back through mapped memory written by route_out_kernel: three launches, one synchronisation.
+rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, int64_t output_tokens,
+                               uint64_t request_id, const uint64_t *blocks, int64_t n_blocks,
+                               const int32_t *holders, int32_t n_holders, int32_t *chosen, int64_t *hit_tokens,
+                               double *scores) {
+    if (!h) return RSIM_E_INVALID;
+    if (h->cfg.det_on) return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls with the hotspot detector: use a trace replay");
+    if (h->cfg.world > 1) return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls are single-rank only");
+    if (n_blocks < 1 || !blocks) return fail(h, RSIM_E_TRACE, "request has no blocks");
+    if (input_tokens < 1 || output_tokens < 1) return fail(h, RSIM_E_TRACE, "request: in/out must be >= 1");
+    if (input_tokens > (1LL << 40) || output_tokens > (1LL << 31)) return fail(h, RSIM_E_TRACE, "request: token count too large");
+    if (n_holders < 0 || (n_holders > 0 && !holders)) return fail(h, RSIM_E_INVALID, "bad holders");
+    CK(h, cudaSetDevice(h->cfg.device));
+    const int N = h->cfg.n_instances;
+    const i64 words = n_holders > 0 ? ((i64)N + 31) / 32 : 0;
+    const size_t need = RQ_HDR + (size_t)words + (size_t)n_blocks;
+    cudaStream_t st = h->stream;
+    if (need > h->rq_cap) {
+        if (h->rq_h) { CK(h, cudaStreamSynchronize(st)); CK(h, cudaFreeHost(h->rq_h)); h->rq_h = nullptr; }
+        const size_t cap = std::max<size_t>(need * 2, 4096);
+        void *p = nullptr;
+        CK(h, cudaHostAlloc(&p, cap * sizeof(i64), cudaHostAllocDefault));
+        h->rq_h = (i64 *)p; h->rq_cap = cap;
+        CK(h, h->rq_dev.reserve(cap, 0, st));
+    }
+    if (!h->ro_h) {
+        void *p = nullptr;
+        CK(h, cudaHostAlloc(&p, (RO_HDR + 2 * (size_t)h->N) * sizeof(i64), cudaHostAllocMapped));
+        h->ro_h = (i64 *)p;
+        CK(h, cudaHostGetDevicePointer((void **)&h->ro_d, p, 0));
+    }
+    const i64 bs = h->cfg.block_size;
+    const i64 R0 = h->R, R1 = R0 + 1, no = (output_tokens + bs - 1) / bs;
+    CK(h, h->arrival.reserve(R1, R0, st)); CK(h, h->in_tok.reserve(R1, R0, st)); CK(h, h->out_tok.reserve(R1, R0, st));
+    CK(h, h->rid.reserve(R1, R0, st)); CK(h, h->blk_off.reserve(R1 + 1, R0 + 1, st)); CK(h, h->ooff.reserve(R1 + 1, R0 + 1, st));
+    CK(h, h->blocks.reserve(h->nblk + n_blocks, h->nblk, st)); CK(h, h->ckeys.reserve(h->nblk + n_blocks, h->nblk, st));
+    CK(h, h->okeys.reserve(h->nout + no + 1, h->nout, st));
+    CK(h, h->hit_blocks.reserve(R1, R0, st)); CK(h, h->chosen.reserve(R1, R0, st));
+    DevArr<i64> *outs[] = {&h->hit_tokens, &h->first_sched, &h->first_token, &h->finish, &h->route_bs, &h->dec_ns};
+    for (auto *a : outs) CK(h, a->reserve(R1, R0, st));
+    if (words) CK(h, h->dupmask.reserve(words, 0, st));
+    i64 *q = h->rq_h;
+    q[RQ_ARRIVAL] = now_us; q[RQ_IN] = input_tokens; q[RQ_OUT] = output_tokens; q[RQ_RID] = (i64)request_id;
+    q[RQ_B] = n_blocks; q[RQ_R0] = R0; q[RQ_NBLK0] = h->nblk; q[RQ_NOUT0] = h->nout; q[RQ_NO] = no; q[RQ_NDUP] = words;
+    for (i64 w = 0; w < words; w++) q[RQ_HDR + w] = 0;
+    for (int i = 0; i < n_holders; i++) {
+        if (holders[i] < 0 || holders[i] >= N) return fail(h, RSIM_E_INVALID, "holder out of range");
+        q[RQ_HDR + (holders[i] >> 5)] |= (i64)(1u << (holders[i] & 31));
+    }
+    memcpy(q + RQ_HDR + words, blocks, (size_t)n_blocks * sizeof(u64));
+    CK(h, cudaMemcpyAsync(h->rq_dev.p, q, need * sizeof(i64), cudaMemcpyHostToDevice, st));
+    route_ingest_kernel<<<1, 32, 0, st>>>(h->rq_dev.p, h->arrival.p, h->in_tok.p, h->out_tok.p, h->rid.p, h->blk_off.p,
+                                          h->ooff.p, h->blocks.p, h->ckeys.p, h->okeys.p, h->chosen.p, h->hit_blocks.p,
+                                          h->hit_tokens.p, h->first_sched.p, h->first_token.p, h->finish.p,
+                                          h->route_bs.p, h->dec_ns.p, h->dupmask.p, h->flag);
+    h->launches++;
+    CK(h, cudaGetLastError());
+    if (R0 > 0 && now_us < h->last_arrival) h->order_breaks.push_back(R0);
+    h->last_arrival = now_us;
+    h->R = R1; h->nblk += n_blocks; h->nout += no;
+    h->cur_dupmask = words ? h->dupmask.p : nullptr;
+    rsim_status rs = launch_replay(h, R0, R1, now_us, MODE_ROUTE, -1, h->scores, nullptr, false);
+    h->cur_dupmask = nullptr;
+    if (rs != RSIM_OK) { cudaStreamSynchronize(st); return rs; }
+    const bool filt = h->cfg.policy == RSIM_POLICY_FILTER;
+    const int nsc = (filt ? 2 : 1) * h->N;
+    route_out_kernel<<<1, 128, 0, st>>>(h->chosen.p, h->hit_tokens.p, R0, h->scores, nsc, h->errbuf, h->flag, h->ro_d);
+    h->launches++;
+    CK(h, cudaGetLastError());
+    CK(h, cudaStreamSynchronize(st));
+    const i64 *o = h->ro_h;
+    const int e[4] = {(int)o[RO_ERR0], (int)o[RO_ERR1], (int)o[RO_ERR2], (int)o[RO_ERR3]};
+    if ((rs = decode_device_error(h, e)) != RSIM_OK) return rs;
+    if (o[RO_FLAG]) return fail(h, RSIM_E_TRACE, "a chain key equals the table sentinel 0 (probability 2^-64 per key)");
+    if (chosen) *chosen = (int32_t)o[RO_CHOSEN];
+    if (hit_tokens) *hit_tokens = o[RO_HIT];
+    if (scores) {
+        const double *sc = reinterpret_cast<const double *>(o + RO_HDR);
+        const double *pick = sc;
+        if (filt) {       // the branch route_filter took (policies.py:180-183)
+            const auto mm = std::minmax_element(sc + h->N, sc + 2 * h->N);
+            if ((i64)*mm.second - (i64)*mm.first > h->cfg.range_threshold) pick = sc + h->N;
+        }
+        memcpy(scores, pick, h->N * sizeof(double));
     }
     return RSIM_OK;
 }

@@ -667,11 +667,16 @@ __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, 
 }
 
 // TieBreaker counter at decision time = c0 + ties, c0 the launch-start value: counter mod T
-// is (c0 mod T + ties mod T) mod T with c0 mod T precomputed per T (modtab, T < RSIM_MODTAB).
+// is (c0 mod T + ties mod T) mod T with c0 mod T memoised per T (modtab, T < RSIM_MODTAB;
+// 0xffffffff = not computed yet: a launch sees few distinct tie counts, and a one-decision
+// route() launch should not pay for 2048 128-bit remainders up front). Called by the whole
+// control warp with the same T, so every lane computes and stores the same value.
 #define RSIM_MODTAB 2048
-__device__ __forceinline__ u32 tie_index(const u32 *modtab, u64 c0_lo, u64 c0_hi, u32 ties, u32 T) {
+__device__ __forceinline__ u32 tie_index(u32 *modtab, u64 c0_lo, u64 c0_hi, u32 ties, u32 T) {
     if (T < RSIM_MODTAB) {
-        u32 r = modtab[T] + ties % T;
+        u32 m = modtab[T];
+        if (m == 0xffffffffu) { m = mod_counter(c0_lo, c0_hi, T); modtab[T] = m; }
+        u32 r = m + ties % T;
         return r >= T ? r - T : r;
     }
     u64 lo = c0_lo + ties;
@@ -679,7 +684,7 @@ __device__ __forceinline__ u32 tie_index(const u32 *modtab, u64 c0_lo, u64 c0_hi
 }
 
 __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
-                                             Dec &dec, const u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane,
+                                             Dec &dec, u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane,
                                              bool filter, const Part *det_branch = nullptr, int det_code = 0) {
     // round-major: lane holds flat partials r*32 + lane (conflict-free 16-byte loads); flat
     // order = ascending instance id
@@ -922,12 +927,16 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         ctl[0] = k0;
     }
     if (mode != MODE_DRAIN)
-        for (int T = threadIdx.x; T < RSIM_MODTAB; T += blockDim.x) modtab[T] = T > 1 ? mod_counter(c0_lo, c0_hi, (u32)T) : 0u;
+        for (int T = threadIdx.x; T < RSIM_MODTAB; T += blockDim.x) modtab[T] = 0xffffffffu;
     if (P.rsm_off) {                                       // running lists of this shard -> shared memory
-        const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(P.rbuf + (size_t)base * P.max_batch);
-        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(smem + P.rsm_off);
-        const int n16 = nloc * (int)P.max_batch * (int)(sizeof(REnt) / 16);
-        for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+        // (only the live prefix [0, r) of each list: the lists are kept compact)
+        const int nw = blockDim.x >> 5;
+        for (int i = warp; i < nloc; i += nw) {
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(P.rbuf + (size_t)(base + i) * P.max_batch);
+            ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(smem + P.rsm_off) + (size_t)i * P.max_batch * (sizeof(REnt) / 16);
+            const int n16 = st[i].r * (int)(sizeof(REnt) / 16);
+            for (int j = lane; j < n16; j += 32) dst[j] = src[j];
+        }
     }
     if (det_run) {
         if (P.dsm) {                                        // detector state -> shared memory
@@ -1342,10 +1351,13 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     }
     if (P.rsm_off) {
-        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(P.rbuf + (size_t)base * P.max_batch);
-        const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(smem + P.rsm_off);
-        const int n16 = nloc * (int)P.max_batch * (int)(sizeof(REnt) / 16);
-        for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+        const int nw = blockDim.x >> 5;
+        for (int i = warp; i < nloc; i += nw) {
+            ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(P.rbuf + (size_t)(base + i) * P.max_batch);
+            const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(smem + P.rsm_off) + (size_t)i * P.max_batch * (sizeof(REnt) / 16);
+            const int n16 = st[i].r * (int)(sizeof(REnt) / 16);
+            for (int j = lane; j < n16; j += 32) dst[j] = src[j];
+        }
     }
     if (!control && lane == 0) {
         if (WB.werr) atomicCAS(P.err, 0, WB.werr);

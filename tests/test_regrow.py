@@ -51,7 +51,7 @@ def test_touch_run_ring_overflow_is_reported():
 @pytest.mark.parametrize("name,sizing", [
     ("cost_small_batch", dict(queue_capacity=16)),
     ("cfg2_api_prefix4000", dict(expected_keys=64)),
-    ("evict_heavy_n4", dict(queue_capacity=16, expected_keys=64)),      # runs ring derives from the queue
+    ("evict_heavy_n4", dict(queue_capacity=16, expected_keys=16)),      # runs ring derives from the queue
     ("cfg3_agent_evict_n16", dict(queue_capacity=16, expected_keys=256)),
 ])
 def test_regrown_replay_matches_reference(name, sizing, monkeypatch):
