@@ -143,7 +143,9 @@ rsim_status rsim_read_request_times(rsim_t *h, int64_t first, int64_t count,
  * r_bs, q_bs, pending, total, dc (live), view r, q, pending, total, dc, busy_until_us, occupancy. */
 rsim_status rsim_read_instances(rsim_t *h, int64_t *out12xN);
 /* Step log: 6 int64 per record (instance, start_us, end_us, prefill_us, bs_after, step_index),
- * unordered; *n_records receives the total (may exceed cap: then RSIM_E_INVALID). */
+ * unordered. With out = NULL, *n_records receives an upper bound of the record count (records
+ * are reserved per device warp in chunks; a bound above cap: RSIM_E_INVALID); with out, the
+ * records written (the unused reserved ones dropped). */
 rsim_status rsim_read_step_log(rsim_t *h, int64_t *out, int64_t cap, int64_t *n_records);
 /* Per-request batch size right after its enqueue (Collector.record_bs at route, cluster.py:152). */
 rsim_status rsim_read_route_bs(rsim_t *h, int64_t first, int64_t count, int64_t *bs);

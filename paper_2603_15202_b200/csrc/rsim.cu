@@ -985,6 +985,14 @@ rsim_status rsim_read_step_log(rsim_t *h, int64_t *out, int64_t cap, int64_t *n_
     if ((i64)n > h->log_cap) return fail(h, RSIM_E_INVALID, "step log overflowed its capacity (%lld)", (long long)h->log_cap);
     if ((i64)n > cap) return fail(h, RSIM_E_INVALID, "output buffer too small");
     if (n) CK(h, cudaMemcpy(out, h->log, n * 6 * sizeof(i64), cudaMemcpyDeviceToHost));
+    // records are reserved per warp in chunks (log_step): drop the unused ones (gi = -1)
+    i64 m = 0;
+    for (i64 i = 0; i < (i64)n; i++)
+        if (out[6 * i] >= 0) {
+            if (m != i) memcpy(out + 6 * m, out + 6 * i, 6 * sizeof(i64));
+            m++;
+        }
+    if (n_records) *n_records = m;
     return RSIM_OK;
 }
 

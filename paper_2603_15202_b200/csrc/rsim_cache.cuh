@@ -359,6 +359,7 @@ struct FinBuf {
     const u64 *tpkeys;          // the request's first 128 chain keys (its staging slot)
     const int *tpsl;            // their probe-found slots, or null
     struct Inst *tpsp;
+    i64 lnext, lend;            // this warp's reserved step-log records [lnext, lend) (log_step)
 };
 
 __device__ int warp_finish_many(const Table &T, const u64 *ckeys, const u64 *okeys, const FinBuf &F, int nf, i64 now,

@@ -182,15 +182,30 @@ __device__ void flush_finishers(const Params &P, int gi, Inst &s, FinBuf &F, int
     if (P.ctr != nullptr && lane == 0) { atomicAdd(P.ctr + 3, (u64)(clock64() - c0)); atomicAdd(P.ctr + 6, (u64)1); }
 }
 
-__device__ __forceinline__ void log_step(const Params &P, int gi, i64 start, i64 end, i64 pre, i64 bs_after,
-                                         i64 idx, int lane) {
+// The step log (record_steps): each warp reserves RSIM_LOG_CHUNK records at a time with one
+// global atomic (a per-step atomic put an L2 round trip on every step of the critical path);
+// the host sorts the log into the reference's loop order (report.py) and drops the unused
+// tail records of each chunk (gi = -1, written at the end of the launch: close_log).
+#define RSIM_LOG_CHUNK 32
+__device__ __forceinline__ void log_step(const Params &P, FinBuf &F, int gi, i64 start, i64 end, i64 pre,
+                                         i64 bs_after, i64 idx, int lane) {
     if (P.log != nullptr && lane == 0) {
-        u64 n = atomicAdd(P.log_n, 1ULL);
-        if ((i64)n < P.log_cap) {
+        i64 n = F.lnext;
+        if (n >= F.lend) { n = (i64)atomicAdd(P.log_n, (u64)RSIM_LOG_CHUNK); F.lend = n + RSIM_LOG_CHUNK; }
+        F.lnext = n + 1;
+        if (n < P.log_cap) {
             i64 *r = P.log + 6 * n;
             r[0] = gi; r[1] = start; r[2] = end; r[3] = pre; r[4] = bs_after; r[5] = idx;
         }
     }
+}
+__device__ __forceinline__ void close_log(const Params &P, FinBuf &F, int lane) {
+    __syncwarp();
+    if (P.log != nullptr)
+        for (i64 n = F.lnext + lane; n < F.lend; n += 32)
+            if (n < P.log_cap) P.log[6 * n] = -1;
+    __syncwarp();
+    if (lane == 0) F.lnext = F.lend = 0;
 }
 
 // Run the pending commit touch + pin of F (if any).
@@ -390,7 +405,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
             sp->next_step = end;
             sp->step_idx = step_idx + 1;
         }
-        log_step(P, gi, t, end, 0, (i64)ndec, step_idx, lane);
+        log_step(P, F, gi, t, end, 0, (i64)ndec, step_idx, lane);
         __syncwarp();
         SP_MARK(7);
 #ifdef RSIM_STEP_PROFILE
@@ -447,7 +462,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
             sp->next_step = end;
             sp->step_idx = step_idx + 1;
         }
-        log_step(P, gi, t, end, 0, (i64)r, step_idx, lane);
+        log_step(P, F, gi, t, end, 0, (i64)r, step_idx, lane);
         __syncwarp();
         SP_MARK(7);
 #ifdef RSIM_STEP_PROFILE
@@ -527,7 +542,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
             if (P.log != nullptr) {
                 end1 = __shfl_sync(FULL, end1, 0); pre1 = __shfl_sync(FULL, pre1, 0);
                 r1 = __shfl_sync(FULL, r1, 0); npop1 = __shfl_sync(FULL, npop1, 0);
-                log_step(P, gi, t, end1, pre1, (i64)(1 - npop1) + r1, step_idx, lane);
+                log_step(P, F, gi, t, end1, pre1, (i64)(1 - npop1) + r1, step_idx, lane);
             }
             __syncwarp();
             SP_MARK(7);
@@ -717,7 +732,7 @@ __device__ __forceinline__ bool inst_step_body(const Params &P, Inst *sp, int gi
         sp->next_step = end;
         sp->step_idx = step_idx + 1;
     }
-    log_step(P, gi, t, end, pre, (i64)(q - npop) + r, step_idx, lane);
+    log_step(P, F, gi, t, end, pre, (i64)(q - npop) + r, step_idx, lane);
     __syncwarp();
     SP_MARK(7);
 #ifdef RSIM_STEP_PROFILE

@@ -917,7 +917,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     u32 ties = 0;                                          // ties resolved in this launch (control warp)
     const int l0 = warp * ipw;
     const int nmine = control ? 0 : max(0, min(ipw, nloc - l0));
-    if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; WB.fin.dnf = 0; WB.fin.npark = 0; WB.fin.tpn = 0; }
+    if (!control && lane == 0) { WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1; WB.fin.dnf = 0; WB.fin.npark = 0; WB.fin.tpn = 0; WB.fin.lnext = WB.fin.lend = 0; }
     if (threadIdx.x == 0) {
         // detector mode: every instance warp also arrives (release) after its plain shared-memory stores
         mbar_init(&mb[0], 1); mbar_init(&mb[1], 1); mbar_init(&dmb[0], 1); mbar_init(&dmb[1], 1);
@@ -1332,6 +1332,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     }
 #undef PHASE
     if (!control && mode != MODE_DRAIN) flush_touch_pin(P, WB.fin, lane, &WB.werr);
+    if (!control) close_log(P, WB.fin, lane);
 #ifdef RSIM_DIAG
     if (prof && lane == 0)
         for (int i = 0; i < 8; i++) if (ph[i]) atomicAdd(P.ctr + 8 + i, ph[i]);

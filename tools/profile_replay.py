@@ -82,7 +82,7 @@ for c, w in shapes:
     if c and c > cfg.n_instances:
         continue
     try:
-        h = _native.Handle(native_config(cfg, sizing_for(trace, cfg), ctas=c, warps_per_cta=w))
+        h = _native.Handle(native_config(cfg, sizing_for(trace, cfg), ctas=c, warps_per_cta=w, record_steps=bool(os.environ.get("RSIM_LOG")), step_log_capacity=(8 * len(trace) + int(trace.out_tokens.sum()) // 2) if os.environ.get("RSIM_LOG") else 0))
     except ValueError as exc:
         print(f"{name} ctas={c} warps={w}: skipped ({exc})")
         continue
