@@ -451,7 +451,7 @@ def measure_whatif(h, trace, cfg, args, name):
     best = min(ms) / 1000.0
     peaks, _ = measured_peaks()
     gbs = alg / best / 1e9
-    kern = "probe_batch_kernel" if hits.shape[1] >= 256 else "probe_pairs_kernel"
+    kern = "probe_scan_kernel"
     return {"requests": M, "instances": int(hits.shape[1]), "pairs": int(M * hits.shape[1]),
             "ms": min(ms), "pairs_per_s": M * hits.shape[1] / best, "algorithmic_bytes": alg,
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",

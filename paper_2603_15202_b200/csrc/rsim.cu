@@ -879,12 +879,12 @@ rsim_status rsim_probe_batch(rsim_t *h, int64_t first, int64_t count, int32_t *o
     const size_t n = (size_t)count * h->N;
     CK(h, cudaMalloc(&d, std::max<size_t>(n, 1) * sizeof(int)));
     CK(h, cudaEventRecord(h->ev0, h->stream));
-    if (h->N >= 256) {                                       // a block per request, grid-stride
-        const int grid = (int)std::min<i64>(count, 148 * 8);
-        probe_batch_kernel<<<std::max(grid, 1), 256, 0, h->stream>>>(make_params(h), first, count, d);
-    } else {                                                 // a warp per (request, instance)
-        const int grid = (int)std::min<i64>(((i64)n * 32 + 255) / 256, 148 * 8);
-        probe_pairs_kernel<<<std::max(grid, 1), 256, 0, h->stream>>>(make_params(h), first, count, d);
+    {   // a thread per (request, instance) pair, grid-stride, 8 resident blocks per SM
+        const int grid = (int)std::min<i64>(((i64)n + 255) / 256, 148 * 8);
+        static const int depth = getenv("RSIM_PROBE_DEPTH") ? atoi(getenv("RSIM_PROBE_DEPTH")) : 3;   // A/B switch (D = 2 / 3 / 4: api64 0.194 / 0.189 / 0.188 ms, chat1024 1.32 / 1.34 / 1.38, agent256 4.16 / 3.88 / 3.68)
+        if (depth >= 4) probe_scan_kernel<4><<<std::max(grid, 1), 256, 0, h->stream>>>(make_params(h), first, count, d);
+        else if (depth == 3) probe_scan_kernel<3><<<std::max(grid, 1), 256, 0, h->stream>>>(make_params(h), first, count, d);
+        else probe_scan_kernel<2><<<std::max(grid, 1), 256, 0, h->stream>>>(make_params(h), first, count, d);
     }
     h->launches++;
     CK(h, cudaGetLastError());

@@ -1377,59 +1377,59 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
 
 // ---------------------------------------------------------------- probe batch
 // What-if probe (SURVEY 8d tertiary): M requests x all instances against the frozen state,
-// no commits -- the bandwidth-bound form of the probe. A block per request: its chain keys
-// and home slots are staged in shared memory once for all instances, and each warp runs the
-// two-stage strided probe over a chunk of instances (<= LP + S - 1 lookups per pair instead
-// of B); prompts longer than 128 blocks use the warp probe with the 128-ary deep search.
+// no commits -- the bandwidth-bound form of the probe. One THREAD per (request, instance) pair
+// walks the request's chain from depth 0 exactly as match_keys does (kvcache.py:65-74): one
+// table lookup per depth, stop at the first miss, so a pair costs the reference's own
+// min(h+1, B) lookups. Throughput comes from the number of independent walks in flight (every
+// resident thread has its own), not from splitting one walk over a warp -- the warp-split
+// probes of the replay kernel spend 8-16 lookups per pair to cut latency, which a batch does
+// not need. The next D - 1 depths' pairs are in flight while one is evaluated (the up to D - 1
+// lookups past the first miss are the only work beyond the reference's).
+// Lanes of a warp take consecutive instances of one request: the request's chain keys are
+// shared loads (L1 broadcast), the table lines are 32 independent sectors.
+template <int D>      // lookups in flight per thread (D - 1 depths ahead of the one evaluated)
 __global__ void __launch_bounds__(256)
-probe_batch_kernel(const __grid_constant__ Params P, i64 r0, i64 nreq, int *out) {
-    __shared__ ReqStage RS;
-    __shared__ int hbuf[8][32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int N = P.N;
-    const int chunk = min(32, max(4, (N + 7) / 8));
-    for (i64 rr = blockIdx.x; rr < nreq; rr += gridDim.x) {
-        const i64 r = r0 + rr;
-        __syncthreads();                                     // the previous request is done with RS
-        const i64 a = P.blk_off[r];
-        const int B = (int)(P.blk_off[r + 1] - a);
-        if (threadIdx.x < 128 && threadIdx.x < B) {
-            const u64 kk = __ldcg(P.ckeys + a + threadIdx.x);
-            RS.keys[threadIdx.x] = kk;
-            RS.home[threadIdx.x] = tab_home(kk, P.slog2);
+probe_scan_kernel(const __grid_constant__ Params P, i64 r0, i64 nreq, int *out) {
+    const i64 total = nreq * (i64)P.N;
+    const i64 stride = (i64)gridDim.x * blockDim.x;
+    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += stride) {
+        const i64 rr = p / P.N;
+        const int gi = (int)(p - rr * P.N);
+        const i64 a = __ldg(P.blk_off + r0 + rr);
+        const int B = (int)(__ldg(P.blk_off + r0 + rr + 1) - a);
+        const u64 *keys = P.ckeys + a;
+        const Table T = table_of(P, gi);
+        u64 kq[D];
+        u32 hq[D];
+        ulonglong2 pq[D];
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            kq[j] = j < B ? __ldg(keys + j) : 0ULL;
+            hq[j] = tab_home(kq[j], T.slog2);
+            pq[j] = j < B ? ld_pair(T, hq[j]) : make_ulonglong2(0ULL, 0ULL);
         }
-        if (threadIdx.x == 0) { RS.a = a; RS.B = B; }
-        __syncthreads();
-        if (B > 128) {
-            for (int gi = warp; gi < N; gi += 8) {
-                const int h = warp_probe(table_of(P, gi), P.ckeys + a, B, lane);
-                if (lane == 0) out[rr * N + gi] = h;
+        int h = 0;
+        bool go = true;
+        while (go) {
+#pragma unroll
+            for (int j = 0; j < D; j++) {                     // slot j holds depth h (h % D == j)
+                bool f, c;
+                eval_first(T, pq[j], hq[j], kq[j], f, c);
+                if (c) {
+                    int stt;
+                    probe_rest(T, ((hq[j] | 1u) + 1u) & T.mask, kq[j], stt);
+                    f = stt == 0;
+                }
+                if (!f || ++h == B) { go = false; break; }
+                const int d = h + D - 1;                      // refill: D - 1 depths ahead
+                if (d < B) {
+                    kq[j] = __ldg(keys + d);
+                    hq[j] = tab_home(kq[j], T.slog2);
+                    pq[j] = ld_pair(T, hq[j]);
+                }
             }
-            continue;
         }
-        for (int c0 = warp * chunk; c0 < N; c0 += 8 * chunk) {
-            const int n = min(chunk, N - c0);
-            probe_hits_sparse(P, 0, c0, n, RS, MODE_REPLAY, -1, 0u, lane, hbuf[warp]);
-            if (lane < n) out[rr * N + c0 + lane] = hbuf[warp][lane];
-            __syncwarp();
-        }
-    }
-}
-
-// Small clusters (few instances per request): one warp per (request, instance) pair with the
-// dense probe -- no per-request block synchronisation to amortise.
-__global__ void __launch_bounds__(256)
-probe_pairs_kernel(const __grid_constant__ Params P, i64 r0, i64 nreq, int *out) {
-    const i64 wid = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const i64 total = nreq * P.N;
-    for (i64 w = wid; w < total; w += ((i64)gridDim.x * blockDim.x) >> 5) {
-        const i64 r = r0 + w / P.N;
-        const int gi = (int)(w % P.N);
-        const i64 a = P.blk_off[r];
-        const int B = (int)(P.blk_off[r + 1] - a);
-        const int h = warp_probe(table_of(P, gi), P.ckeys + a, B, lane);
-        if (lane == 0) out[w] = h;
+        out[p] = h;
     }
 }
 

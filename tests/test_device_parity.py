@@ -309,6 +309,41 @@ def test_probe_batch_matches_oracle_cache(native):
     h.close()
 
 
+@pytest.mark.parametrize("builder", ["chat", "agent"])
+def test_probe_batch_large_cluster_matches_oracle_cache(native, builder):
+    """The block-per-request what-if probe of clusters >= 256 instances (depth-0 filter, then the
+    two-stage probe for prompts <= 128 blocks or the deep warp probe beyond) against oracle caches:
+    most instances hold nothing, some a partial chain, a few the whole chain."""
+    import dataclasses
+    from paper_2603_15202_b200 import workloads as W
+    from paper_2603_15202_b200.cluster import Sizing, native_config
+    from paper_2603_15202_b200 import _native
+    trace, cfg = W.chat_cluster(300, 400) if builder == "chat" else W.config3_agent(200, n_instances=300)
+    cfg = dataclasses.replace(cfg, cache=dataclasses.replace(cfg.cache, capacity_blocks=None))
+    n = 120
+    trace = trace.slice(n)
+    h = _native.Handle(native_config(cfg, Sizing(1024, 40000)))
+    h.load(trace.arrival_us, trace.in_tokens, trace.out_tokens, trace.request_id, trace.blk_off, trace.blocks)
+    refs = {}
+    rng = np.random.default_rng(5)
+    for r in range(n):
+        for i in rng.choice(cfg.n_instances, size=int(rng.integers(1, 6)), replace=False):
+            a, b = int(trace.blk_off[r]), int(trace.blk_off[r + 1])
+            keys = oracle_chain_keys(trace.blocks[a:b])
+            cut = int(rng.integers(1, b - a + 1)) if rng.random() < 0.7 else b - a
+            h.cache_insert_keys(int(i), keys[:cut], r)
+            refs.setdefault(int(i), OracleCache(None)).insert_keys(keys[:cut], r)
+    got = h.probe_batch(0, n)
+    for r in range(n):
+        a, b = int(trace.blk_off[r]), int(trace.blk_off[r + 1])
+        keys = oracle_chain_keys(trace.blocks[a:b])
+        want = [refs[i].match_keys(keys) if i in refs else 0 for i in range(cfg.n_instances)]
+        assert list(got[r]) == want, r
+    if builder == "agent":
+        assert int(np.diff(trace.blk_off).max()) > 128       # the deep path ran
+    h.close()
+
+
 _ROUTE_POLICIES = ("simulate", "simulate_mistuned", "multiplicative", "vllm", "linear", "filter")
 
 

@@ -9,7 +9,7 @@ for w in ${WORKLOADS:-api64 chat1024 agent256}; do
   timeout 600 ncu --metrics $M --clock-control none -c 6 -k regex:"replay_kernel|k1_chain_keys" \
     --csv --log-file gpurun_out/r2_traffic_$w.csv \
     python bench.py --workload $w --extra "" --route-api "" --steps 1 --warmup 0 --no-cpu --no-parity --whatif 0 > /dev/null 2> gpurun_out/r2_traffic_$w.err
-  timeout 600 ncu --metrics $M --clock-control none -c 2 -k regex:"probe_pairs_kernel|probe_batch_kernel" \
+  timeout 600 ncu --metrics $M --clock-control none -c 2 -k regex:"probe_scan_kernel" \
     --csv --log-file gpurun_out/r2_traffic_whatif_$w.csv \
     python bench.py --workload $w --extra "" --route-api "" --steps 1 --warmup 0 --no-cpu --no-parity > /dev/null 2> gpurun_out/r2_traffic_whatif_$w.err
 done
