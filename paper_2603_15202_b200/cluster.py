@@ -64,7 +64,13 @@ def sizing_for(trace: PackedTrace | None, config: ClusterConfig) -> Sizing:
     # the tables hold DISTINCT keys: 1.15x the estimated mean per instance (measured max/mean:
     # 1.04 api64, 1.15 chat1024) -- sizing from non-distinct keys made chat1024's tables 10x
     # too large for L2
-    est = int(1.15 * distinct_keys_per_instance(trace, N, bs)) + maxchain + 128
+    # (memoised on the trace: a sizing guess is never a correctness matter -- an underestimate
+    # regrows on device, RSIM_E_TABLE_FULL -- and repeated run() calls on one trace skip the sample)
+    memo = trace.__dict__.setdefault("_distinct_memo", {})
+    dk = memo.get((N, bs))
+    if dk is None:
+        dk = memo[(N, bs)] = distinct_keys_per_instance(trace, N, bs)
+    est = int(1.15 * dk) + maxchain + 128
     cap = config.cache.capacity_blocks
     if cap is not None:
         est = min(est, cap + maxchain + 64)
@@ -390,6 +396,7 @@ class ClusterSim:
         self._log_cap = 1 << 16 if record_steps else 0
         self._ops: list = []                  # state-changing calls, replayed onto a regrown handle
         self._stateful = False                # any logged call other than a trace load
+        self._log_read = None                 # the step log read by the last run op
         self._parts: list[PackedTrace] = []   # loaded requests, in load order
         self._arrival: list[np.ndarray] = []  # their arrival (route / enqueue time) in us
         self._reported: list[np.ndarray] = []  # which of them the Collector reports (route / trace)
@@ -513,6 +520,7 @@ class ClusterSim:
                 log, needed = h.step_log()
                 if log is None:
                     raise _StepLogOverflow(needed)
+                self._log_read = log                  # _report's copy (the log is read once per run)
             return queued
         raise ValueError(kind)
 
@@ -688,7 +696,8 @@ class ClusterSim:
             alltr = _take(alltr, np.flatnonzero(rep_mask))
         log = None
         if self.record_steps:
-            log, needed = h.step_log()
+            log = self._log_read if self._log_read is not None else h.step_log()[0]
+            self._log_read = None
         rep = RunReport(self.config.policy.kind, self.config.seed, self.config.n_instances, self.block_size,
                         trace=alltr, columns=cols, step_log=log, end_us=end_us,
                         queued_at_last_arrival=queued_last, hash_trace=trace)

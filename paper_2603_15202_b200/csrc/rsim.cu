@@ -125,6 +125,7 @@ struct rsim {
     DevArr<i64> rq_dev;             // its device copy
     size_t rq_cap = 0;              // i64 words
     i64 *ro_h = nullptr, *ro_d = nullptr;
+    i64 *log_pin = nullptr;         // rsim_read_step_log's pinned bounce buffer
 };
 
 static rsim_status fail(rsim_t *h, rsim_status st, const char *fmt, ...) {
@@ -441,6 +442,8 @@ void rsim_destroy(rsim_t *h) {
     h->dsegs.free_(); h->seen.free_(); h->dupmask.free_();
     if (h->rq_h) cudaFreeHost(h->rq_h);
     if (h->ro_h) cudaFreeHost(h->ro_h);
+    if (h->log_pin) cudaFreeHost(h->log_pin);
+    h->log_pin = nullptr;
     h->rq_h = h->ro_h = h->ro_d = nullptr; h->rq_cap = 0;
     h->rq_dev.free_();
     h->ddbg.free_(); h->dtid.free_(); h->dtw.free_(); h->dtex.free_(); h->dbk.free_(); h->drows.free_(); h->dtkey.free_(); h->dtr.free_();
@@ -984,14 +987,30 @@ rsim_status rsim_read_step_log(rsim_t *h, int64_t *out, int64_t cap, int64_t *n_
     if (!h->log) return fail(h, RSIM_E_INVALID, "step log disabled (record_steps = 0)");
     if ((i64)n > h->log_cap) return fail(h, RSIM_E_INVALID, "step log overflowed its capacity (%lld)", (long long)h->log_cap);
     if ((i64)n > cap) return fail(h, RSIM_E_INVALID, "output buffer too small");
-    if (n) CK(h, cudaMemcpy(out, h->log, n * 6 * sizeof(i64), cudaMemcpyDeviceToHost));
-    // records are reserved per warp in chunks (log_step): drop the unused ones (gi = -1)
+    // through a pinned bounce buffer, double-buffered (the DMA of chunk c+1 runs while chunk c is
+    // compacted into out); records are reserved per warp in chunks (log_step): drop the unused
+    // ones (gi = -1)
+    const i64 CH = 1 << 17;                                   // records per chunk (6 MB)
+    if (!h->log_pin) {
+        void *p = nullptr;
+        CK(h, cudaHostAlloc(&p, 2 * CH * 6 * sizeof(i64), cudaHostAllocDefault));
+        h->log_pin = (i64 *)p;
+    }
     i64 m = 0;
-    for (i64 i = 0; i < (i64)n; i++)
-        if (out[6 * i] >= 0) {
-            if (m != i) memcpy(out + 6 * m, out + 6 * i, 6 * sizeof(i64));
-            m++;
+    const i64 nc = ((i64)n + CH - 1) / CH;
+    if (nc) CK(h, cudaMemcpyAsync(h->log_pin, h->log, std::min<i64>(CH, n) * 6 * sizeof(i64), cudaMemcpyDeviceToHost, h->stream));
+    for (i64 c = 0; c < nc; c++) {
+        CK(h, cudaStreamSynchronize(h->stream));
+        if (c + 1 < nc) {
+            const i64 o = (c + 1) * CH, len = std::min<i64>(CH, (i64)n - o);
+            CK(h, cudaMemcpyAsync(h->log_pin + ((c + 1) & 1) * CH * 6, h->log + o * 6, len * 6 * sizeof(i64),
+                                  cudaMemcpyDeviceToHost, h->stream));
         }
+        const i64 *src = h->log_pin + (c & 1) * CH * 6;
+        const i64 len = std::min<i64>(CH, (i64)n - c * CH);
+        for (i64 i = 0; i < len; i++)
+            if (src[6 * i] >= 0) { memcpy(out + 6 * m, src + 6 * i, 6 * sizeof(i64)); m++; }
+    }
     if (n_records) *n_records = m;
     return RSIM_OK;
 }
