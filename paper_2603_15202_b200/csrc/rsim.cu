@@ -350,7 +350,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     W = std::max(1, std::min(RSIM_MAX_WARPS, W));
     int ipw = (per_cta + W - 1) / W;
     if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
-    if (C * W > 256) { delete h; return fail(nullptr, RSIM_E_INVALID, "cluster too large"); }
+    if (C * W > 128) { delete h; return fail(nullptr, RSIM_E_INVALID, "cluster too large"); }   // decide_phase: <= 4 rounds of 32
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
     h->smem_bytes = (size_t)per_cta * sizeof(Inst) + (size_t)(6 * W * C) * sizeof(Part) + RSIM_SLOTS * sizeof(ReqStage) + 2 * sizeof(Dec) + 8 * sizeof(u64) + RSIM_MODTAB * sizeof(u32) + (size_t)W * sizeof(WarpBuf) +
                      (c.staleness_us > 0 ? (size_t)per_cta * sizeof(HistHead) : 0) +

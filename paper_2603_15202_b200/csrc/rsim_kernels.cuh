@@ -683,7 +683,8 @@ __device__ __forceinline__ u32 tie_index(u32 *modtab, u64 c0_lo, u64 c0_hi, u32 
     return mod_counter(lo, c0_hi + (lo < c0_lo), T);
 }
 
-__device__ __forceinline__ void decide_phase(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
+template <int NRT>      // rounds of 32 partials (CW <= 16 CTAs x 8 warps = 128: NRT <= 4)
+__device__ __forceinline__ void decide_phase_n(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
                                              Dec &dec, u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane,
                                              bool filter, const Part *det_branch = nullptr, int det_code = 0) {
     // round-major: lane holds flat partials r*32 + lane (conflict-free 16-byte loads); flat
@@ -692,8 +693,8 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
     const bool dg = P.ctr != nullptr && cta == 0 && lane == 0;
     long long dt0 = clock64(), dt1 = 0, dt2 = 0, dt3 = 0;
 #endif
-    u64 pm[8];
-    u32 pc[8];
+    u64 pm[NRT];
+    u32 pc[NRT];
     u64 mn = ~0ULL;
     u32 er = 0;
     const int NR = (CW + 31) >> 5;
@@ -703,7 +704,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         u64 bmn = ~0ULL;
         u32 bmx = 0;
 #pragma unroll
-        for (int r = 0; r < 8; r++) {
+        for (int r = 0; r < NRT; r++) {
             const int idx = r * 32 + lane;
             if (r < NR && idx < CW) {
                 const ulonglong2 q = lds_v2u64(pp + CW + idx);
@@ -717,7 +718,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         bs_branch = bs_hi - bs_lo > P.range_thr;
     }
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
+    for (int r = 0; r < NRT; r++) {
         const int idx = r * 32 + lane;
         pm[r] = ~0ULL; pc[r] = 0;
         if (r < NR && idx < CW) {
@@ -730,7 +731,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
     }
     u32 cl = 0;                                   // largest tie count of any partial
 #pragma unroll
-    for (int r = 0; r < 8; r++) cl = max(cl, pc[r]);
+    for (int r = 0; r < NRT; r++) cl = max(cl, pc[r]);
     // 64-bit min with two 32-bit redux ops
     const u32 hmin = __reduce_min_sync(FULL, (u32)(mn >> 32));
     const u32 cmax = __reduce_max_sync(FULL, cl);
@@ -740,10 +741,10 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
     // every partial holds at most one tie (one instance per warp, or no intra-warp ties):
     // the tied partials are ballot bits, the kk-th one is a bit position, no prefix scan
     const bool single = cmax <= 1;
-    u32 tb[8];
+    u32 tb[NRT];
     u32 lc = 0, T = 0;
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
+    for (int r = 0; r < NRT; r++) {
         pc[r] = pm[r] == gmin ? pc[r] : 0u;
         lc += pc[r];
         tb[r] = (single && r < NR) ? __ballot_sync(FULL, pc[r] > 0) : 0u;
@@ -810,7 +811,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         u32 pre = 0, kr = 0, bm = 0;
         int rb = -1;
 #pragma unroll
-        for (int r = 0; r < 8; r++) {
+        for (int r = 0; r < NRT; r++) {
             const u32 S = __popc(tb[r]);
             if (rb < 0 && kk < pre + S) { rb = r; kr = kk - pre; bm = tb[r]; }
             pre += S;
@@ -823,7 +824,7 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
         u32 pre = 0, kr = 0, c = 0;
         int rb = -1;
 #pragma unroll
-        for (int r = 0; r < 8; r++) {
+        for (int r = 0; r < NRT; r++) {
             if (r < NR) {
                 const u32 S = __reduce_add_sync(FULL, pc[r]);
                 if (rb < 0 && kk < pre + S) { rb = r; kr = kk - pre; c = pc[r]; }
@@ -844,6 +845,16 @@ __device__ __forceinline__ void decide_phase(const Params &P, const Part *part, 
     if (dg) { atomicAdd(P.ctr + 35, (u64)(dt1 - dt0)); atomicAdd(P.ctr + 36, (u64)(dt2 - dt1)); atomicAdd(P.ctr + 37, (u64)(dt3 - dt2)); }
 #endif
     if (lane == 0) dec = d;
+}
+
+// The per-launch partial count fixes the rounds: instantiate the decide for 1, 2 or 4 rounds
+// (api64: 16 x 4 partials = 2 rounds) instead of predicating 8.
+__device__ __forceinline__ void decide_phase(const Params &P, const Part *part, int CW, int W, int cta, i64 k, int par,
+                                             Dec &dec, u32 *modtab, u64 c0_lo, u64 c0_hi, u32 &ties, int lane,
+                                             bool filter, const Part *det_branch = nullptr, int det_code = 0) {
+    if (CW <= 32) decide_phase_n<1>(P, part, CW, W, cta, k, par, dec, modtab, c0_lo, c0_hi, ties, lane, filter, det_branch, det_code);
+    else if (CW <= 64) decide_phase_n<2>(P, part, CW, W, cta, k, par, dec, modtab, c0_lo, c0_hi, ties, lane, filter, det_branch, det_code);
+    else decide_phase_n<4>(P, part, CW, W, cta, k, par, dec, modtab, c0_lo, c0_hi, ties, lane, filter, det_branch, det_code);
 }
 
 __device__ __forceinline__ void bar_warps(int nthreads) {       // named barrier 1: the instance warps only
