@@ -817,7 +817,7 @@ __device__ __forceinline__ void decide_phase_n(const Params &P, const Part *part
             pre += S;
         }
         const int owner = rb * 32 + nth_set_bit_warp(bm, (int)kr, lane);
-        if (owner / W == cta) { d.owner_warp = owner % W; d.kk = 0; }
+        if ((unsigned)(owner - cta * W) < (unsigned)W) { d.owner_warp = owner - cta * W; d.kk = 0; }   // (no division)
         d.oflat = owner; d.okk = 0;
     } else if (!d.err && mine) {
         // the round holding the kk-th tie, then the lane inside it
@@ -836,7 +836,7 @@ __device__ __forceinline__ void decide_phase_n(const Params &P, const Part *part
         const int L = __ffs(ge) - 1;
         const u32 okk = __shfl_sync(FULL, kr - (incl - c), L);
         const int owner = rb * 32 + L;
-        if (owner / W == cta) { d.owner_warp = owner % W; d.kk = (int)okk; }
+        if ((unsigned)(owner - cta * W) < (unsigned)W) { d.owner_warp = owner - cta * W; d.kk = (int)okk; }   // (no division)
         d.oflat = owner; d.okk = (int)okk;
     }
     d.pad = det_branch ? det_code : (bs_branch ? 1 : 0);   // the owner picks its tie among the chosen branch
