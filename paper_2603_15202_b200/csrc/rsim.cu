@@ -18,6 +18,9 @@
 #ifndef RSIM_SLOT_MULT
 #define RSIM_SLOT_MULT 8   // table slots >= 8/3 x expected keys at least: load <= 3/8
 #endif
+#ifndef RSIM_CENTRAL
+#define RSIM_CENTRAL 1
+#endif
 #ifndef RSIM_TABLE_BUDGET
 #define RSIM_TABLE_BUDGET (256ull << 20)   // all N tables: keep chat1024's inside L2-friendly sizes
 #endif
@@ -60,6 +63,7 @@ struct rsim {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int C = 1, W = 1, ipw = 1, per_cta = 1;
     size_t smem_bytes = 0;
+    bool central = false;           // replay_kernel's central mode: one extra decider CTA
     bool no_rsm = getenv("RSIM_NO_SMEM_RUNNING") != nullptr;   // A/B switch: running lists stay in HBM
     int qlog2 = 0, slog2 = 0;
     i64 max_occ = 0;
@@ -157,6 +161,7 @@ static Params make_params(rsim_t *h) {
     P.first_sched = h->first_sched.p; P.first_token = h->first_token.p; P.finish = h->finish.p;
     P.route_bs = h->route_bs.p; P.dec_ns = h->dec_ns.p;
     P.N = h->N; P.C = h->C; P.W = h->W; P.ipw = h->ipw; P.per_cta = h->per_cta;
+    P.central = h->central ? 1 : 0;
     P.bs = h->cfg.block_size; P.policy = h->cfg.policy; P.kv_ind = h->cfg.kv_indicator;
     P.kvw = h->cfg.kv_weight; P.bsn = h->cfg.bs_norm_cap; P.range_thr = h->cfg.range_threshold;
     P.bal_ind = h->cfg.balance_indicator; P.debug = h->cfg.debug_checks;
@@ -340,15 +345,28 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
         h->N = base + (c.rank < extra ? 1 : 0);
     }
     const int N = h->N;
-    int C = c.ctas;
-    if (C <= 0) C = std::min(16, N);       // measured: spreading instances over SMs wins (profiles/)
-    C = std::max(1, std::min(16, std::min(C, N)));
-    int per_cta = (N + C - 1) / C;
-    // default: the lean kernel (<= 7 instance warps, 255 registers) unless a warp would own > 32 instances
-    int W = c.warps_per_cta > 0 ? c.warps_per_cta : std::min(RSIM_LEAN_WARPS, per_cta);
-    if (c.warps_per_cta <= 0 && (per_cta + W - 1) / W > 32) W = std::min(RSIM_MAX_WARPS, per_cta);
-    W = std::max(1, std::min(RSIM_MAX_WARPS, W));
-    int ipw = (per_cta + W - 1) / W;
+    // the extended kernel (launch_replay's choice); the plain one runs with a central decider CTA
+    // (replay_kernel: central mode) when the instance shard still fits 15 CTAs
+    const bool ext = c.policy == RSIM_POLICY_FILTER || (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0)) ||
+                     c.staleness_us > 0 || c.det_on || c.policy == RSIM_POLICY_SIMULATE;
+    int C = 0, per_cta = 0, W = 0, ipw = 0;
+    auto shape = [&](int cmax) {
+        C = c.ctas;
+        if (C <= 0) C = std::min(cmax, N);     // measured: spreading instances over SMs wins (profiles/)
+        C = std::max(1, std::min(cmax, std::min(C, N)));
+        per_cta = (N + C - 1) / C;
+        // default: the lean kernel (<= 7 instance warps, 255 registers) unless a warp would own > 32 instances
+        W = c.warps_per_cta > 0 ? c.warps_per_cta : std::min(RSIM_LEAN_WARPS, per_cta);
+        if (c.warps_per_cta <= 0 && (per_cta + W - 1) / W > 32) W = std::min(RSIM_MAX_WARPS, per_cta);
+        W = std::max(1, std::min(RSIM_MAX_WARPS, W));
+        ipw = (per_cta + W - 1) / W;
+    };
+    h->central = false;
+    if (!ext && RSIM_CENTRAL && !getenv("RSIM_NO_CENTRAL") && c.ctas <= 15) {
+        shape(15);
+        h->central = ipw <= 32;
+    }
+    if (!h->central) shape(16);
     if (ipw > 32) { delete h; return fail(nullptr, RSIM_E_INVALID, "too many instances per GPU (%d per warp > 32)", ipw); }
     if (C * W > 128) { delete h; return fail(nullptr, RSIM_E_INVALID, "cluster too large"); }   // decide_phase: <= 4 rounds of 32
     h->C = C; h->W = W; h->ipw = ipw; h->per_cta = per_cta;
@@ -543,7 +561,8 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
                     "use ctas=1", h->dT);
     cudaLaunchConfig_t lc;
     memset(&lc, 0, sizeof(lc));
-    lc.gridDim = dim3(h->C, 1, 1);
+    const int cs = h->C + (h->central ? 1 : 0);    // + the decider CTA
+    lc.gridDim = dim3(cs, 1, 1);
     lc.blockDim = dim3(32 * (h->W + 1), 1, 1);   // + the control warp
     lc.dynamicSmemBytes = h->smem_bytes + (P.dsm ? (size_t)h->dT * (sizeof(DTrack) + sizeof(u64)) : 0);
     {   // small shards keep their running lists in shared memory for the launch
@@ -554,7 +573,7 @@ static rsim_status launch_replay(rsim_t *h, i64 k0, i64 k1, i64 until, int mode,
     lc.stream = h->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = h->C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
     if (sync) CK(h, cudaEventRecord(h->ev0, h->stream));

@@ -142,6 +142,9 @@ struct Params {
     // small shards: this CTA's running lists live in shared memory during a launch (byte offset of
     // the region in dynamic shared memory; 0 = global rbuf)
     int rsm_off;
+    // one extra CTA (rank C of the cluster) decides every decision alone and broadcasts it
+    // (replay_kernel, non-extended kernel): the instance CTAs' control warps only stage requests
+    int central;
     // route() API: instances (global-id bitmap) already holding the routed request id -- a decision
     // for one of them raises DuplicateRequestError after the tie-break (engine.py:266-267); null = none
     const u32 *dupmask;

@@ -884,7 +884,15 @@ template <int MAXW, bool FILTER>      // FILTER: the two-branch partials of rout
 __global__ void __launch_bounds__(32 * (MAXW + 1), 1)
 replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int mode, int target) {
     const int C = P.C, W = P.W, ipw = P.ipw, CW = P.C * P.W;
-    const int cta = (C > 1) ? (int)cluster_ctarank() : 0;
+    // central mode: CTA C of the cluster is the decider (its control warp alone waits for the
+    // partials, decides and st.async-broadcasts the decision to every instance CTA's release
+    // mbarrier). Decide latency is sensitive to what else issues on its SM (measured: 4 warps
+    // merely reading the landed partials next to it cost +4 % per decision), so it gets an SM of
+    // its own, and each instance warp publishes one partial instead of C.
+    const bool central = !FILTER && P.central != 0;
+    const int CS = C + (central ? 1 : 0);                  // cluster size
+    const int cta = (CS > 1) ? (int)cluster_ctarank() : 0;
+    const bool decider = central && cta == C;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool control = warp == W;
     const int base = cta * P.per_cta;
@@ -963,7 +971,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
         }
     }
     __syncthreads();
-    if (C > 1) cluster_sync_all();
+    if (CS > 1) cluster_sync_all();
 
     // per-phase SM-cycle accounting of CTA 0 (ctr[8..15]): warp 0: staging wait, drain,
     // probe + score, publish + advance + probe-ahead, -, -, decision wait, commit;
@@ -981,6 +989,48 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
 #endif
     if (mode == MODE_DRAIN) {
         if (!control) drain_phase<FILTER>(P, st, base, l0, nmine, until, 0u, lane, WB);
+    } else if (central && decider) {
+        if (control) {      // ---- the decider: partials of k -> decision -> every instance CTA
+            u32 mb_phase = 0u;
+            for (i64 k = k0; k < k1; k++) {
+                const int par = (int)(k & 1);
+                if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * 16));
+                while (!mbar_try_wait(&mb[par], (mb_phase >> par) & 1u)) { }
+                mb_phase ^= 1u << par;
+                decide_phase(P, part, CW, W, 0, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, false);
+                __syncwarp();
+                const Dec d = dec[par];   // (owner_warp, kk, err, pad) <- (flat owner, its tie index, err, branch)
+                const u64 a = ((u64)(u32)d.okk << 32) | (u32)d.oflat;
+                const u64 b = ((u64)(u32)d.pad << 32) | (u32)d.err;
+                if (lane < C) st_async_16(&dec[par], &dmb[par], (u32)lane, a, b);
+                if (d.err) break;
+            }
+        }
+    } else if (central && control) {
+        // ---- instance CTA's control warp: stage ahead; arm each decision's release mbarrier for
+        //      the decider's 16-byte broadcast
+        u32 dph_c = 0u;
+        i64 staged = k0;
+        auto stage_upto = [&](i64 lim) {
+            lim = min(lim, k1);
+            if (staged >= lim) return;
+            while (staged < lim) { stage_request(P, rq[staged % RSIM_SLOTS], staged, mode, until, lane); staged++; }
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) ctl[0] = staged;
+            __syncwarp();
+        };
+        stage_upto(k0 + RSIM_SLOTS - 1);
+        for (i64 k = k0; k < k1; k++) {
+            const int par = (int)(k & 1);
+            if (lane == 0) mbar_arrive_expect(&dmb[par], 16u);
+            while (!mbar_try_wait(&dmb[par], (dph_c >> par) & 1u)) { }
+            dph_c ^= 1u << par;
+            if (dec[par].err) break;
+            // the decider had every warp's partial of k, so every warp committed k-1 and ran the
+            // touch + pin of k-2: slots of decisions < k-1 are free
+            stage_upto(k - 2 + RSIM_SLOTS);
+        }
     } else if (control) {
         // ---- control warp: stage ahead, then per decision wait for the partials and decide
         u32 mb_phase = 0u;                                  // bit p: phase of mbarrier mb[p]
@@ -1099,7 +1149,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             // (which reads its request's staged keys): slots of decisions < k-1 are free
             stage_upto(k - 2 + RSIM_SLOTS);
         }
-    } else {
+    } else if (!decider) {
         i64 staged_seen = k0;
         u32 dph = 0u;                                       // bit p: phase of decision-release mbarrier dmb[p]
         u32 d0ph = 0u;                                      // bit p: phase of round-0 mbarrier mb0[p]
@@ -1235,7 +1285,8 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             {   // publish this warp's partial(s) to every CTA of the cluster
                 const u64 w1 = ((u64)(u32)WB.werr << 32) | (u32)__popc(tmask);
                 Part *dst = part + par * 2 * CW + cta * W + warp;
-                if (lane < C) st_async_16(dst, &mb[par], (u32)lane, wmin, w1);
+                if (central) { if (lane == 0) st_async_16(dst, &mb[par], (u32)C, wmin, w1); }   // the decider
+                else if (lane < C) st_async_16(dst, &mb[par], (u32)lane, wmin, w1);
                 if (FILTER && P.policy == 4) {           // second partial: (min bs, ties | max bs << 32)
                     const Inst &sv = st[l0 + lane];
                     const u32 bsmax = __reduce_max_sync(FULL, lane < nmine ? (u32)(stale ? hhc[l0 + lane].r + hhc[l0 + lane].q : sv.v_r + sv.v_q) : 0u);
@@ -1315,7 +1366,11 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 reinterpret_cast<u64 *>(P.crit + (size_t)P.crit_cap * CW * 8)[(size_t)(k - k0) * (CW + 4) + CW + 2] = globaltimer();
 #endif
             DIAG(t_rel = clock64());
-            const Dec d = dec[par];
+            Dec d = dec[par];
+            if (central) {                                  // the broadcast names the owner by flat warp index
+                const int ow = d.owner_warp - cta * W;
+                d.owner_warp = (unsigned)ow < (unsigned)W ? ow : -1;
+            }
             if (d.err) {
                 if (lane == 0 && WB.werr == 0) WB.werr = d.err;
                 break;
@@ -1378,12 +1433,12 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             if (WB.c_steps) atomicAdd(P.ctr + 1, WB.c_steps);
         }
     }
-    if (cta == 0 && control && lane == 0 && mode != MODE_DRAIN) {
+    if ((central ? decider : cta == 0) && control && lane == 0 && mode != MODE_DRAIN) {
         const u64 lo = c0_lo + ties;
         P.tie[0] = lo;
         P.tie[1] = c0_hi + (lo < c0_lo);
     }
-    if (C > 1) cluster_sync_all();
+    if (CS > 1) cluster_sync_all();
 }
 
 // ---------------------------------------------------------------- probe batch
