@@ -160,13 +160,23 @@ rsim_status rsim_route_one(rsim_t *h, int64_t r, int64_t now_us, int32_t *chosen
 rsim_status rsim_route_one_excl(rsim_t *h, int64_t r, int64_t now_us, const int32_t *holders, int32_t n_holders,
                                 int32_t *chosen, int64_t *hit_tokens, double *scores);
 /* ClusterSim.route(record, now_us) of a request that is not loaded yet (cluster.py:130-154):
+ * scores (N, may be NULL) are RoutingDecision.scores, NaN for a candidate the detector excluded;
+ * branch (may be NULL) receives the detector verdict applied (0 none, 2 holders excluded, 3 forced
+ * least_bs, 4 excluded + route_filter's batch-size branch). Otherwise as follows:
  * appends it to the loaded trace (as rsim_load_trace of one request would) and decides it, with
  * the holders semantics of rsim_route_one_excl -- one fused call (the request goes in and the
  * decision comes out through mapped pinned memory, three launches, one stream synchronisation). */
 rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, int64_t output_tokens,
                                uint64_t request_id, const uint64_t *blocks, int64_t n_blocks,
                                const int32_t *holders, int32_t n_holders, int32_t *chosen, int64_t *hit_tokens,
-                               double *scores);
+                               double *scores, int32_t *branch);
+/* route() with the hotspot detector (cluster.py:133-139: verdict before choose, observe after the
+ * enqueue): the class of the request the next rsim_route_request appends -- its track, numbered
+ * densely by first arrival (track == the current track count opens a new one, whose exemplar is
+ * that request's first exemplar_len chain keys; detector.py:303-307) and class key -- and the
+ * DetectorRows to keep room for (window rolls so far + 1, times top_k). */
+rsim_status rsim_detector_next(rsim_t *h, int32_t track, int32_t exemplar_len, uint64_t class_key,
+                               int64_t rows_capacity);
 /* InstanceSim.queue / .running (engine.py:212-213) of a local instance: 8 int64 per slot -- the FIFO
  * queue in order, then the running list: request index, kind (0 queued / 1 running), pending,
  * generated, hit blocks, input tokens, output tokens, flags (bit0: prefill scheduled). out may be

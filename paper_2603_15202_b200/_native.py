@@ -135,7 +135,8 @@ def lib():
         "rsim_route_one_excl": ([P, I64, I64, P, I32, P, P, P], C.c_int),
         "rsim_read_slots": ([P, I32, P, I64, P, P], C.c_int),
         "rsim_unschedule": ([P], C.c_int),
-        "rsim_route_request": ([P, I64, I64, I64, C.c_uint64, P, I64, P, I32, P, P, P], C.c_int),
+        "rsim_route_request": ([P, I64, I64, I64, C.c_uint64, P, I64, P, I32, P, P, P, P], C.c_int),
+        "rsim_detector_next": ([P, I32, I32, C.c_uint64, I64], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -157,7 +158,7 @@ EXPORTED = ("rsim_create", "rsim_destroy", "rsim_last_error", "rsim_reset", "rsi
             "rsim_set_peer", "rsim_open_peer_ipc", "rsim_load_detector", "rsim_detector_finalize",
             "rsim_read_detector", "rsim_detector_debug", "rsim_config_size", "rsim_check_invariants",
             "rsim_debug_corrupt", "rsim_route_one_excl", "rsim_read_slots", "rsim_unschedule",
-            "rsim_route_request")
+            "rsim_route_request", "rsim_detector_next")
 
 
 def _p(a):
@@ -283,15 +284,26 @@ class Handle:
         self._ck(self._L.rsim_route_request(self._h, now_us, input_tokens, output_tokens,
                                             request_id & 0xFFFFFFFFFFFFFFFF, _p(b) if b.size else None, b.size,
                                             _p(hd), 0 if hd is None else int(hd.size), self._rr_ch_p, self._rr_ht_p,
-                                            _p(sc)))
+                                            _p(sc), self._rr_br_p))
         return int(out[0][0]), int(out[1][0]), sc
+
+    @property
+    def last_branch(self) -> int:
+        """The detector verdict the last route_request applied (0 none, 2 holders excluded,
+        3 forced least_bs, 4 excluded + route_filter's batch-size branch)."""
+        return int(self._rr_out[2][0])
+
+    def detector_next(self, track: int, exemplar_len: int, class_key: int, rows_capacity: int):
+        """The class of the request the next route_request appends (route() with a detector)."""
+        self._ck(self._L.rsim_detector_next(self._h, track, exemplar_len, class_key & 0xFFFFFFFFFFFFFFFF,
+                                            rows_capacity))
 
     @property
     def _rr_out(self):
         o = getattr(self, "_rr", None)
         if o is None:
-            o = self._rr = (np.zeros(1, np.int32), np.zeros(1, np.int64))
-            self._rr_ch_p, self._rr_ht_p = _p(o[0]), _p(o[1])
+            o = self._rr = (np.zeros(1, np.int32), np.zeros(1, np.int64), np.zeros(1, np.int32))
+            self._rr_ch_p, self._rr_ht_p, self._rr_br_p = _p(o[0]), _p(o[1]), _p(o[2])
         return o
 
     def slots(self, instance: int) -> np.ndarray:

@@ -28,7 +28,7 @@ from . import _native
 from .config import ClusterConfig, DuplicateRequestError
 from .hashing import MASK64, stable_key
 from .report import DetectorRow, RoutingDecision, RunReport
-from .trace import PackedTrace, TraceRecord, validate_against_block_size
+from .trace import PackedTrace, TraceRecord, class_key, validate_against_block_size
 
 _POLICY = {"multiplicative": 0, "vllm": 1, "least_bs": 2, "linear": 3, "filter": 4, "simulate": 5}
 INT64_MAX = (1 << 63) - 1
@@ -397,6 +397,7 @@ class ClusterSim:
         self._ops: list = []                  # state-changing calls, replayed onto a regrown handle
         self._stateful = False                # any logged call other than a trace load
         self._log_read = None                 # the step log read by the last run op
+        self._det_tracks: dict[int, int] = {}  # route() with the detector: class key -> track
         self._parts: list[PackedTrace] = []   # loaded requests, in load order
         self._arrival: list[np.ndarray] = []  # their arrival (route / enqueue time) in us
         self._reported: list[np.ndarray] = []  # which of them the Collector reports (route / trace)
@@ -494,9 +495,12 @@ class ClusterSim:
             _, idx, now, holders = op
             return h.route_one(idx, now, holders=holders)
         if kind == "route_request":       # load + decide in one device call (rsim_route_request)
-            _, rec, now, holders = op
-            return h.route_request(now, rec.input_tokens, rec.output_tokens, rec.request_id, rec.prefix_blocks,
-                                   holders=holders)
+            _, rec, now, holders, det = op
+            if det is not None:
+                h.detector_next(*det)
+            res = h.route_request(now, rec.input_tokens, rec.output_tokens, rec.request_id, rec.prefix_blocks,
+                                  holders=holders)
+            return res + (h.last_branch,)
         if kind == "enqueue":
             _, inst, idx, now = op
             return h.enqueue(inst, idx, now)
@@ -604,24 +608,45 @@ class ClusterSim:
         """Snapshot, score, enqueue on the winner. A request id already present on the chosen
         instance raises DuplicateRequestError after the decision (the TieBreaker counter moved),
         as InstanceSim.enqueue does (engine.py:266-267)."""
-        if self.config.detector is not None:
-            from .config import UnsupportedConfigError
-            raise UnsupportedConfigError("route() with the hotspot detector: replay a trace with run_trace")
         now_us = int(now_us)
         self._advance_clock(now_us, "route()")
         holders = tuple(sorted(self._holders(record.request_id))) if record.request_id in self._by_rid else ()
         idx = self._n
+        det = self._det_class(record, now_us) if self.config.detector is not None else None
         try:
-            chosen, _ht, scores = self._do(("route_request", record, now_us, holders),
-                                           expected=(DuplicateRequestError,))
+            chosen, _ht, scores, branch = self._do(("route_request", record, now_us, holders, det),
+                                                   expected=(DuplicateRequestError,))
         except DuplicateRequestError:
-            self._routed(record, now_us, idx)
+            self._routed(record, now_us, idx, observed=False)
             raise
         self._routed(record, now_us, idx)
+        kind = self.config.policy.kind
+        if branch == 3:                           # verdict force_least_bs (policies.py:228-229)
+            kind = "least_bs"
+        if branch in (2, 4):                      # holders excluded: scores over the kept candidates only
+            excl = np.isnan(scores)
+            return RoutingDecision(chosen=chosen, scores={i: s for i, s in enumerate(scores.tolist()) if not excl[i]},
+                                   filtered=frozenset(np.flatnonzero(excl).tolist()), kind=kind, time_us=now_us)
         return RoutingDecision(chosen=chosen, scores=dict(enumerate(scores.tolist())),
-                               filtered=frozenset(), kind=self.config.policy.kind, time_us=now_us)
+                               filtered=frozenset(), kind=kind, time_us=now_us)
 
-    def _routed(self, record: TraceRecord, now_us: int, idx: int) -> None:
+    def _det_class(self, record: TraceRecord, now_us: int):
+        """route() with the detector: the request's track (dense by first arrival, the order
+        Detector.observe creates tracks, detector.py:303-307), exemplar length and class key
+        (detector.py:41-45, 296-297), and the rows to keep room for (one per top class per window
+        roll, detector.py:350-372)."""
+        det = self.config.detector
+        ck = class_key(record.prefix_blocks, det.class_key_blocks)
+        t = self._det_tracks.get(ck)
+        if t is None:                 # (registered when the call succeeds: a failed call creates none)
+            t = len(self._det_tracks)
+        rows = (int(now_us / 1e6 / det.window_s) + 3) * det.top_k_classes
+        return (t, min(det.class_key_blocks, len(record.prefix_blocks)), ck, rows)
+
+    def _routed(self, record: TraceRecord, now_us: int, idx: int, observed: bool = True) -> None:
+        if self.config.detector is not None and observed:
+            self._det_tracks.setdefault(class_key(record.prefix_blocks, self.config.detector.class_key_blocks),
+                                        len(self._det_tracks))
         self._pending.append((record, now_us))
         self._n += 1
         self._by_rid.setdefault(record.request_id, []).append(idx)

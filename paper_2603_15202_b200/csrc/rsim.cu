@@ -108,7 +108,10 @@ struct rsim {
     DevArr<u64> dtkey;
     DevArr<DTrack> dtr;
     i64 *dtot = nullptr, *dglob = nullptr;
-    int dT = 0, dbclog2 = 0;
+    int dT = 0, dTs = 0, dbclog2 = 0;   // tracks, bucket-ring track stride, window bucket log2
+    int det_next_track = -1, det_next_len = 0;   // rsim_detector_next: the next routed request's class
+    u64 det_next_key = 0;
+    i64 det_next_rows = 0;
     i64 drows_cap = 0;
     bool det_loaded = false;
     DevArr<i64> ddbg;
@@ -188,7 +191,7 @@ static Params make_params(rsim_t *h) {
     P.dbk = h->dbk.p; P.dtot = h->dtot; P.dglob = h->dglob; P.drows = h->drows.p; P.drows_cap = h->drows_cap;
     P.dwin = h->cfg.det_window_s; P.dmult = h->cfg.det_consecutive_multiplier;
     P.dwin_i = (i64)h->cfg.det_window_s; P.dcool = (i64)(h->cfg.det_window_s * 1e6);
-    P.dT = h->dT; P.dtopk = h->cfg.det_top_k_classes; P.dforce = h->cfg.det_mitigation == 1;
+    P.dT = h->dT; P.dTs = h->dTs; P.dtopk = h->cfg.det_top_k_classes; P.dforce = h->cfg.det_mitigation == 1;
     P.dmean = h->cfg.det_compare_mean_non_holder; P.dbclog2 = h->dbclog2;
     P.ddbg = h->ddbg.p;
     P.dsm = (P.dtid != nullptr && h->dT <= RSIM_DET_SMEM_T &&
@@ -429,7 +432,9 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaMalloc(&h->errbuf, 4 * sizeof(int)));
     CK(nullptr, cudaMalloc(&h->flag, sizeof(int)));
     CK(nullptr, cudaMalloc(&h->log_n, sizeof(u64)));
-    CK(nullptr, cudaMalloc(&h->scores, 2 * N * sizeof(double)));   // [N..2N): filter's second branch
+    // [N..2N): filter's second branch; with the detector, for route(): [2N..3N) batch sizes (least_bs),
+    // [3N..4N) holders of the request's class, [4N..5N) kept-set scores, [5N] the verdict's branch
+    CK(nullptr, cudaMalloc(&h->scores, (5 * (size_t)N + 1) * sizeof(double)));
     CK(nullptr, cudaMalloc(&h->scratch_res, 4 * sizeof(i64)));
     CK(nullptr, cudaMalloc(&h->ctr, 48 * sizeof(u64)));   // [16..47]: diagnostics builds
     CK(nullptr, cudaMalloc(&h->mbox, 2 * 8 * 4 * sizeof(u64)));
@@ -697,6 +702,64 @@ rsim_status rsim_route_one_excl(rsim_t *h, int64_t r, int64_t now_us, const int3
     return RSIM_OK;
 }
 
+// Detector state for route() API calls, grown in place: per-request track ids for R requests,
+// T tracks (new ones zeroed; the per-CTA bucket rings re-laid out when the track stride grows,
+// doubling) and room for `rows` DetectorRows. The first call initialises (Detector.__init__).
+static rsim_status det_ensure(rsim_t *h, int T, i64 R, i64 rows) {
+    cudaStream_t s = h->stream;
+    int bl = 0;
+    while ((1LL << bl) < (i64)h->cfg.det_window_s + 2) bl++;
+    const bool first = !h->det_loaded;
+    const int T0 = first ? 0 : h->dT;
+    if (!first && bl != h->dbclog2) return fail(h, RSIM_E_DETECTOR, "detector window changed");
+    CK(h, h->dtid.reserve(R, first ? 0 : h->R, s));
+    if (T > T0) {
+        CK(h, h->dtw.reserve(T, T0, s)); CK(h, h->dtex.reserve(T, T0, s)); CK(h, h->dtkey.reserve(T, T0, s));
+        CK(h, h->dtr.reserve(T, T0, s));
+        CK(h, cudaMemsetAsync(h->dtr.p + T0, 0, (size_t)(T - T0) * sizeof(DTrack), s));
+        if (T > h->dTs) {                                   // bucket rings [C][stride][3 << bl]
+            const int ns = std::max(T, 2 * h->dTs + 8);
+            const size_t ring = (size_t)3 << bl;
+            i64 *nb = nullptr;
+            CK(h, cudaMalloc(&nb, (size_t)ns * ring * h->C * sizeof(i64)));
+            if (h->dTs > 0 && h->dbk.p)
+                CK(h, cudaMemcpy2DAsync(nb, (size_t)ns * ring * sizeof(i64), h->dbk.p, (size_t)h->dTs * ring * sizeof(i64),
+                                        (size_t)h->dTs * ring * sizeof(i64), h->C, cudaMemcpyDeviceToDevice, s));
+            CK(h, cudaStreamSynchronize(s));
+            h->dbk.free_();
+            h->dbk.p = nb; h->dbk.cap = (size_t)ns * ring * h->C;
+            h->dTs = ns;
+        }
+    }
+    if (rows > h->drows_cap) {
+        CK(h, h->drows.reserve((size_t)rows * 7, (size_t)h->drows_cap * 7, s));
+        h->drows_cap = rows;
+    }
+    if (!h->dtot || bl > h->dbclog2) {
+        if (h->dtot) cudaFree(h->dtot);
+        CK(h, cudaMalloc(&h->dtot, ((size_t)2 << bl) * h->C * sizeof(i64)));
+    }
+    if (!h->dglob) CK(h, cudaMalloc(&h->dglob, DG_N * sizeof(i64)));
+    h->dT = std::max(T, T0); h->dbclog2 = bl;
+    if (first) {
+        h->det_loaded = true;
+        return det_reset(h, s);
+    }
+    return RSIM_OK;
+}
+
+rsim_status rsim_detector_next(rsim_t *h, int32_t track, int32_t exemplar_len, uint64_t class_key,
+                               int64_t rows_capacity) {
+    if (!h) return RSIM_E_INVALID;
+    if (!h->cfg.det_on) return fail(h, RSIM_E_INVALID, "handle was created without a detector");
+    const int T0 = h->det_loaded ? h->dT : 0;
+    if (track < 0 || track > T0) return fail(h, RSIM_E_INVALID, "track ids must be numbered by first arrival");
+    if (track == T0 && exemplar_len < 1) return fail(h, RSIM_E_INVALID, "bad exemplar length");
+    h->det_next_track = track; h->det_next_len = exemplar_len; h->det_next_key = class_key;
+    h->det_next_rows = std::max<i64>(rows_capacity, 16);
+    return RSIM_OK;
+}
+
 // ClusterSim.route(record, now_us) of a request that is not loaded yet (cluster.py:130-154): the
 // request is appended to the device trace by route_ingest_kernel straight from mapped pinned
 // memory, decided by a one-decision replay launch, and the decision + scores + device error word
@@ -704,9 +767,10 @@ rsim_status rsim_route_one_excl(rsim_t *h, int64_t r, int64_t now_us, const int3
 rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, int64_t output_tokens,
                                uint64_t request_id, const uint64_t *blocks, int64_t n_blocks,
                                const int32_t *holders, int32_t n_holders, int32_t *chosen, int64_t *hit_tokens,
-                               double *scores) {
+                               double *scores, int32_t *branch) {
     if (!h) return RSIM_E_INVALID;
-    if (h->cfg.det_on) return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls with the hotspot detector: use a trace replay");
+    if (h->cfg.det_on && h->det_next_track < 0)
+        return fail(h, RSIM_E_INVALID, "route() with the hotspot detector: rsim_detector_next names the request's class first");
     if (h->cfg.world > 1) return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls are single-rank only");
     if (n_blocks < 1 || !blocks) return fail(h, RSIM_E_TRACE, "request has no blocks");
     if (input_tokens < 1 || output_tokens < 1) return fail(h, RSIM_E_TRACE, "request: in/out must be >= 1");
@@ -741,9 +805,19 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
     DevArr<i64> *outs[] = {&h->hit_tokens, &h->first_sched, &h->first_token, &h->finish, &h->route_bs, &h->dec_ns};
     for (auto *a : outs) CK(h, a->reserve(R1, R0, st));
     if (words) CK(h, h->dupmask.reserve(words, 0, st));
+    int trk = -1, newt = -1;
+    if (h->cfg.det_on) {                      // the request's class (rsim_detector_next)
+        trk = h->det_next_track;
+        const int T0 = h->det_loaded ? h->dT : 0;
+        newt = trk == T0 ? trk : -1;
+        rsim_status ds = det_ensure(h, std::max(T0, trk + 1), R1, h->det_next_rows);
+        if (ds != RSIM_OK) return ds;
+        h->det_next_track = -1;
+    }
     i64 *q = h->rq_h;
     q[RQ_ARRIVAL] = now_us; q[RQ_IN] = input_tokens; q[RQ_OUT] = output_tokens; q[RQ_RID] = (i64)request_id;
     q[RQ_B] = n_blocks; q[RQ_R0] = R0; q[RQ_NBLK0] = h->nblk; q[RQ_NOUT0] = h->nout; q[RQ_NO] = no; q[RQ_NDUP] = words;
+    q[RQ_TRACK] = trk; q[RQ_NEWT] = newt; q[RQ_EXLEN] = h->det_next_len; q[RQ_CKEY] = (i64)h->det_next_key;
     for (i64 w = 0; w < words; w++) q[RQ_HDR + w] = 0;
     for (int i = 0; i < n_holders; i++) {
         if (holders[i] < 0 || holders[i] >= N) return fail(h, RSIM_E_INVALID, "holder out of range");
@@ -754,7 +828,8 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
     route_ingest_kernel<<<1, 32, 0, st>>>(h->rq_dev.p, h->arrival.p, h->in_tok.p, h->out_tok.p, h->rid.p, h->blk_off.p,
                                           h->ooff.p, h->blocks.p, h->ckeys.p, h->okeys.p, h->chosen.p, h->hit_blocks.p,
                                           h->hit_tokens.p, h->first_sched.p, h->first_token.p, h->finish.p,
-                                          h->route_bs.p, h->dec_ns.p, h->dupmask.p, h->flag);
+                                          h->route_bs.p, h->dec_ns.p, h->dupmask.p, h->flag,
+                                          h->cfg.det_on ? h->dtid.p : nullptr, h->dtw.p, h->dtex.p, h->dtkey.p);
     h->launches++;
     CK(h, cudaGetLastError());
     if (R0 > 0 && now_us < h->last_arrival) h->order_breaks.push_back(R0);
@@ -765,7 +840,7 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
     h->cur_dupmask = nullptr;
     if (rs != RSIM_OK) { cudaStreamSynchronize(st); return rs; }
     const bool filt = h->cfg.policy == RSIM_POLICY_FILTER;
-    const int nsc = (filt ? 2 : 1) * h->N;
+    const int nsc = h->cfg.det_on ? 5 * h->N + 1 : (filt ? 2 : 1) * h->N;
     route_out_kernel<<<1, 128, 0, st>>>(h->chosen.p, h->hit_tokens.p, R0, h->scores, nsc, h->errbuf, h->flag, h->ro_d);
     h->launches++;
     CK(h, cudaGetLastError());
@@ -776,14 +851,25 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
     if (o[RO_FLAG]) return fail(h, RSIM_E_TRACE, "a chain key equals the table sentinel 0 (probability 2^-64 per key)");
     if (chosen) *chosen = (int32_t)o[RO_CHOSEN];
     if (hit_tokens) *hit_tokens = o[RO_HIT];
+    const double *sc = reinterpret_cast<const double *>(o + RO_HDR);
+    // the detector's verdict (policies.py:222-236): 0 none (or fail open), 2 holders excluded,
+    // 3 forced least_bs, 4 holders excluded and route_filter's batch-size branch over the rest
+    const int code = h->cfg.det_on ? (int)sc[5 * N] : 0;
+    if (branch) *branch = code;
     if (scores) {
-        const double *sc = reinterpret_cast<const double *>(o + RO_HDR);
         const double *pick = sc;
-        if (filt) {       // the branch route_filter took (policies.py:180-183)
-            const auto mm = std::minmax_element(sc + h->N, sc + 2 * h->N);
-            if ((i64)*mm.second - (i64)*mm.first > h->cfg.range_threshold) pick = sc + h->N;
+        if (code == 3) {
+            pick = sc + 2 * N;                                  // least_bs: float(bs)
+        } else if (code == 2 || code == 4) {                    // the kept candidates only (NaN: excluded)
+            const double *base = code == 4 ? sc + N
+                               : (h->cfg.policy == RSIM_POLICY_LINEAR && !(h->cfg.bs_norm_cap > 0)) ? sc + 4 * N : sc;
+            for (int i = 0; i < N; i++) scores[i] = sc[3 * N + i] != 0.0 ? std::nan("") : base[i];
+            return RSIM_OK;
+        } else if (filt) {       // the branch route_filter took (policies.py:180-183)
+            const auto mm = std::minmax_element(sc + N, sc + 2 * N);
+            if ((i64)*mm.second - (i64)*mm.first > h->cfg.range_threshold) pick = sc + N;
         }
-        memcpy(scores, pick, h->N * sizeof(double));
+        memcpy(scores, pick, N * sizeof(double));
     }
     return RSIM_OK;
 }
@@ -836,7 +922,6 @@ rsim_status rsim_unschedule(rsim_t *h) {
 
 rsim_status rsim_enqueue(rsim_t *h, int32_t instance, int64_t r, int64_t now_us, int64_t *hit_tokens) {
     if (!h) return RSIM_E_INVALID;
-    if (h->cfg.det_on) return fail(h, RSIM_E_UNSUPPORTED, "route/enqueue API calls with the hotspot detector: use a trace replay");
     if (r < 0 || r >= h->R) return fail(h, RSIM_E_INVALID, "request index out of range");
     if (instance < 0 || instance >= h->N) return fail(h, RSIM_E_INVALID, "instance out of range");
     CK(h, cudaSetDevice(h->cfg.device));
@@ -1231,7 +1316,7 @@ rsim_status rsim_load_detector(rsim_t *h, int64_t n, const int32_t *track_of_req
     CK(h, cudaMemcpyAsync(h->dtw.p, exemplar_len, T * sizeof(int), cudaMemcpyHostToDevice, s));
     CK(h, cudaMemcpyAsync(h->dtex.p, exemplar_offset, T * sizeof(i64), cudaMemcpyHostToDevice, s));
     CK(h, cudaMemcpyAsync(h->dtkey.p, class_key, T * sizeof(u64), cudaMemcpyHostToDevice, s));
-    h->dT = T; h->dbclog2 = bl; h->drows_cap = rc;
+    h->dT = T; h->dTs = T; h->dbclog2 = bl; h->drows_cap = rc;
     if (getenv("RSIM_DET_DEBUG")) {
         CK(h, h->ddbg.reserve((size_t)n * (8 + h->N), 0, s));
         CK(h, cudaMemsetAsync(h->ddbg.p, 0xff, (size_t)n * (8 + h->N) * sizeof(i64), s));

@@ -7,7 +7,8 @@
 #include "rsim_device.cuh"
 
 // request block layout (i64 words), written by the host before the launch
-enum { RQ_ARRIVAL = 0, RQ_IN, RQ_OUT, RQ_RID, RQ_B, RQ_R0, RQ_NBLK0, RQ_NOUT0, RQ_NO, RQ_NDUP, RQ_HDR = 16 };
+enum { RQ_ARRIVAL = 0, RQ_IN, RQ_OUT, RQ_RID, RQ_B, RQ_R0, RQ_NBLK0, RQ_NOUT0, RQ_NO, RQ_NDUP,
+       RQ_TRACK, RQ_NEWT, RQ_EXLEN, RQ_CKEY, RQ_HDR = 16 };   // + the detector class (route() with a detector)
 // result block layout
 enum { RO_CHOSEN = 0, RO_HIT, RO_ERR0, RO_ERR1, RO_ERR2, RO_ERR3, RO_FLAG, RO_HDR = 8 };
 
@@ -18,7 +19,7 @@ __global__ void __launch_bounds__(32)
 route_ingest_kernel(const i64 *__restrict__ rq, i64 *arrival, i64 *in_tok, i64 *out_tok, u64 *rid, i64 *blk_off,
                     i64 *ooff, u64 *blocks, u64 *ckeys, u64 *okeys, int *chosen, int *hit_blocks, i64 *hit_tokens,
                     i64 *first_sched, i64 *first_token, i64 *finish, i64 *route_bs, i64 *dec_ns, u32 *dupmask,
-                    int *flag) {
+                    int *flag, int *dtid, int *dtw, i64 *dtex, u64 *dtkey) {
     const int lane = threadIdx.x;
     const i64 B = rq[RQ_B], R0 = rq[RQ_R0], nb0 = rq[RQ_NBLK0], no0 = rq[RQ_NOUT0], no = rq[RQ_NO];
     const i64 ndup = rq[RQ_NDUP];
@@ -31,6 +32,11 @@ route_ingest_kernel(const i64 *__restrict__ rq, i64 *arrival, i64 *in_tok, i64 *
         ooff[R0] = no0; ooff[R0 + 1] = no0 + no;
         chosen[R0] = -1; hit_blocks[R0] = 0;
         hit_tokens[R0] = first_sched[R0] = first_token[R0] = finish[R0] = route_bs[R0] = dec_ns[R0] = -1;
+        if (dtid != nullptr) {                 // the request's detector track; a new track's exemplar is
+            dtid[R0] = (int)rq[RQ_TRACK];      // this request's own leading chain keys
+            const i64 t = rq[RQ_NEWT];
+            if (t >= 0) { dtw[t] = (int)rq[RQ_EXLEN]; dtex[t] = nb0; dtkey[t] = (u64)rq[RQ_CKEY]; }
+        }
     }
     __syncwarp();
     if (lane == 0) {

@@ -134,6 +134,7 @@ struct Params {
     i64 *drows; i64 drows_cap;         // emitted DetectorRows, 7 words each
     double dwin, dmult; i64 dwin_i, dcool;
     int dT, dtopk, dforce, dmean, dbclog2;
+    int dTs;                           // track stride of the per-CTA bucket rings (>= dT)
     int dsm;                           // 1: the replay keeps tracks in shared memory
     i64 *ddbg;                         // diagnostics: 8 words per decision (rsim_detector_debug), null = off
     // simulate policy (policies.py:142-157, engine.py:419-460): the sim cost model and per-warp scratch

@@ -273,7 +273,7 @@ __device__ __noinline__ void stage_request(const Params &P, ReqStage &R, i64 k, 
     for (int q = 0; q < 4; q++)
         if (32 * q + lane < B) { R.keys[32 * q + lane] = kk[q]; R.home[32 * q + lane] = tab_home(kk[q], P.slog2); }
     if (lane == 0) { R.t = t; R.a = a; R.in = in; R.oa = oa; R.B = B; R.out = (int)out; }
-    if (P.dtid != nullptr && lane == 0) { R.dtid = P.dtid[k]; R.dw = P.dtw[R.dtid]; }
+    if (P.dtid != nullptr && mode != MODE_ENQUEUE && lane == 0) { R.dtid = P.dtid[k]; R.dw = P.dtw[R.dtid]; }
 }
 
 // ---- drain: advance instances [l0, l0+n) of this warp through steps starting before `until`
@@ -635,6 +635,11 @@ __device__ __forceinline__ u64 score_phase(const Params &P, Inst *st, int base, 
             const i64 bsz = (i64)vr + vq;
             WB.prod[lane] = (vp + nw) * (bsz > 1 ? bsz : 1);
             WB.bsv[lane] = (int)bsz;
+            if (mode == MODE_ROUTE && P.scores != nullptr) {   // route()'s RoutingDecision under a verdict
+                P.scores[2 * P.N + gi] = __ll2double_rn(bsz);
+                P.scores[3 * P.N + gi] = h >= R.dw ? 1.0 : 0.0;
+                P.scores[4 * P.N + gi] = sc;
+            }
         }
         bits = (u64)__double_as_longlong(sc);
         if (P.scores != nullptr) P.scores[gi] = sc;
@@ -910,16 +915,17 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
     WarpBuf *wbuf = (WarpBuf *)(modtab + RSIM_MODTAB);     // [W]
     WarpBuf &WB = wbuf[control ? 0 : warp];
     HistHead *hhc = (HistHead *)(wbuf + W);                // [per_cta] history heads (FILTER, staleness > 0)
-    const bool det = FILTER && P.dtid != nullptr;          // hotspot detector (single CTA)
+    // hotspot detector: trace replays and route() decisions (an enqueue() API call does not involve it)
+    const bool det = FILTER && P.dtid != nullptr && mode != MODE_ENQUEUE;
     DetCtl *dctl = (DetCtl *)(hhc + (P.stal > 0 ? P.per_cta : 0));
     Part *dpart = (Part *)(dctl + 1);                      // [2 parity][masked, least bs, products][C*W]
     unsigned char *ecnt = (unsigned char *)(dpart + 8 * CW);   // [2 parity][C*W][RSIM_DLMAX] listed holder counts
     const int BCd = 1 << P.dbclog2;
-    DetView DV{P.dtr, P.dtkey, P.dglob, P.dbk + (size_t)cta * P.dT * BCd * 3, P.dtot + (size_t)cta * BCd * 2, cta == 0};
+    DetView DV{P.dtr, P.dtkey, P.dglob, P.dbk + (size_t)cta * P.dTs * BCd * 3, P.dtot + (size_t)cta * BCd * 2, cta == 0};
     if (det && P.dsm) {                                    // tracks in shared memory (one copy per CTA)
         DV.tr = (DTrack *)(ecnt + 2 * CW * RSIM_DLMAX); DV.key = (const u64 *)(DV.tr + P.dT); DV.g = dctl->g;
     }
-    const bool det_run = det && mode == MODE_REPLAY && k0 < k1;
+    const bool det_run = det && (mode == MODE_REPLAY || mode == MODE_ROUTE) && k0 < k1;
 
     {   // load this CTA's instance shard
         const u64 *src = (const u64 *)(P.inst + base);
@@ -1095,6 +1101,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     if ((i64)bmx - lo > P.range_thr) code = 4;
                 }
                 det_code = code;
+                if (mode == MODE_ROUTE && P.scores != nullptr && cta == 0 && lane == 0) P.scores[5 * P.N] = (double)code;
                 decide_phase(P, part, CW, W, cta, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane,
                              FILTER && P.policy == 4,
                              code == 2 ? dp : code == 3 ? dp + CW : code == 4 ? dp + 3 * CW : nullptr, code);
@@ -1133,8 +1140,9 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                     g[6] = det_hb >= Rk.dw; g[7] = nl;
                 }
                 DIAG(const long long tdw1 = clock64());
-                det_observe(P, DV, *dctl, Rk.dtid, Rk.t, lane, ht, det_hb >= Rk.dw, det_pc, det_nh, det_pmin, det_psum,
-                            dctl->cnt);
+                if (det_pc >= 0)
+                    det_observe(P, DV, *dctl, Rk.dtid, Rk.t, lane, ht, det_hb >= Rk.dw, det_pc, det_nh, det_pmin, det_psum,
+                                dctl->cnt);
                 DIAG(const long long tdw2 = clock64());
                 if (k + 1 < k1) {
                     const ReqStage &Rn = rq[(k + 1) % RSIM_SLOTS];   // staged (slots up to k-2+RSIM_SLOTS)
@@ -1252,8 +1260,10 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 const bool cand = lane < nmine;
                 const bool held = cand && WB.hit[lane] >= R.dw;          // holders of class(k)
                 u64 kb = mybits;                          // the kept-set score (uncapped linear renormalises)
-                if (FILTER && P.policy == 3 && !(P.bsn > 0) && cand && !held)
+                if (FILTER && P.policy == 3 && !(P.bsn > 0) && cand && !held) {
                     kb = (u64)__double_as_longlong(score_of(P, WB.bsv[lane], 0, 0, 0, WB.hit[lane], R.in, bsn_kept));
+                    if (mode == MODE_ROUTE && P.scores != nullptr) P.scores[4 * P.N + base + l0 + lane] = __longlong_as_double((long long)kb);
+                }
                 const u64 bx = (cand && !held) ? kb : ~0ULL;
                 const u64 bl = cand ? (u64)__double_as_longlong((double)WB.bsv[lane]) : ~0ULL;
                 const u64 pn = (cand && !held) ? (u64)WB.prod[lane] : ~0ULL;
@@ -1379,12 +1389,15 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
             if (warp == d.owner_warp) {
                 const int s = nth_set_bit_warp(d.pad == 0 ? tmask : d.pad == 1 ? tmask_bs : WB.tm[d.pad], d.kk, lane);   // d.pad: the branch
                 const int h = WB.hit[s];
-                if (det && lane < C)     // (hit, product) of the chosen instance to every CTA's observe(k)
-                    st_async_16(&dctl->own[par][0], &dctl->mbd[par], (u32)lane, (u64)(u32)h, (u64)WB.prod[s]);
+                const int gch = P.gbase + base + l0 + s;
+                const bool dup = mode == MODE_ROUTE && P.dupmask != nullptr && ((P.dupmask[gch >> 5] >> (gch & 31)) & 1u);
+                // (hit, product) of the chosen instance to every CTA's observe(k); a duplicate request
+                // is refused by enqueue before observe runs (cluster.py:140-142): product -1
+                if (det && lane < C)
+                    st_async_16(&dctl->own[par][0], &dctl->mbd[par], (u32)lane, (u64)(u32)h, dup ? ~0ULL : (u64)WB.prod[s]);
                 int werr = 0;
                 flush_touch_pin(P, WB.fin, lane, &WB.werr);      // (normally already run after the publish)
-                const int gch = P.gbase + base + l0 + s;
-                if (mode == MODE_ROUTE && P.dupmask != nullptr && ((P.dupmask[gch >> 5] >> (gch & 31)) & 1u)) {
+                if (dup) {
                     if (lane == 0) WB.werr = DEV_E_DUPLICATE;          // chosen (the counter moved), never enqueued
                 } else
                 commit(P, st + l0 + s, base + l0 + s, k, h, R.t, R.keys,

@@ -52,3 +52,41 @@ def test_session_survives_regrow():
         cluster.sizing_for = real
         cluster._LEARNED.clear()
     assert got == want
+
+
+@pytest.mark.parametrize("name", ["det_exclude", "det_force_least_bs", "det_enqueue_mix", "det_many_instances"])
+def test_detector_route_session_matches_reference(name):
+    """route() with the prefix-hotspot detector (cluster.py:133-139: verdict before choose, observe
+    after the enqueue) on the device: holders made by cache.insert(), the hot trace routed call by
+    call -- suspects, phase-2 streaks, alarms and both mitigations show in the decisions (each
+    session routes >= 55 requests differently from the same session without the detector)."""
+    import make_api_golden as M
+    from paper_2603_15202_b200 import workloads as W
+    want = json.load(open(os.path.join(G.GOLDEN, "api_sessions.json")))[name]
+    cfg, (holders, n_route, extra) = M.DET_SESSIONS[name]
+    hot = W.hotspot(8, 600, 0.6, 20.0, seed=4)[0]
+    steps = M._hot_steps(hot, holders, n_route, extra)
+    got = json.loads(json.dumps(M.run_session(cfg, steps, hot, _ours())))
+    assert len(got) == len(want)
+    for i, (g, w) in enumerate(zip(got, want)):
+        assert g == w, f"step {i} ({steps[i]}): {str(g)[:300]} != {str(w)[:300]}"
+
+
+def test_detector_route_session_survives_regrow():
+    """The detector session on rings too small: every regrow replays the logged route() calls
+    (with their detector classes) onto a fresh handle, and the decisions still match."""
+    import make_api_golden as M
+    from paper_2603_15202_b200 import cluster, workloads as W
+    want = json.load(open(os.path.join(G.GOLDEN, "api_sessions.json")))["det_exclude"]
+    cfg, (holders, n_route, extra) = M.DET_SESSIONS["det_exclude"]
+    hot = W.hotspot(8, 600, 0.6, 20.0, seed=4)[0]
+    steps = M._hot_steps(hot, holders, n_route, extra)
+    real = cluster.sizing_for
+    try:
+        cluster.sizing_for = lambda t, c: cluster.Sizing(16, 64) if t is None else real(t, c)
+        cluster._LEARNED.clear()
+        got = json.loads(json.dumps(M.run_session(cfg, steps, hot, _ours())))
+    finally:
+        cluster.sizing_for = real
+        cluster._LEARNED.clear()
+    assert got == want

@@ -38,6 +38,36 @@ SESSIONS = {
                            [("route", i) for i in range(40)] + [("queues",), ("run", 40, 120)]),
 }
 
+# route() with the prefix-hotspot detector (cluster.py:133-139): the hot class's prefix is inserted
+# into a few instances (route() runs no engine step, so API inserts are what makes holders), then
+# the hot trace is routed -- phase 1 suspects, phase-2 streaks, alarms and the mitigation (holders
+# excluded / least batch size) all show in the decisions; enqueue() calls in between.
+def _det_cfg(n, mitigation="exclude_holders", window_s=2.0, kind="multiplicative", seed=3):
+    from paper_2603_15202_b200.config import DetectorConfig
+    return ClusterConfig(n_instances=n, policy=PolicyConfig(kind=kind), seed=seed,
+                         detector=DetectorConfig(window_s=window_s, mitigation=mitigation, top_k_classes=4))
+
+
+def _hot_steps(trace, holders, n_route, extra=()):
+    from collections import Counter
+    from paper_2603_15202_b200.trace import class_key
+    recs = trace.records()
+    ck = [class_key(r.prefix_blocks, 2) for r in recs]
+    hot = Counter(ck).most_common(1)[0][0]
+    first = ck.index(hot)
+    steps = [("insert", h, first, 0) for h in holders] + [("route", i) for i in range(n_route)]
+    for pos, st in extra:
+        steps.insert(pos, st)
+    return steps
+
+
+DET_SESSIONS = {   # name: (config, (holders, routes, extra steps))
+    "det_exclude": (_det_cfg(8), ((0, 1), 400, ())),
+    "det_force_least_bs": (_det_cfg(8, mitigation="force_least_bs"), ((2, 5), 400, ())),
+    "det_enqueue_mix": (_det_cfg(6, kind="vllm", window_s=1.0), ((0,), 300, [(150, ("enqueue_now", 3, 500)), (151, ("queues",))])),
+    "det_many_instances": (_det_cfg(40, window_s=3.0), ((0, 7, 13, 21), 500, ())),
+}
+
 
 def run_session(cfg, steps, trace, api):
     """api: (ClusterSim class, record converter, DuplicateRequestError). Returns the observations."""
@@ -61,23 +91,26 @@ def run_session(cfg, steps, trace, api):
         if kind == "route_after":
             clock += 1000
             d = sim.route(recs[st[1]], clock)
-            obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)]])
+            obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)], d.kind, sorted(d.filtered)])
             continue
         if kind == "route":
             r = recs[st[1]]
             d = sim.route(r, int(trace.arrival_us[st[1]]))
             clock = max(clock, int(trace.arrival_us[st[1]]))
-            obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)]])
+            obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)], d.kind, sorted(d.filtered)])
         elif kind == "route_dup":
             r = recs[st[1]]
             clock = max(clock, st[2])
             try:
                 d = sim.route(r, st[2])
-                obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)]])
+                obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)], d.kind, sorted(d.filtered)])
             except Dup:
                 obs.append(["dup"])
         elif kind == "enqueue":
             a = sim.instances[st[1]].enqueue(recs[st[2]], int(trace.arrival_us[st[2]]))
+            obs.append(["enqueue", a.hit_blocks, a.hit_tokens, a.pending_prefill])
+        elif kind == "enqueue_now":          # enqueue a later record at the time reached so far
+            a = sim.instances[st[1]].enqueue(recs[st[2]], clock)
             obs.append(["enqueue", a.hit_blocks, a.hit_tokens, a.pending_prefill])
         elif kind == "enqueue_dup":
             try:
@@ -114,6 +147,11 @@ def main():
         out[name] = run_session(to_ref_config(cfg), steps, trace,
                                 (ClusterSim, to_ref_records, DuplicateRequestError))
         print(name, [o[0] if o[0] != "route" else o[1] for o in out[name]][:40])
+    hot = W.hotspot(8, 600, 0.6, 20.0, seed=4)[0]
+    for name, (cfg, (holders, n_route, extra)) in DET_SESSIONS.items():
+        steps = _hot_steps(hot, holders, n_route, extra)
+        out[name] = run_session(to_ref_config(cfg), steps, hot, (ClusterSim, to_ref_records, DuplicateRequestError))
+        print(name, [o[1] for o in out[name] if o[0] == "route"][:60])
     with open(os.path.join(ROOT, "tests", "golden", "api_sessions.json"), "w") as fh:
         json.dump(out, fh)
 
