@@ -1471,8 +1471,9 @@ __global__ void __launch_bounds__(256)
 probe_scan_kernel(const __grid_constant__ Params P, i64 r0, i64 nreq, int *out) {
     const i64 total = nreq * (i64)P.N;
     const i64 stride = (i64)gridDim.x * blockDim.x;
+    const bool narrow = total <= 0xffffffffLL;               // 32-bit pair -> (request, instance)
     for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += stride) {
-        const i64 rr = p / P.N;
+        const i64 rr = narrow ? (i64)((u32)p / (u32)P.N) : p / P.N;
         const int gi = (int)(p - rr * P.N);
         const i64 a = __ldg(P.blk_off + r0 + rr);
         const int B = (int)(__ldg(P.blk_off + r0 + rr + 1) - a);
