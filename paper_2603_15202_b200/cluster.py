@@ -311,8 +311,11 @@ class _InstanceProxy:
         """InstanceSim.enqueue (engine.py:262-289): DuplicateRequestError when this instance
         already holds the request id, before any state changes."""
         sim = self._sim
-        if self.id in sim._holders(record.request_id):
+        live = sim._holders(record.request_id)
+        if self.id in live:
             raise DuplicateRequestError(f"request {record.request_id} already present")
+        if live:
+            sim._shared_ids.add(record.request_id)
         sim._advance_clock(int(now_us), "enqueue()")
         idx = sim._do(("load", PackedTrace.from_records([record]), np.array([now_us], np.int64)))
         ht = sim._do(("enqueue", self.id, idx, int(now_us)))
@@ -398,6 +401,7 @@ class ClusterSim:
         self._stateful = False                # any logged call other than a trace load
         self._log_read = None                 # the step log read by the last run op
         self._det_tracks: dict[int, int] = {}  # route() with the detector: class key -> track
+        self._shared_ids: set[int] = set()     # request ids routed / enqueued while live elsewhere
         self._parts: list[PackedTrace] = []   # loaded requests, in load order
         self._arrival: list[np.ndarray] = []  # their arrival (route / enqueue time) in us
         self._reported: list[np.ndarray] = []  # which of them the Collector reports (route / trace)
@@ -532,10 +536,10 @@ class ClusterSim:
     def _flush(self) -> None:
         """Fold the records route() appended since the last fold into the loaded parts."""
         if self._pending:
-            recs = [r for r, _ in self._pending]
+            recs = [r for r, _, _ in self._pending]
             self._parts.append(PackedTrace.from_records(recs))
-            self._arrival.append(np.fromiter((t for _, t in self._pending), np.int64, len(recs)))
-            self._reported.append(np.ones(len(recs), bool))
+            self._arrival.append(np.fromiter((t for _, t, _ in self._pending), np.int64, len(recs)))
+            self._reported.append(np.fromiter((ok for _, _, ok in self._pending), bool, len(recs)))
             self._pending = []
 
     def _record(self, idx: int) -> TraceRecord:
@@ -620,6 +624,8 @@ class ClusterSim:
             self._routed(record, now_us, idx, observed=False)
             raise
         self._routed(record, now_us, idx)
+        if holders:                               # the id is now live on several instances at once
+            self._shared_ids.add(record.request_id)
         kind = self.config.policy.kind
         if branch == 3:                           # verdict force_least_bs (policies.py:228-229)
             kind = "least_bs"
@@ -644,12 +650,16 @@ class ClusterSim:
         return (t, min(det.class_key_blocks, len(record.prefix_blocks)), ck, rows)
 
     def _routed(self, record: TraceRecord, now_us: int, idx: int, observed: bool = True) -> None:
+        """Bookkeeping of a routed record (loaded on the device either way). A duplicate
+        (observed=False) was decided but never enqueued: the Collector does not report it and
+        it is present nowhere (cluster.py:140-152, engine.py:266-267)."""
         if self.config.detector is not None and observed:
             self._det_tracks.setdefault(class_key(record.prefix_blocks, self.config.detector.class_key_blocks),
                                         len(self._det_tracks))
-        self._pending.append((record, now_us))
+        self._pending.append((record, now_us, observed))
         self._n += 1
-        self._by_rid.setdefault(record.request_id, []).append(idx)
+        if observed:
+            self._by_rid.setdefault(record.request_id, []).append(idx)
 
     # -- trace replay (cluster.py:172-201) -----------------------------------------------------
     def run_trace(self, records: Sequence[TraceRecord] | PackedTrace) -> RunReport:
@@ -669,6 +679,13 @@ class ClusterSim:
                                                if int(r) in self._by_rid):
             from .config import UnsupportedConfigError
             raise UnsupportedConfigError("trace request ids still present from earlier route()/enqueue() calls")
+        if self._shared_ids and any(self._holders(r) for r in self._shared_ids):
+            # the reference's Collector keeps one entry per id for events (metrics.py:116-139): the
+            # steps of every live copy would report into the newest copy's RequestMetrics, which
+            # the per-copy device columns do not reproduce -- refused rather than answered differently
+            from .config import UnsupportedConfigError
+            raise UnsupportedConfigError("run_trace() while a request id is live on several instances "
+                                         "(route()/enqueue() of an id already present elsewhere)")
         if len(trace) and self._ops:
             self._advance_clock(int(trace.arrival_us[0]), "run_trace()'s first arrival")
         fresh = not self._ops

@@ -1003,8 +1003,17 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 if (lane == 0) mbar_arrive_expect(&mb[par], (u32)(CW * 16));
                 while (!mbar_try_wait(&mb[par], (mb_phase >> par) & 1u)) { }
                 mb_phase ^= 1u << par;
+#ifdef RSIM_DIAG
+                u64 *tlc = (P.crit != nullptr && lane == 0 && k - k0 < P.crit_cap)
+                               ? reinterpret_cast<u64 *>(P.crit + (size_t)P.crit_cap * CW * 8) + (size_t)(k - k0) * (CW + 4) + CW
+                               : nullptr;
+                if (tlc) tlc[0] = globaltimer();
+#endif
                 decide_phase(P, part, CW, W, 0, k, par, dec[par], modtab, c0_lo, c0_hi, ties, lane, false);
                 __syncwarp();
+#ifdef RSIM_DIAG
+                if (tlc) tlc[1] = globaltimer();
+#endif
                 const Dec d = dec[par];   // (owner_warp, kk, err, pad) <- (flat owner, its tie index, err, branch)
                 const u64 a = ((u64)(u32)d.okk << 32) | (u32)d.oflat;
                 const u64 b = ((u64)(u32)d.pad << 32) | (u32)d.err;

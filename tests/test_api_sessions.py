@@ -21,7 +21,8 @@ def _ours():
     return ClusterSim, (lambda tr: tr.records()), DuplicateRequestError
 
 
-@pytest.mark.parametrize("name", ["route_then_run", "run_twice", "duplicates", "enqueue_dup", "small_batch_queues"])
+@pytest.mark.parametrize("name", ["route_then_run", "run_twice", "duplicates", "duplicates_then_run", "enqueue_dup",
+                                  "small_batch_queues"])
 def test_session_matches_reference(name):
     import make_api_golden as M
     from paper_2603_15202_b200 import workloads as W
@@ -90,3 +91,29 @@ def test_detector_route_session_survives_regrow():
         cluster.sizing_for = real
         cluster._LEARNED.clear()
     assert got == want
+
+
+def test_run_trace_refused_while_an_id_is_live_on_two_instances():
+    """The reference's Collector files every event under the newest RequestMetrics of an id
+    (metrics.py:116-139): once one id is live on two instances, the per-copy device columns would
+    report differently, so run_trace refuses (UnsupportedConfigError) instead of diverging."""
+    import make_api_golden as M
+    from paper_2603_15202_b200 import workloads as W
+    from paper_2603_15202_b200.config import UnsupportedConfigError
+    ClusterSim, conv, Dup = _ours()
+    cfg, steps = M.SESSIONS["duplicates"]
+    trace = W.config1_chatbot()[0].slice(600)
+    recs = conv(trace)
+    sim = ClusterSim(cfg)
+    sim.route(recs[0], int(trace.arrival_us[0]))
+    placed = 1
+    for j in range(1, 40):                   # until the id lands on a second instance
+        try:
+            sim.route(recs[0], 70_000 + j)
+            placed += 1
+            break
+        except Dup:
+            pass
+    assert placed == 2
+    with pytest.raises(UnsupportedConfigError):
+        sim.run_trace(recs[300:320])

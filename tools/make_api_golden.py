@@ -32,6 +32,11 @@ SESSIONS = {
     "duplicates": (ClusterConfig(n_instances=3, policy=PolicyConfig(kind="vllm"), seed=0),
                    [("route", 0), ("route", 1)] + [("route_dup", j % 2, 70_000 + 10 * j) for j in range(2, 26)]
                    + [("route_after", 2), ("queues",)]),
+    # refused duplicates (one instance: every repeat lands on the holder) are decided -- the
+    # tie-break counter moves -- but never enqueued nor reported by the Collector
+    "duplicates_then_run": (ClusterConfig(n_instances=1, seed=4),
+                            [("route", 0), ("route", 1)] + [("route_dup", j % 2, 70_000 + 10 * j) for j in range(2, 12)]
+                            + [("route_after", 2), ("run_after", 300, 420)]),
     "enqueue_dup": (ClusterConfig(n_instances=2, seed=0),
                     [("enqueue", 0, 0), ("enqueue_dup", 0, 0), ("enqueue", 1, 0), ("route", 1), ("queues",)]),
     "small_batch_queues": (ClusterConfig(n_instances=3, cost_model=CostModel(chunk_tokens=64, max_batch_requests=2), seed=5),
