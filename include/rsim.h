@@ -162,7 +162,8 @@ rsim_status rsim_route_one_excl(rsim_t *h, int64_t r, int64_t now_us, const int3
 /* ClusterSim.route(record, now_us) of a request that is not loaded yet (cluster.py:130-154):
  * scores (N, may be NULL) are RoutingDecision.scores, NaN for a candidate the detector excluded;
  * branch (may be NULL) receives the detector verdict applied (0 none, 2 holders excluded, 3 forced
- * least_bs, 4 excluded + route_filter's batch-size branch). Otherwise as follows:
+ * least_bs, 4 excluded + route_filter's batch-size branch). One launch (route_kernel) for the plain
+ * policies on <= 256 instances, else three. Otherwise as follows:
  * appends it to the loaded trace (as rsim_load_trace of one request would) and decides it, with
  * the holders semantics of rsim_route_one_excl -- one fused call (the request goes in and the
  * decision comes out through mapped pinned memory, three launches, one stream synchronisation). */

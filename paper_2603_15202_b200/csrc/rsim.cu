@@ -64,6 +64,7 @@ struct rsim {
     int C = 1, W = 1, ipw = 1, per_cta = 1;
     size_t smem_bytes = 0;
     bool central = false;           // replay_kernel's central mode: one extra decider CTA
+    bool route1 = false;            // rsim_route_request in one launch (route_kernel)
     bool no_rsm = getenv("RSIM_NO_SMEM_RUNNING") != nullptr;   // A/B switch: running lists stay in HBM
     int qlog2 = 0, slog2 = 0;
     i64 max_occ = 0;
@@ -364,6 +365,8 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
         W = std::max(1, std::min(RSIM_MAX_WARPS, W));
         ipw = (per_cta + W - 1) / W;
     };
+    // (one CTA: up to 256 instances; a larger shard probes faster spread over the replay cluster)
+    h->route1 = !ext && world == 1 && N <= 256 && !getenv("RSIM_ROUTE_3LAUNCH");
     h->central = false;
     if (!ext && RSIM_CENTRAL && !getenv("RSIM_NO_CENTRAL") && c.ctas <= 15) {
         shape(15);
@@ -386,6 +389,8 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
                 cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
                 cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             }
+            cudaFuncSetAttribute((const void *)route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(RK_MAXW * sizeof(WarpBuf)));
         });
     }
 
@@ -825,6 +830,22 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
     }
     memcpy(q + RQ_HDR + words, blocks, (size_t)n_blocks * sizeof(u64));
     CK(h, cudaMemcpyAsync(h->rq_dev.p, q, need * sizeof(i64), cudaMemcpyHostToDevice, st));
+    const bool filt = h->cfg.policy == RSIM_POLICY_FILTER;
+    const int nsc = h->cfg.det_on ? 5 * h->N + 1 : (filt ? 2 : 1) * h->N;
+    rsim_status rs = RSIM_OK;
+    if (h->route1) {
+        // plain policies on one rank with <= 1024 instances: the whole call is one launch
+        Params P = make_params(h);
+        P.scores = h->scores;
+        P.dupmask = words ? h->dupmask.p : nullptr;
+        const int nw = std::min(RK_MAXW, h->N);         // instances spread over up to 32 warps
+        route_kernel<<<1, 32 * nw, (size_t)nw * sizeof(WarpBuf), st>>>(P, h->rq_dev.p, h->ro_d, nsc, h->blocks.p);
+        h->launches++;
+        CK(h, cudaGetLastError());
+        if (R0 > 0 && now_us < h->last_arrival) h->order_breaks.push_back(R0);
+        h->last_arrival = now_us;
+        h->R = R1; h->nblk += n_blocks; h->nout += no;
+    } else {
     route_ingest_kernel<<<1, 32, 0, st>>>(h->rq_dev.p, h->arrival.p, h->in_tok.p, h->out_tok.p, h->rid.p, h->blk_off.p,
                                           h->ooff.p, h->blocks.p, h->ckeys.p, h->okeys.p, h->chosen.p, h->hit_blocks.p,
                                           h->hit_tokens.p, h->first_sched.p, h->first_token.p, h->finish.p,
@@ -836,14 +857,13 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
     h->last_arrival = now_us;
     h->R = R1; h->nblk += n_blocks; h->nout += no;
     h->cur_dupmask = words ? h->dupmask.p : nullptr;
-    rsim_status rs = launch_replay(h, R0, R1, now_us, MODE_ROUTE, -1, h->scores, nullptr, false);
+    rs = launch_replay(h, R0, R1, now_us, MODE_ROUTE, -1, h->scores, nullptr, false);
     h->cur_dupmask = nullptr;
     if (rs != RSIM_OK) { cudaStreamSynchronize(st); return rs; }
-    const bool filt = h->cfg.policy == RSIM_POLICY_FILTER;
-    const int nsc = h->cfg.det_on ? 5 * h->N + 1 : (filt ? 2 : 1) * h->N;
     route_out_kernel<<<1, 128, 0, st>>>(h->chosen.p, h->hit_tokens.p, R0, h->scores, nsc, h->errbuf, h->flag, h->ro_d);
     h->launches++;
     CK(h, cudaGetLastError());
+    }
     CK(h, cudaStreamSynchronize(st));
     const i64 *o = h->ro_h;
     const int e[4] = {(int)o[RO_ERR0], (int)o[RO_ERR1], (int)o[RO_ERR2], (int)o[RO_ERR3]};

@@ -372,6 +372,14 @@ def test_route_api_sequence_matches_reference(native, name):
     sim.close()
 
 
+@pytest.mark.parametrize("name", ["multiplicative", "vllm", "linear"])
+def test_route_api_sequence_three_launch_path(native, name, monkeypatch):
+    """The same route() sequences through the three-launch path (ingest, one-decision replay
+    launch, output) that large shards and the extended kernel use, instead of route_kernel."""
+    monkeypatch.setenv("RSIM_ROUTE_3LAUNCH", "1")
+    test_route_api_sequence_matches_reference(native, name)
+
+
 @pytest.mark.parametrize("kind,seed", [("simulate", 0), ("simulate", 1), ("filter", 0), ("filter", 1), ("filter", 2),
                                        ("linear", 0), ("linear", 1), ("linear", 2)])
 def test_random_detector_simulate_match_oracle(native, kind, seed):
