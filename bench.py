@@ -48,6 +48,7 @@ WORKLOADS = {
     "chat16": ("config1_chatbot()", "synthetic chatbot trace, 16 instances, ~10k requests (BASELINE configs[0])"),
     "agent256": ("config3_agent(20_000)", "multi-turn coding-agent trace, 32k-token prompts, 256 instances, capacity 16384 (BASELINE configs[2])"),
     "large4096": ("config4_large(1_000_000)", "4096-instance chat cluster, ~1M requests (BASELINE configs[3])"),
+    "adv64": ("adversarial_stream(64, 100_000)", "adversarial stream (N-way same-time ties, bs 0 vs 1, full hits, out = 1, ragged inputs, tight-capacity evictions), 64 instances, 100k requests (BASELINE configs[4])"),
     "hot64det": ("hotspot_detector(64, 20_000)", "prefix-hotspot trace (one class 60 % of arrivals), 64 instances, reference detector on (SURVEY 8f rank 1)"),
 }
 METRIC = "routing decisions/sec"
@@ -606,7 +607,7 @@ def main():
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
                     help="default: api64 on 1 GPU, large4096 sharded over N > 1")
     ap.add_argument("--requests", type=int, default=0, help="sharded runs: replay only the first R requests (0: all)")
-    ap.add_argument("--extra", default="chat1024,agent256", help="comma list of extra workloads reported beside the headline")
+    ap.add_argument("--extra", default="chat1024,agent256,adv64", help="comma list of extra workloads reported beside the headline")
     ap.add_argument("--ref-budget-s", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", dest="parity", action="store_false",

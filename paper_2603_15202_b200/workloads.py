@@ -262,3 +262,39 @@ def adversarial(case: str, n_instances: int = 16, seed: int = 0):
 
 ADVERSARIAL_CASES = ("same_time_ties", "zero_bs", "full_hits", "ragged", "out1", "step_boundary",
                      "tight_capacity", "mixed")
+
+
+def adversarial_stream(n_instances: int = 64, n_requests: int = 100_000, capacity: int = 256, seed: int = 5):
+    """BASELINE configs[4] at bench scale: the multiplication-failure conditions of
+    ``adversarial`` interleaved over a long trace -- bursts of identical requests at one
+    timestamp onto idle instances (N-way ties through the max(bs, 1) floor and the rotating
+    tie-break), full-cache hits of a few short families (new_prefill floor 1), single-token
+    outputs, ragged inputs, arrivals repeating timestamps, and a tight KV$ capacity whose
+    evictions meet equal (touch, depth) siblings."""
+    rng = np.random.default_rng(seed)
+    bs = 16
+    kind = rng.choice(4, size=n_requests, p=[0.3, 0.3, 0.15, 0.25])
+    gaps = rng.choice([0.0, 0.0, 0.0005, 0.002, 0.0082, 0.021], size=n_requests)
+    burst = kind == 0                      # bursts: the same timestamp as the previous request
+    gaps[burst] = 0.0
+    arrival = np.cumsum(gaps) * (64.0 / n_instances)
+    rows = []
+    for k in range(n_requests):
+        c = int(kind[k])
+        if c == 0:                         # identical requests: one of 4 tiny families
+            fam = int(rng.integers(0, 4))
+            rows.append((float(arrival[k]), [7 + fam, 8 + fam], 32, 2))
+        elif c == 1:                       # full hits of short families, input 1 token short or exact
+            fam = int(rng.integers(0, 6))
+            nb = 2 + fam % 3
+            rows.append((float(arrival[k]), [9000 + 10 * fam + j for j in range(nb)],
+                         nb * bs - int(rng.integers(0, 2)) * 7, int(rng.integers(1, 6))))
+        elif c == 2:                       # single-token outputs
+            rows.append((float(arrival[k]), [31, 32 + k % 5], 32, 1))
+        else:                              # ragged inputs over a shared first block
+            n_in = int(rng.integers(1, 200))
+            nb = -(-n_in // bs)
+            blocks = [777 + int(rng.integers(0, 4))] + [int(x) for x in rng.integers(1, 1 << 62, size=nb - 1)]
+            rows.append((float(arrival[k]), blocks, n_in, int(rng.integers(1, 40))))
+    return _records(rows), ClusterConfig(n_instances=n_instances, cost_model=CostModel(),
+                                         cache=CacheConfig(bs, capacity), seed=seed, policy=PolicyConfig())

@@ -62,6 +62,9 @@ CASES = {
     "adv_step_boundary": ("W.adversarial('step_boundary', 16, 0)", None),
     "adv_tight_capacity": ("W.adversarial('tight_capacity', 16, 0)", None),
     "adv_mixed_n16": ("W.adversarial('mixed', 16, 0)", None),
+    # BASELINE configs[4] at bench scale (the bench line's adv64 workload): ties, bs 0, full hits,
+    # out = 1, ragged inputs, repeated timestamps and tight-capacity evictions, interleaved
+    "adv_stream_prefix6000": ("W.adversarial_stream()", 6000),
     "adv_mixed_n3": ("W.adversarial('mixed', 3, 1)", None),
     "adv_mixed_n33": ("W.adversarial('mixed', 33, 2)", None),
     "adv_mixed_n64": ("W.adversarial('mixed', 64, 3)", None),
