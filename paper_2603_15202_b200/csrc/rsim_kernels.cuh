@@ -256,6 +256,14 @@ __device__ __forceinline__ u32 mod_counter(u64 lo, u64 hi, u32 T) {
 }
 
 #define RSIM_SLOTS 8            // request staging ring depth
+#ifndef RSIM_DECODE_RUNS
+// runs of pure decode steps in registers: 0 off, 1 every drain, 2 the drains off the critical path
+// only. A/B on one B200 (us/decision, off / 1 / 2): api64 4.72 / 4.88 / 4.82, chat1024 6.61 /
+// 6.75 / 6.67, agent256 19.37 / 18.32 / 18.95, adv64 7.96 / 8.20 / 7.97 -- the end-of-trace drain
+// launch halves (chat1024 0.87 -> 0.45 ms) but the added code costs the replay loop more than
+// the runs save on the headline shapes: off by default (profiles/r2_ab/ab_dr2.txt)
+#define RSIM_DECODE_RUNS 0
+#endif
 #define RSIM_MAX_WARPS 8        // instance warps per CTA (+1 control warp)
 #define RSIM_LEAN_WARPS 7       // up to 7 instance warps: 8 warps per CTA = 2 per SM sub-partition,
                                 // which lifts the register budget from 168 to 255 per thread
@@ -279,7 +287,7 @@ __device__ __noinline__ void stage_request(const Params &P, ReqStage &R, i64 k, 
 // ---- drain: advance instances [l0, l0+n) of this warp through steps starting before `until`
 //      (cluster.py:250-273); skip_mask marks instances that must not move yet. The check is
 //      inline; the (noinline) step function is only called when a step is due.
-template <bool STALE>
+template <bool STALE, bool RUNS = (RSIM_DECODE_RUNS == 1)>
 __device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base, int l0, int n, i64 until,
                                             u32 skip_mask, int lane, WarpBuf &WB, Defer *df = nullptr) {
     u32 due = __ballot_sync(FULL, lane < n && !((skip_mask >> lane) & 1u) && st[l0 + lane].next_step < until);
@@ -289,6 +297,36 @@ __device__ __forceinline__ void drain_phase(const Params &P, Inst *st, int base,
         Inst *sp = st + l0 + s;
         u64 steps = 0;
         while (sp->next_step < until && !WB.werr) {
+#if RSIM_DECODE_RUNS
+            if (RUNS && !(STALE && P.stal > 0) && sp->q == 0 && sp->r > 0 && sp->next_finish != sp->step_idx) {
+                // a run of pure decode steps (no queue to plan, no finish before the next finish
+                // step): inst_step_body's fast path step after step, on lane-uniform registers, with
+                // one write-back -- each step flushes the view at its start (engine.py:293), adds
+                // one token per running request and ends after decode_cost_us (engine.py:333-352)
+                const int nd = sp->r;
+                const i64 nf = sp->next_finish;
+                i64 t = sp->next_step, si = sp->step_idx, dcs = sp->dcs, total = sp->total;
+                bool fl = sp->due <= t, any = false;
+                i64 fv_total = 0, fv_dc = 0, n = 0;
+                const int gi = base + l0 + s;
+                do {
+                    if (fl) { fv_total = total; fv_dc = dcs; any = true; }
+                    const i64 end = t + decode_cost_us(P, nd, dcs);
+                    log_step(P, WB.fin, gi, t, end, 0, (i64)nd, si, lane);
+                    total += nd; dcs += nd; si++; t = end; n++;
+                    fl = true;                                   // (due = this end from here on)
+                } while (t < until && si != nf);
+                __syncwarp();
+                if (lane == 0) {
+                    if (any) { sp->v_r = nd; sp->v_q = 0; sp->v_pend = sp->pend; sp->v_total = fv_total; sp->v_dc = fv_dc; }
+                    sp->total = total; sp->dcs = dcs; sp->step_idx = si;
+                    sp->busy_until = t; sp->due = t; sp->next_step = t;
+                }
+                __syncwarp();
+                steps += (u64)n;
+                continue;
+            }
+#endif
             if (STALE && P.stal > 0 && sp->due <= sp->next_step) {   // the step's flush (engine.py:293), recorded
                 __syncwarp();
                 if (lane == 0) flush_view_hist(P, *sp, base + l0 + s, sp->next_step);
@@ -994,7 +1032,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
 #define DIAG(x)
 #endif
     if (mode == MODE_DRAIN) {
-        if (!control) drain_phase<FILTER>(P, st, base, l0, nmine, until, 0u, lane, WB);
+        if (!control) drain_phase<FILTER, (RSIM_DECODE_RUNS >= 1)>(P, st, base, l0, nmine, until, 0u, lane, WB);
     } else if (central && decider) {
         if (control) {      // ---- the decider: partials of k -> decision -> every instance CTA
             u32 mb_phase = 0u;
@@ -1358,7 +1396,7 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                                                             (!(FILTER && P.policy == 4) || bits_bs != wmin_bs)) &
                                     ~det_keep;      // detector: the other argmin branches' candidates stay
                     DIAG(const long long t_s0 = clock64());
-                    if (adv) drain_phase<FILTER>(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
+                    if (adv) drain_phase<FILTER, (RSIM_DECODE_RUNS >= 1)>(P, st, base, l0, nmine, R1.t, ~adv, lane, WB);
                     DIAG(const long long t_s1 = clock64());
                     // probe-ahead of request k+1 (valid while the instance's tabver holds)
                     if (nmine >= 2 && R1.B <= 128) {   // (one instance: the dense probe's single round trip wins)
