@@ -837,7 +837,7 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
         // plain policies on one rank with <= 1024 instances: the whole call is one launch
         Params P = make_params(h);
         P.scores = h->scores;
-        P.dupmask = words ? h->dupmask.p : nullptr;
+        P.dupmask = nullptr;                      // (route_kernel reads the holders from the request block)
         const int nw = std::min(RK_MAXW, h->N);         // instances spread over up to 32 warps
         route_kernel<<<1, 32 * nw, (size_t)nw * sizeof(WarpBuf), st>>>(P, h->rq_dev.p, h->ro_d, nsc, h->blocks.p);
         h->launches++;
@@ -867,7 +867,12 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
     CK(h, cudaStreamSynchronize(st));
     const i64 *o = h->ro_h;
     const int e[4] = {(int)o[RO_ERR0], (int)o[RO_ERR1], (int)o[RO_ERR2], (int)o[RO_ERR3]};
-    if ((rs = decode_device_error(h, e)) != RSIM_OK) return rs;
+    if ((rs = decode_device_error(h, e)) != RSIM_OK) {
+        // a refused duplicate never reaches Detector.observe (cluster.py:140-142): a track it
+        // opened was not created, and the next new class takes its slot
+        if (rs == RSIM_E_DUPLICATE && newt >= 0) h->dT = newt;
+        return rs;
+    }
     if (o[RO_FLAG]) return fail(h, RSIM_E_TRACE, "a chain key equals the table sentinel 0 (probability 2^-64 per key)");
     if (chosen) *chosen = (int32_t)o[RO_CHOSEN];
     if (hit_tokens) *hit_tokens = o[RO_HIT];

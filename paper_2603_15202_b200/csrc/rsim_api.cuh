@@ -165,7 +165,7 @@ route_kernel(const __grid_constant__ Params P, const i64 *__restrict__ rq, i64 *
         const int gi = l0 + s, gch = P.gbase + gi;
         const int h = WB.hit[s];
         int werr = 0;
-        if (P.dupmask != nullptr && ((P.dupmask[gch >> 5] >> (gch & 31)) & 1u)) {
+        if (ndup > 0 && ((rq[RQ_HDR + (gch >> 5)] >> (gch & 31)) & 1)) {   // holders bitmap of this call
             werr = DEV_E_DUPLICATE;                    // chosen (the counter moved), never enqueued
         } else {
             commit(P, P.inst + gi, gi, R0, h, R.t, R.keys, nullptr, R.a, R.B, R.in, R.out, R.oa, lane, werr, WB.fin, false);

@@ -55,7 +55,8 @@ def test_session_survives_regrow():
     assert got == want
 
 
-@pytest.mark.parametrize("name", ["det_exclude", "det_force_least_bs", "det_enqueue_mix", "det_many_instances"])
+@pytest.mark.parametrize("name", ["det_exclude", "det_force_least_bs", "det_enqueue_mix", "det_many_instances",
+                                  "det_dup_new_class"])
 def test_detector_route_session_matches_reference(name):
     """route() with the prefix-hotspot detector (cluster.py:133-139: verdict before choose, observe
     after the enqueue) on the device: holders made by cache.insert(), the hot trace routed call by

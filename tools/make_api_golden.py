@@ -71,6 +71,9 @@ DET_SESSIONS = {   # name: (config, (holders, routes, extra steps))
     "det_force_least_bs": (_det_cfg(8, mitigation="force_least_bs"), ((2, 5), 400, ())),
     "det_enqueue_mix": (_det_cfg(6, kind="vllm", window_s=1.0), ((0,), 300, [(150, ("enqueue_now", 3, 500)), (151, ("queues",))])),
     "det_many_instances": (_det_cfg(40, window_s=3.0), ((0, 7, 13, 21), 500, ())),
+    # one instance: a request id routed again is always refused -- here under another class's
+    # record, so the refused call's class is never observed and the next new class takes its track
+    "det_dup_new_class": (_det_cfg(1, window_s=1.0), ((0,), 60, [(4, ("route_dup_as", 39, 0, None))])),
 }
 
 
@@ -108,6 +111,15 @@ def run_session(cfg, steps, trace, api):
             clock = max(clock, st[2])
             try:
                 d = sim.route(r, st[2])
+                obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)], d.kind, sorted(d.filtered)])
+            except Dup:
+                obs.append(["dup"])
+        elif kind == "route_dup_as":        # record st[1] under record st[2]'s request id
+            r = dataclasses.replace(recs[st[1]], request_id=recs[st[2]].request_id)
+            now = clock if st[3] is None else st[3]
+            clock = max(clock, now)
+            try:
+                d = sim.route(r, now)
                 obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)], d.kind, sorted(d.filtered)])
             except Dup:
                 obs.append(["dup"])
