@@ -118,3 +118,20 @@ def test_run_trace_refused_while_an_id_is_live_on_two_instances():
     assert placed == 2
     with pytest.raises(UnsupportedConfigError):
         sim.run_trace(recs[300:320])
+
+
+@pytest.mark.parametrize("name", ["fuzz_mult_n5", "fuzz_vllm_n12", "fuzz_linear_n3", "fuzz_filter_n7", "fuzz_mult_n300"])
+def test_fuzz_session_matches_reference(name):
+    """Seeded random API sessions (route, repeated ids, enqueue, cache.insert, queue views) on
+    the one-launch route path (plain policies, <= 256 instances) and the three-launch path
+    (filter, 300 instances), against the reference's ClusterSim."""
+    import make_api_golden as M
+    from paper_2603_15202_b200 import workloads as W
+    want = json.load(open(os.path.join(G.GOLDEN, "api_sessions.json")))[name]
+    cfg, seed = M.FUZZ_SESSIONS[name]
+    steps = M._fuzz_steps(seed, cfg.n_instances)
+    trace = W.config1_chatbot()[0].slice(600)
+    got = json.loads(json.dumps(M.run_session(cfg, steps, trace, _ours())))
+    assert len(got) == len(want)
+    for i, (g, w) in enumerate(zip(got, want)):
+        assert g == w, f"step {i} ({steps[i]}): {str(g)[:300]} != {str(w)[:300]}"

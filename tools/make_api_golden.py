@@ -66,6 +66,36 @@ def _hot_steps(trace, holders, n_route, extra=()):
     return steps
 
 
+def _fuzz_steps(seed, n_inst, n_steps=160):
+    """A seeded random mix of route() / repeated ids / enqueue() / cache.insert() / queue views
+    over the chat trace, in non-decreasing time (the device path's contract)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    steps, nxt = [], 0
+    for _ in range(n_steps):
+        u = rng.random()
+        if u < 0.6 or nxt < 2:
+            steps.append(("route", nxt)); nxt += 1
+        elif u < 0.75:
+            steps.append(("route_dup_now", int(rng.integers(0, nxt))))
+        elif u < 0.85:
+            steps.append(("enqueue_now", int(rng.integers(0, n_inst)), 400 + nxt)); nxt += 1
+        elif u < 0.95:
+            steps.append(("insert_now", int(rng.integers(0, n_inst)), int(rng.integers(0, 590))))
+        else:
+            steps.append(("queues",))
+    return steps
+
+
+FUZZ_SESSIONS = {   # name: (config, seed)
+    "fuzz_mult_n5": (ClusterConfig(n_instances=5, seed=11), 0),
+    "fuzz_vllm_n12": (ClusterConfig(n_instances=12, policy=PolicyConfig(kind="vllm", q_weight=0.5), seed=12), 1),
+    "fuzz_linear_n3": (ClusterConfig(n_instances=3, policy=PolicyConfig(kind="linear", bs_norm_cap=6.0),
+                                     cost_model=CostModel(chunk_tokens=96, max_batch_requests=3), seed=13), 2),
+    "fuzz_filter_n7": (ClusterConfig(n_instances=7, policy=PolicyConfig(kind="filter", range_threshold=2), seed=14), 3),
+    "fuzz_mult_n300": (ClusterConfig(n_instances=300, seed=15), 4),
+}
+
 DET_SESSIONS = {   # name: (config, (holders, routes, extra steps))
     "det_exclude": (_det_cfg(8), ((0, 1), 400, ())),
     "det_force_least_bs": (_det_cfg(8, mitigation="force_least_bs"), ((2, 5), 400, ())),
@@ -114,6 +144,12 @@ def run_session(cfg, steps, trace, api):
                 obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)], d.kind, sorted(d.filtered)])
             except Dup:
                 obs.append(["dup"])
+        elif kind == "route_dup_now":        # an id again, at the time reached so far
+            try:
+                d = sim.route(recs[st[1]], clock)
+                obs.append(["route", d.chosen, [d.scores.get(i) for i in range(cfg.n_instances)], d.kind, sorted(d.filtered)])
+            except Dup:
+                obs.append(["dup"])
         elif kind == "route_dup_as":        # record st[1] under record st[2]'s request id
             r = dataclasses.replace(recs[st[1]], request_id=recs[st[2]].request_id)
             now = clock if st[3] is None else st[3]
@@ -135,6 +171,9 @@ def run_session(cfg, steps, trace, api):
                 obs.append(["enqueue_ok"])
             except Dup:
                 obs.append(["dup"])
+        elif kind == "insert_now":           # cache.insert at the time reached so far
+            sim.instances[st[1]].cache.insert(recs[st[2]].prefix_blocks, clock)
+            obs.append(["insert"])
         elif kind == "insert":
             sim.instances[st[1]].cache.insert(recs[st[2]].prefix_blocks, st[3])
             obs.append(["insert"])
@@ -162,6 +201,10 @@ def main():
     out = {}
     for name, (cfg, steps) in SESSIONS.items():
         out[name] = run_session(to_ref_config(cfg), steps, trace,
+                                (ClusterSim, to_ref_records, DuplicateRequestError))
+        print(name, [o[0] if o[0] != "route" else o[1] for o in out[name]][:40])
+    for name, (cfg, seed) in FUZZ_SESSIONS.items():
+        out[name] = run_session(to_ref_config(cfg), _fuzz_steps(seed, cfg.n_instances), trace,
                                 (ClusterSim, to_ref_records, DuplicateRequestError))
         print(name, [o[0] if o[0] != "route" else o[1] for o in out[name]][:40])
     hot = W.hotspot(8, 600, 0.6, 20.0, seed=4)[0]
