@@ -354,11 +354,11 @@ def measure_workload(name, args, dev_index, with_cpu: bool, rank: int):
     }
     if with_cpu:
         n = reference_samples(trace, cfg, args.ref_budget_s)
-        ref = time_reference(trace, cfg, n)
+        ref = time_reference(trace, cfg, n, repeats=3)      # best of 3
         cpu = host_cpu()
         if ref is not None:
             out["cpu_baseline"] = {"value": ref, "unit": "decisions/s", "cores": 1, "kind": "reference",
-                                   "sample": f"first {n} of {R} requests, routesim.run from baseline/_ref (CPython, 1 thread)",
+                                   "sample": f"first {n} of {R} requests, routesim.run from baseline/_ref (CPython, 1 thread), best of 3",
                                    "host_cpu": cpu}
     if args.parity:
         # the C oracle over the benched trace (or its first --parity-max requests): the timed CPU port
