@@ -616,6 +616,11 @@ class ClusterSim:
         self._advance_clock(now_us, "route()")
         holders = tuple(sorted(self._holders(record.request_id))) if record.request_id in self._by_rid else ()
         idx = self._n
+        if self.config.detector is not None and self._runs:
+            # (the device detector's tracks of a replayed trace are numbered by that trace and
+            # its window was closed by the report's finalize: not continued call by call)
+            from .config import UnsupportedConfigError
+            raise UnsupportedConfigError("route() with the hotspot detector after a run_trace() on the same ClusterSim")
         det = self._det_class(record, now_us) if self.config.detector is not None else None
         try:
             chosen, _ht, scores, branch = self._do(("route_request", record, now_us, holders, det),
