@@ -94,7 +94,7 @@ struct rsim {
     i64 *scratch_res = nullptr;
     u64 *ctr = nullptr;            // device counters (Params.ctr)
     int N = 0, gbase = 0;          // local shard size, global id of local instance 0
-    u64 *mbox = nullptr;           // multi-GPU mailbox [2][8][4]
+    u64 *mbox = nullptr;           // multi-GPU mailbox [2 parity][8 ranks][RSIM_MBOX_W]
     u64 *peer[8] = {nullptr};
     bool peer_ipc[8] = {false};
     u64 epoch = 1;
@@ -312,8 +312,6 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
         if (c.world > 1) return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector is single-rank on the device path");
         if (c.det_window_s > 1e6) return fail(nullptr, RSIM_E_UNSUPPORTED, "detector window longer than 1e6 s");
     }
-    if (c.policy == RSIM_POLICY_FILTER && c.world > 1)
-        return fail(nullptr, RSIM_E_UNSUPPORTED, "filter policy is single-rank on the device path");
     if (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0) && c.world > 1)
         return fail(nullptr, RSIM_E_UNSUPPORTED, "linear policy without bs_norm_cap is single-rank on the device path");
     if (c.prefill_base_ms < 0 || c.prefill_per_token_ms < 0 || c.decode_base_ms < 0 || c.decode_per_seq_ms < 0 ||
@@ -442,8 +440,8 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
     CK(nullptr, cudaMalloc(&h->scores, (5 * (size_t)N + 1) * sizeof(double)));
     CK(nullptr, cudaMalloc(&h->scratch_res, 4 * sizeof(i64)));
     CK(nullptr, cudaMalloc(&h->ctr, 48 * sizeof(u64)));   // [16..47]: diagnostics builds
-    CK(nullptr, cudaMalloc(&h->mbox, 2 * 8 * 4 * sizeof(u64)));
-    CK(nullptr, cudaMemset(h->mbox, 0, 2 * 8 * 4 * sizeof(u64)));
+    CK(nullptr, cudaMalloc(&h->mbox, 2 * 8 * RSIM_MBOX_W * sizeof(u64)));
+    CK(nullptr, cudaMemset(h->mbox, 0, 2 * 8 * RSIM_MBOX_W * sizeof(u64)));
     h->peer[world > 1 ? c.rank : 0] = h->mbox;
     if (c.record_steps) {
         h->log_cap = c.step_log_capacity > 0 ? c.step_log_capacity : (1 << 20);

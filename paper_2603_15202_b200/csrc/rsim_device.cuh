@@ -187,6 +187,11 @@ __device__ __forceinline__ i64 warp_min_i64(i64 v) {
     for (int o = 16; o > 0; o >>= 1) { i64 w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
     return v;
 }
+__device__ __forceinline__ i64 warp_max_i64(i64 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { i64 w = __shfl_xor_sync(FULL, v, o); v = w > v ? w : v; }
+    return v;
+}
 __device__ __forceinline__ u64 warp_min_u64(u64 v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) { u64 w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }

@@ -256,6 +256,7 @@ __device__ __forceinline__ u32 mod_counter(u64 lo, u64 hi, u32 T) {
 }
 
 #define RSIM_SLOTS 8            // request staging ring depth
+#define RSIM_MBOX_W 8           // u64 words per (parity, rank) mailbox slot (filter: both branches + range)
 #ifndef RSIM_DECODE_RUNS
 // runs of pure decode steps in registers: 0 off, 1 every drain, 2 the drains off the critical path
 // only. A/B on one B200 (us/decision, off / 1 / 2): api64 4.72 / 4.88 / 4.82, chat1024 6.61 /
@@ -743,6 +744,9 @@ __device__ __forceinline__ void decide_phase_n(const Params &P, const Part *part
     const int NR = (CW + 31) >> 5;
     const Part *pp = part + par * 2 * CW;
     bool bs_branch = false;
+    bool pre = false;                            // filter across ranks: the exchange already ran
+    u64 pre_min = ~0ULL;
+    u32 pre_T = 0u, pre_er = 0u;
     if (filter) {              // route_filter (policies.py:168-192): bs range over all candidates
         u64 bmn = ~0ULL;
         u32 bmx = 0;
@@ -759,6 +763,70 @@ __device__ __forceinline__ void decide_phase_n(const Params &P, const Part *part
         const i64 bs_lo = gb == ~0ULL ? 0 : (i64)__longlong_as_double((long long)gb);
         const i64 bs_hi = (i64)__reduce_max_sync(FULL, bmx);
         bs_branch = bs_hi - bs_lo > P.range_thr;
+        if (P.world > 1) {
+            // route_filter's range is over ALL candidates, i.e. every rank's: each rank sends both
+            // branches' (min, tie count) with its range in one mailbox message, and every rank
+            // picks the branch from the global range (then the winner as for one policy)
+            u64 m0 = ~0ULL, m1 = ~0ULL;
+            u32 e0 = 0u;
+#pragma unroll
+            for (int r = 0; r < NRT; r++) {
+                const int idx = r * 32 + lane;
+                if (r < NR && idx < CW) {
+                    const ulonglong2 q0 = lds_v2u64(pp + idx), q1 = lds_v2u64(pp + CW + idx);
+                    m0 = min(m0, q0.x); m1 = min(m1, q1.x); e0 |= (u32)(q0.y >> 32);
+                }
+            }
+            const u64 g0 = warp_min_u64(m0), g1 = warp_min_u64(m1);
+            u32 t0 = 0u, t1 = 0u;
+#pragma unroll
+            for (int r = 0; r < NRT; r++) {
+                const int idx = r * 32 + lane;
+                if (r < NR && idx < CW) {
+                    const ulonglong2 q0 = lds_v2u64(pp + idx), q1 = lds_v2u64(pp + CW + idx);
+                    t0 += q0.x == g0 ? (u32)q0.y : 0u; t1 += q1.x == g1 ? (u32)q1.y : 0u;
+                }
+            }
+            t0 = __reduce_add_sync(FULL, t0); t1 = __reduce_add_sync(FULL, t1);
+            e0 = __reduce_or_sync(FULL, e0);
+            const u64 seq = (P.epoch << 40) | (u64)(k + 1);
+            if (cta == 0 && lane < P.world) {
+                u64 *slot = P.peer[lane] + (size_t)((par * 8 + P.rank) * RSIM_MBOX_W);
+                st_relaxed_sys(slot + 0, g0);
+                st_relaxed_sys(slot + 1, ((u64)e0 << 32) | t0);
+                st_relaxed_sys(slot + 3, g1);
+                st_relaxed_sys(slot + 4, (u64)t1);
+                st_relaxed_sys(slot + 5, (u64)bs_lo);
+                st_relaxed_sys(slot + 6, (u64)bs_hi);
+                st_release_sys(slot + 2, seq);
+            }
+            u64 a0 = ~0ULL, a1 = ~0ULL;
+            u32 c0 = 0u, c1 = 0u, re = 0u;
+            i64 lo = INT64_MAX, hi = INT64_MIN;
+            if (lane < P.world) {
+                const u64 *slot = P.mbox + (size_t)((par * 8 + lane) * RSIM_MBOX_W);
+                const u64 tt = globaltimer();
+                while (ld_relaxed_sys(slot + 2) != seq) {
+                    if ((i64)(globaltimer() - tt) > P.timeout_ns) { re = DEV_E_COMM; break; }
+                }
+                asm volatile("fence.acq_rel.sys;" ::: "memory");
+                if (!re) {
+                    a0 = ld_relaxed_sys(slot + 0);
+                    const u64 ce = ld_relaxed_sys(slot + 1);
+                    c0 = (u32)ce; re = (u32)(ce >> 32);
+                    a1 = ld_relaxed_sys(slot + 3);
+                    c1 = (u32)ld_relaxed_sys(slot + 4);
+                    lo = (i64)ld_relaxed_sys(slot + 5);
+                    hi = (i64)ld_relaxed_sys(slot + 6);
+                }
+            }
+            lo = warp_min_i64(lo); hi = warp_max_i64(hi);
+            bs_branch = hi - lo > P.range_thr;
+            pre_min = bs_branch ? a1 : a0;
+            pre_T = bs_branch ? c1 : c0;
+            pre_er = re;
+            pre = true;
+        }
     }
 #pragma unroll
     for (int r = 0; r < NRT; r++) {
@@ -803,16 +871,16 @@ __device__ __forceinline__ void decide_phase_n(const Params &P, const Part *part
     u32 Tg = T;
     if (P.world > 1) {          // ---- one (min, tie count) partial per rank over peer-mapped mailboxes
         const u64 seq = (P.epoch << 40) | (u64)(k + 1);
-        if (cta == 0 && lane < P.world) {
-            u64 *slot = P.peer[lane] + (size_t)((par * 8 + P.rank) * 4);
+        if (!pre && cta == 0 && lane < P.world) {
+            u64 *slot = P.peer[lane] + (size_t)((par * 8 + P.rank) * RSIM_MBOX_W);
             st_relaxed_sys(slot + 0, gmin);
             st_relaxed_sys(slot + 1, ((u64)er << 32) | T);
             st_release_sys(slot + 2, seq);
         }
-        u64 rmin = ~0ULL;
-        u32 rT = 0, rer = 0;
-        if (lane < P.world) {
-            const u64 *slot = P.mbox + (size_t)((par * 8 + lane) * 4);
+        u64 rmin = pre ? pre_min : ~0ULL;
+        u32 rT = pre ? pre_T : 0u, rer = pre ? pre_er : 0u;
+        if (!pre && lane < P.world) {
+            const u64 *slot = P.mbox + (size_t)((par * 8 + lane) * RSIM_MBOX_W);
             const u64 t0 = globaltimer();
             // relaxed polls (an acquire load at sys scope flushes L1 on every iteration), one
             // acquire fence once the sequence word matches

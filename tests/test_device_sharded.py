@@ -13,7 +13,10 @@ pytestmark = pytest.mark.gpu
                                         ("cfg2_api_prefix4000", 4), ("adv_same_time_ties", 4),
                                         ("evict_heavy_n4", 2), ("stale_50ms_n16", 3), ("stale_5ms", 2),
                                         ("policy_simulate_mistuned", 3), ("policy_simulate_agent_evict", 2),
-                                        ("cfg1_chatbot_full", 8), ("adv_mixed_n33", 8), ("cfg2_api_prefix4000", 8)])
+                                        ("cfg1_chatbot_full", 8), ("adv_mixed_n33", 8), ("cfg2_api_prefix4000", 8),
+                                        # route_filter across ranks: the batch-size range is global
+                                        ("policy_filter", 2), ("policy_filter_r2", 3), ("policy_filter", 8),
+                                        ("stale_filter_evict", 2)])
 def test_sharded_matches_reference(name, world):
     from paper_2603_15202_b200.distributed import run_sharded_local
     trace, cfg = G.build(name)
@@ -40,3 +43,24 @@ def test_sharded_processes_match_reference(name, world, n):
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
     assert "OK" in p.stdout
+
+
+@pytest.mark.parametrize("world,seed", [(2, 0), (3, 1), (5, 2)])
+def test_sharded_filter_random_matches_oracle(world, seed):
+    """route_filter with the instances split over ranks: random clusters, thresholds and cost
+    models (the range test flips between branches decision by decision) vs the oracle."""
+    import dataclasses
+    from oracle.oracle import run_oracle
+    from paper_2603_15202_b200 import workloads as W
+    from paper_2603_15202_b200.config import CostModel, PolicyConfig
+    from paper_2603_15202_b200.distributed import run_sharded_local
+    rng = np.random.default_rng(700 + seed)
+    N = int(rng.choice([5, 11, 24]))
+    trace, cfg = W.chat_cluster(N, 1500, float(rng.uniform(1.0, 6.0)), seed=seed)
+    cfg = dataclasses.replace(cfg, policy=PolicyConfig(kind="filter", range_threshold=int(rng.integers(0, 4))),
+                              cost_model=CostModel(chunk_tokens=int(rng.choice([256, 2048])),
+                                                   max_batch_requests=int(rng.choice([4, 256]))))
+    got = run_sharded_local(trace, cfg, world)
+    want = run_oracle(trace, cfg)
+    assert np.array_equal(got["chosen"], want.chosen)
+    assert np.array_equal(got["finish_us"], want.finish_us)
