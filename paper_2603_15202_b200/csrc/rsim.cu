@@ -312,8 +312,6 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
         if (c.world > 1) return fail(nullptr, RSIM_E_UNSUPPORTED, "the hotspot detector is single-rank on the device path");
         if (c.det_window_s > 1e6) return fail(nullptr, RSIM_E_UNSUPPORTED, "detector window longer than 1e6 s");
     }
-    if (c.policy == RSIM_POLICY_LINEAR && !(c.bs_norm_cap > 0) && c.world > 1)
-        return fail(nullptr, RSIM_E_UNSUPPORTED, "linear policy without bs_norm_cap is single-rank on the device path");
     if (c.prefill_base_ms < 0 || c.prefill_per_token_ms < 0 || c.decode_base_ms < 0 || c.decode_per_seq_ms < 0 ||
         c.decode_per_ctx_token_ms < 0)
         return fail(nullptr, RSIM_E_INVALID, "cost model coefficients must be non-negative");

@@ -1347,6 +1347,28 @@ replay_kernel(const __grid_constant__ Params P, i64 k0, i64 k1, i64 until, int m
                 }
                 gm = __reduce_max_sync(FULL, gm);
                 gmk = __reduce_max_sync(FULL, gmk);
+                if (P.world > 1) {      // the max is over ALL instances: one more mailbox round
+                    const u64 seq = (P.epoch << 40) | (u64)(k + 1);   // (words 3, 4, 7 of the slot)
+                    if (cta == 0 && warp == 0 && lane < P.world) {
+                        u64 *slot = P.peer[lane] + (size_t)((par * 8 + P.rank) * RSIM_MBOX_W);
+                        st_relaxed_sys(slot + 3, (u64)gm);
+                        st_relaxed_sys(slot + 4, (u64)gmk);
+                        st_release_sys(slot + 7, seq);
+                    }
+                    u32 rg = 0u, rgk = 0u, rer = 0u;
+                    if (lane < P.world) {
+                        const u64 *slot = P.mbox + (size_t)((par * 8 + lane) * RSIM_MBOX_W);
+                        const u64 tt = globaltimer();
+                        while (ld_relaxed_sys(slot + 7) != seq) {
+                            if ((i64)(globaltimer() - tt) > P.timeout_ns) { rer = DEV_E_COMM; break; }
+                        }
+                        asm volatile("fence.acq_rel.sys;" ::: "memory");
+                        if (!rer) { rg = (u32)ld_relaxed_sys(slot + 3); rgk = (u32)ld_relaxed_sys(slot + 4); }
+                    }
+                    gm = __reduce_max_sync(FULL, rg);
+                    gmk = __reduce_max_sync(FULL, rgk);
+                    if (__reduce_or_sync(FULL, rer) && lane == 0) WB.werr = DEV_E_COMM;
+                }
                 bsn = (double)(gm > 1u ? gm : 1u);
                 bsn_kept = (double)(gmk > 1u ? gmk : 1u);
             }

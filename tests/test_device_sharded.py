@@ -16,7 +16,9 @@ pytestmark = pytest.mark.gpu
                                         ("cfg1_chatbot_full", 8), ("adv_mixed_n33", 8), ("cfg2_api_prefix4000", 8),
                                         # route_filter across ranks: the batch-size range is global
                                         ("policy_filter", 2), ("policy_filter_r2", 3), ("policy_filter", 8),
-                                        ("stale_filter_evict", 2)])
+                                        ("stale_filter_evict", 2),
+                                        # linear without a cap: the per-decision bs max over every rank
+                                        ("policy_linear", 2), ("policy_linear", 8), ("stale_linear", 3)])
 def test_sharded_matches_reference(name, world):
     from paper_2603_15202_b200.distributed import run_sharded_local
     trace, cfg = G.build(name)
