@@ -385,8 +385,7 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
                 cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
                 cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             }
-            cudaFuncSetAttribute((const void *)route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(RK_MAXW * sizeof(WarpBuf)));
+            cudaFuncSetAttribute((const void *)route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         });
     }
 
@@ -792,7 +791,8 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
     }
     if (!h->ro_h) {
         void *p = nullptr;
-        CK(h, cudaHostAlloc(&p, (RO_HDR + 2 * (size_t)h->N) * sizeof(i64), cudaHostAllocMapped));
+        // decision, error word, flag + up to 5N + 1 scores (the detector's route() layout) + diagnostics
+        CK(h, cudaHostAlloc(&p, (RO_HDR + 5 * (size_t)h->N + 16) * sizeof(i64), cudaHostAllocMapped));
         h->ro_h = (i64 *)p;
         CK(h, cudaHostGetDevicePointer((void **)&h->ro_d, p, 0));
     }
@@ -835,7 +835,9 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
         P.scores = h->scores;
         P.dupmask = nullptr;                      // (route_kernel reads the holders from the request block)
         const int nw = std::min(RK_MAXW, h->N);         // instances spread over up to 32 warps
-        route_kernel<<<1, 32 * nw, (size_t)nw * sizeof(WarpBuf), st>>>(P, h->rq_dev.p, h->ro_d, nsc, h->blocks.p);
+        // (results straight to mapped memory: a device block + D2H copy measured 7-10 us slower)
+        route_kernel<<<1, 32 * nw, (size_t)nw * sizeof(WarpBuf) + (size_t)h->N * sizeof(Inst), st>>>(
+            P, h->rq_dev.p, h->ro_d, nsc, h->blocks.p);
         h->launches++;
         CK(h, cudaGetLastError());
         if (R0 > 0 && now_us < h->last_arrival) h->order_breaks.push_back(R0);
@@ -862,6 +864,18 @@ rsim_status rsim_route_request(rsim_t *h, int64_t now_us, int64_t input_tokens, 
     }
     CK(h, cudaStreamSynchronize(st));
     const i64 *o = h->ro_h;
+#ifdef RSIM_ROUTE_TIMING
+    if (h->route1) {            // diagnostics: route_kernel phase times (ns), averaged at destroy
+        static double acc[8] = {0};
+        static long calls = 0;
+        for (int i = 0; i < 7; i++) acc[i] += (double)(o[RO_HDR + nsc + i + 1] - o[RO_HDR + nsc + i]);
+        if (++calls % 1000 == 0) {
+            fprintf(stderr, "[route_kernel ns/phase over %ld calls] ingest %.0f load %.0f probe+score %.0f "
+                    "warpmin %.0f decide %.0f commit %.0f tail %.0f\n", calls, acc[0] / calls, acc[1] / calls,
+                    acc[2] / calls, acc[3] / calls, acc[4] / calls, acc[5] / calls, acc[6] / calls);
+        }
+    }
+#endif
     const int e[4] = {(int)o[RO_ERR0], (int)o[RO_ERR1], (int)o[RO_ERR2], (int)o[RO_ERR3]};
     if ((rs = decode_device_error(h, e)) != RSIM_OK) {
         // a refused duplicate never reaches Detector.observe (cluster.py:140-142): a track it

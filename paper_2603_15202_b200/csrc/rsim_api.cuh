@@ -87,9 +87,13 @@ route_kernel(const __grid_constant__ Params P, const i64 *__restrict__ rq, i64 *
     __shared__ u32 pcnt[RK_MAXW];
     __shared__ int dec_owner, dec_kk, dec_err;
     WarpBuf *wbuf = reinterpret_cast<WarpBuf *>(rk_smem);
+    Inst *st = reinterpret_cast<Inst *>(wbuf + (blockDim.x >> 5));   // the shard's instance records
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = blockDim.x >> 5;
     WarpBuf &WB = wbuf[warp];
     const i64 B = rq[RQ_B], R0 = rq[RQ_R0], nb0 = rq[RQ_NBLK0], no0 = rq[RQ_NOUT0], no = rq[RQ_NO];
+#ifdef RSIM_ROUTE_TIMING
+    if (threadIdx.x == 0) ro[RO_HDR + nsc + 0] = (i64)globaltimer();
+#endif
     const i64 ndup = rq[RQ_NDUP];
     const i64 *src = rq + RQ_HDR + ndup;
     if (warp == 0) {                                   // ingest (route_ingest_kernel's body)
@@ -125,7 +129,20 @@ route_kernel(const __grid_constant__ Params P, const i64 *__restrict__ rq, i64 *
         WB.c_bytes = 0; WB.c_steps = 0; WB.werr = 0; WB.fins = 0; WB.spk = -1;
         WB.fin.dnf = 0; WB.fin.npark = 0; WB.fin.tpn = 0; WB.fin.lnext = WB.fin.lend = 0;
     }
+#ifdef RSIM_ROUTE_TIMING
+    if (threadIdx.x == 0) ro[RO_HDR + nsc + 1] = (i64)globaltimer();
+#endif
+    {   // the instance records into shared memory (one coalesced pass; the snapshot flushes and the
+        // commit's read-modify-writes then cost shared-memory latency), back at the end
+        const u64 *src = reinterpret_cast<const u64 *>(P.inst);
+        u64 *dst = reinterpret_cast<u64 *>(st);
+        const int words = P.N * (int)(sizeof(Inst) / 8);
+        for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+    }
     __syncthreads();
+#ifdef RSIM_ROUTE_TIMING
+    if (threadIdx.x == 0) ro[RO_HDR + nsc + 2] = (i64)globaltimer();
+#endif
     // probe + score this warp's instances
     const int ipw = (P.N + NW - 1) / NW, l0 = warp * ipw;
     const int n = max(0, min(ipw, P.N - l0));
@@ -135,12 +152,18 @@ route_kernel(const __grid_constant__ Params P, const i64 *__restrict__ rq, i64 *
         if (n >= 2 && R.B <= 128) probe_hits_sparse(P, 0, l0, n, R, MODE_ROUTE, -1, 0u, lane, WB.hit);
         else probe_hits(P, 0, l0, n, R, MODE_ROUTE, -1, 0u, lane, WB.hit, WB.slot[0]);
         u64 bits_bs;
-        mybits = score_phase(P, P.inst, 0, l0, n, R, MODE_ROUTE, -1, lane, WB, bits_bs, false, P.bsn, false, nullptr);
+        mybits = score_phase(P, st, 0, l0, n, R, MODE_ROUTE, -1, lane, WB, bits_bs, false, P.bsn, false, nullptr);
     }
+#ifdef RSIM_ROUTE_TIMING
+    if (threadIdx.x == 0) ro[RO_HDR + nsc + 3] = (i64)globaltimer();
+#endif
     const u64 wmin = warp_min_u64(lane < n ? mybits : ~0ULL);
     tmask = __ballot_sync(FULL, lane < n && mybits == wmin && wmin != ~0ULL);
     if (lane == 0) { pmin[warp] = wmin; pcnt[warp] = (u32)__popc(tmask); }
     __syncthreads();
+#ifdef RSIM_ROUTE_TIMING
+    if (threadIdx.x == 0) ro[RO_HDR + nsc + 4] = (i64)globaltimer();
+#endif
     if (warp == 0) {                                   // argmin over the warps in instance order + tie-break
         const u64 m = lane < NW ? pmin[lane] : ~0ULL;
         const u64 g = warp_min_u64(m);
@@ -160,6 +183,9 @@ route_kernel(const __grid_constant__ Params P, const i64 *__restrict__ rq, i64 *
         if (lane == 0) { dec_owner = ow; dec_kk = (int)(kk - bef); dec_err = T ? 0 : 11; }   // 11: NoInstancesError
     }
     __syncthreads();
+#ifdef RSIM_ROUTE_TIMING
+    if (threadIdx.x == 0) ro[RO_HDR + nsc + 5] = (i64)globaltimer();
+#endif
     if (warp == dec_owner) {
         const int s = nth_set_bit_warp(tmask, dec_kk, lane);
         const int gi = l0 + s, gch = P.gbase + gi;
@@ -168,14 +194,26 @@ route_kernel(const __grid_constant__ Params P, const i64 *__restrict__ rq, i64 *
         if (ndup > 0 && ((rq[RQ_HDR + (gch >> 5)] >> (gch & 31)) & 1)) {   // holders bitmap of this call
             werr = DEV_E_DUPLICATE;                    // chosen (the counter moved), never enqueued
         } else {
-            commit(P, P.inst + gi, gi, R0, h, R.t, R.keys, nullptr, R.a, R.B, R.in, R.out, R.oa, lane, werr, WB.fin, false);
+            commit(P, st + gi, gi, R0, h, R.t, R.keys, nullptr, R.a, R.B, R.in, R.out, R.oa, lane, werr, WB.fin, false);
             flush_touch_pin(P, WB.fin, lane, &werr);
         }
         if (lane == 0 && werr) atomicCAS(P.err, 0, werr);
     }
+#ifdef RSIM_ROUTE_TIMING
+    if (threadIdx.x == 0) ro[RO_HDR + nsc + 6] = (i64)globaltimer();
+#endif
     if (lane == 0 && WB.werr) atomicCAS(P.err, 0, WB.werr);
     if (dec_err && threadIdx.x == 0) atomicCAS(P.err, 0, dec_err);
     __syncthreads();
+    {
+        u64 *dst = reinterpret_cast<u64 *>(P.inst);
+        const u64 *src = reinterpret_cast<const u64 *>(st);
+        const int words = P.N * (int)(sizeof(Inst) / 8);
+        for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+    }
+#ifdef RSIM_ROUTE_TIMING
+    if (threadIdx.x == 0) ro[RO_HDR + nsc + 7] = (i64)globaltimer();
+#endif
     __threadfence();
     if (threadIdx.x == 0) {
         ro[RO_CHOSEN] = P.chosen[R0]; ro[RO_HIT] = P.hit_tokens[R0];
