@@ -271,6 +271,35 @@ rsim_status rsim_read_detector(rsim_t *h, int64_t *rows, int64_t capacity, int64
 /* Diagnostics: 8 words per decision when RSIM_DET_DEBUG was set at rsim_load_detector. */
 rsim_status rsim_detector_debug(rsim_t *h, int64_t *out, int64_t n);
 
+/* ---- synthetic traces on the device (reference trace.py:218-268 generate_synthetic) ---- */
+/* One ClassSpec (trace.py:58-69): weight, shared_blocks, suffix_blocks = [suffix_lo, suffix_hi],
+ * output_tokens = [output_lo, output_hi] (inclusive ranges, each narrower than 2^31). */
+typedef struct {
+    double weight;
+    int64_t shared_blocks;
+    int64_t suffix_lo, suffix_hi;
+    int64_t output_lo, output_hi;
+} rsim_synth_class;
+typedef struct rsim_synth rsim_synth_t;
+/* generate_synthetic(SyntheticSpec(duration_s, mean_rate_rps, classes, seed, block_size)) on
+ * `device`, bit-identical to the reference's records (the same random.Random streams, draw
+ * order, (t, class, seq) sort and stable_key hashes; glibc's log for expovariate). Spec errors
+ * are the reference's TraceError messages (RSIM_E_TRACE). The trace stays in device memory
+ * until rsim_synth_free; *n_requests / *n_blocks size the rsim_synth_read buffers. Messages
+ * go to rsim_last_error(NULL). seed = the spec's seed mod 2^64. Replaces the reference's
+ * generate_synthetic (trace.py:218), which the Python mirror calls
+ * paper_2603_15202_b200.trace.generate_synthetic_device. */
+rsim_status rsim_synth_generate(const rsim_synth_class *classes, int32_t n_classes, double duration_s,
+                                double mean_rate_rps, uint64_t seed, int64_t block_size, int32_t device,
+                                rsim_synth_t **out, int64_t *n_requests, int64_t *n_blocks);
+/* Host copies of the PackedTrace columns (any pointer may be NULL): request_id[n], arrival_s[n],
+ * in_tokens[n], out_tokens[n], class_key[n], blk_off[n+1], blocks[n_blocks]. */
+rsim_status rsim_synth_read(const rsim_synth_t *g, uint64_t *request_id, double *arrival_s, int64_t *in_tokens,
+                            int64_t *out_tokens, uint64_t *class_key, int64_t *blk_off, uint64_t *blocks);
+/* The same seven columns' device pointers (valid until rsim_synth_free). */
+rsim_status rsim_synth_device_arrays(const rsim_synth_t *g, const void **arrays);
+void rsim_synth_free(rsim_synth_t *g);
+
 #ifdef __cplusplus
 }
 #endif

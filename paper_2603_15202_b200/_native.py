@@ -137,6 +137,10 @@ def lib():
         "rsim_unschedule": ([P], C.c_int),
         "rsim_route_request": ([P, I64, I64, I64, C.c_uint64, P, I64, P, I32, P, P, P, P], C.c_int),
         "rsim_detector_next": ([P, I32, I32, C.c_uint64, I64], C.c_int),
+        "rsim_synth_generate": ([P, I32, C.c_double, C.c_double, C.c_uint64, I64, I32, P, P, P], C.c_int),
+        "rsim_synth_read": ([P, P, P, P, P, P, P, P], C.c_int),
+        "rsim_synth_device_arrays": ([P, P], C.c_int),
+        "rsim_synth_free": ([P], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -158,7 +162,42 @@ EXPORTED = ("rsim_create", "rsim_destroy", "rsim_last_error", "rsim_reset", "rsi
             "rsim_set_peer", "rsim_open_peer_ipc", "rsim_load_detector", "rsim_detector_finalize",
             "rsim_read_detector", "rsim_detector_debug", "rsim_config_size", "rsim_check_invariants",
             "rsim_debug_corrupt", "rsim_route_one_excl", "rsim_read_slots", "rsim_unschedule",
-            "rsim_route_request", "rsim_detector_next")
+            "rsim_route_request", "rsim_detector_next", "rsim_synth_generate", "rsim_synth_read",
+            "rsim_synth_device_arrays", "rsim_synth_free")
+
+
+class SynthClass(C.Structure):
+    """rsim_synth_class (include/rsim.h): one ClassSpec (reference trace.py:58-69)."""
+    _fields_ = [("weight", C.c_double), ("shared_blocks", C.c_int64), ("suffix_lo", C.c_int64),
+                ("suffix_hi", C.c_int64), ("output_lo", C.c_int64), ("output_hi", C.c_int64)]
+
+
+def synth_generate(spec, device: int = 0):
+    """generate_synthetic(spec) on the GPU (rsim_synth_generate): the PackedTrace columns as
+    host arrays (request_id, arrival_s, in_tokens, out_tokens, class_key, blk_off, blocks)."""
+    L = lib()
+    n_cls = len(spec.classes)
+    arr = (SynthClass * max(n_cls, 1))()
+    for i, c in enumerate(spec.classes):
+        arr[i] = SynthClass(float(c.weight), int(c.shared_blocks), int(c.suffix_blocks[0]), int(c.suffix_blocks[1]),
+                            int(c.output_tokens[0]), int(c.output_tokens[1]))
+    g, n, nb = C.c_void_p(), C.c_int64(), C.c_int64()
+    st = L.rsim_synth_generate(C.cast(arr, C.c_void_p), n_cls, float(spec.duration_s), float(spec.mean_rate_rps),
+                               int(spec.seed) & ((1 << 64) - 1), int(spec.block_size), device, C.byref(g),
+                               C.byref(n), C.byref(nb))
+    if st != RSIM_OK:
+        msg = L.rsim_last_error(None).decode()
+        raise _EXC[st](msg) if st in _EXC else RsimError(st, msg)
+    try:
+        n, nb = n.value, nb.value
+        cols = (np.empty(n, np.uint64), np.empty(n, np.float64), np.empty(n, np.int64), np.empty(n, np.int64),
+                np.empty(n, np.uint64), np.empty(n + 1, np.int64), np.empty(nb, np.uint64))
+        st = L.rsim_synth_read(g, *[c.ctypes.data_as(C.c_void_p) for c in cols])
+        if st != RSIM_OK:
+            raise RsimError(st, L.rsim_last_error(None).decode())
+        return cols
+    finally:
+        L.rsim_synth_free(g)
 
 
 def _p(a):

@@ -26,6 +26,9 @@
 #endif
 #include "rsim_check.cuh"
 #include "rsim_api.cuh"
+#include "rsim_synth.cuh"
+#include <cub/device/device_scan.cuh>
+#include <cmath>
 
 namespace {
 
@@ -1389,5 +1392,173 @@ rsim_status rsim_read_detector(rsim_t *h, int64_t *rows, int64_t capacity, int64
 rsim_status rsim_detector_debug(rsim_t *h, int64_t *out, int64_t n) {
     if (!h || !h->ddbg.p) return RSIM_E_INVALID;
     CK(h, cudaMemcpy(out, h->ddbg.p, (size_t)std::min<i64>(n, h->R) * (8 + h->N) * sizeof(i64), cudaMemcpyDeviceToHost));
+    return RSIM_OK;
+}
+
+// ---------------------------------------------------------------- generate_synthetic
+// The reference's trace generator (trace.py:218-268) on the device: rsim_synth.cuh.
+struct rsim_synth {
+    int device = 0;
+    i64 n = 0, nb = 0;
+    double *arrival = nullptr;
+    u64 *rid = nullptr, *ckey = nullptr, *blocks = nullptr;
+    i64 *in_tok = nullptr, *out_tok = nullptr, *blk_off = nullptr;
+};
+
+static rsim_status synth_fail(rsim_status st, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_create_err, sizeof(g_create_err), fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+void rsim_synth_free(rsim_synth_t *g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    for (void *p : {(void *)g->arrival, (void *)g->rid, (void *)g->ckey, (void *)g->blocks, (void *)g->in_tok,
+                    (void *)g->out_tok, (void *)g->blk_off})
+        if (p) cudaFree(p);
+    delete g;
+}
+
+rsim_status rsim_synth_generate(const rsim_synth_class *classes, int32_t n_classes, double duration_s,
+                                double mean_rate_rps, uint64_t seed, int64_t block_size, int32_t device,
+                                rsim_synth_t **out, int64_t *n_requests, int64_t *n_blocks) {
+    if (!out || !classes) return synth_fail(RSIM_E_INVALID, "null argument");
+    *out = nullptr;
+    // SyntheticSpec.validate (trace.py:86-100)
+    if (!(duration_s > 0) || !(mean_rate_rps > 0) || block_size < 1)
+        return synth_fail(RSIM_E_TRACE, "duration, rate, and block size must be positive");
+    if (n_classes < 1) return synth_fail(RSIM_E_TRACE, "at least one request class is required");
+    double total = 0.0;
+    for (int c = 0; c < n_classes; c++) total += classes[c].weight;
+    if (std::fabs(total - 1.0) > 1e-9) return synth_fail(RSIM_E_TRACE, "class weights must sum to 1.0, got %.17g", total);
+    std::vector<SynClass> hc(n_classes);
+    for (int c = 0; c < n_classes; c++) {
+        const rsim_synth_class &k = classes[c];
+        if (!(k.weight > 0)) return synth_fail(RSIM_E_TRACE, "class weights must be positive");
+        if (k.shared_blocks < 0 || k.suffix_lo < 0) return synth_fail(RSIM_E_TRACE, "block counts must be non-negative");
+        if (k.shared_blocks + k.suffix_lo < 1) return synth_fail(RSIM_E_TRACE, "each request needs at least one block");
+        if (k.suffix_lo > k.suffix_hi) return synth_fail(RSIM_E_TRACE, "suffix_blocks range is inverted");
+        if (k.output_lo < 1 || k.output_lo > k.output_hi)
+            return synth_fail(RSIM_E_TRACE, "output_tokens range must be >= 1 and ordered");
+        if (k.suffix_hi - k.suffix_lo >= (1ll << 31) || k.output_hi - k.output_lo >= (1ll << 31) ||
+            k.shared_blocks + k.suffix_hi >= (1ll << 31) || k.output_hi >= (1ll << 31))
+            return synth_fail(RSIM_E_UNSUPPORTED, "size ranges wider than 2^31 are not generated on the device");
+        hc[c] = SynClass{k.weight * mean_rate_rps, k.shared_blocks, k.suffix_lo, k.suffix_hi, k.output_lo, k.output_hi};
+    }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return synth_fail(RSIM_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    rsim_synth_t *g = new rsim_synth_t();
+    g->device = device;
+    SynClass *dcls = nullptr;
+    i64 *dtoff = nullptr, *dcount = nullptr, *dcoff = nullptr, *row_seq = nullptr, *row_len = nullptr;
+    int *nsuf = nullptr, *nout = nullptr, *row_cls = nullptr;
+    double *times = nullptr;
+    void *tmp = nullptr;
+    cudaStream_t s = nullptr;
+    rsim_status st = RSIM_OK;
+    std::vector<i64> toff(n_classes + 1, 0), cnt(n_classes, 0), coff(n_classes + 1, 0);
+#define SY(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t _e = (call);                                                                   \
+        if (_e != cudaSuccess) { st = synth_fail(RSIM_E_CUDA, "%s: %s", #call, cudaGetErrorString(_e)); goto done; } \
+    } while (0)
+    SY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    SY(cudaMalloc(&dcls, n_classes * sizeof(SynClass)));
+    SY(cudaMemcpyAsync(dcls, hc.data(), n_classes * sizeof(SynClass), cudaMemcpyHostToDevice, s));
+    SY(cudaMalloc(&dtoff, (n_classes + 1) * sizeof(i64)));
+    SY(cudaMalloc(&dcoff, (n_classes + 1) * sizeof(i64)));
+    SY(cudaMalloc(&dcount, n_classes * sizeof(i64)));
+    for (int c = 0; c < n_classes; c++) {      // Poisson(rate * duration) + 12 sigma; a rerun if short
+        const double lam = hc[c].rate * duration_s;
+        toff[c + 1] = toff[c] + (i64)std::ceil(lam + 12.0 * std::sqrt(lam) + 64.0);
+    }
+    for (int pass = 0; pass < 2; pass++) {
+        if (times) { cudaFree(times); times = nullptr; }
+        SY(cudaMalloc(&times, std::max<i64>(toff[n_classes], 1) * sizeof(double)));
+        SY(cudaMemcpyAsync(dtoff, toff.data(), (n_classes + 1) * sizeof(i64), cudaMemcpyHostToDevice, s));
+        synth_arrivals_kernel<<<n_classes, 32, 0, s>>>(dcls, seed, duration_s, dtoff, times, dcount);
+        SY(cudaGetLastError());
+        SY(cudaMemcpyAsync(cnt.data(), dcount, n_classes * sizeof(i64), cudaMemcpyDeviceToHost, s));
+        SY(cudaStreamSynchronize(s));
+        bool fits = true;
+        for (int c = 0; c < n_classes; c++) fits &= cnt[c] <= toff[c + 1] - toff[c];
+        if (fits) break;
+        for (int c = 0; c < n_classes; c++) toff[c + 1] = toff[c] + cnt[c];
+    }
+    for (int c = 0; c < n_classes; c++) coff[c + 1] = coff[c] + cnt[c];
+    g->n = coff[n_classes];
+    {
+        const i64 n = g->n, n1 = std::max<i64>(n, 1);
+        SY(cudaMemcpyAsync(dcoff, coff.data(), (n_classes + 1) * sizeof(i64), cudaMemcpyHostToDevice, s));
+        SY(cudaMalloc(&nsuf, n1 * sizeof(int)));
+        SY(cudaMalloc(&nout, n1 * sizeof(int)));
+        SY(cudaMalloc(&row_cls, n1 * sizeof(int)));
+        SY(cudaMalloc(&row_seq, n1 * sizeof(i64)));
+        SY(cudaMalloc(&row_len, n1 * sizeof(i64)));
+        SY(cudaMalloc(&g->arrival, n1 * sizeof(double)));
+        SY(cudaMalloc(&g->out_tok, n1 * sizeof(i64)));
+        SY(cudaMalloc(&g->in_tok, n1 * sizeof(i64)));
+        SY(cudaMalloc(&g->rid, n1 * sizeof(u64)));
+        SY(cudaMalloc(&g->ckey, n1 * sizeof(u64)));
+        SY(cudaMalloc(&g->blk_off, (n + 1) * sizeof(i64)));
+        SY(cudaMemsetAsync(g->blk_off, 0, sizeof(i64), s));
+        if (n > 0) {
+            synth_sizes_kernel<<<n_classes, 32, 0, s>>>(dcls, seed, dcoff, nsuf, nout);
+            SY(cudaGetLastError());
+            synth_order_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dcls, n_classes, dtoff, dcoff, times, nsuf,
+                                                                          nout, n, g->arrival, row_cls, row_seq,
+                                                                          row_len, g->out_tok);
+            SY(cudaGetLastError());
+            size_t tb = 0;
+            SY(cub::DeviceScan::InclusiveSum(nullptr, tb, row_len, g->blk_off + 1, (int)n, s));
+            SY(cudaMalloc(&tmp, tb));
+            SY(cub::DeviceScan::InclusiveSum(tmp, tb, row_len, g->blk_off + 1, (int)n, s));
+        }
+        SY(cudaMemcpyAsync(&g->nb, g->blk_off + n, sizeof(i64), cudaMemcpyDeviceToHost, s));
+        SY(cudaStreamSynchronize(s));
+        SY(cudaMalloc(&g->blocks, std::max<i64>(g->nb, 1) * sizeof(u64)));
+        if (n > 0) {
+            synth_blocks_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(dcls, seed, n, block_size, row_cls, row_seq,
+                                                                       g->blk_off, g->blocks, g->rid, g->in_tok,
+                                                                       g->ckey);
+            SY(cudaGetLastError());
+        }
+        SY(cudaStreamSynchronize(s));
+    }
+#undef SY
+done:
+    for (void *p : {(void *)dcls, (void *)dtoff, (void *)dcount, (void *)dcoff, (void *)row_seq, (void *)row_len,
+                    (void *)nsuf, (void *)nout, (void *)row_cls, (void *)times, tmp})
+        if (p) cudaFree(p);
+    if (s) cudaStreamDestroy(s);
+    if (st != RSIM_OK) { rsim_synth_free(g); return st; }
+    *out = g;
+    if (n_requests) *n_requests = g->n;
+    if (n_blocks) *n_blocks = g->nb;
+    return RSIM_OK;
+}
+
+rsim_status rsim_synth_read(const rsim_synth_t *g, uint64_t *request_id, double *arrival_s, int64_t *in_tokens,
+                            int64_t *out_tokens, uint64_t *class_key, int64_t *blk_off, uint64_t *blocks) {
+    if (!g) return synth_fail(RSIM_E_INVALID, "null generator");
+    cudaError_t e = cudaSetDevice(g->device);
+    const size_t n = (size_t)g->n;
+    struct { void *dst; const void *src; size_t bytes; } cp[] = {
+        {request_id, g->rid, n * 8}, {arrival_s, g->arrival, n * 8}, {in_tokens, g->in_tok, n * 8},
+        {out_tokens, g->out_tok, n * 8}, {class_key, g->ckey, n * 8}, {blk_off, g->blk_off, (n + 1) * 8},
+        {blocks, g->blocks, (size_t)g->nb * 8}};
+    for (auto &c : cp)
+        if (e == cudaSuccess && c.dst && c.bytes) e = cudaMemcpy(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return synth_fail(RSIM_E_CUDA, "rsim_synth_read: %s", cudaGetErrorString(e));
+    return RSIM_OK;
+}
+
+rsim_status rsim_synth_device_arrays(const rsim_synth_t *g, const void **arrays) {
+    if (!g || !arrays) return synth_fail(RSIM_E_INVALID, "null argument");
+    const void *a[7] = {g->rid, g->arrival, g->in_tok, g->out_tok, g->ckey, g->blk_off, g->blocks};
+    for (int i = 0; i < 7; i++) arrays[i] = a[i];
     return RSIM_OK;
 }

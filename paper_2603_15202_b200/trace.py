@@ -440,5 +440,15 @@ def generate_synthetic_packed(spec: SyntheticSpec) -> PackedTrace:
                        np.asarray(ck, dtype=np.uint64).reshape(n), off, blocks)
 
 
+def generate_synthetic_device(spec: SyntheticSpec, device: int = 0) -> PackedTrace:
+    """generate_synthetic on the GPU (librsim rsim_synth_generate, csrc/rsim_synth.cuh):
+    the same trace as generate_synthetic_packed, bit for bit, in milliseconds instead of
+    seconds at 1M requests. Raises TraceError for an invalid spec, like the reference."""
+    spec.validate()
+    from . import _native
+    rid, t, inp, out, ck, off, blocks = _native.synth_generate(spec, device)
+    return PackedTrace(rid, t, inp, out, ck, off, blocks)
+
+
 def generate_synthetic(spec: SyntheticSpec) -> list[TraceRecord]:
     return generate_synthetic_packed(spec).records()
