@@ -639,6 +639,8 @@ def main():
     ndev = torch.cuda.device_count()
     dev_index = local % max(ndev, 1)                 # ranks share a GPU only when fewer GPUs than ranks
     torch.cuda.set_device(dev_index)
+    from paper_2603_15202_b200 import workloads as W
+    W.use_device_generator(dev_index)                # synthetic traces built on the GPU (bit-identical)
     pg, backend = None, None
     if world > 1:
         import torch.distributed as dist

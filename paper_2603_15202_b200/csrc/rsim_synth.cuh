@@ -19,8 +19,8 @@
 //   synth_arrivals_kernel  one warp per class: the warp twists MT19937 624 words at a time,
 //                          lanes turn word pairs into gaps (glibc_log), lane 0 folds the
 //                          gaps in order (the float sum is sequential by definition)
-//   synth_sizes_kernel     one warp per class: twisted + tempered words in SMEM, lane 0 runs
-//                          the rejection sampler for the class's requests in seq order
+//   synth_sizes_kernel     one warp per class: the rejection sampler over the class's stream,
+//                          32 words per step by a scan of its two-state machine
 //   synth_order_kernel     thread per arrival: rank in the (t, ci, seq) order by binary
 //                          search in the other classes' sorted times; scatters the rows
 //   (cub inclusive scan of block counts -> blk_off)
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(32)
 synth_arrivals_kernel(const SynClass *__restrict__ cls, u64 seed, double duration,
                       const i64 *__restrict__ toff, double *__restrict__ times, i64 *__restrict__ count) {
     __shared__ u32 mt[MT_N];
-    __shared__ double gap[MT_N / 2];
+    __shared__ double gap[MT_N / 2], tsum[MT_N / 2];
     const int c = blockIdx.x, lane = threadIdx.x;
     if (lane == 0) mt_seed(mt, syn_key(syn_key(syn_key(RSIM_GOLDEN, seed), SYN_RNG_SALT), (u64)c));
     __syncwarp();
@@ -115,14 +115,21 @@ synth_arrivals_kernel(const SynClass *__restrict__ cls, u64 seed, double duratio
             gap[j] = __ddiv_rn(-glibc_log(__dsub_rn(1.0, u), g_log_tab), rate);
         }
         __syncwarp();
-        if (lane == 0) {
-            for (int j = 0; j < MT_N / 2; j++) {
-                t = first ? gap[j] : __dadd_rn(t, gap[j]);
-                first = false;
-                if (!(t < duration)) { done = true; break; }
-                if (n < cap) out[n] = t;
-                n++;
-            }
+        if (lane == 0) {                 // the float sum is sequential by definition: lane 0
+            int j0 = 0;                  // runs only the add chain (loads are independent of t)
+            if (first) { t = gap[0]; tsum[0] = t; j0 = 1; first = false; }
+            #pragma unroll 8
+            for (int j = j0; j < MT_N / 2; j++) { t = __dadd_rn(t, gap[j]); tsum[j] = t; }
+        }
+        __syncwarp();
+        for (int base = 0; base < MT_N / 2; base += 32) {   // keep the prefix below duration
+            const int j = base + lane;
+            const bool in = j < MT_N / 2;
+            const u32 bad = __ballot_sync(FULL, in && !(tsum[in ? j : 0] < duration));
+            const int m = bad ? __ffs(bad) - 1 : min(32, MT_N / 2 - base);   // valid: [0, m)
+            if (lane < m && n + lane < cap) out[n + lane] = tsum[j];
+            n += m;
+            if (bad) { done = true; break; }
         }
         done = __shfl_sync(FULL, done, 0);
     }
@@ -133,35 +140,53 @@ synth_arrivals_kernel(const SynClass *__restrict__ cls, u64 seed, double duratio
 __device__ __forceinline__ int syn_bitlen(u64 n) { return 64 - __clzll((long long)n); }
 
 // nsuf / nout[coff[c] + seq]: the class's size draws in seq (= arrival) order; coff is the
-// exclusive prefix of the classes' arrival counts.
+// exclusive prefix of the classes' arrival counts. The sampler is a two-state machine over the
+// stream's words (state 0: the suffix draw of the next request, 1: its output draw; a word
+// below the state's bound is accepted and flips the state, one above is redrawn). Each word is
+// a map {0,1} -> {0,1}; maps compose associatively, so a warp takes 32 words at once: a
+// shuffle scan of the maps gives every lane its entry state, a ballot numbers the accepted
+// draws, and accepted lanes write their draw in parallel.
 __global__ void __launch_bounds__(32)
 synth_sizes_kernel(const SynClass *__restrict__ cls, u64 seed, const i64 *__restrict__ coff,
                    int *__restrict__ nsuf, int *__restrict__ nout) {
     __shared__ u32 mt[MT_N];
-    __shared__ u32 w[MT_N];
     const int c = blockIdx.x, lane = threadIdx.x;
     if (lane == 0) mt_seed(mt, syn_key(syn_key(syn_key(syn_key(RSIM_GOLDEN, seed), SYN_RNG_SALT), (u64)c), 1ull));
     __syncwarp();
     const SynClass C = cls[c];
     const u64 ns = (u64)(C.suf_hi - C.suf_lo) + 1, no = (u64)(C.out_hi - C.out_lo) + 1;
     const int ks = syn_bitlen(ns), ko = syn_bitlen(no);
-    const i64 total = coff[c + 1] - coff[c];
-    i64 r = 0;
-    int which = 0;                     // 0: the suffix draw of request r, 1: its output draw
-    while (r < total) {
+    const i64 need = 2 * (coff[c + 1] - coff[c]);   // draws
+    int *suf = nsuf + coff[c], *outp = nout + coff[c];
+    i64 d = 0;                                      // draws accepted so far (state = d & 1)
+    while (d < need) {
         mt_twist(mt, lane);
-        for (int j = lane; j < MT_N; j += 32) w[j] = mt_temper(mt[j]);
-        __syncwarp();
-        if (lane == 0) {
-            for (int j = 0; j < MT_N && r < total; j++) {
-                const u32 v = w[j] >> (32 - (which ? ko : ks));
-                if ((u64)v >= (which ? no : ns)) continue;            // _randbelow redraw
-                if (which == 0) { nsuf[coff[c] + r] = (int)(C.suf_lo + v); which = 1; }
-                else { nout[coff[c] + r] = (int)(C.out_lo + v); which = 0; r++; }
+        for (int base = 0; base < MT_N && d < need; base += 32) {
+            const int j = base + lane;
+            const u32 w = j < MT_N ? mt_temper(mt[j]) : 0u;
+            const u32 v0 = w >> (32 - ks), v1 = w >> (32 - ko);
+            const bool a0 = j < MT_N && (u64)v0 < ns, a1 = j < MT_N && (u64)v1 < no;
+            // map as 2 bits: bit s = image of state s
+            u32 f = (a0 ? 1u : 0u) | ((a1 ? 0u : 1u) << 1);
+            u32 pre = f;                            // inclusive scan: pre = f_lane o ... o f_0
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 g = __shfl_up_sync(FULL, pre, o);
+                if (lane >= o) pre = ((pre >> ((g >> 0) & 1)) & 1) | (((pre >> ((g >> 1) & 1)) & 1) << 1);
             }
+            u32 ex = __shfl_up_sync(FULL, pre, 1);  // exclusive: maps of the lanes before
+            if (lane == 0) ex = 2u;                 // identity: 0 -> 0, 1 -> 1
+            const int s0 = (int)(d & 1);
+            const int st = (int)((ex >> s0) & 1);   // this lane's entry state
+            const bool acc = st ? a1 : a0;
+            const u32 ball = __ballot_sync(FULL, acc);
+            const i64 di = d + __popc(ball & ((1u << lane) - 1u));
+            if (acc && di < need) {
+                if (st == 0) suf[di >> 1] = (int)(C.suf_lo + v0);
+                else outp[di >> 1] = (int)(C.out_lo + v1);
+            }
+            d += __popc(ball);
         }
-        r = __shfl_sync(FULL, r, 0);
-        which = __shfl_sync(FULL, which, 0);
     }
 }
 

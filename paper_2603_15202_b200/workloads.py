@@ -17,6 +17,15 @@ from .trace import (CLASS_SALT, ClassSpec, PackedTrace, SyntheticSpec, concat_pa
                     generate_synthetic_packed)
 
 OUTPUT_SALT = 0x0F_0C0DE  # reference engine.py:34
+_generate = generate_synthetic_packed
+
+
+def use_device_generator(device: int = 0) -> None:
+    """Build the synthetic workloads with the GPU generator (trace.generate_synthetic_device,
+    bit-identical to the host one) -- bench.py's setup; tests keep the host generator."""
+    global _generate
+    from .trace import generate_synthetic_device
+    _generate = lambda spec: generate_synthetic_device(spec, device)  # noqa: E731
 CHAT_CLASSES = tuple(ClassSpec(1 / 8, 8 + 4 * i, (2, 12), (16, 128)) for i in range(8))
 
 
@@ -27,7 +36,7 @@ def chat_spec(n_requests: float, rate_rps: float, seed: int = 0) -> SyntheticSpe
 
 def config1_chatbot(seed: int = 0):
     """16 instances, ~10k requests at 48 req/s (SURVEY cfg 1)."""
-    trace = generate_synthetic_packed(chat_spec(10000, 48.0, seed))
+    trace = _generate(chat_spec(10000, 48.0, seed))
     return trace, ClusterConfig(n_instances=16, cache=CacheConfig(16, 40000), seed=0)
 
 
@@ -36,14 +45,14 @@ def config2_api(n_requests: int = 100_000, seed: int = 1):
     spec = SyntheticSpec(duration_s=n_requests / 384.0, mean_rate_rps=384.0,
                          classes=tuple(ClassSpec(1 / 32, 64, (1, 4), (8, 64)) for _ in range(32)),
                          seed=seed)
-    return generate_synthetic_packed(spec), ClusterConfig(n_instances=64,
+    return _generate(spec), ClusterConfig(n_instances=64,
                                                           cache=CacheConfig(16, 40000), seed=0)
 
 
 def chat_cluster(n_instances: int, n_requests: int, per_instance_rps: float = 3.0, seed: int = 0):
     """Chat class mix at ``per_instance_rps`` per instance (SURVEY cfg 4 / 1024-instance target)."""
     rate = per_instance_rps * n_instances
-    trace = generate_synthetic_packed(chat_spec(n_requests, rate, seed))
+    trace = _generate(chat_spec(n_requests, rate, seed))
     return trace, ClusterConfig(n_instances=n_instances, cache=CacheConfig(16, 40000), seed=0)
 
 
@@ -56,7 +65,7 @@ def hotspot(n_instances: int = 16, n_requests: int = 3000, hot_fraction: float =
     classes = (ClassSpec(hot_fraction, 16, (1, 3), (16, 96)),) + tuple(
         ClassSpec(cold, 8, (1, 4), (16, 64)) for _ in range(n_cold))
     spec = SyntheticSpec(duration_s=n_requests / rate_rps, mean_rate_rps=rate_rps, classes=classes, seed=seed)
-    return generate_synthetic_packed(spec), ClusterConfig(n_instances=n_instances, cache=CacheConfig(16, 40000),
+    return _generate(spec), ClusterConfig(n_instances=n_instances, cache=CacheConfig(16, 40000),
                                                           seed=seed)
 
 

@@ -24,11 +24,23 @@ def main():
     spec = W.chat_spec(1_000_000, 12288.0, 0)
     generate_synthetic_device(W.chat_spec(1000, 48.0, 0))          # context + module load
     dev, a = best(lambda: generate_synthetic_device(spec), 5)
+    import ctypes as C
+    from paper_2603_15202_b200 import _native
+    L = _native.lib()
+    arr = (_native.SynthClass * len(spec.classes))(*[_native.SynthClass(c.weight, c.shared_blocks, *c.suffix_blocks,
+                                                                         *c.output_tokens) for c in spec.classes])
+
+    def gen_only():
+        g = C.c_void_p()
+        assert L.rsim_synth_generate(C.cast(arr, C.c_void_p), len(spec.classes), spec.duration_s,
+                                     spec.mean_rate_rps, spec.seed, spec.block_size, 0, C.byref(g), None, None) == 0
+        L.rsim_synth_free(g)
+    gen, _ = best(gen_only, 5)
     host, b = best(lambda: generate_synthetic_packed(spec), 1)
     same = all((getattr(a, c).view("u8") == getattr(b, c).view("u8")).all() for c in
                ("request_id", "arrival_s", "in_tokens", "out_tokens", "class_key", "blk_off", "blocks"))
     print(json.dumps({"spec": "config4 chat mix, 1M requests", "n": len(a), "n_blocks": int(a.blk_off[-1]),
-                      "device_s": round(dev, 4), "host_numpy_s": round(host, 3), "identical": bool(same)}))
+                      "device_s": round(dev, 4), "device_generate_only_s": round(gen, 4), "host_numpy_s": round(host, 3), "identical": bool(same)}))
 
 
 if __name__ == "__main__":
