@@ -80,3 +80,22 @@ def test_binding_reproduces_reference(name):
     got = ns["run_on_gpu"](list(trace.records()), cfg)
     assert np.array_equal(np.array([c for c, _ in got]), want["chosen"])
     assert np.array_equal(np.array([h for _, h in got]), want["hit_tokens"])
+
+
+@pytest.mark.gpu
+def test_binding_generates_reference_trace():
+    """The binding's generate_synthetic_on_gpu returns the reference generator's records
+    (fingerprints in tests/golden/synth_golden.json)."""
+    import hashlib
+    import json
+    from paper_2603_15202_b200.trace import ClassSpec, PackedTrace, SyntheticSpec, TraceRecord
+    ns = _binding()
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "synth_golden.json")))
+    for name in ("chat_cfg1", "rejection_ranges", "seed_negative"):
+        dur, rate, classes, seed, bs = eval(gold[name]["spec"])
+        spec = SyntheticSpec(dur, rate, tuple(ClassSpec(*c) for c in classes), seed=seed, block_size=bs)
+        recs = ns["generate_synthetic_on_gpu"](spec, record=TraceRecord)
+        tr = PackedTrace.from_records(recs)
+        assert len(recs) == gold[name]["n"]
+        for col, want in gold[name]["sha256"].items():
+            assert hashlib.sha256(np.ascontiguousarray(getattr(tr, col)).tobytes()).hexdigest() == want, (name, col)
