@@ -314,9 +314,13 @@ class Handle:
                       holders=(), want_scores: bool = True):
         """ClusterSim.route of a request not loaded yet: rsim_route_request appends it to the device
         trace and decides it in one call. ``blocks``: u64 array (or sequence) of its block hashes."""
-        b = blocks if isinstance(blocks, np.ndarray) and blocks.dtype == np.uint64 else \
-            np.fromiter((x & 0xFFFFFFFFFFFFFFFF for x in blocks), np.uint64)
-        b = np.ascontiguousarray(b)
+        if isinstance(blocks, np.ndarray) and blocks.dtype == np.uint64:
+            b = np.ascontiguousarray(blocks)
+        else:
+            try:                                  # hashes already in [0, 2^64)
+                b = np.array(blocks, dtype=np.uint64)
+            except (OverflowError, TypeError, ValueError):
+                b = np.fromiter((x & 0xFFFFFFFFFFFFFFFF for x in blocks), np.uint64)
         out = self._rr_out
         sc = np.empty(self.n_local, np.float64) if want_scores else None
         hd = np.asarray(sorted(holders), np.int32) if holders else None

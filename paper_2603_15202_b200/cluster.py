@@ -34,6 +34,19 @@ _POLICY = {"multiplicative": 0, "vllm": 1, "least_bs": 2, "linear": 3, "filter":
 INT64_MAX = (1 << 63) - 1
 
 
+
+def _scores_dict(scores: np.ndarray, skip_nan: bool) -> dict:
+    """RoutingDecision.scores (policies.py:84-89) from the device's score buffer: the C helper
+    _rsimpy (csrc/rsim_py.c, built by __graft_entry__.build) when present."""
+    try:
+        from ._rsimpy import scores_dict
+    except ImportError:
+        if skip_nan:
+            return {i: s for i, s in enumerate(scores.tolist()) if s == s}
+        return dict(enumerate(scores.tolist()))
+    s = np.ascontiguousarray(scores, dtype=np.float64)
+    return scores_dict(s.ctypes.data, s.shape[0], skip_nan)
+
 def _next_pow2_log2(v: int) -> int:
     return max(0, int(v - 1).bit_length())
 
@@ -636,9 +649,9 @@ class ClusterSim:
             kind = "least_bs"
         if branch in (2, 4):                      # holders excluded: scores over the kept candidates only
             excl = np.isnan(scores)
-            return RoutingDecision(chosen=chosen, scores={i: s for i, s in enumerate(scores.tolist()) if not excl[i]},
+            return RoutingDecision(chosen=chosen, scores=_scores_dict(scores, True),
                                    filtered=frozenset(np.flatnonzero(excl).tolist()), kind=kind, time_us=now_us)
-        return RoutingDecision(chosen=chosen, scores=dict(enumerate(scores.tolist())),
+        return RoutingDecision(chosen=chosen, scores=_scores_dict(scores, False),
                                filtered=frozenset(), kind=kind, time_us=now_us)
 
     def _det_class(self, record: TraceRecord, now_us: int):
