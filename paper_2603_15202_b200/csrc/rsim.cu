@@ -1481,8 +1481,8 @@ rsim_status rsim_synth_generate(const rsim_synth_class *classes, int32_t n_class
     SY(cudaMallocAsync(&dcount, n_classes * sizeof(i64), s));
     for (int c = 0; c < n_classes; c++) {      // Poisson(rate * duration) + 12 sigma; a rerun if short
         const double lam = hc[c].rate * duration_s;
-        toff[c + 1] = toff[c] + (i64)std::ceil(lam + 12.0 * std::sqrt(lam) + 64.0);
-    }
+        toff[c + 1] = toff[c] + (getenv("RSIM_SYNTH_TIGHT") ? 1 : (i64)std::ceil(lam + 12.0 * std::sqrt(lam) + 64.0));
+    }                                          // (RSIM_SYNTH_TIGHT: tests force the rerun pass)
     for (int pass = 0; pass < 2; pass++) {
         if (times) { cudaFreeAsync(times, s); times = nullptr; }
         SY(cudaMallocAsync(&times, std::max<i64>(toff[n_classes], 1) * sizeof(double), s));

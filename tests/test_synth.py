@@ -102,3 +102,13 @@ def test_device_generator_spec_errors():
     g = C.c_void_p()
     st = L.rsim_synth_generate(C.cast(arr, C.c_void_p), 1, 10.0, 1.0, 0, 16, 0, C.byref(g), None, None)
     assert st == _native.E_TRACE and b"at least one block" in L.rsim_last_error(None)
+
+
+@pytest.mark.gpu
+def test_device_generator_rerun_when_arrivals_overflow(monkeypatch):
+    """Arrival buffers sized one per class (RSIM_SYNTH_TIGHT) overflow: the generator counts,
+    reruns the arrival pass with exact room, and still matches the reference."""
+    from paper_2603_15202_b200.trace import generate_synthetic_device
+    monkeypatch.setenv("RSIM_SYNTH_TIGHT", "1")
+    for name in ("chat_cfg1", "many_classes", "sparse_short"):
+        _check(generate_synthetic_device(_spec(name)), name)
