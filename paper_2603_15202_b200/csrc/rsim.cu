@@ -22,7 +22,10 @@
 #define RSIM_CENTRAL 1
 #endif
 #ifndef RSIM_TABLE_BUDGET
-#define RSIM_TABLE_BUDGET (256ull << 20)   // all N tables: keep chat1024's inside L2-friendly sizes
+#define RSIM_TABLE_BUDGET (256ull << 20)   // all N tables at load <= 3/32 only within this (L2-friendly)
+#endif
+#ifndef RSIM_TABLE_MAX
+#define RSIM_TABLE_MAX (8ull << 30)        // load <= 3/16 up to this much HBM, else down to <= 3/8
 #endif
 #include "rsim_check.cuh"
 #include "rsim_api.cuh"
@@ -400,14 +403,21 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
         i64 expect = c.expected_keys > 0 ? c.expected_keys : 3000;   // callers size from the trace
         // A low load factor keeps nearly every lookup inside the aligned 16-B slot pair at its
         // home (linear probing: a miss at load a scans ~(1 + 1/(1-a)^2)/2 slots). Load <= 3/32
-        // while the N tables (24 B per slot) stay within RSIM_TABLE_BUDGET, else down to <= 3/8
+        // while the N tables (24 B per slot) stay within RSIM_TABLE_BUDGET, else <= 3/16
         // (A/B on one B200, us/decision at load <= 3/4, 3/8, 3/16, 3/32: api64 6.05 / 5.20 /
         // 4.95 / 4.88; chat1024 7.07 / 6.80 / 6.71 / 6.82 -- but 3.2x the algorithmic DRAM bytes
         // at 3/32 (805 MB of tables); agent256 - / 19.1 / 18.4 / 18.3; large4096 12.7 / 12.2 /
         // 12.9 / 13.4).
+        // Below 3/16 only when even that needs more than RSIM_TABLE_MAX (large4096, 1M requests:
+        // 15.97 us/decision at load <= 3/8 in 400 MB of tables, 14.72 at <= 3/16 in 1.6 GB).
         int mult = 32;
         sl = ilog2_ceil(expect * mult / 3 + 64);
-        while (mult > RSIM_SLOT_MULT && ((size_t)N << sl) * 24 > (size_t)RSIM_TABLE_BUDGET) {
+        auto tab_bytes = [&] { return ((size_t)N << sl) * 24; };
+        while (mult > 16 && tab_bytes() > (size_t)RSIM_TABLE_BUDGET) {
+            mult /= 2;
+            sl = ilog2_ceil(expect * mult / 3 + 64);
+        }
+        while (mult > RSIM_SLOT_MULT && tab_bytes() > (size_t)RSIM_TABLE_MAX) {
             mult /= 2;
             sl = ilog2_ceil(expect * mult / 3 + 64);
         }
