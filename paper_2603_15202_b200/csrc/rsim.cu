@@ -403,21 +403,27 @@ rsim_status rsim_create(const rsim_config *cfg, rsim_t **out) {
         i64 expect = c.expected_keys > 0 ? c.expected_keys : 3000;   // callers size from the trace
         // A low load factor keeps nearly every lookup inside the aligned 16-B slot pair at its
         // home (linear probing: a miss at load a scans ~(1 + 1/(1-a)^2)/2 slots). Load <= 3/32
-        // while the N tables (24 B per slot) stay within RSIM_TABLE_BUDGET, else <= 3/16
+        // while the N tables (24 B per slot) stay within RSIM_TABLE_BUDGET, else <= 3/8
         // (A/B on one B200, us/decision at load <= 3/4, 3/8, 3/16, 3/32: api64 6.05 / 5.20 /
         // 4.95 / 4.88; chat1024 7.07 / 6.80 / 6.71 / 6.82 -- but 3.2x the algorithmic DRAM bytes
         // at 3/32 (805 MB of tables); agent256 - / 19.1 / 18.4 / 18.3; large4096 12.7 / 12.2 /
         // 12.9 / 13.4).
-        // Below 3/16 only when even that needs more than RSIM_TABLE_MAX (large4096, 1M requests:
-        // 15.97 us/decision at load <= 3/8 in 400 MB of tables, 14.72 at <= 3/16 in 1.6 GB).
+        // Shards of more than 2048 instances keep 3/16 while the tables fit RSIM_TABLE_MAX and
+        // 1 MB per instance (large4096, 1M requests: 15.97 us/decision at load <= 3/8 in 400 MB
+        // of tables, 15.12 at <= 3/16 in 3.2 GB). Smaller shards go to 3/8: chat1024 at 3/16
+        // replays no faster and moves 10.1 GB of DRAM per launch instead of 1.6 GB
+        // (profiles/r2_ab/traffic_chat1024_tables_2p14.csv); agent256's 3 MB tables at 3/16
+        // replay 3 % faster but halve the what-if probe's throughput.
         int mult = 32;
         sl = ilog2_ceil(expect * mult / 3 + 64);
         auto tab_bytes = [&] { return ((size_t)N << sl) * 24; };
-        while (mult > 16 && tab_bytes() > (size_t)RSIM_TABLE_BUDGET) {
+        const bool over = tab_bytes() > (size_t)RSIM_TABLE_BUDGET;   // (tables within it keep 3/32)
+        const int floor16 = N > 2048 ? 16 : RSIM_SLOT_MULT;
+        while (mult > floor16 && tab_bytes() > (size_t)RSIM_TABLE_BUDGET) {
             mult /= 2;
             sl = ilog2_ceil(expect * mult / 3 + 64);
         }
-        while (mult > RSIM_SLOT_MULT && tab_bytes() > (size_t)RSIM_TABLE_MAX) {
+        while (over && mult > RSIM_SLOT_MULT && (tab_bytes() > (size_t)RSIM_TABLE_MAX || (24ull << sl) > (1ull << 20))) {
             mult /= 2;
             sl = ilog2_ceil(expect * mult / 3 + 64);
         }
